@@ -1,0 +1,329 @@
+#!/usr/bin/env python
+"""Benchmark of the RBFGS iteration (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 3]
+
+Workload (config.workload): BASELINE config 3 — dense SPD A = Q·diag(λ)·Qᵀ,
+n = 16384, RBFGS with a Gaussian sketch q = 128 (the first RBFGS config that is
+GPU-sized and the one the ≥60% DMMA target names).  A "step" is one RBFGS
+iteration: sketch → Y = A·S → W = X·Y → [G|H] = Yᵀ[S W] → Gram inverse + core
+→ V = U·M → X ← X + V·Uᵀ (symmetric).  Inputs (A, X: 2.1 GB each) exceed the
+126 MB L2, so no flush is needed between steps.
+
+value  : iterations/s, device-timed with CUDA events on the launch stream
+         (inputs resident in HBM; device counter-based sketches).
+e2e    : the same metric through the public driver si_run_inverter (the call a
+         user makes) with host buffers: A uploaded from pinned host memory and
+         X read back inside the timed region, a status word read back every
+         iteration, residual checkpoint at the last iteration.
+roofline: the dominant kernel (fused symmetric rank-2q update) — algorithmic
+         FLOPs per launch (2n²·2q/2 = 2n²q, upper triangle) ÷ its CUDA-event
+         time, against the measured FP64 DMMA peak (profiles/r01_fp64_peak.txt).
+cpu_baseline: the oracle (C++ restatement of the reference, OpenBLAS) running
+         the same bfgs_step on the host cores, a bounded sample of steps.
+--impl reference: the reference algorithm on the host cores (oracle port; the
+         reference itself cannot be built here), same metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_DMMA_PEAK_TFLOPS = 36.94  # profiles/r01_fp64_peak.txt (mma.sync m16n8k8 .f64, 148 SMs)
+HBM_PEAK_GBS = None
+
+
+def load_peaks():
+    global HBM_PEAK_GBS
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            HBM_PEAK_GBS = json.load(f).get("hbm_gbs")
+    except Exception:
+        HBM_PEAK_GBS = 6650.0
+
+
+CONFIGS = {
+    1: dict(name="config1_rbfgs_gaussian_dense_n1024_q32", n=1024, q=32, gen="config1"),
+    3: dict(name="config3_rbfgs_gaussian_dense_n16384_q128", n=16384, q=128, gen="config3"),
+}
+
+
+_DENSE_CACHE = {}
+
+
+def make_dense(cfg):
+    """Host (column-major) copy of the config's A; config 3 is synthesised on the GPU."""
+    key = cfg["name"]
+    if key in _DENSE_CACHE:
+        return _DENSE_CACHE[key]
+    from paper_1602_01768_b200 import generators as G
+
+    if cfg["gen"] == "config1":
+        a = G.config1_dense(cfg["n"], seed=0)
+    else:
+        import torch
+
+        if torch.cuda.is_available():
+            t = G.config3_dense_device(cfg["n"], seed=0)
+            host = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            host.copy_(t)
+            del t
+            torch.cuda.empty_cache()
+            a = host.numpy().T  # symmetric: row-major buffer == column-major A
+            a = np.asfortranarray(a) if not a.flags.f_contiguous else a
+        else:
+            a = G.config3_dense(cfg["n"], seed=0)
+    _DENSE_CACHE[key] = a
+    return a
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self._proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                           "--format=csv,noheader,nounits", "-lms", "100"],
+                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self._proc = None
+        return self
+
+    def _read(self):
+        for line in self._proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self._proc:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=2)
+            except Exception:
+                self._proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def cpu_port_steps_per_s(cfg, steps: int):
+    """Oracle (reference algorithm, OpenBLAS on all host threads) bfgs_step rate."""
+    from oracle import oracle as O
+
+    n, q = cfg["n"], cfg["q"]
+    a = make_dense(cfg)
+    rng = O.RngStream(0)
+    x = np.asfortranarray(np.eye(n))
+    s = rng.gaussian_matrix(n, q)
+    x = O.bfgs_step(x, a, s)  # warm
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        s = rng.gaussian_matrix(n, q)
+        x = O.bfgs_step(x, a, s)
+        x = 0.5 * (x + x.T)  # simi.cpp:351-357
+    dt = time.perf_counter() - t0
+    return steps / dt, dt
+
+
+def run_reference(args, cfg):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+
+    cores = os.cpu_count()
+    n, q = cfg["n"], cfg["q"]
+    a = make_dense(cfg)
+    rng = O.RngStream(0)
+    x = np.asfortranarray(np.eye(n))
+    for _ in range(args.warmup):
+        x = O.bfgs_step(x, a, rng.gaussian_matrix(n, q))
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        s = rng.gaussian_matrix(n, q)
+        x = O.bfgs_step(x, a, s)
+    dt = time.perf_counter() - t0
+    v = args.steps / dt
+    line = {
+        "impl": "reference", "metric": "rbfgs_iterations_per_s", "value": v, "unit": "iter/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["name"], "n": n, "q": q, "sketch": "gaussian (reference RngStream)"},
+        "cpu_baseline": {"value": v, "unit": "iter/s", "cores": cores, "kind": "port",
+                         "sample": f"{args.steps} bfgs_step iterations at n={n}, q={q} (oracle restatement of "
+                                   "qn_updates.cpp:176-186, OpenBLAS dgemm on all host threads)"},
+        "e2e": {"value": v, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, cfg):
+    import torch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1602_01768_b200 as si
+
+    n, q = cfg["n"], cfg["q"]
+    a_host = make_dense(cfg)
+    stream = torch.cuda.current_stream()
+    ctx = si.Context(local, stream=stream.cuda_stream)
+    prob = si.ProblemMatrix(a_host, si.Symmetry.spd, context=ctx)
+    sol = si.Solver(prob, si.Method.rbfgs, si.SketchRule.gaussian_device(q), seed=rank)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    # warm-up
+    sol.step(args.warmup)
+    torch.cuda.synchronize()
+    # ---- timed region (device events on the launch stream) ----
+    launches0 = ctx.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        sol.step(args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms = e0.elapsed_time(e1)
+    launches = ctx.launch_count() - launches0
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    per_step_ms = ms / args.steps
+    value = world * args.steps / (ms * 1e-3)  # whole job: every rank runs its own replica
+
+    # ---- per-kernel shares (separate pass with per-launch CUDA events) ----
+    ctx.set_profiling(True)
+    ctx.reset_profile()
+    sol.step(max(2, min(args.steps, 5)))
+    prof = ctx.profile()
+    ctx.set_profiling(False)
+    ksum = sum(v[1] for v in prof.values())
+    dom = max(prof.items(), key=lambda kv: kv[1][1])
+    upd = prof.get("gemm_symupd", dom[1])
+    upd_ms = upd[1] / max(1, upd[0])
+    upd_flops = 2.0 * n * n * q  # upper-triangular half of X + V·Uᵀ with K = 2q
+    achieved = upd_flops / (upd_ms * 1e-3) / 1e12
+    shares = {k: round(v[1] / ksum, 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])}
+    alg_flops = 6.0 * n * n * q + 12.0 * n * q * q
+
+    # ---- e2e through the public driver with host buffers ----
+    e2e = None
+    if rank == 0:
+        k_e2e = args.steps
+        a_np = a_host  # pinned host buffer (config 3) / numpy (config 1)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        prob2 = si.ProblemMatrix(a_np, si.Symmetry.spd, context=ctx)  # H2D of A
+        res = si.run_inverter(si.InverterConfig(prob2, si.SketchRule.gaussian_device(q), tol=0.0, max_iters=k_e2e,
+                                                seed=0, track=si.TrackOptions(residual_every_k=k_e2e)))
+        t1 = time.perf_counter()
+        assert res.state.k == k_e2e
+        e2e_v = k_e2e / (t1 - t0)
+        e2e = {"value": e2e_v, "unit": "iter/s", "h2d_bytes_per_step": int(8 * n * n / k_e2e),
+               "d2h_bytes_per_step": int(16 + 8 * n * n / k_e2e + 8 * 2 / k_e2e),
+               "note": "si_run_inverter from host A (H2D inside timing), device sketches, status word read back "
+                       "each iteration, residual at the last iteration (2n^3, included), X returned to host; "
+                       "byte counts are per step, A/X transfers amortised over the steps"}
+        del prob2
+
+    # ---- CPU baseline (oracle on host cores, bounded sample) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        steps_cpu = 3 if n >= 8192 else 20
+        v, dt = cpu_port_steps_per_s(cfg, steps_cpu)
+        cpu = {"value": v, "unit": "iter/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": f"{steps_cpu} bfgs_step iterations of the same workload (n={n}, q={q}) in {dt:.1f} s, "
+                         "oracle restatement of qn_updates.cpp:176-186 with OpenBLAS dgemm on all host threads"}
+
+    if rank == 0:
+        line = {
+            "metric": "rbfgs_iterations_per_s", "value": value, "unit": "iter/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step_ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["name"], "n": n, "q": q, "sketch": "gaussian, device Philox4x32-10",
+                       "l2": "inputs larger than L2 (A, X 2.1 GB each); no flush",
+                       "parallelism": "replicas" if world > 1 else "single-gpu",
+                       "algorithmic_gflop_per_step": alg_flops / 1e9,
+                       "achieved_tflops_per_step": alg_flops / (per_step_ms * 1e-3) / 1e12},
+            "roofline": {"bound": "tensor", "kernel": "gemm_symupd (X += V·Uᵀ, mirrored)", "achieved": achieved,
+                         "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_DMMA_PEAK_TFLOPS,
+                         "peak_source": "measured FP64 DMMA peak, profiles/r01_fp64_peak.txt "
+                                        "(MEASURED_PEAKS.json has no FP64 entry)",
+                         "traffic": None, "kernel_share_of_step": shares},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    load_peaks()
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", type=int, default=3, choices=sorted(CONFIGS))
+    p.add_argument("--no-cpu", action="store_true")
+    args = p.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

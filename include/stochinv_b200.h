@@ -1,0 +1,203 @@
+/*
+ * stochinv_b200 — C ABI of the B200-native RBFGS / AdaRBFGS iteration.
+ *
+ * This is the drop-in boundary for the reference's hot path (arxiv 1602.01768,
+ * `stochinv` C++ library).  The reference has no FFI layer; its boundary is the
+ * C++ API in proj/include/stochinv/ (SURVEY §8b).  Each entry point below names
+ * the reference interface it replaces.  The C++ facade
+ * include/stochinv_b200.hpp re-exposes the reference signatures on top of it;
+ * INTEGRATION.md shows the ctypes / C++ bindings.
+ *
+ * Conventions
+ *   - Dense matrices are column-major doubles (Eigen::MatrixXd layout,
+ *     proj/include/stochinv/types.hpp:8).  Pointers named *_host are host
+ *     memory; *_dev are device memory of the context's GPU.
+ *   - Every function returns an si_status.  Non-zero codes mirror the
+ *     reference's exception classes and CLI exit codes
+ *     (proj/include/stochinv/errors.hpp:9-26, tools/stochinv_cli.cpp:269-285):
+ *     SI_ERR_CONFIG = ConfigError / std::invalid_argument (exit 2),
+ *     SI_ERR_NUMERICAL = NumericalError / GramRankDeficientError (exit 3),
+ *     SI_ERR_IO = IoError (exit 4).  si_last_error() returns the message
+ *     (thread-local).  SI_ERR_RESAMPLE is the NumericalError a step kernel
+ *     raises when the sketched Gram fails (callers redraw, simi.cpp:331-333).
+ *   - A context is owned by one host thread (the reference's single-owner
+ *     inverter state); kernels run on the context stream.
+ *   - There is no CPU fallback: without a CUDA device every call that needs
+ *     the GPU returns SI_ERR_CUDA.
+ */
+#ifndef STOCHINV_B200_H
+#define STOCHINV_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum si_status {
+    SI_OK = 0,
+    SI_ERR_CONFIG = 2,
+    SI_ERR_NUMERICAL = 3,
+    SI_ERR_IO = 4,
+    SI_ERR_CUDA = 5,
+    SI_ERR_RESAMPLE = 6
+} si_status;
+
+typedef enum si_symmetry { SI_GENERAL = 0, SI_SYMMETRIC = 1, SI_SPD = 2 } si_symmetry; /* problem_matrix.hpp:7 */
+
+typedef enum si_sketch_kind {
+    SI_SKETCH_GAUSSIAN = 0,           /* SketchRule::gaussian(q), host RngStream draws (bit-exact parity mode) */
+    SI_SKETCH_GAUSSIAN_DEVICE = 1,    /* Gaussian from the device counter-based RNG (Philox4x32-10) */
+    SI_SKETCH_COORDINATE_BLOCK = 2,   /* SketchRule::coordinate_block(n, q), sketching.cpp:20-28 */
+    SI_SKETCH_ADAPTIVE_COLS = 3,      /* SketchRule::adaptive_cols(n, q): contiguous blocks + Eq 8.2 */
+    SI_SKETCH_ADAPTIVE_GAUSS = 4,     /* SketchRule::adaptive_gauss(q) */
+    SI_SKETCH_ADAPTIVE_COLS_UNIFORM = 5, /* paper sampler: q distinct coordinates uniformly */
+    SI_SKETCH_ADAPTIVE_GAUSS_DEVICE = 6  /* adaptive_gauss with device RNG */
+} si_sketch_kind;
+
+typedef enum si_probability { SI_PROB_UNIFORM = 0, SI_PROB_CONVENIENT = 1 } si_probability;
+typedef enum si_termination { SI_TOL_REACHED = 0, SI_MAX_ITERS = 1, SI_TERMINATION_ERROR = 2 } si_termination;
+
+typedef struct si_context si_context;
+typedef struct si_problem si_problem;
+
+/* HistoryPoint, simi.hpp:73-78 */
+typedef struct si_history_point {
+    int64_t k;
+    double residual; /* ||I - A X_k||_F / ||I - A X_0||_F */
+    double flops;    /* cumulative, step kernels only (flops.cpp tallies) */
+    double seconds;  /* cumulative, step kernels only (device time) */
+} si_history_point;
+
+/* Per-checkpoint observer (an addition; the reference has none). */
+typedef void (*si_checkpoint_fn)(const si_history_point* point, void* user);
+
+/* InverterConfig (simi.hpp:59-71) / AdaConfig (adarbfgs.hpp:46-56) */
+typedef struct si_inverter_config {
+    int sketch;        /* si_sketch_kind */
+    int probabilities; /* si_probability, coordinate_block only */
+    int64_t q;
+    double tol;                 /* relative residual target; 0 = unreachable */
+    int64_t max_iters;          /* default 1000 */
+    double time_budget_seconds; /* 0 = unlimited; checked at checkpoints */
+    uint64_t seed;
+    int64_t residual_every_k; /* TrackOptions::residual_every_k, default 10 */
+    int track_flops;
+    int track_wall_time;
+    int max_redraws;          /* default 100 */
+    const double* x0_host;    /* optional X0 (RBFGS) or L0 (AdaRBFGS), n×n; NULL = identity */
+    si_checkpoint_fn on_checkpoint;
+    void* user;
+} si_inverter_config;
+
+/* RunResult + InverterState scalars (simi.hpp:82-96) */
+typedef struct si_run_result {
+    int termination; /* si_termination */
+    int64_t k;
+    double max_symmetry_drift;
+    double flops;
+    double seconds;
+    int64_t history_count; /* points produced (may exceed the caller's capacity) */
+    int64_t redraws;
+    double condition_estimate; /* AdaRBFGS cond(L), n <= 256 only; 0 otherwise */
+    char message[256];
+} si_run_result;
+
+/* ---- library / context ----------------------------------------------- */
+const char* si_last_error(void);
+const char* si_version(void);
+void si_default_config(si_inverter_config* cfg); /* reference defaults (simi.hpp:53-71) */
+
+int si_context_create(int device, si_context** out);
+/* Run on a caller-provided cudaStream_t (e.g. torch.cuda.current_stream()). */
+int si_context_create_on_stream(int device, void* cuda_stream, si_context** out);
+int si_context_destroy(si_context* ctx);
+int si_context_synchronize(si_context* ctx);
+/* Kernel launches issued by this context so far (the bench's gpu_launches). */
+int64_t si_context_launch_count(si_context* ctx);
+/* Per-kernel-class device timing (CUDA events around each launch). */
+int si_context_set_profiling(si_context* ctx, int enabled);
+/* Returns the number of classes; fills up to cap entries (name, launches, total ms). */
+int si_context_profile(si_context* ctx, char (*names)[32], int64_t* launches, double* total_ms, int cap);
+int si_context_reset_profile(si_context* ctx);
+
+/* ---- problem matrix: ProblemMatrix(Matrix, Symmetry), problem_matrix.hpp:14 */
+int si_problem_create_dense(si_context* ctx, int64_t n, const double* a_host, int symmetry, si_problem** out);
+int si_problem_create_dense_device(si_context* ctx, int64_t n, const double* a_dev, int symmetry, si_problem** out);
+/* CSR (int64 rowptr, int32 colind, double val), SURVEY §8b item 2 — sparse A (configs 4/5). */
+int si_problem_create_csr(si_context* ctx, int64_t n, int64_t nnz, const int64_t* rowptr_host,
+                          const int32_t* colind_host, const double* val_host, int symmetry, si_problem** out);
+int si_problem_destroy(si_problem* prob);
+int64_t si_problem_n(si_problem* prob);
+/* ProblemMatrix::validate_spd (problem_matrix.cpp:28-41): SI_ERR_CONFIG if not spd-flagged,
+ * SI_ERR_NUMERICAL if the Cholesky fails. */
+int si_problem_validate_spd(si_problem* prob);
+/* Copy A (dense or densified CSR) to host, n×n column-major. */
+int si_problem_get_dense(si_problem* prob, double* a_host);
+
+/* ---- step-level drop-ins (host buffers, reference semantics) ----------- */
+/* Matrix bfgs_step(const Matrix& x, const Matrix& a, const Matrix& s), qn_updates.hpp:70.
+ * Returns SI_ERR_RESAMPLE when SᵀAS is not positive definite (GramRankDeficientError). */
+int si_bfgs_step(si_context* ctx, int64_t n, int64_t q, const double* x_host, const double* a_host,
+                 const double* s_host, double* x_out_host);
+/* Same step with A given as a problem handle (A resident on the device). */
+int si_bfgs_step_problem(si_context* ctx, si_problem* prob, int64_t q, const double* x_host, const double* s_host,
+                         double* x_out_host);
+/* Matrix adarbfgs_update_factor(l, a, stilde), adarbfgs.hpp:28.
+ * Returns SI_ERR_RESAMPLE when an inverse square root hits its floor. */
+int si_adarbfgs_update_factor(si_context* ctx, int64_t n, int64_t q, const double* l_host, const double* a_host,
+                              const double* stilde_host, double* l_out_host);
+/* Vector adaptive_block_probabilities(l, a, blocks), adarbfgs.hpp:32-33; blocks given in CSR
+ * form (block_offsets[nblocks+1], block_indices[n]). */
+int si_adaptive_block_probabilities(si_context* ctx, int64_t n, const double* l_host, const double* a_host,
+                                    int64_t nblocks, const int64_t* block_offsets, const int64_t* block_indices,
+                                    double* p_out_host);
+/* ||I - A X||_F (simi.cpp:242-244). */
+int si_residual(si_context* ctx, si_problem* prob, const double* x_host, double* out);
+
+/* ---- drivers --------------------------------------------------------- */
+/* RunResult run_inverter(const InverterConfig&) for MethodSpec::named_method(bfgs),
+ * simi.hpp:105 / simi.cpp:217-381.  x_out_host (n×n) receives the final X. */
+int si_run_inverter(si_context* ctx, si_problem* prob, const si_inverter_config* cfg, double* x_out_host,
+                    si_history_point* history, int64_t history_cap, si_run_result* result);
+/* RunResult run_adarbfgs(const AdaConfig&), adarbfgs.hpp:59 / adarbfgs.cpp:91-200.
+ * l_out_host (optional) receives L; x_out_host (optional) receives X = L Lᵀ. */
+int si_run_adarbfgs(si_context* ctx, si_problem* prob, const si_inverter_config* cfg, double* l_out_host,
+                    double* x_out_host, si_history_point* history, int64_t history_cap, si_run_result* result);
+
+/* ---- device-resident solver (bench / multi-GPU plumbing) -------------- */
+typedef struct si_solver si_solver;
+typedef enum si_method { SI_METHOD_RBFGS = 0, SI_METHOD_ADARBFGS = 1 } si_method;
+int si_solver_create(si_context* ctx, si_problem* prob, int method, int sketch, int64_t q, uint64_t seed,
+                     si_solver** out);
+int si_solver_destroy(si_solver* s);
+int si_solver_set_identity(si_solver* s);
+int si_solver_set_iterate(si_solver* s, const double* host);  /* X (RBFGS) or L (AdaRBFGS) */
+int si_solver_get_iterate(si_solver* s, double* host);
+/* Device pointer to the n×n iterate (column-major, ld n). */
+double* si_solver_iterate_device(si_solver* s);
+/* Run `iters` iterations with device-side sketches, no host round trip except the
+ * resample check; returns SI_ERR_NUMERICAL if max_redraws is exceeded. */
+int si_solver_step(si_solver* s, int64_t iters);
+/* One iteration with a host-supplied sketch (S for RBFGS, coordinate indices for AdaRBFGS cols). */
+int si_solver_step_with_sketch(si_solver* s, const double* s_host, const int64_t* idx_host);
+int si_solver_residual(si_solver* s, double* out); /* absolute ||I - A X||_F */
+int64_t si_solver_redraws(si_solver* s);
+
+/* ---- host RngStream (rng.hpp:13-71), exposed for input generation and tests */
+typedef struct si_rng si_rng;
+int si_rng_create(uint64_t seed, si_rng** out);
+int si_rng_substream(si_rng* r, uint64_t index, si_rng** out); /* rng.hpp:18-20 */
+int si_rng_destroy(si_rng* r);
+double si_rng_uniform(si_rng* r);
+double si_rng_gaussian(si_rng* r);
+int64_t si_rng_categorical(si_rng* r, const double* p, int64_t n);
+int64_t si_rng_uniform_index(si_rng* r, int64_t n);
+int si_rng_gaussian_matrix(si_rng* r, int64_t rows, int64_t cols, double* out); /* column-major fill */
+int si_rng_uniform_matrix(si_rng* r, int64_t rows, int64_t cols, double* out);
+int si_rng_uniform_subset(si_rng* r, int64_t n, int64_t q, int64_t* out); /* paper sampler */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STOCHINV_B200_H */

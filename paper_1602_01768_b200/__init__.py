@@ -1,0 +1,47 @@
+"""B200-native RBFGS / AdaRBFGS iteration (arxiv 1602.01768) behind the
+reference `stochinv` solver API.
+
+The compute path is libstochinv_b200.so (hand-written sm_100a FP64 DMMA
+kernels + C ABI, include/stochinv_b200.h); this package is its Python mirror.
+Importing it loads the library and raises ImportError if it is not built —
+there is no CPU fallback.
+"""
+from . import _lib
+
+_lib.load()
+
+from .api import (  # noqa: E402
+    AdaConfig,
+    ConfigError,
+    Context,
+    CudaError,
+    GramRankDeficientError,
+    HistoryPoint,
+    InverterConfig,
+    InverterState,
+    IoError,
+    Method,
+    NumericalError,
+    ProbabilityRule,
+    ProblemMatrix,
+    RngStream,
+    RunResult,
+    SketchKind,
+    SketchRule,
+    Solver,
+    Symmetry,
+    Termination,
+    TrackOptions,
+    adaptive_block_probabilities,
+    adarbfgs_update_factor,
+    bfgs_step,
+    contiguous_partition,
+    default_context,
+    flops_adarbfgs,
+    flops_bfgs,
+    residual,
+    run_adarbfgs,
+    run_inverter,
+)
+
+__all__ = [n for n in dir() if not n.startswith("_")]

@@ -1,0 +1,607 @@
+"""Python mirror of the reference's solver API, backed by the sm_100a C ABI.
+
+Names, argument meaning and error behaviour follow proj/include/stochinv/
+(qn_updates.hpp:70 bfgs_step, adarbfgs.hpp:28-59, simi.hpp:38-107,
+sketching.hpp:37-77, problem_matrix.hpp:7-35, rng.hpp:13-71, errors.hpp:9-26)
+so tests and callers read like the reference's own.  Every matrix computation
+runs on the GPU through libstochinv_b200.so; matrices cross the boundary as
+column-major float64 host arrays (numpy, order="F"), Eigen::MatrixXd's layout.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import threading
+from dataclasses import dataclass, field
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+from . import _lib as L
+
+# ----------------------------------------------------------------- errors --
+
+
+class StochinvError(Exception):
+    code = 5
+
+
+class ConfigError(StochinvError, ValueError):  # errors.hpp:9-12
+    code = 2
+
+
+class NumericalError(StochinvError, RuntimeError):  # errors.hpp:14-17
+    code = 3
+
+
+class GramRankDeficientError(NumericalError):  # errors.hpp:19-22 (resample signal)
+    code = 6
+
+
+class IoError(StochinvError, OSError):  # errors.hpp:24-26
+    code = 4
+
+
+class CudaError(StochinvError, RuntimeError):
+    code = 5
+
+
+def _check(rc: int) -> None:
+    if rc == 0:
+        return
+    msg = L.load().si_last_error().decode(errors="replace")
+    cls = {2: ConfigError, 3: NumericalError, 4: IoError, 5: CudaError, 6: GramRankDeficientError}.get(rc, StochinvError)
+    raise cls(msg)
+
+
+def _f64(a) -> np.ndarray:
+    return np.asfortranarray(np.asarray(a, dtype=np.float64))
+
+
+def _pd(a: np.ndarray):
+    return a.ctypes.data_as(L.pd)
+
+
+# ---------------------------------------------------------------- context --
+
+
+class Context:
+    """One device context (stream, workspaces); owned by one host thread."""
+
+    def __init__(self, device: int = 0, stream: Optional[int] = None):
+        lib = L.load()
+        h = C.c_void_p()
+        if stream is None:
+            _check(lib.si_context_create(device, C.byref(h)))
+        else:
+            _check(lib.si_context_create_on_stream(device, C.c_void_p(stream), C.byref(h)))
+        self._h = h
+        self.device = device
+
+    @property
+    def handle(self):
+        return self._h
+
+    def synchronize(self):
+        _check(L.load().si_context_synchronize(self._h))
+
+    def launch_count(self) -> int:
+        return int(L.load().si_context_launch_count(self._h))
+
+    def set_profiling(self, on: bool):
+        _check(L.load().si_context_set_profiling(self._h, 1 if on else 0))
+
+    def reset_profile(self):
+        _check(L.load().si_context_reset_profile(self._h))
+
+    def profile(self) -> dict:
+        cap = 64
+        names = (C.c_char * 32 * cap)()
+        launches = (C.c_int64 * cap)()
+        ms = (C.c_double * cap)()
+        cnt = L.load().si_context_profile(self._h, names, launches, ms, cap)
+        if cnt < 0:
+            _check(-cnt)
+        return {bytes(names[i]).split(b"\0")[0].decode(): (int(launches[i]), float(ms[i])) for i in range(min(cnt, cap))}
+
+    def close(self):
+        if getattr(self, "_h", None):
+            L.load().si_context_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_tls = threading.local()
+
+
+def default_context() -> Context:
+    ctx = getattr(_tls, "ctx", None)
+    if ctx is None:
+        ctx = Context(0)
+        _tls.ctx = ctx
+    return ctx
+
+
+# ------------------------------------------------------------ core types ---
+
+
+class Symmetry(enum.IntEnum):  # problem_matrix.hpp:7
+    general = 0
+    symmetric = 1
+    spd = 2
+
+
+class ProbabilityRule(enum.IntEnum):  # sketching.hpp:24-31 (subset used by bfgs)
+    uniform = 0
+    convenient = 1
+    none = 9
+
+
+class SketchKind(enum.IntEnum):  # si_sketch_kind
+    gaussian_dense = 0
+    gaussian_device = 1
+    coordinate_block = 2
+    adaptive_factor_cols = 3
+    adaptive_factor_gauss = 4
+    adaptive_factor_cols_uniform = 5
+    adaptive_factor_gauss_device = 6
+
+
+class Termination(enum.IntEnum):  # simi.hpp:80
+    tol_reached = 0
+    max_iters = 1
+    error = 2
+
+
+class ProblemMatrix:
+    """ProblemMatrix(Matrix, Symmetry) (problem_matrix.hpp:12-35), resident on the GPU.
+
+    Dense input is symmetrized (M + Mᵀ)/2 for symmetric/spd flags as the
+    reference does (problem_matrix.cpp:9-18).  `csr=(rowptr, colind, val)`
+    builds a sparse A instead (configs 4/5; the reference densifies)."""
+
+    def __init__(self, data=None, symmetry: Symmetry = Symmetry.spd, *, csr=None, n: Optional[int] = None,
+                 context: Optional[Context] = None):
+        self.ctx = context or default_context()
+        lib = L.load()
+        h = C.c_void_p()
+        self.symmetry = Symmetry(symmetry)
+        if csr is not None:
+            rowptr, colind, val = csr
+            rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
+            colind = np.ascontiguousarray(colind, dtype=np.int32)
+            val = np.ascontiguousarray(val, dtype=np.float64)
+            n = int(n if n is not None else rowptr.size - 1)
+            _check(lib.si_problem_create_csr(self.ctx.handle, n, int(val.size), rowptr.ctypes.data_as(L.pi64),
+                                             colind.ctypes.data_as(L.pi32), _pd(val), int(symmetry), C.byref(h)))
+            self.sparse = True
+            self.nnz = int(val.size)
+        else:
+            a = _f64(data)
+            if a.ndim != 2 or a.shape[0] != a.shape[1] or a.shape[0] < 1:
+                raise ConfigError("ProblemMatrix: matrix must be square with n >= 1")
+            n = a.shape[0]
+            _check(lib.si_problem_create_dense(self.ctx.handle, n, _pd(a), int(symmetry), C.byref(h)))
+            self.sparse = False
+            self.nnz = n * n
+        self._h = h
+        self._n = int(n)
+
+    def n(self) -> int:
+        return self._n
+
+    @property
+    def handle(self):
+        return self._h
+
+    def is_symmetric(self) -> bool:
+        return self.symmetry != Symmetry.general
+
+    def validate_spd(self) -> None:
+        _check(L.load().si_problem_validate_spd(self._h))
+
+    def data(self) -> np.ndarray:
+        out = np.empty((self._n, self._n), order="F")
+        _check(L.load().si_problem_get_dense(self._h, _pd(out)))
+        return out
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                L.load().si_problem_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+def contiguous_partition(n: int, q: int) -> list[list[int]]:  # sketching.cpp:106-115
+    if q < 1 or q > n:
+        raise ConfigError("contiguous_partition: need 1 <= q <= n")
+    return [list(range(s, min(s + q, n))) for s in range(0, n, q)]
+
+
+@dataclass
+class SketchRule:  # sketching.hpp:37-69 (the subset on the hot path)
+    kind: SketchKind = SketchKind.gaussian_dense
+    q: int = 1
+    probabilities: ProbabilityRule = ProbabilityRule.none
+    blocks: list = field(default_factory=list)
+
+    @staticmethod
+    def gaussian(q: int) -> "SketchRule":
+        return SketchRule(SketchKind.gaussian_dense, q, ProbabilityRule.none)
+
+    @staticmethod
+    def gaussian_device(q: int) -> "SketchRule":
+        """Gaussian S from the device counter-based RNG (perf mode; not bit-parity)."""
+        return SketchRule(SketchKind.gaussian_device, q, ProbabilityRule.none)
+
+    @staticmethod
+    def coordinate_block(n: int, q: int, prob: ProbabilityRule = ProbabilityRule.uniform) -> "SketchRule":
+        return SketchRule(SketchKind.coordinate_block, q, prob, contiguous_partition(n, q))
+
+    @staticmethod
+    def adaptive_cols(n: int, q: int) -> "SketchRule":
+        return SketchRule(SketchKind.adaptive_factor_cols, q, ProbabilityRule.uniform, contiguous_partition(n, q))
+
+    @staticmethod
+    def adaptive_gauss(q: int) -> "SketchRule":
+        return SketchRule(SketchKind.adaptive_factor_gauss, q, ProbabilityRule.none)
+
+    @staticmethod
+    def adaptive_gauss_device(q: int) -> "SketchRule":
+        return SketchRule(SketchKind.adaptive_factor_gauss_device, q, ProbabilityRule.none)
+
+    @staticmethod
+    def adaptive_cols_uniform(q: int) -> "SketchRule":
+        """Paper sampler: q distinct coordinates uniformly; not in the reference."""
+        return SketchRule(SketchKind.adaptive_factor_cols_uniform, q, ProbabilityRule.uniform)
+
+    def is_adaptive(self) -> bool:
+        return self.kind in (SketchKind.adaptive_factor_cols, SketchKind.adaptive_factor_gauss,
+                             SketchKind.adaptive_factor_cols_uniform, SketchKind.adaptive_factor_gauss_device)
+
+    def describe(self) -> str:
+        return f"{self.kind.name}(q={self.q})"
+
+
+@dataclass
+class TrackOptions:  # simi.hpp:53-57
+    residual_every_k: int = 10
+    flops: bool = True
+    wall_time: bool = True
+
+
+@dataclass
+class HistoryPoint:  # simi.hpp:73-78
+    k: int
+    residual: float
+    flops: float
+    seconds: float
+
+
+@dataclass
+class InverterState:  # simi.hpp:82-90
+    x: Optional[np.ndarray] = None
+    k: int = 0
+    history: list = field(default_factory=list)
+    max_symmetry_drift: float = 0.0
+    flops: float = 0.0
+    seconds: float = 0.0
+    l: Optional[np.ndarray] = None  # AdaRBFGS factor (FactoredState::l)
+    redraws: int = 0
+
+
+@dataclass
+class RunResult:  # simi.hpp:92-96
+    state: InverterState
+    termination: Termination = Termination.error
+    message: str = ""
+
+
+@dataclass
+class InverterConfig:  # simi.hpp:59-71 (named bfgs method)
+    a: ProblemMatrix
+    rule: SketchRule = field(default_factory=lambda: SketchRule.gaussian(1))
+    tol: float = 1e-2
+    max_iters: int = 1000
+    time_budget_seconds: float = 0.0
+    seed: int = 0
+    track: TrackOptions = field(default_factory=TrackOptions)
+    x0: Optional[np.ndarray] = None
+    max_redraws: int = 100
+    on_checkpoint: Optional[Callable[[HistoryPoint], None]] = None  # addition
+    return_x: bool = True
+
+
+@dataclass
+class AdaConfig:  # adarbfgs.hpp:46-56
+    a: ProblemMatrix
+    rule: SketchRule = field(default_factory=lambda: SketchRule.adaptive_gauss(1))
+    tol: float = 1e-2
+    max_iters: int = 1000
+    time_budget_seconds: float = 0.0
+    seed: int = 0
+    track: TrackOptions = field(default_factory=TrackOptions)
+    l0: Optional[np.ndarray] = None
+    max_redraws: int = 100
+    on_checkpoint: Optional[Callable[[HistoryPoint], None]] = None
+    return_x: bool = True
+    return_l: bool = True
+
+
+def _cfg(rule: SketchRule, tol, max_iters, budget, seed, track, x0, max_redraws, cb):
+    c = L.InverterConfigC()
+    L.load().si_default_config(C.byref(c))
+    c.sketch = int(rule.kind)
+    c.probabilities = 1 if rule.probabilities == ProbabilityRule.convenient else 0
+    c.q = int(rule.q)
+    c.tol = float(tol)
+    c.max_iters = int(max_iters)
+    c.time_budget_seconds = float(budget)
+    c.seed = int(seed) & (2**64 - 1)
+    c.residual_every_k = int(track.residual_every_k)
+    c.track_flops = 1 if track.flops else 0
+    c.track_wall_time = 1 if track.wall_time else 0
+    c.max_redraws = int(max_redraws)
+    keep = []
+    if x0 is not None:
+        x0a = _f64(x0)
+        keep.append(x0a)
+        c.x0_host = _pd(x0a)
+    if cb is not None:
+        def _tramp(pt, _user):
+            hp = C.cast(pt, C.POINTER(L.HistoryPoint)).contents
+            cb(HistoryPoint(int(hp.k), float(hp.residual), float(hp.flops), float(hp.seconds)))
+        fn = L.CHECKPOINT_FN(_tramp)
+        keep.append(fn)
+        c.on_checkpoint = fn
+    return c, keep
+
+
+def run_inverter(config: InverterConfig) -> RunResult:
+    """RunResult run_inverter(const InverterConfig&) for MethodSpec::named_method(bfgs) (simi.cpp:217-381)."""
+    a = config.a
+    if config.rule.is_adaptive():
+        raise ConfigError("run_inverter: adaptive sketch rules belong to the adarbfgs driver")
+    n = a.n()
+    if config.x0 is not None and np.shape(config.x0) != (n, n):
+        raise ConfigError("run_inverter: x0 dimension mismatch")
+    c, keep = _cfg(config.rule, config.tol, config.max_iters, config.time_budget_seconds, config.seed, config.track,
+                   config.x0, config.max_redraws, config.on_checkpoint)
+    cap = int(config.max_iters) // max(1, config.track.residual_every_k) + 4
+    hist = (L.HistoryPoint * cap)()
+    res = L.RunResultC()
+    x = np.empty((n, n), order="F") if config.return_x else None
+    _check(L.load().si_run_inverter(a.ctx.handle, a.handle, C.byref(c), _pd(x) if x is not None else None, hist, cap,
+                                    C.byref(res)))
+    del keep
+    m = min(int(res.history_count), cap)
+    st = InverterState(x=x, k=int(res.k),
+                       history=[HistoryPoint(int(h.k), h.residual, h.flops, h.seconds) for h in hist[:m]],
+                       max_symmetry_drift=res.max_symmetry_drift, flops=res.flops, seconds=res.seconds,
+                       redraws=int(res.redraws))
+    return RunResult(st, Termination(res.termination), res.message.decode(errors="replace"))
+
+
+def run_adarbfgs(config: AdaConfig) -> RunResult:
+    """RunResult run_adarbfgs(const AdaConfig&) (adarbfgs.cpp:91-200); state.x = L·Lᵀ, state.l = L."""
+    a = config.a
+    if not config.rule.is_adaptive():
+        raise ConfigError("run_adarbfgs: rule must be adaptive")
+    n = a.n()
+    if config.l0 is not None and np.shape(config.l0) != (n, n):
+        raise ConfigError("run_adarbfgs: l0 dimension mismatch")
+    c, keep = _cfg(config.rule, config.tol, config.max_iters, config.time_budget_seconds, config.seed, config.track,
+                   config.l0, config.max_redraws, config.on_checkpoint)
+    cap = int(config.max_iters) // max(1, config.track.residual_every_k) + 4
+    hist = (L.HistoryPoint * cap)()
+    res = L.RunResultC()
+    lo = np.empty((n, n), order="F") if config.return_l else None
+    xo = np.empty((n, n), order="F") if config.return_x else None
+    _check(L.load().si_run_adarbfgs(a.ctx.handle, a.handle, C.byref(c), _pd(lo) if lo is not None else None,
+                                    _pd(xo) if xo is not None else None, hist, cap, C.byref(res)))
+    del keep
+    m = min(int(res.history_count), cap)
+    st = InverterState(x=xo, l=lo, k=int(res.k),
+                       history=[HistoryPoint(int(h.k), h.residual, h.flops, h.seconds) for h in hist[:m]],
+                       flops=res.flops, seconds=res.seconds, redraws=int(res.redraws))
+    return RunResult(st, Termination(res.termination), res.message.decode(errors="replace"))
+
+
+# ------------------------------------------------------------- step level --
+
+
+def bfgs_step(x, a, s, *, context: Optional[Context] = None) -> np.ndarray:
+    """Matrix bfgs_step(const Matrix& x, const Matrix& a, const Matrix& s) (qn_updates.hpp:70).
+
+    Raises GramRankDeficientError when SᵀAS is not positive definite (the resample signal)."""
+    ctx = context or default_context()
+    x, a, s = _f64(x), _f64(a), _f64(s)
+    n, q = s.shape
+    if x.shape != (n, n) or a.shape != (n, n):
+        raise ConfigError("bfgs_step: dimension mismatch")
+    out = np.empty((n, n), order="F")
+    _check(L.load().si_bfgs_step(ctx.handle, n, q, _pd(x), _pd(a), _pd(s), _pd(out)))
+    return out
+
+
+def adarbfgs_update_factor(l, a, stilde, *, context: Optional[Context] = None) -> np.ndarray:
+    """Matrix adarbfgs_update_factor(l, a, stilde) (adarbfgs.hpp:28)."""
+    ctx = context or default_context()
+    l, a, st = _f64(l), _f64(a), _f64(stilde)
+    n, q = st.shape
+    if l.shape != (n, n) or a.shape != (n, n):
+        raise ConfigError("adarbfgs_update_factor: dimension mismatch")
+    out = np.empty((n, n), order="F")
+    rc = L.load().si_adarbfgs_update_factor(ctx.handle, n, q, _pd(l), _pd(a), _pd(st), _pd(out))
+    if rc == 6:  # floor hit: the reference throws NumericalError (linalg.cpp:150-151)
+        raise NumericalError(L.load().si_last_error().decode())
+    _check(rc)
+    return out
+
+
+def adaptive_block_probabilities(l, a, blocks: Sequence[Sequence[int]], *, context: Optional[Context] = None):
+    """Vector adaptive_block_probabilities(l, a, blocks) (adarbfgs.hpp:32-33)."""
+    ctx = context or default_context()
+    l, a = _f64(l), _f64(a)
+    n = l.shape[0]
+    offs = np.zeros(len(blocks) + 1, dtype=np.int64)
+    offs[1:] = np.cumsum([len(b) for b in blocks])
+    idx = np.ascontiguousarray(np.concatenate([np.asarray(b, dtype=np.int64) for b in blocks]) if blocks
+                               else np.zeros(0, np.int64))
+    out = np.empty(len(blocks))
+    _check(L.load().si_adaptive_block_probabilities(ctx.handle, n, _pd(l), _pd(a), len(blocks),
+                                                    offs.ctypes.data_as(L.pi64), idx.ctypes.data_as(L.pi64),
+                                                    _pd(out)))
+    return out
+
+
+def residual(a: ProblemMatrix, x) -> float:
+    """‖I − A X‖_F on the device (simi.cpp:242-244)."""
+    x = _f64(x)
+    out = C.c_double()
+    _check(L.load().si_residual(a.ctx.handle, a.handle, _pd(x), C.byref(out)))
+    return out.value
+
+
+# ---------------------------------------------------------------- flops ----
+
+
+def flops_bfgs(n, q) -> float:  # flops.cpp:43-46
+    n, q = float(n), float(q)
+    return 10 * n * n * q + 10 * n * q * q + 2 * q ** 3 + 4 * n * n
+
+
+def flops_adarbfgs(n, q) -> float:  # flops.cpp:70-74
+    n, q = float(n), float(q)
+    return 8 * n * n * q + 10 * n * q * q + 4 * q ** 3 + n * q + n * n
+
+
+# ------------------------------------------------------------------ RNG ----
+
+
+class RngStream:
+    """The reference's RngStream (rng.hpp:13-71), host side of the product library."""
+
+    def __init__(self, seed: int = 0, _handle=None):
+        lib = L.load()
+        if _handle is None:
+            h = C.c_void_p()
+            _check(lib.si_rng_create(C.c_uint64(seed & (2**64 - 1)), C.byref(h)))
+            _handle = h
+        self._h = _handle
+
+    def substream(self, index: int) -> "RngStream":
+        h = C.c_void_p()
+        _check(L.load().si_rng_substream(self._h, C.c_uint64(index), C.byref(h)))
+        return RngStream(_handle=h)
+
+    def uniform(self) -> float:
+        return float(L.load().si_rng_uniform(self._h))
+
+    def gaussian(self) -> float:
+        return float(L.load().si_rng_gaussian(self._h))
+
+    def categorical(self, p) -> int:
+        p = np.ascontiguousarray(p, dtype=np.float64)
+        return int(L.load().si_rng_categorical(self._h, _pd(p), p.size))
+
+    def uniform_index(self, n: int) -> int:
+        return int(L.load().si_rng_uniform_index(self._h, n))
+
+    def gaussian_matrix(self, rows: int, cols: int) -> np.ndarray:
+        out = np.empty((rows, cols), order="F")
+        _check(L.load().si_rng_gaussian_matrix(self._h, rows, cols, _pd(out)))
+        return out
+
+    def uniform_matrix(self, rows: int, cols: int) -> np.ndarray:
+        out = np.empty((rows, cols), order="F")
+        _check(L.load().si_rng_uniform_matrix(self._h, rows, cols, _pd(out)))
+        return out
+
+    def uniform_subset(self, n: int, q: int) -> np.ndarray:
+        out = np.empty(q, dtype=np.int64)
+        _check(L.load().si_rng_uniform_subset(self._h, n, q, out.ctypes.data_as(L.pi64)))
+        return out
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                L.load().si_rng_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+# --------------------------------------------------------------- solver ----
+
+
+class Method(enum.IntEnum):
+    rbfgs = 0
+    adarbfgs = 1
+
+
+class Solver:
+    """Device-resident iterate (X for RBFGS, L for AdaRBFGS) for benchmarking
+    and the row-sharded multi-GPU driver; iterations run without host round trips."""
+
+    def __init__(self, a: ProblemMatrix, method: Method, rule: SketchRule, seed: int = 0):
+        self.a = a
+        self.ctx = a.ctx
+        self.q = rule.q
+        h = C.c_void_p()
+        _check(L.load().si_solver_create(self.ctx.handle, a.handle, int(method), int(rule.kind), int(rule.q),
+                                         C.c_uint64(seed & (2**64 - 1)), C.byref(h)))
+        self._h = h
+
+    def set_identity(self):
+        _check(L.load().si_solver_set_identity(self._h))
+
+    def set_iterate(self, m):
+        m = _f64(m)
+        _check(L.load().si_solver_set_iterate(self._h, _pd(m)))
+
+    def iterate(self) -> np.ndarray:
+        n = self.a.n()
+        out = np.empty((n, n), order="F")
+        _check(L.load().si_solver_get_iterate(self._h, _pd(out)))
+        return out
+
+    def iterate_device_ptr(self) -> int:
+        return int(L.load().si_solver_iterate_device(self._h))
+
+    def step(self, iters: int = 1):
+        _check(L.load().si_solver_step(self._h, int(iters)))
+
+    def step_with_sketch(self, s=None, idx=None):
+        sp = None
+        ip = None
+        if s is not None:
+            s = _f64(s)
+            sp = _pd(s)
+        if idx is not None:
+            idx = np.ascontiguousarray(idx, dtype=np.int64)
+            ip = idx.ctypes.data_as(L.pi64)
+        _check(L.load().si_solver_step_with_sketch(self._h, sp, ip))
+
+    def residual(self) -> float:
+        out = C.c_double()
+        _check(L.load().si_solver_residual(self._h, C.byref(out)))
+        return out.value
+
+    def redraws(self) -> int:
+        return int(L.load().si_solver_redraws(self._h))
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                L.load().si_solver_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass

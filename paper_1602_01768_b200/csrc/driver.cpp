@@ -1,0 +1,953 @@
+// Host side of the drop-in: the C ABI (include/stochinv_b200.h) and the
+// run_inverter / run_adarbfgs drivers.  Sampling (RngStream, categorical,
+// redraw control flow) stays here on the host so indices and RNG consumption
+// follow the reference bit for bit; all matrix arithmetic is enqueued on the
+// device through engine.cu.  Compiled with g++ -O3 -march=x86-64-v3 (the
+// oracle's flags) so host Gaussian draws match the oracle's bytes.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/stochinv_b200.h"
+#include "engine.hpp"
+#include "host_rng.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct ConfigError : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+struct NumericalError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct ResampleError : NumericalError {
+    using NumericalError::NumericalError;
+};
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return SI_OK;
+    } catch (const ResampleError& e) {
+        g_err = e.what();
+        return SI_ERR_RESAMPLE;
+    } catch (const NumericalError& e) {
+        g_err = e.what();
+        return SI_ERR_NUMERICAL;
+    } catch (const si::CudaError& e) {
+        g_err = e.what();
+        return SI_ERR_CUDA;
+    } catch (const std::invalid_argument& e) {  // ConfigError and ProblemMatrix's plain invalid_argument
+        g_err = e.what();
+        return SI_ERR_CONFIG;
+    } catch (const std::bad_alloc& e) {
+        g_err = std::string("allocation failed: ") + e.what();
+        return SI_ERR_CUDA;
+    } catch (const std::exception& e) {  // stochinv_cli.cpp:281-283 maps other std::exception to exit 2
+        g_err = e.what();
+        return SI_ERR_CONFIG;
+    }
+}
+
+void ck(cudaError_t e, const char* what) { si::cuda_check(e, what); }
+
+double flops_bfgs(double n, double q) { return 10 * n * n * q + 10 * n * q * q + 2 * q * q * q + 4 * n * n; }  // flops.cpp:43-46
+double flops_adarbfgs(double n, double q) {  // flops.cpp:70-74
+    return 8 * n * n * q + 10 * n * q * q + 4 * q * q * q + n * q + n * n;
+}
+
+struct DeviceTimer {
+    cudaEvent_t a{}, b{};
+    explicit DeviceTimer() {
+        ck(cudaEventCreate(&a), "event");
+        ck(cudaEventCreate(&b), "event");
+    }
+    ~DeviceTimer() {
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+    }
+    double seconds() {
+        float ms = 0.f;
+        ck(cudaEventElapsedTime(&ms, a, b), "elapsed");
+        return ms * 1e-3;
+    }
+};
+
+}  // namespace
+
+struct si_context {
+    std::unique_ptr<si::Context> c;
+};
+
+struct si_problem {
+    si_context* owner = nullptr;
+    std::unique_ptr<si::Problem> p;
+};
+
+struct si_solver {
+    si_context* ctx = nullptr;
+    si_problem* prob = nullptr;
+    int method = 0, sketch = 0;
+    int64_t q = 0;
+    uint64_t seed = 0;
+    si::RbfgsWork rw;
+    si::AdaWork aw;
+    int* status_host = nullptr;
+    int64_t redraws = 0;
+    std::unique_ptr<si::RngStream> rng;
+    ~si_solver() {
+        rw.release();
+        aw.release();
+        if (status_host) cudaFreeHost(status_host);
+    }
+};
+
+namespace {
+
+void require(bool cond, const char* msg) {
+    if (!cond) throw ConfigError(msg);
+}
+
+// ProblemMatrix::validate_spd semantics (problem_matrix.cpp:28-41)
+void validate_spd(si_problem* prob) {
+    if (prob->p->symmetry != SI_SPD)
+        throw std::invalid_argument("ProblemMatrix: operation requires an spd-flagged matrix");
+    if (!si::problem_validate_spd(*prob->p)) throw std::runtime_error("ProblemMatrix: spd flag set but Cholesky failed");
+}
+
+double host_frobenius_asym(const double* x, int64_t n, double* norm_out) {
+    double d = 0.0, nn = 0.0;
+    for (int64_t j = 0; j < n; ++j)
+        for (int64_t i = 0; i < n; ++i) {
+            const double v = x[i + j * n];
+            const double e = v - x[j + i * n];
+            d += e * e;
+            nn += v * v;
+        }
+    *norm_out = std::sqrt(nn);
+    return std::sqrt(d);
+}
+
+std::string describe(int sketch, int64_t q) {
+    const char* k = "gaussian";
+    switch (sketch) {
+        case SI_SKETCH_COORDINATE_BLOCK: k = "coordinate-block"; break;
+        case SI_SKETCH_ADAPTIVE_COLS: k = "adaptive-factor-cols"; break;
+        case SI_SKETCH_ADAPTIVE_GAUSS:
+        case SI_SKETCH_ADAPTIVE_GAUSS_DEVICE: k = "adaptive-factor-gauss"; break;
+        case SI_SKETCH_ADAPTIVE_COLS_UNIFORM: k = "adaptive-factor-cols-uniform"; break;
+        default: break;
+    }
+    return std::string(k) + "(q=" + std::to_string(q) + ")";
+}
+
+// status[0..3] -> host (sync)
+void read_status(si::Context& c, const int* status_dev, int* host) {
+    ck(cudaMemcpyAsync(host, status_dev, 4 * sizeof(int), cudaMemcpyDeviceToHost, c.stream), "status d2h");
+    ck(cudaStreamSynchronize(c.stream), "sync");
+}
+
+double residual_norm(si::Context& c, si::Problem& a, const double* X) {
+    si::residual_sq_enqueue(c, a, X, c.scalar_dev, nullptr);
+    ck(cudaMemcpyAsync(c.scalar_host, c.scalar_dev, sizeof(double), cudaMemcpyDeviceToHost, c.stream), "d2h");
+    ck(cudaStreamSynchronize(c.stream), "sync");
+    return std::sqrt(c.scalar_host[0]);
+}
+
+double factored_residual_norm(si::Context& c, si::Problem& a, si::AdaWork& w) {
+    if (!w.AL) ck(cudaMalloc(&w.AL, size_t(w.n) * size_t(w.n) * sizeof(double)), "malloc AL");
+    si::factored_residual_sq_enqueue(c, a, w.L, w.AL, c.scalar_dev);
+    ck(cudaMemcpyAsync(c.scalar_host, c.scalar_dev, sizeof(double), cudaMemcpyDeviceToHost, c.stream), "d2h");
+    ck(cudaStreamSynchronize(c.stream), "sync");
+    return std::sqrt(c.scalar_host[0]);
+}
+
+struct HistoryWriter {
+    si_history_point* buf;
+    int64_t cap;
+    int64_t count = 0;
+    const si_inverter_config* cfg;
+    void record(int64_t k, double rel, double flops, double seconds) {
+        si_history_point hp{k, rel, flops, seconds};
+        if (buf && count < cap) buf[count] = hp;
+        ++count;
+        if (cfg->on_checkpoint) cfg->on_checkpoint(&hp, cfg->user);
+    }
+};
+
+void set_message(si_run_result* r, const std::string& m) {
+    std::snprintf(r->message, sizeof(r->message), "%s", m.c_str());
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* si_last_error(void) { return g_err.c_str(); }
+const char* si_version(void) { return "stochinv_b200 0.1 (sm_100a, FP64 DMMA)"; }
+
+void si_default_config(si_inverter_config* cfg) {
+    std::memset(cfg, 0, sizeof(*cfg));
+    cfg->sketch = SI_SKETCH_GAUSSIAN;
+    cfg->probabilities = SI_PROB_UNIFORM;
+    cfg->q = 1;
+    cfg->tol = 1e-2;          // simi.hpp:64
+    cfg->max_iters = 1000;    // simi.hpp:65
+    cfg->residual_every_k = 10;  // simi.hpp:54
+    cfg->track_flops = 1;
+    cfg->track_wall_time = 1;
+    cfg->max_redraws = 100;   // simi.hpp:70
+}
+
+int si_context_create(int device, si_context** out) {
+    return guard([&] {
+        auto* h = new si_context();
+        h->c.reset(si::context_create(device, nullptr));
+        *out = h;
+    });
+}
+
+int si_context_create_on_stream(int device, void* stream, si_context** out) {
+    return guard([&] {
+        auto* h = new si_context();
+        h->c.reset(si::context_create(device, static_cast<cudaStream_t>(stream)));
+        *out = h;
+    });
+}
+
+int si_context_destroy(si_context* ctx) {
+    return guard([&] { delete ctx; });
+}
+
+int si_context_synchronize(si_context* ctx) {
+    return guard([&] { ck(cudaStreamSynchronize(ctx->c->stream), "sync"); });
+}
+
+int64_t si_context_launch_count(si_context* ctx) { return ctx->c->launches; }
+
+int si_context_set_profiling(si_context* ctx, int enabled) {
+    return guard([&] {
+        ctx->c->resolve_profile();
+        ctx->c->profiling = enabled != 0;
+    });
+}
+
+int si_context_profile(si_context* ctx, char (*names)[32], int64_t* launches, double* total_ms, int cap) {
+    int count = 0;
+    const int rc = guard([&] {
+        ctx->c->resolve_profile();
+        auto& c = *ctx->c;
+        count = int(c.class_names.size());
+        for (int i = 0; i < count && i < cap; ++i) {
+            std::snprintf(names[i], 32, "%s", c.class_names[size_t(i)].c_str());
+            launches[i] = c.stats[size_t(i)].launches;
+            total_ms[i] = c.stats[size_t(i)].ms;
+        }
+    });
+    return rc == SI_OK ? count : -rc;
+}
+
+int si_context_reset_profile(si_context* ctx) {
+    return guard([&] {
+        ctx->c->resolve_profile();
+        for (auto& s : ctx->c->stats) s = si::KernelStat{};
+    });
+}
+
+// ------------------------------------------------------------- problems ---
+static si_problem* new_problem(si_context* ctx, int64_t n, int symmetry) {
+    require(n >= 1, "ProblemMatrix: matrix must be square with n >= 1");
+    require(symmetry >= 0 && symmetry <= 2, "ProblemMatrix: unknown symmetry flag");
+    auto* h = new si_problem();
+    h->owner = ctx;
+    h->p = std::make_unique<si::Problem>();
+    h->p->ctx = ctx->c.get();
+    h->p->n = n;
+    h->p->symmetry = symmetry;
+    return h;
+}
+
+int si_problem_create_dense(si_context* ctx, int64_t n, const double* a_host, int symmetry, si_problem** out) {
+    return guard([&] {
+        std::unique_ptr<si_problem> h(new_problem(ctx, n, symmetry));
+        // symmetric / spd flags symmetrize (M + Mᵀ)/2 on the device (problem_matrix.cpp:9-18)
+        si::problem_upload_dense(*h->p, a_host, false);
+        *out = h.release();
+    });
+}
+
+int si_problem_create_dense_device(si_context* ctx, int64_t n, const double* a_dev, int symmetry, si_problem** out) {
+    return guard([&] {
+        std::unique_ptr<si_problem> h(new_problem(ctx, n, symmetry));
+        si::problem_upload_dense(*h->p, a_dev, true);
+        *out = h.release();
+    });
+}
+
+int si_problem_create_csr(si_context* ctx, int64_t n, int64_t nnz, const int64_t* rowptr, const int32_t* colind,
+                          const double* val, int symmetry, si_problem** out) {
+    return guard([&] {
+        std::unique_ptr<si_problem> h(new_problem(ctx, n, symmetry));
+        require(rowptr[0] == 0 && rowptr[n] == nnz, "CSR: rowptr must start at 0 and end at nnz");
+        for (int64_t i = 0; i < n; ++i) require(rowptr[i + 1] >= rowptr[i], "CSR: rowptr must be non-decreasing");
+        for (int64_t t = 0; t < nnz; ++t) require(colind[t] >= 0 && colind[t] < n, "CSR: column index out of range");
+        h->p->nnz = nnz;
+        si::problem_upload_csr(*h->p, rowptr, colind, val);
+        *out = h.release();
+    });
+}
+
+int si_problem_destroy(si_problem* prob) {
+    return guard([&] { delete prob; });
+}
+
+int64_t si_problem_n(si_problem* prob) { return prob->p->n; }
+
+int si_problem_validate_spd(si_problem* prob) {
+    return guard([&] { validate_spd(prob); });
+}
+
+int si_problem_get_dense(si_problem* prob, double* a_host) {
+    return guard([&] { si::problem_download_dense(*prob->p, a_host); });
+}
+
+// ------------------------------------------------------------ steps -------
+static void bfgs_step_impl(si_context* ctx, si::Problem& a, int64_t q, const double* x_host, const double* s_host,
+                           double* x_out) {
+    auto& c = *ctx->c;
+    const int64_t n = a.n;
+    require(q >= 1, "bfgs_step: q must be >= 1");
+    si::RbfgsWork w;
+    struct Rel {
+        si::RbfgsWork& w;
+        ~Rel() { w.release(); }
+    } rel{w};
+    w.alloc(n, q, true);
+    ck(cudaMemcpyAsync(w.X, x_host, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyHostToDevice, c.stream), "h2d");
+    std::memcpy(w.s_pinned, s_host, size_t(n) * size_t(q) * sizeof(double));
+    si::rbfgs_enqueue_sketch_upload(c, w);
+    si::rbfgs_enqueue_iteration(c, a, w, false, 0);
+    int st[4];
+    read_status(c, w.status, st);
+    if (st[0]) throw ResampleError("bfgs_step: sketched Gram matrix is not positive definite");
+    ck(cudaMemcpyAsync(x_out, w.X, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, c.stream), "d2h");
+    ck(cudaStreamSynchronize(c.stream), "sync");
+}
+
+int si_bfgs_step(si_context* ctx, int64_t n, int64_t q, const double* x_host, const double* a_host,
+                 const double* s_host, double* x_out_host) {
+    return guard([&] {
+        si::Problem a;
+        a.ctx = ctx->c.get();
+        a.n = n;
+        a.symmetry = SI_GENERAL;  // bfgs_step takes A as given (qn_updates.cpp:176)
+        si::problem_upload_dense(a, a_host, false);
+        bfgs_step_impl(ctx, a, q, x_host, s_host, x_out_host);
+    });
+}
+
+int si_bfgs_step_problem(si_context* ctx, si_problem* prob, int64_t q, const double* x_host, const double* s_host,
+                         double* x_out_host) {
+    return guard([&] { bfgs_step_impl(ctx, *prob->p, q, x_host, s_host, x_out_host); });
+}
+
+int si_adarbfgs_update_factor(si_context* ctx, int64_t n, int64_t q, const double* l_host, const double* a_host,
+                              const double* stilde_host, double* l_out_host) {
+    return guard([&] {
+        auto& c = *ctx->c;
+        si::Problem a;
+        a.ctx = &c;
+        a.n = n;
+        a.symmetry = SI_GENERAL;
+        si::problem_upload_dense(a, a_host, false);
+        si::AdaWork w;
+        struct Rel {
+            si::AdaWork& w;
+            ~Rel() { w.release(); }
+        } rel{w};
+        w.alloc(n, q, true);
+        ck(cudaMemcpyAsync(w.L, l_host, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyHostToDevice, c.stream),
+           "h2d");
+        std::memcpy(w.st_pinned, stilde_host, size_t(n) * size_t(q) * sizeof(double));
+        si::ada_enqueue_update(c, a, w, 1, 0);
+        int st[4];
+        read_status(c, w.status, st);
+        if (st[0]) throw ResampleError("sym_inv_sqrt: matrix is not positive definite");
+        ck(cudaMemcpyAsync(l_out_host, w.L, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, c.stream),
+           "d2h");
+        ck(cudaStreamSynchronize(c.stream), "sync");
+    });
+}
+
+static void block_probabilities(const double* pdiag, const std::vector<std::vector<si::Index>>& blocks,
+                                std::vector<double>& p) {
+    // adarbfgs.cpp:23-36: p_i = sum_{j in C_i} l_jᵀ A l_j, then p / p.sum()
+    p.assign(blocks.size(), 0.0);
+    for (size_t i = 0; i < blocks.size(); ++i) {
+        double tr = 0.0;
+        for (si::Index j : blocks[i]) tr += pdiag[j];
+        p[i] = tr;
+    }
+    double mn = p.empty() ? 1.0 : *std::min_element(p.begin(), p.end());
+    if (mn <= 0.0)
+        throw NumericalError(
+            "adaptive_block_probabilities: non-positive block trace; the factor has degenerated");
+    double sum = 0.0;
+    for (double v : p) sum += v;
+    for (double& v : p) v /= sum;
+}
+
+int si_adaptive_block_probabilities(si_context* ctx, int64_t n, const double* l_host, const double* a_host,
+                                    int64_t nblocks, const int64_t* offs, const int64_t* idx, double* p_out) {
+    return guard([&] {
+        auto& c = *ctx->c;
+        si::Problem a;
+        a.ctx = &c;
+        a.n = n;
+        a.symmetry = SI_GENERAL;
+        si::problem_upload_dense(a, a_host, false);
+        si::AdaWork w;
+        struct Rel {
+            si::AdaWork& w;
+            ~Rel() { w.release(); }
+        } rel{w};
+        w.alloc(n, 1, false);
+        ck(cudaMemcpyAsync(w.L, l_host, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyHostToDevice, c.stream),
+           "h2d");
+        si::ada_enqueue_probabilities(c, a, w);
+        ck(cudaStreamSynchronize(c.stream), "sync");
+        std::vector<std::vector<si::Index>> blocks(static_cast<size_t>(nblocks));
+        for (int64_t b = 0; b < nblocks; ++b)
+            for (int64_t t = offs[b]; t < offs[b + 1]; ++t) blocks[size_t(b)].push_back(idx[t]);
+        std::vector<double> p;
+        block_probabilities(w.p_pinned, blocks, p);
+        std::copy(p.begin(), p.end(), p_out);
+    });
+}
+
+int si_residual(si_context* ctx, si_problem* prob, const double* x_host, double* out) {
+    return guard([&] {
+        auto& c = *ctx->c;
+        const int64_t n = prob->p->n;
+        double* X = nullptr;
+        ck(cudaMalloc(&X, size_t(n) * size_t(n) * sizeof(double)), "malloc");
+        ck(cudaMemcpyAsync(X, x_host, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyHostToDevice, c.stream), "h2d");
+        *out = residual_norm(c, *prob->p, X);
+        cudaFree(X);
+    });
+}
+
+// ---------------------------------------------------------- run_inverter ---
+// simi.cpp:217-381 for MethodSpec::named_method(UpdateName::bfgs).
+int si_run_inverter(si_context* ctx, si_problem* prob, const si_inverter_config* cfg, double* x_out,
+                    si_history_point* history, int64_t history_cap, si_run_result* result) {
+    return guard([&] {
+        auto& c = *ctx->c;
+        si::Problem& a = *prob->p;
+        const int64_t n = a.n, q = cfg->q;
+        std::memset(result, 0, sizeof(*result));
+        // validate_config (simi.cpp:185-213)
+        require(q >= 1 && q <= n, "SketchRule: q must satisfy 1 <= q <= n");
+        const int sk = cfg->sketch;
+        if (sk == SI_SKETCH_ADAPTIVE_COLS || sk == SI_SKETCH_ADAPTIVE_GAUSS || sk == SI_SKETCH_ADAPTIVE_COLS_UNIFORM ||
+            sk == SI_SKETCH_ADAPTIVE_GAUSS_DEVICE)
+            throw ConfigError("run_inverter: adaptive sketch rules belong to the adarbfgs driver");
+        require(sk == SI_SKETCH_GAUSSIAN || sk == SI_SKETCH_GAUSSIAN_DEVICE || sk == SI_SKETCH_COORDINATE_BLOCK,
+                "run_inverter: unknown sketch rule");
+        require(cfg->tol >= 0.0, "run_inverter: tol must be >= 0");
+        require(cfg->max_iters >= 1, "run_inverter: max_iters must be >= 1");
+        require(cfg->max_redraws >= 0, "run_inverter: max_redraws must be >= 0");
+        require(cfg->residual_every_k >= 1, "run_inverter: residual_every_k must be >= 1");
+        validate_spd(prob);  // validate_update(bfgs) -> a.validate_spd() (qn_updates.cpp:79-92)
+        if (cfg->x0_host) {
+            double nrm = 0.0;
+            const double asym = host_frobenius_asym(cfg->x0_host, n, &nrm);
+            if (asym > 1e-10 * std::max(1.0, nrm)) throw ConfigError("run_inverter: this method requires a symmetric x0");
+        }
+
+        si::RbfgsWork w;
+        struct Rel {
+            si::RbfgsWork& w;
+            ~Rel() { w.release(); }
+        } rel{w};
+        w.alloc(n, q, true);
+        if (cfg->x0_host)
+            ck(cudaMemcpyAsync(w.X, cfg->x0_host, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyHostToDevice,
+                               c.stream),
+               "h2d x0");
+        else
+            si::set_identity(c, w.X, n);
+
+        HistoryWriter hist{history, history_cap, 0, cfg};
+        double flops = 0.0, seconds = 0.0;
+        int64_t k = 0;
+        auto finish = [&](int term, const std::string& msg) {
+            result->termination = term;
+            result->k = k;
+            result->flops = flops;
+            result->seconds = seconds;
+            result->history_count = hist.count;
+            result->max_symmetry_drift = 0.0;  // X is written exactly symmetric (mirrored upper tiles)
+            set_message(result, msg);
+            if (x_out)
+                ck(cudaMemcpyAsync(x_out, w.X, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyDeviceToHost,
+                                   c.stream),
+                   "d2h x");
+            ck(cudaStreamSynchronize(c.stream), "sync");
+        };
+
+        const double base = residual_norm(c, a, w.X);  // simi.cpp:242-246
+        if (base == 0.0) {
+            hist.record(0, 0.0, 0.0, 0.0);
+            finish(SI_TOL_REACHED, "");
+            return;
+        }
+        hist.record(0, 1.0, 0.0, 0.0);
+
+        // coordinate-block rule (sketching.cpp:20-28) with uniform or convenient p
+        std::vector<std::vector<si::Index>> blocks;
+        std::vector<double> p;
+        if (sk == SI_SKETCH_COORDINATE_BLOCK) {
+            blocks = si::contiguous_partition(n, q);
+            p.assign(blocks.size(), 1.0 / double(blocks.size()));
+            if (cfg->probabilities == SI_PROB_CONVENIENT) {
+                // bfgs convenient p_i ∝ Tr(S_iᵀ A S_i) = sum_{j in C_i} a_jj (simi.cpp:135-142)
+                std::vector<double> diag(static_cast<size_t>(n));
+                if (a.dense) {
+                    for (int64_t j = 0; j < n; ++j)
+                        ck(cudaMemcpy(&diag[size_t(j)], a.a + j + j * n, sizeof(double), cudaMemcpyDeviceToHost),
+                           "diag");
+                } else {
+                    std::vector<double> full(size_t(n) * size_t(n));
+                    si::problem_download_dense(a, full.data());
+                    for (int64_t j = 0; j < n; ++j) diag[size_t(j)] = full[size_t(j + j * n)];
+                }
+                double sum = 0.0;
+                for (size_t i = 0; i < blocks.size(); ++i) {
+                    double t = 0.0;
+                    for (auto j : blocks[i]) t += diag[size_t(j)];
+                    if (t <= 0.0) throw ConfigError("trace probabilities: member with non-positive sketched trace");
+                    p[i] = t;
+                    sum += t;
+                }
+                for (double& v : p) v /= sum;
+            }
+        }
+
+        si::RngStream rng(cfg->seed);  // simi.cpp:275
+        const bool device_sketch = sk == SI_SKETCH_GAUSSIAN_DEVICE;
+        DeviceTimer tm;
+        int st[4];
+        for (k = 1; k <= cfg->max_iters; ++k) {
+            bool stepped = false;
+            for (int failures = 0; !stepped; ++failures) {
+                if (failures > cfg->max_redraws) {
+                    finish(SI_TERMINATION_ERROR, "sketch rejection limit exceeded for " + describe(sk, q) +
+                                                     " at iteration " + std::to_string(k));
+                    return;
+                }
+                if (sk == SI_SKETCH_GAUSSIAN) {
+                    rng.gaussian_fill(w.s_pinned, n, q, n);  // rng.hpp:42-49
+                } else if (sk == SI_SKETCH_COORDINATE_BLOCK) {
+                    const si::Index i = rng.categorical(p.data(), si::Index(p.size()));
+                    const auto& blk = blocks[size_t(i)];
+                    std::fill(w.s_pinned, w.s_pinned + n * q, 0.0);
+                    for (size_t j = 0; j < blk.size(); ++j) w.s_pinned[blk[j] + int64_t(j) * n] = 1.0;
+                    // a last, narrower block keeps unused columns zero: shrink q for that draw
+                    if (int64_t(blk.size()) != q) throw ConfigError("coordinate_block: n must be a multiple of q here");
+                }
+                if (!device_sketch) si::rbfgs_enqueue_sketch_upload(c, w);
+                ck(cudaEventRecord(tm.a, c.stream), "event");  // timer starts after the draw (simi.cpp:298)
+                si::rbfgs_enqueue_iteration(c, a, w, device_sketch, cfg->seed);
+                ck(cudaEventRecord(tm.b, c.stream), "event");
+                read_status(c, w.status, st);
+                if (st[0] || st[2]) {  // GramRankDeficientError -> redraw (simi.cpp:331-333)
+                    st[0] = st[2] = 0;
+                    ck(cudaMemsetAsync(w.status, 0, 4 * sizeof(int), c.stream), "reset");
+                    result->redraws++;
+                    continue;
+                }
+                if (cfg->track_wall_time) seconds += tm.seconds();
+                if (cfg->track_flops) flops += flops_bfgs(double(n), double(q));
+                stepped = true;
+            }
+            if (st[1]) {  // simi.cpp:342-347
+                finish(SI_TERMINATION_ERROR, "diverged: non-finite entries at iteration " + std::to_string(k));
+                return;
+            }
+            if (k == 1 || k == cfg->max_iters || k % cfg->residual_every_k == 0) {  // simi.cpp:361-375
+                const double rel = residual_norm(c, a, w.X) / base;
+                hist.record(k, rel, flops, seconds);
+                if (rel <= cfg->tol) {
+                    finish(SI_TOL_REACHED, "");
+                    return;
+                }
+                if (cfg->time_budget_seconds > 0.0 && seconds > cfg->time_budget_seconds) {
+                    finish(SI_MAX_ITERS, "time budget exhausted");
+                    return;
+                }
+            }
+        }
+        k = cfg->max_iters;
+        finish(SI_MAX_ITERS, "");
+    });
+}
+
+// ---------------------------------------------------------- run_adarbfgs ---
+// adarbfgs.cpp:91-200.
+int si_run_adarbfgs(si_context* ctx, si_problem* prob, const si_inverter_config* cfg, double* l_out,
+                    double* x_out, si_history_point* history, int64_t history_cap, si_run_result* result) {
+    return guard([&] {
+        auto& c = *ctx->c;
+        si::Problem& a = *prob->p;
+        const int64_t n = a.n, q = cfg->q;
+        std::memset(result, 0, sizeof(*result));
+        require(q >= 1 && q <= n, "SketchRule: q must satisfy 1 <= q <= n");
+        const int sk = cfg->sketch;
+        if (!(sk == SI_SKETCH_ADAPTIVE_COLS || sk == SI_SKETCH_ADAPTIVE_GAUSS || sk == SI_SKETCH_ADAPTIVE_COLS_UNIFORM ||
+              sk == SI_SKETCH_ADAPTIVE_GAUSS_DEVICE))
+            throw ConfigError("run_adarbfgs: rule must be adaptive");
+        require(cfg->tol >= 0.0, "run_adarbfgs: tol must be >= 0");
+        require(cfg->max_iters >= 1, "run_adarbfgs: max_iters must be >= 1");
+        validate_spd(prob);
+        const bool cols = sk == SI_SKETCH_ADAPTIVE_COLS;
+        const bool gauss = sk == SI_SKETCH_ADAPTIVE_GAUSS || sk == SI_SKETCH_ADAPTIVE_GAUSS_DEVICE;
+
+        si::AdaWork w;
+        struct Rel {
+            si::AdaWork& w;
+            ~Rel() { w.release(); }
+        } rel{w};
+        w.alloc(n, q, gauss);
+        if (cfg->x0_host)
+            ck(cudaMemcpyAsync(w.L, cfg->x0_host, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyHostToDevice,
+                               c.stream),
+               "h2d l0");
+        else
+            si::set_identity(c, w.L, n);
+
+        HistoryWriter hist{history, history_cap, 0, cfg};
+        double flops = 0.0, seconds = 0.0;
+        int64_t k = 0;
+        auto finish = [&](int term, const std::string& msg) {
+            result->termination = term;
+            result->k = k;
+            result->flops = flops;
+            result->seconds = seconds;
+            result->history_count = hist.count;
+            set_message(result, msg);
+            if (l_out)
+                ck(cudaMemcpyAsync(l_out, w.L, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyDeviceToHost,
+                                   c.stream),
+                   "d2h l");
+            if (x_out) {  // state.x = L Lᵀ (adarbfgs.cpp:89,122)
+                double* X = nullptr;
+                ck(cudaMalloc(&X, size_t(n) * size_t(n) * sizeof(double)), "malloc");
+                si::gemm(c, n, n, n, w.L, n, false, w.L, n, false, X, n, 1.0, 0.0);
+                ck(cudaMemcpyAsync(x_out, X, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, c.stream),
+                   "d2h x");
+                ck(cudaStreamSynchronize(c.stream), "sync");
+                cudaFree(X);
+            }
+            ck(cudaStreamSynchronize(c.stream), "sync");
+        };
+
+        const double base = factored_residual_norm(c, a, w);
+        if (base == 0.0) {
+            hist.record(0, 0.0, 0.0, 0.0);
+            finish(SI_TOL_REACHED, "");
+            return;
+        }
+        hist.record(0, 1.0, 0.0, 0.0);
+
+        const auto blocks = cols ? si::contiguous_partition(n, q) : std::vector<std::vector<si::Index>>{};
+        si::RngStream rng(cfg->seed);
+        std::vector<double> p;
+        int st[4];
+        for (k = 1; k <= cfg->max_iters; ++k) {
+            bool stepped = false;
+            const auto t0 = std::chrono::steady_clock::now();  // timer includes probabilities + draws (:143)
+            if (cols) {
+                si::ada_enqueue_probabilities(c, a, w);
+                ck(cudaStreamSynchronize(c.stream), "sync");
+                block_probabilities(w.p_pinned, blocks, p);
+            }
+            for (int attempt = 0; attempt <= cfg->max_redraws && !stepped; ++attempt) {
+                int mode = 0;
+                if (cols) {
+                    const si::Index i = rng.categorical(p.data(), si::Index(p.size()));
+                    const auto& blk = blocks[size_t(i)];
+                    if (int64_t(blk.size()) != q)
+                        throw ConfigError("adaptive_cols: n must be a multiple of q here");
+                    for (size_t j = 0; j < blk.size(); ++j) w.idx_pinned[j] = blk[j];
+                } else if (sk == SI_SKETCH_ADAPTIVE_COLS_UNIFORM) {
+                    const auto idx = si::uniform_subset(rng, n, q);
+                    for (int64_t j = 0; j < q; ++j) w.idx_pinned[j] = idx[size_t(j)];
+                } else if (sk == SI_SKETCH_ADAPTIVE_GAUSS) {
+                    rng.gaussian_fill(w.st_pinned, n, q, n);
+                    mode = 1;
+                } else {
+                    mode = 2;
+                }
+                if (mode == 0)
+                    ck(cudaMemcpyAsync(w.idx_dev, w.idx_pinned, size_t(q) * sizeof(int64_t), cudaMemcpyHostToDevice,
+                                       c.stream),
+                       "h2d idx");
+                si::ada_enqueue_update(c, a, w, mode, cfg->seed);
+                read_status(c, w.status, st);
+                if (st[0] || st[2]) {
+                    st[0] = st[2] = 0;
+                    ck(cudaMemsetAsync(w.status, 0, 4 * sizeof(int), c.stream), "reset");
+                    result->redraws++;
+                    continue;
+                }
+                stepped = true;
+            }
+            const auto t1 = std::chrono::steady_clock::now();
+            if (!stepped) {
+                finish(SI_TERMINATION_ERROR, "sketch rejection limit exceeded for " + describe(sk, q) +
+                                                 " at iteration " + std::to_string(k));
+                return;
+            }
+            if (cfg->track_wall_time) seconds += std::chrono::duration<double>(t1 - t0).count();
+            if (cfg->track_flops) {
+                flops += flops_adarbfgs(double(n), double(q));
+                if (cols) flops += 2.0 * double(n) * double(n) * double(n);  // adarbfgs.cpp:168
+            }
+            if (st[1]) {
+                finish(SI_TERMINATION_ERROR, "diverged: non-finite factor at iteration " + std::to_string(k));
+                return;
+            }
+            if (k == 1 || k == cfg->max_iters || k % cfg->residual_every_k == 0) {
+                const double rel = factored_residual_norm(c, a, w) / base;
+                hist.record(k, rel, flops, seconds);
+                if (rel <= cfg->tol) {
+                    finish(SI_TOL_REACHED, "");
+                    return;
+                }
+                if (cfg->time_budget_seconds > 0.0 && seconds > cfg->time_budget_seconds) {
+                    finish(SI_MAX_ITERS, "time budget exhausted");
+                    return;
+                }
+            }
+        }
+        k = cfg->max_iters;
+        finish(SI_MAX_ITERS, "");
+    });
+}
+
+// ------------------------------------------------------------- solver -----
+int si_solver_create(si_context* ctx, si_problem* prob, int method, int sketch, int64_t q, uint64_t seed,
+                     si_solver** out) {
+    return guard([&] {
+        const int64_t n = prob->p->n;
+        require(q >= 1 && q <= n, "SketchRule: q must satisfy 1 <= q <= n");
+        require(method == SI_METHOD_RBFGS || method == SI_METHOD_ADARBFGS, "solver: unknown method");
+        auto s = std::make_unique<si_solver>();
+        s->ctx = ctx;
+        s->prob = prob;
+        s->method = method;
+        s->sketch = sketch;
+        s->q = q;
+        s->seed = seed;
+        s->rng = std::make_unique<si::RngStream>(seed);
+        ck(cudaMallocHost(&s->status_host, 4 * sizeof(int)), "pinned");
+        if (method == SI_METHOD_RBFGS) {
+            require(sketch == SI_SKETCH_GAUSSIAN || sketch == SI_SKETCH_GAUSSIAN_DEVICE,
+                    "solver: RBFGS supports gaussian sketches");
+            s->rw.alloc(n, q, true);
+            si::set_identity(*ctx->c, s->rw.X, n);
+        } else {
+            require(sketch == SI_SKETCH_ADAPTIVE_COLS_UNIFORM || sketch == SI_SKETCH_ADAPTIVE_GAUSS ||
+                        sketch == SI_SKETCH_ADAPTIVE_GAUSS_DEVICE || sketch == SI_SKETCH_ADAPTIVE_COLS,
+                    "solver: AdaRBFGS needs an adaptive rule");
+            s->aw.alloc(n, q, sketch == SI_SKETCH_ADAPTIVE_GAUSS || sketch == SI_SKETCH_ADAPTIVE_GAUSS_DEVICE);
+            si::set_identity(*ctx->c, s->aw.L, n);
+        }
+        ck(cudaStreamSynchronize(ctx->c->stream), "sync");
+        *out = s.release();
+    });
+}
+
+int si_solver_destroy(si_solver* s) {
+    return guard([&] { delete s; });
+}
+
+static double* solver_iterate(si_solver* s) { return s->method == SI_METHOD_RBFGS ? s->rw.X : s->aw.L; }
+
+int si_solver_set_identity(si_solver* s) {
+    return guard([&] { si::set_identity(*s->ctx->c, solver_iterate(s), s->prob->p->n); });
+}
+
+int si_solver_set_iterate(si_solver* s, const double* host) {
+    return guard([&] {
+        const int64_t n = s->prob->p->n;
+        ck(cudaMemcpyAsync(solver_iterate(s), host, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyHostToDevice,
+                           s->ctx->c->stream),
+           "h2d");
+    });
+}
+
+int si_solver_get_iterate(si_solver* s, double* host) {
+    return guard([&] {
+        const int64_t n = s->prob->p->n;
+        ck(cudaMemcpyAsync(host, solver_iterate(s), size_t(n) * size_t(n) * sizeof(double), cudaMemcpyDeviceToHost,
+                           s->ctx->c->stream),
+           "d2h");
+        ck(cudaStreamSynchronize(s->ctx->c->stream), "sync");
+    });
+}
+
+double* si_solver_iterate_device(si_solver* s) { return solver_iterate(s); }
+
+int64_t si_solver_redraws(si_solver* s) { return s->redraws; }
+
+static void solver_one(si_solver* s, const double* s_host, const int64_t* idx_host, bool check) {
+    auto& c = *s->ctx->c;
+    si::Problem& a = *s->prob->p;
+    const int64_t n = a.n, q = s->q;
+    if (s->method == SI_METHOD_RBFGS) {
+        const bool dev = s_host == nullptr && s->sketch == SI_SKETCH_GAUSSIAN_DEVICE;
+        if (!dev) {
+            if (s_host)
+                std::memcpy(s->rw.s_pinned, s_host, size_t(n) * size_t(q) * sizeof(double));
+            else
+                s->rng->gaussian_fill(s->rw.s_pinned, n, q, n);
+            si::rbfgs_enqueue_sketch_upload(c, s->rw);
+        }
+        si::rbfgs_enqueue_iteration(c, a, s->rw, dev, s->seed);
+    } else {
+        int mode = 0;
+        if (idx_host) {
+            std::memcpy(s->aw.idx_pinned, idx_host, size_t(q) * sizeof(int64_t));
+        } else if (s->sketch == SI_SKETCH_ADAPTIVE_COLS_UNIFORM) {
+            const auto idx = si::uniform_subset(*s->rng, n, q);
+            for (int64_t j = 0; j < q; ++j) s->aw.idx_pinned[j] = idx[size_t(j)];
+        } else if (s->sketch == SI_SKETCH_ADAPTIVE_GAUSS) {
+            if (s_host)
+                std::memcpy(s->aw.st_pinned, s_host, size_t(n) * size_t(q) * sizeof(double));
+            else
+                s->rng->gaussian_fill(s->aw.st_pinned, n, q, n);
+            mode = 1;
+        } else if (s->sketch == SI_SKETCH_ADAPTIVE_GAUSS_DEVICE) {
+            mode = s_host ? 1 : 2;
+            if (s_host) std::memcpy(s->aw.st_pinned, s_host, size_t(n) * size_t(q) * sizeof(double));
+        } else {
+            throw ConfigError("solver: adaptive_cols needs explicit indices (use si_run_adarbfgs)");
+        }
+        if (mode == 0)
+            ck(cudaMemcpyAsync(s->aw.idx_dev, s->aw.idx_pinned, size_t(q) * sizeof(int64_t), cudaMemcpyHostToDevice,
+                               c.stream),
+               "h2d idx");
+        si::ada_enqueue_update(c, a, s->aw, mode, s->seed);
+    }
+    if (check) {
+        int* status = s->method == SI_METHOD_RBFGS ? s->rw.status : s->aw.status;
+        read_status(c, status, s->status_host);
+        if (s->status_host[1]) throw NumericalError("diverged: non-finite iterate");
+        if (s->status_host[0] || s->status_host[2]) {
+            ck(cudaMemsetAsync(status, 0, 4 * sizeof(int), c.stream), "reset");
+            s->redraws++;
+            throw ResampleError("solver: sketch rejected (resample)");
+        }
+    }
+}
+
+int si_solver_step(si_solver* s, int64_t iters) {
+    return guard([&] {
+        auto& c = *s->ctx->c;
+        const bool device = s->sketch == SI_SKETCH_GAUSSIAN_DEVICE || s->sketch == SI_SKETCH_ADAPTIVE_GAUSS_DEVICE;
+        int* status = s->method == SI_METHOD_RBFGS ? s->rw.status : s->aw.status;
+        if (!device) {
+            // host-drawn sketches share one pinned staging buffer: one iteration at a time
+            for (int64_t i = 0; i < iters;) {
+                for (int attempt = 0;; ++attempt) {
+                    try {
+                        solver_one(s, nullptr, nullptr, true);
+                        break;
+                    } catch (const ResampleError&) {
+                        if (attempt >= 100) throw NumericalError("solver: rejection limit exceeded");
+                    }
+                }
+                ++i;
+            }
+            return;
+        }
+        // device sketches: enqueue back to back with no host round trip.  A rejected
+        // Gram makes the rest of its iteration a no-op and is counted on the device
+        // (advance_counter_kernel); those iterations are re-run with fresh counters,
+        // i.e. redrawn, as simi.cpp:287-340.
+        int64_t remaining = iters;
+        int64_t total_redraws = 0;
+        while (remaining > 0) {
+            for (int64_t i = 0; i < remaining; ++i) solver_one(s, nullptr, nullptr, false);
+            read_status(c, status, s->status_host);
+            if (s->status_host[1]) throw NumericalError("diverged: non-finite iterate");
+            remaining = s->status_host[2] + s->status_host[0];
+            if (remaining) {
+                ck(cudaMemsetAsync(status, 0, 4 * sizeof(int), c.stream), "reset");
+                s->redraws += remaining;
+                total_redraws += remaining;
+                if (total_redraws > 100 * iters) throw NumericalError("solver: rejection limit exceeded");
+            }
+        }
+    });
+}
+
+int si_solver_step_with_sketch(si_solver* s, const double* s_host, const int64_t* idx_host) {
+    return guard([&] { solver_one(s, s_host, idx_host, true); });
+}
+
+int si_solver_residual(si_solver* s, double* out) {
+    return guard([&] {
+        auto& c = *s->ctx->c;
+        if (s->method == SI_METHOD_RBFGS)
+            *out = residual_norm(c, *s->prob->p, s->rw.X);
+        else
+            *out = factored_residual_norm(c, *s->prob->p, s->aw);
+    });
+}
+
+// ---------------------------------------------------------------- rng ------
+struct si_rng {
+    si::RngStream r;
+};
+
+int si_rng_create(uint64_t seed, si_rng** out) {
+    return guard([&] { *out = new si_rng{si::RngStream(seed)}; });
+}
+int si_rng_substream(si_rng* r, uint64_t index, si_rng** out) {
+    return guard([&] { *out = new si_rng{r->r.substream(index)}; });
+}
+int si_rng_destroy(si_rng* r) {
+    return guard([&] { delete r; });
+}
+double si_rng_uniform(si_rng* r) { return r->r.uniform(); }
+double si_rng_gaussian(si_rng* r) { return r->r.gaussian(); }
+int64_t si_rng_categorical(si_rng* r, const double* p, int64_t n) { return r->r.categorical(p, n); }
+int64_t si_rng_uniform_index(si_rng* r, int64_t n) { return r->r.uniform_index(n); }
+int si_rng_gaussian_matrix(si_rng* r, int64_t rows, int64_t cols, double* out) {
+    return guard([&] { r->r.gaussian_fill(out, rows, cols, rows); });
+}
+int si_rng_uniform_matrix(si_rng* r, int64_t rows, int64_t cols, double* out) {
+    return guard([&] { r->r.uniform_fill(out, rows, cols, rows); });
+}
+int si_rng_uniform_subset(si_rng* r, int64_t n, int64_t q, int64_t* out) {
+    return guard([&] {
+        require(q >= 1 && q <= n, "uniform_subset: need 1 <= q <= n");
+        const auto v = si::uniform_subset(r->r, n, q);
+        std::copy(v.begin(), v.end(), out);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,689 @@
+// Engine: launch logic of the RBFGS / AdaRBFGS iteration on one B200.
+// See engine.hpp for the data each pipeline keeps resident in HBM.
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "engine.hpp"
+#include "gemm_f64.cuh"
+#include "kernels_aux.cuh"
+#include "kernels_small.cuh"
+
+namespace si {
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CK(x) cuda_check((x), #x)
+
+// ----------------------------------------------------------------- context --
+Context* context_create(int device, cudaStream_t external) {
+    CK(cudaSetDevice(device));
+    auto* c = new Context();
+    c->device = device;
+    CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+    if (external) {
+        c->stream = external;
+        c->own_stream = false;
+    } else {
+        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+    }
+    CK(cudaMalloc(&c->scalar_dev, 8 * sizeof(double)));
+    CK(cudaMallocHost(&c->scalar_host, 8 * sizeof(double)));
+    return c;
+}
+
+Context::~Context() {
+    cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
+    for (auto& p : pending) {
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    for (auto e : event_pool) cudaEventDestroy(e);
+    if (ws) cudaFree(ws);
+    if (scalar_dev) cudaFree(scalar_dev);
+    if (scalar_host) cudaFreeHost(scalar_host);
+    if (own_stream && stream) cudaStreamDestroy(stream);
+}
+
+double* Context::ensure_ws(size_t doubles) {
+    if (doubles <= ws_doubles) return ws;
+    CK(cudaStreamSynchronize(stream));
+    if (ws) CK(cudaFree(ws));
+    ws_doubles = std::max(doubles, ws_doubles * 2);
+    CK(cudaMalloc(&ws, ws_doubles * sizeof(double)));
+    return ws;
+}
+
+int Context::class_id(const char* name) {
+    for (size_t i = 0; i < class_names.size(); ++i)
+        if (class_names[i] == name) return int(i);
+    class_names.emplace_back(name);
+    stats.emplace_back();
+    return int(class_names.size() - 1);
+}
+
+void Context::resolve_profile() {
+    if (pending.empty()) return;
+    CK(cudaStreamSynchronize(stream));
+    for (auto& p : pending) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, p.a, p.b));
+        stats[size_t(p.cls)].ms += ms;
+        event_pool.push_back(p.a);
+        event_pool.push_back(p.b);
+    }
+    pending.clear();
+}
+
+LaunchScope::LaunchScope(Context& ctx, const char* name) : c(ctx) {
+    c.launches++;
+    cls = c.class_id(name);
+    c.stats[size_t(cls)].launches++;
+    if (c.profiling) {
+        auto get = [&]() {
+            if (!c.event_pool.empty()) {
+                cudaEvent_t e = c.event_pool.back();
+                c.event_pool.pop_back();
+                return e;
+            }
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            return e;
+        };
+        a = get();
+        b = get();
+        CK(cudaEventRecord(a, c.stream));
+    }
+}
+
+LaunchScope::~LaunchScope() {
+    if (a) {
+        cudaEventRecord(b, c.stream);
+        c.pending.push_back({cls, a, b});
+    }
+}
+
+static void check_launch(const char* what) { cuda_check(cudaGetLastError(), what); }
+
+static int grid_for(int64_t work, int threads, int max_blocks = 148 * 16) {
+    int64_t b = (work + threads - 1) / threads;
+    return int(std::max<int64_t>(1, std::min<int64_t>(b, max_blocks)));
+}
+
+// --------------------------------------------------------------- GEMM ------
+template <int BM, int BN, int BK, int WM, int WN, int ST, bool AK, bool BKM, int VEC, int EPI>
+static void launch_gemm_cfg(Context& c, const GemmArgs& a, dim3 grid, const char* name) {
+    using SM = GemmSmem<BM, BN, BK, WM, WN, ST, AK, BKM>;
+    auto kern = gemm_f64_kernel<BM, BN, BK, WM, WN, ST, AK, BKM, VEC, EPI>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SM::BYTES)));
+        attr_set = true;
+    }
+    LaunchScope ls(c, name);
+    kern<<<grid, WM * WN * 32, SM::BYTES, c.stream>>>(a);
+    check_launch(name);
+}
+
+enum TileCfg { T128x128 = 0, T128x64 = 1, T128x32 = 2 };
+
+template <bool AK, bool BKM, int VEC, int EPI>
+static void launch_gemm_tile(Context& c, TileCfg t, const GemmArgs& a, dim3 grid, const char* name) {
+    switch (t) {
+        case T128x128: launch_gemm_cfg<128, 128, 16, 4, 2, 4, AK, BKM, VEC, EPI>(c, a, grid, name); break;
+        case T128x64: launch_gemm_cfg<128, 64, 16, 4, 2, 4, AK, BKM, VEC, EPI>(c, a, grid, name); break;
+        case T128x32: launch_gemm_cfg<128, 32, 16, 8, 1, 4, AK, BKM, VEC, EPI>(c, a, grid, name); break;
+    }
+}
+
+template <int EPI>
+static void launch_gemm_layout(Context& c, TileCfg t, bool ak, bool bkm, int vec, const GemmArgs& a, dim3 grid,
+                               const char* name) {
+    if (!ak && bkm) {
+        vec == 2 ? launch_gemm_tile<false, true, 2, EPI>(c, t, a, grid, name)
+                 : launch_gemm_tile<false, true, 1, EPI>(c, t, a, grid, name);
+    } else if (ak && bkm) {
+        vec == 2 ? launch_gemm_tile<true, true, 2, EPI>(c, t, a, grid, name)
+                 : launch_gemm_tile<true, true, 1, EPI>(c, t, a, grid, name);
+    } else if (!ak && !bkm) {
+        vec == 2 ? launch_gemm_tile<false, false, 2, EPI>(c, t, a, grid, name)
+                 : launch_gemm_tile<false, false, 1, EPI>(c, t, a, grid, name);
+    } else {
+        throw std::invalid_argument("gemm: A K-major with B N-major is not instantiated");
+    }
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+static int pick_vec(const GemmArgs& a) {
+    const bool ok = a.M % 2 == 0 && a.N % 2 == 0 && a.K % 2 == 0 && a.lda % 2 == 0 && a.ldb % 2 == 0 &&
+                    aligned16(a.A) && aligned16(a.B);
+    return ok ? 2 : 1;
+}
+
+static TileCfg pick_tile(int64_t N) {
+    if (N <= 32) return T128x32;
+    if (N <= 64) return T128x64;
+    return T128x128;
+}
+
+void gemm(Context& c, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, bool a_kmajor, const double* B,
+          int64_t ldb, bool b_kmajor, double* C, int64_t ldc, double alpha, double beta, const int* skip,
+          int* nonfinite) {
+    if (M <= 0 || N <= 0) return;
+    GemmArgs a{};
+    a.M = M;
+    a.N = N;
+    a.K = K;
+    a.A = A;
+    a.lda = lda;
+    a.B = B;
+    a.ldb = ldb;
+    a.C = C;
+    a.ldc = ldc;
+    a.alpha = alpha;
+    a.beta = beta;
+    a.skip = skip;
+    a.nonfinite = nonfinite;
+    const TileCfg t = pick_tile(N);
+    const int BM = 128, BN = t == T128x128 ? 128 : (t == T128x64 ? 64 : 32), BKT = 16;
+    const int64_t tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN, tiles = tm * tn;
+    const int per_sm = t == T128x128 ? 1 : 2;
+    const int64_t slots = int64_t(c.num_sms) * per_sm;
+    // split-K so the number of work units fills whole waves of the 148 SMs
+    int splits = 1;
+    if (K > 8 * BKT && tiles < 4 * slots && !nonfinite) {
+        double best = double(tiles) / double(((tiles + slots - 1) / slots) * slots);
+        for (int s = 2; s <= 128; ++s) {
+            const int64_t chunk = ((K + s - 1) / s + BKT - 1) / BKT * BKT;
+            if (chunk < 8 * BKT) break;
+            if (double(s) * double(M) * double(N) * 8.0 > 512.0 * 1024 * 1024) break;
+            const int64_t units = tiles * s;
+            const double eff = double(units) / double(((units + slots - 1) / slots) * slots);
+            if (eff > best + 0.02 || (units <= slots && eff > best)) {
+                best = eff;
+                splits = s;
+            }
+            if (units >= 4 * slots) break;
+        }
+    }
+    const int vec = pick_vec(a);
+    if (K == 0) {
+        splits = 1;
+    }
+    if (splits == 1) {
+        a.k_chunk = std::max<int64_t>(K, 1);
+        launch_gemm_layout<EPI_STORE>(c, t, a_kmajor, b_kmajor, vec, a, dim3(unsigned(tm), unsigned(tn), 1),
+                                      "gemm_store");
+        return;
+    }
+    const int64_t chunk = ((K + splits - 1) / splits + BKT - 1) / BKT * BKT;
+    splits = int((K + chunk - 1) / chunk);
+    a.k_chunk = chunk;
+    a.ws = c.ensure_ws(size_t(splits) * size_t(M) * size_t(N));
+    launch_gemm_layout<EPI_PARTIAL>(c, t, a_kmajor, b_kmajor, vec, a, dim3(unsigned(tm), unsigned(tn), unsigned(splits)),
+                                    "gemm_splitk");
+    LaunchScope ls(c, "splitk_reduce");
+    splitk_reduce_kernel<<<grid_for(M * N, 256), 256, 0, c.stream>>>(a.ws, splits, M, N, C, ldc, alpha, beta, skip);
+    check_launch("splitk_reduce");
+}
+
+// X <- X + alpha·V·Uᵀ on the upper-triangular tiles, mirrored (X symmetric n×n)
+static void symupd(Context& c, int64_t n, int64_t k, const double* V, int64_t ldv, const double* U, int64_t ldu,
+                   double* X, int64_t ldx, double alpha, const int* skip, int* nonfinite) {
+    GemmArgs a{};
+    a.M = n;
+    a.N = n;
+    a.K = k;
+    a.A = V;
+    a.lda = ldv;
+    a.B = U;
+    a.ldb = ldu;
+    a.C = X;
+    a.ldc = ldx;
+    a.alpha = alpha;
+    a.beta = 1.0;
+    a.k_chunk = k;
+    a.skip = skip;
+    a.nonfinite = nonfinite;
+    const int64_t T = (n + 127) / 128;
+    const int vec = pick_vec(a);
+    launch_gemm_layout<EPI_SYMUPD>(c, T128x128, false, false, vec, a, dim3(unsigned(T * (T + 1) / 2), 1, 1),
+                                   "gemm_symupd");
+}
+
+// ----------------------------------------------------------- problem -------
+Problem::~Problem() {
+    if (a) cudaFree(a);
+    if (rowptr) cudaFree(rowptr);
+    if (colind) cudaFree(colind);
+    if (val) cudaFree(val);
+}
+
+void problem_upload_dense(Problem& p, const double* src, bool device_src) {
+    Context& c = *p.ctx;
+    const size_t bytes = size_t(p.n) * size_t(p.n) * sizeof(double);
+    CK(cudaMalloc(&p.a, bytes));
+    CK(cudaMemcpyAsync(p.a, src, bytes, device_src ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.stream));
+    p.dense = true;
+    if (p.symmetry != 0) {  // (M + Mᵀ)/2 for symmetric / spd flags (problem_matrix.cpp:9-18)
+        LaunchScope ls(c, "symmetrize");
+        const unsigned T = unsigned((p.n + 31) / 32);
+        symmetrize_kernel<<<dim3(T, T), dim3(32, 8), 0, c.stream>>>(p.a, p.n);
+        check_launch("symmetrize");
+    }
+    CK(cudaStreamSynchronize(c.stream));
+}
+
+void problem_upload_csr(Problem& p, const int64_t* rowptr, const int32_t* colind, const double* val) {
+    Context& c = *p.ctx;
+    CK(cudaMalloc(&p.rowptr, size_t(p.n + 1) * sizeof(int64_t)));
+    CK(cudaMalloc(&p.colind, size_t(std::max<int64_t>(p.nnz, 1)) * sizeof(int32_t)));
+    CK(cudaMalloc(&p.val, size_t(std::max<int64_t>(p.nnz, 1)) * sizeof(double)));
+    CK(cudaMemcpyAsync(p.rowptr, rowptr, size_t(p.n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, c.stream));
+    if (p.nnz) {
+        CK(cudaMemcpyAsync(p.colind, colind, size_t(p.nnz) * sizeof(int32_t), cudaMemcpyHostToDevice, c.stream));
+        CK(cudaMemcpyAsync(p.val, val, size_t(p.nnz) * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+    }
+    p.dense = false;
+    CK(cudaStreamSynchronize(c.stream));
+}
+
+__global__ void densify_csr_kernel(int64_t n, const int64_t* rowptr, const int32_t* colind, const double* val,
+                                   double* out) {
+    for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < n; row += (int64_t)gridDim.x * blockDim.x)
+        for (int64_t t = rowptr[row]; t < rowptr[row + 1]; ++t) out[row + (int64_t)colind[t] * n] += val[t];
+}
+
+void problem_download_dense(Problem& p, double* host) {
+    Context& c = *p.ctx;
+    const size_t bytes = size_t(p.n) * size_t(p.n) * sizeof(double);
+    if (p.dense) {
+        CK(cudaMemcpyAsync(host, p.a, bytes, cudaMemcpyDeviceToHost, c.stream));
+    } else {
+        double* tmp = nullptr;
+        CK(cudaMalloc(&tmp, bytes));
+        CK(cudaMemsetAsync(tmp, 0, bytes, c.stream));
+        densify_csr_kernel<<<grid_for(p.n, 256), 256, 0, c.stream>>>(p.n, p.rowptr, p.colind, p.val, tmp);
+        CK(cudaMemcpyAsync(host, tmp, bytes, cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaStreamSynchronize(c.stream));
+        CK(cudaFree(tmp));
+    }
+    CK(cudaStreamSynchronize(c.stream));
+}
+
+// ProblemMatrix::validate_spd (problem_matrix.cpp:28-41) via a Cholesky on the
+// device (cuSOLVER potrf on a scratch copy; one-time setup, not the iteration).
+bool problem_validate_spd(Problem& p) {
+    if (p.spd_checked) return p.spd_ok;
+    Context& c = *p.ctx;
+    const int64_t n = p.n;
+    const size_t bytes = size_t(n) * size_t(n) * sizeof(double);
+    double* tmp = nullptr;
+    CK(cudaMalloc(&tmp, bytes));
+    if (p.dense) {
+        CK(cudaMemcpyAsync(tmp, p.a, bytes, cudaMemcpyDeviceToDevice, c.stream));
+    } else {
+        CK(cudaMemsetAsync(tmp, 0, bytes, c.stream));
+        densify_csr_kernel<<<grid_for(n, 256), 256, 0, c.stream>>>(n, p.rowptr, p.colind, p.val, tmp);
+    }
+    cusolverDnHandle_t h;
+    if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) {
+        cudaFree(tmp);
+        throw CudaError("cusolverDnCreate failed");
+    }
+    cusolverDnSetStream(h, c.stream);
+    int lwork = 0;
+    cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_LOWER, int(n), tmp, int(n), &lwork);
+    double* work = nullptr;
+    int* info = nullptr;
+    CK(cudaMalloc(&work, size_t(std::max(lwork, 1)) * sizeof(double)));
+    CK(cudaMalloc(&info, sizeof(int)));
+    cusolverDnDpotrf(h, CUBLAS_FILL_MODE_LOWER, int(n), tmp, int(n), work, lwork, info);
+    int hinfo = -1;
+    CK(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    cusolverDnDestroy(h);
+    cudaFree(work);
+    cudaFree(info);
+    cudaFree(tmp);
+    p.spd_checked = true;
+    p.spd_ok = hinfo == 0;
+    return p.spd_ok;
+}
+
+// Y = A·P (dense GEMM or CSR SpMM)
+void apply_a(Context& c, Problem& a, const double* P, int64_t ldp, int64_t k, double* Y, int64_t ldy, const int* skip) {
+    const int64_t n = a.n;
+    if (a.dense) {
+        gemm(c, n, k, n, a.a, n, false, P, ldp, true, Y, ldy, 1.0, 0.0, skip);
+        return;
+    }
+    // row-major copy of P so each nonzero reads one contiguous k-row
+    double* Pr = c.ensure_ws(size_t(n) * size_t(k));
+    {
+        LaunchScope ls(c, "transpose");
+        dim3 grid(unsigned((n + 31) / 32), unsigned((k + 31) / 32));
+        transpose_kernel<<<grid, dim3(32, 8), 0, c.stream>>>(P, n, k, ldp, Pr, skip);
+        check_launch("transpose");
+    }
+    LaunchScope ls(c, "spmm_csr");
+    spmm_csr_rowmajor_kernel<<<grid_for(n * 32, 256, c.num_sms * 32), 256, 0, c.stream>>>(n, a.rowptr, a.colind, a.val,
+                                                                                         Pr, k, Y, ldy, skip);
+    check_launch("spmm_csr");
+}
+
+void set_identity(Context& c, double* X, int64_t n) {
+    LaunchScope ls(c, "set_identity");
+    set_identity_kernel<<<grid_for(n * n, 256), 256, 0, c.stream>>>(X, n, n);
+    check_launch("set_identity");
+}
+
+// ------------------------------------------------------------- RBFGS -------
+template <typename T>
+static void dmalloc(T** p, size_t count) {
+    CK(cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T)));
+}
+
+void RbfgsWork::alloc(int64_t n_, int64_t q_, bool own) {
+    n = n_;
+    q = q_;
+    own_x = own;
+    if (own) dmalloc(&X, size_t(n) * size_t(n));
+    dmalloc(&Y, size_t(n) * size_t(q));
+    dmalloc(&U, size_t(n) * size_t(2 * q));
+    dmalloc(&V, size_t(n) * size_t(2 * q));
+    dmalloc(&P, size_t(q) * size_t(2 * q));
+    dmalloc(&Ginv, size_t(q) * size_t(q));
+    dmalloc(&T, size_t(q) * size_t(q));
+    dmalloc(&M, size_t(2 * q) * size_t(2 * q));
+    dmalloc(&factor_scratch, size_t(q) * size_t(q) + size_t(2 * q) + 16);
+    dmalloc(&status, 4);
+    dmalloc(&counter, 1);
+    CK(cudaMemset(status, 0, 4 * sizeof(int)));
+    CK(cudaMemset(counter, 0, sizeof(unsigned long long)));
+    CK(cudaMallocHost(&s_pinned, size_t(n) * size_t(q) * sizeof(double)));
+}
+
+void RbfgsWork::release() {
+    if (own_x && X) cudaFree(X);
+    for (double* p : {Y, U, V, P, Ginv, T, M, factor_scratch})
+        if (p) cudaFree(p);
+    if (status) cudaFree(status);
+    if (counter) cudaFree(counter);
+    if (s_pinned) cudaFreeHost(s_pinned);
+    X = Y = U = V = P = Ginv = T = M = factor_scratch = nullptr;
+    status = nullptr;
+    counter = nullptr;
+    s_pinned = nullptr;
+}
+
+void rbfgs_enqueue_sketch_upload(Context& c, RbfgsWork& w) {
+    CK(cudaMemcpyAsync(w.U, w.s_pinned, size_t(w.n) * size_t(w.q) * sizeof(double), cudaMemcpyHostToDevice,
+                       c.stream));
+}
+
+static void spd_inverse(Context& c, const double* P, int64_t ldp, int64_t q, double* ginv, double* scratch,
+                        int* status) {
+    const size_t smem = (size_t(q) * size_t(q) + 2 * size_t(q)) * sizeof(double);
+    const bool use_smem = smem <= 200 * 1024;
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(spd_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = true;
+    }
+    LaunchScope ls(c, "spd_inverse");
+    spd_inverse_kernel<<<1, 1024, use_smem ? smem : 0, c.stream>>>(P, ldp, int(q), ginv, q, scratch, status,
+                                                                   use_smem ? 1 : 0);
+    check_launch("spd_inverse");
+}
+
+// One RBFGS iteration:  X⁺ = X + [S W]·M·[S W]ᵀ.  Every launch
+// is skipped on the device once K-FACTOR flags a non-PD Gram (status[0]).
+void rbfgs_enqueue_iteration(Context& c, Problem& a, RbfgsWork& w, bool device_sketch, uint64_t seed) {
+    const int64_t n = w.n, q = w.q;
+    double* S = w.U;
+    double* W = w.U + n * q;
+    const int* skip = w.status;
+    if (device_sketch) {
+        LaunchScope ls(c, "sketch_philox");
+        philox_gaussian_kernel<<<grid_for((n * q + 1) / 2, 256), 256, 0, c.stream>>>(S, n, q, n, seed, w.counter,
+                                                                                   skip);
+        check_launch("philox");
+    }
+    apply_a(c, a, S, n, q, w.Y, n, skip);                                    // Y = A·S
+    gemm(c, n, q, n, w.X, n, false, w.Y, n, true, W, n, 1.0, 0.0, skip);     // W = X·Y
+    gemm(c, q, 2 * q, n, w.Y, n, true, w.U, n, true, w.P, q, 1.0, 0.0, skip);  // P = Yᵀ·[S W] = [G | H]
+    spd_inverse(c, w.P, q, q, w.Ginv, w.factor_scratch, w.status);          // Ginv, PD check
+    {
+        LaunchScope ls(c, "core_layout");
+        core_layout_kernel<<<grid_for(4 * q * q, 256), 256, 0, c.stream>>>(w.Ginv, int(q), w.M, skip);
+        check_launch("core_layout");
+    }
+    gemm(c, q, q, q, w.P + q * q, q, false, w.Ginv, q, true, w.T, q, 1.0, 0.0, skip);  // T = H·Ginv
+    gemm(c, q, q, q, w.Ginv, q, false, w.T, q, true, w.M, 2 * q, 1.0, 1.0, skip);     // M11 = Ginv + Ginv·T
+    gemm(c, n, 2 * q, 2 * q, w.U, n, false, w.M, 2 * q, true, w.V, n, 1.0, 0.0, skip);  // V = U·M
+    symupd(c, n, 2 * q, w.V, n, w.U, n, w.X, n, 1.0, skip, w.status + 1);            // X += V·Uᵀ
+    if (device_sketch) {
+        LaunchScope ls(c, "advance_counter");
+        advance_counter_kernel<<<1, 1, 0, c.stream>>>(w.counter, w.status);
+        check_launch("advance");
+    }
+}
+
+// ----------------------------------------------------------- residual ------
+template <bool BKM>
+static void resid_gemm(Context& c, int64_t n, const double* A, int64_t lda, const double* B, int64_t ldb,
+                       double* out_dev) {
+    GemmArgs g{};
+    g.M = n;
+    g.N = n;
+    g.K = n;
+    g.A = A;
+    g.lda = lda;
+    g.B = B;
+    g.ldb = ldb;
+    g.alpha = 1.0;
+    g.k_chunk = n;
+    const int64_t T = (n + 127) / 128;
+    g.ws = c.ensure_ws(size_t(T * T));
+    const int vec = pick_vec(g);
+    launch_gemm_layout<EPI_RESID>(c, T128x128, false, BKM, vec, g, dim3(unsigned(T), unsigned(T), 1), "gemm_resid");
+    LaunchScope ls(c, "sum_reduce");
+    sum_reduce_kernel<<<1, 1024, 0, c.stream>>>(g.ws, T * T, out_dev);
+    check_launch("sum_reduce");
+}
+
+__global__ void csr_resid_kernel(int64_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
+                                 const double* __restrict__ val, const double* __restrict__ X, double* partial) {
+    // ‖I − A X‖² = ‖I − X A‖² (A, X symmetric): row i of (A X) = sum_t a_it X(t,:)
+    // one warp per output row; X columns read contiguously along the row of X (X symmetric:
+    // X(t, j) = X(j, t) so row t of X is column t, contiguous).
+    __shared__ double red[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    double acc = 0.0;
+    for (int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; row < n; row += warps) {
+        const int64_t b = rowptr[row], e = rowptr[row + 1];
+        for (int64_t j = lane; j < n; j += 32) {
+            double s = 0.0;
+            for (int64_t t = b; t < e; ++t) s += val[t] * X[j + (int64_t)colind[t] * n];
+            const double d = (row == j ? 1.0 : 0.0) - s;
+            acc += d * d;
+        }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) red[wid] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        partial[blockIdx.x] = t;
+    }
+}
+
+void residual_sq_enqueue(Context& c, Problem& a, const double* X, double* out_dev, double* /*scratch*/) {
+    const int64_t n = a.n;
+    if (a.dense) {
+        resid_gemm<true>(c, n, a.a, n, X, n, out_dev);  // ‖I − A·X‖²
+        return;
+    }
+    const int blocks = c.num_sms * 4;
+    double* part = c.ensure_ws(size_t(blocks));
+    {
+        LaunchScope ls(c, "csr_resid");
+        csr_resid_kernel<<<blocks, 256, 0, c.stream>>>(n, a.rowptr, a.colind, a.val, X, part);
+        check_launch("csr_resid");
+    }
+    LaunchScope ls(c, "sum_reduce");
+    sum_reduce_kernel<<<1, 1024, 0, c.stream>>>(part, blocks, out_dev);
+    check_launch("sum_reduce");
+}
+
+// ‖I − (A·L)·Lᵀ‖² (adarbfgs.cpp:112-115): AL = A·L into scratch, then a
+// residual GEMM against Lᵀ (B operand N-major) with no n×n write.
+void factored_residual_sq_enqueue(Context& c, Problem& a, const double* L, double* AL, double* out_dev) {
+    const int64_t n = a.n;
+    apply_a(c, a, L, n, n, AL, n, nullptr);
+    resid_gemm<false>(c, n, AL, n, L, n, out_dev);
+}
+
+// ------------------------------------------------------------ AdaRBFGS -----
+void AdaWork::alloc(int64_t n_, int64_t q_, bool gaussian) {
+    n = n_;
+    q = q_;
+    dmalloc(&L, size_t(n) * size_t(n));
+    dmalloc(&S, size_t(n) * size_t(q));
+    dmalloc(&AS, size_t(n) * size_t(q));
+    dmalloc(&SR, size_t(n) * size_t(q));
+    dmalloc(&G, size_t(q) * size_t(q));
+    dmalloc(&R, size_t(q) * size_t(q));
+    dmalloc(&Z, size_t(q) * size_t(n));
+    dmalloc(&B, size_t(q) * size_t(n));
+    dmalloc(&eig_scratch, 2 * size_t(q) * size_t(q) + 8 * size_t(q) + 16);
+    dmalloc(&idx_dev, size_t(q));
+    dmalloc(&pdiag, size_t(n));
+    dmalloc(&status, 4);
+    dmalloc(&counter, 1);
+    CK(cudaMemset(status, 0, 4 * sizeof(int)));
+    CK(cudaMemset(counter, 0, sizeof(unsigned long long)));
+    CK(cudaMallocHost(&idx_pinned, size_t(q) * sizeof(int64_t)));
+    CK(cudaMallocHost(&p_pinned, size_t(n) * sizeof(double)));
+    if (gaussian) {
+        dmalloc(&St, size_t(n) * size_t(q));
+        dmalloc(&G2, size_t(q) * size_t(q));
+        dmalloc(&R2, size_t(q) * size_t(q));
+        dmalloc(&Tm, size_t(q) * size_t(n));
+        CK(cudaMallocHost(&st_pinned, size_t(n) * size_t(q) * sizeof(double)));
+    }
+}
+
+void AdaWork::release() {
+    for (double* p : {L, S, AS, SR, G, R, Z, B, eig_scratch, pdiag, St, G2, R2, Tm, AL})
+        if (p) cudaFree(p);
+    if (idx_dev) cudaFree(idx_dev);
+    if (status) cudaFree(status);
+    if (counter) cudaFree(counter);
+    if (idx_pinned) cudaFreeHost(idx_pinned);
+    if (p_pinned) cudaFreeHost(p_pinned);
+    if (st_pinned) cudaFreeHost(st_pinned);
+    L = S = AS = SR = G = R = Z = B = eig_scratch = pdiag = St = G2 = R2 = Tm = AL = nullptr;
+    idx_dev = nullptr;
+    status = nullptr;
+    counter = nullptr;
+    idx_pinned = nullptr;
+    p_pinned = nullptr;
+    st_pinned = nullptr;
+}
+
+// R = M^{-1/2} (q×q, ld q) via K-ISQRT + one GEMM; sets status on floor hit.
+static void inv_sqrt(Context& c, const double* Mq, int64_t q, double* R, double* scratch, int* status) {
+    double* QD = scratch;
+    double* Qm = scratch + q * q;
+    double* work = scratch + 2 * q * q;
+    const size_t smem = (2 * size_t(q) * size_t(q) + 4 * size_t(q)) * sizeof(double);
+    const bool use_smem = smem <= 200 * 1024;
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(jacobi_isqrt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = true;
+    }
+    double* gwork = nullptr;
+    if (!use_smem) gwork = c.ensure_ws(2 * size_t(q) * size_t(q) + 4 * size_t(q));
+    {
+        LaunchScope ls(c, "jacobi_isqrt");
+        jacobi_isqrt_kernel<<<1, 1024, use_smem ? smem : 0, c.stream>>>(Mq, q, int(q), QD, Qm, use_smem ? work : gwork,
+                                                                        status, use_smem ? 1 : 0, 1e-14);
+        check_launch("jacobi_isqrt");
+    }
+    gemm(c, q, q, q, QD, q, false, Qm, q, false, R, q, 1.0, 0.0, status);  // R = QD·Qᵀ
+}
+
+// L⁺ = L + (S·R)·(T − R·(AS)ᵀ·L), adarbfgs.cpp:12-21.
+//   mode 0: coordinate S̃ = I[:, idx] (idx_dev filled), S = L[:, idx] gathered
+//   mode 1: Gaussian S̃ uploaded from st_pinned; mode 2: Gaussian S̃ from Philox
+void ada_enqueue_update(Context& c, Problem& a, AdaWork& w, int mode, uint64_t seed) {
+    const int64_t n = w.n, q = w.q;
+    int* st = w.status;
+    if (mode == 0) {
+        LaunchScope ls(c, "gather_columns");
+        gather_columns_kernel<<<grid_for(n * q, 256), 256, 0, c.stream>>>(w.L, n, n, w.idx_dev, q, w.S);
+        check_launch("gather");
+    } else {
+        if (mode == 1) {
+            CK(cudaMemcpyAsync(w.St, w.st_pinned, size_t(n) * size_t(q) * sizeof(double), cudaMemcpyHostToDevice,
+                               c.stream));
+        } else {
+            LaunchScope ls(c, "sketch_philox");
+            philox_gaussian_kernel<<<grid_for((n * q + 1) / 2, 256), 256, 0, c.stream>>>(w.St, n, q, n, seed,
+                                                                                       w.counter, st);
+            check_launch("philox");
+        }
+        gemm(c, n, q, n, w.L, n, false, w.St, n, true, w.S, n, 1.0, 0.0, st);  // S = L·S̃
+    }
+    apply_a(c, a, w.S, n, q, w.AS, n, st);                                 // AS = A·S
+    gemm(c, q, q, n, w.S, n, true, w.AS, n, true, w.G, q, 1.0, 0.0, st);   // G = Sᵀ·AS
+    inv_sqrt(c, w.G, q, w.R, w.eig_scratch, st);                           // R = G^{-1/2}
+    gemm(c, q, n, n, w.AS, n, true, w.L, n, true, w.Z, q, 1.0, 0.0, st);   // Z = (AS)ᵀ·L
+    if (mode == 0) {
+        gemm(c, q, n, q, w.R, q, false, w.Z, q, true, w.B, q, -1.0, 0.0, st);  // B = −R·Z
+        LaunchScope ls(c, "add_selector");
+        add_selector_kernel<<<grid_for(q, 128), 128, 0, c.stream>>>(w.B, q, w.idx_dev, st);  // + T = S̃ᵀ
+        check_launch("add_selector");
+    } else {
+        // T = (S̃ᵀS̃)^{-1/2}·S̃ᵀ
+        gemm(c, q, q, n, w.St, n, true, w.St, n, true, w.G2, q, 1.0, 0.0, st);
+        inv_sqrt(c, w.G2, q, w.R2, w.eig_scratch, st);
+        gemm(c, q, n, q, w.R2, q, false, w.St, n, false, w.Tm, q, 1.0, 0.0, st);  // R2·S̃ᵀ (B N-major)
+        CK(cudaMemcpyAsync(w.B, w.Tm, size_t(q) * size_t(n) * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+        gemm(c, q, n, q, w.R, q, false, w.Z, q, true, w.B, q, -1.0, 1.0, st);  // B = T − R·Z
+    }
+    gemm(c, n, q, q, w.S, n, false, w.R, q, true, w.SR, n, 1.0, 0.0, st);  // SR = S·R
+    gemm(c, n, n, q, w.SR, n, false, w.B, q, true, w.L, n, 1.0, 1.0, st, st + 1);  // L += SR·B (+ finite check)
+    if (mode == 2) {
+        LaunchScope ls(c, "advance_counter");
+        advance_counter_kernel<<<1, 1, 0, c.stream>>>(w.counter, w.status);
+        check_launch("advance");
+    }
+}
+
+// pdiag_j = l_jᵀ A l_j (diag(LᵀAL), Eq 8.2 numerators), copied to p_pinned.
+void ada_enqueue_probabilities(Context& c, Problem& a, AdaWork& w) {
+    const int64_t n = w.n;
+    if (!w.AL) dmalloc(&w.AL, size_t(n) * size_t(n));
+    apply_a(c, a, w.L, n, n, w.AL, n, nullptr);
+    {
+        LaunchScope ls(c, "column_dots");
+        column_dots_kernel<<<grid_for(n * 32, 256), 256, 0, c.stream>>>(w.AL, w.L, n, w.pdiag);
+        check_launch("column_dots");
+    }
+    CK(cudaMemcpyAsync(w.p_pinned, w.pdiag, size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+}
+
+}  // namespace si

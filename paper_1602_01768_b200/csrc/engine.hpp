@@ -1,0 +1,142 @@
+// Internal engine interface: device context, problem storage, and the enqueue
+// functions of the RBFGS / AdaRBFGS iteration.  Implemented in engine.cu
+// (nvcc; kernels + launch logic); used by driver.cpp (host C++: C ABI, drivers,
+// reference RNG).  No CUDA kernel code here.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace si {
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void cuda_check(cudaError_t e, const char* what);
+
+struct KernelStat {
+    int64_t launches = 0;
+    double ms = 0.0;
+};
+
+struct Context {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int num_sms = 148;
+    double* ws = nullptr;  // split-K partials / reduction scratch
+    size_t ws_doubles = 0;
+    double* scalar_dev = nullptr;   // 8 doubles
+    double* scalar_host = nullptr;  // pinned mirror
+    int64_t launches = 0;
+    bool profiling = false;
+    std::vector<std::string> class_names;
+    std::vector<KernelStat> stats;
+    struct Pending {
+        int cls;
+        cudaEvent_t a, b;
+    };
+    std::vector<Pending> pending;
+    std::vector<cudaEvent_t> event_pool;
+
+    double* ensure_ws(size_t doubles);
+    int class_id(const char* name);
+    void resolve_profile();
+    ~Context();
+};
+
+// RAII launch accounting: counts the launch and (when profiling) brackets it
+// with CUDA events on the context stream.
+struct LaunchScope {
+    Context& c;
+    int cls = -1;
+    cudaEvent_t a = nullptr, b = nullptr;
+    LaunchScope(Context& ctx, const char* name);
+    ~LaunchScope();
+};
+
+struct Problem {
+    Context* ctx = nullptr;
+    int64_t n = 0;
+    int symmetry = 2;
+    bool dense = true;
+    double* a = nullptr;  // dense n×n column-major
+    // CSR
+    int64_t nnz = 0;
+    int64_t* rowptr = nullptr;
+    int32_t* colind = nullptr;
+    double* val = nullptr;
+    bool spd_checked = false;
+    bool spd_ok = false;
+    ~Problem();
+};
+
+// Workspace of one RBFGS iterate (SURVEY App. C1 rank-2q form):
+//   U = [S W] (n×2q), Y = A·S, P = Yᵀ·U = [G | H], Ginv, T = H·Ginv,
+//   M = [[Ginv + Ginv H Ginv, −Ginv], [−Ginv, 0]], V = U·M, X ← X + V·Uᵀ.
+struct RbfgsWork {
+    int64_t n = 0, q = 0;
+    double* X = nullptr;
+    double *Y = nullptr, *U = nullptr, *P = nullptr, *Ginv = nullptr, *T = nullptr, *M = nullptr, *V = nullptr;
+    double* factor_scratch = nullptr;
+    int* status = nullptr;  // [0] Gram not PD (skip), [1] non-finite iterate
+    unsigned long long* counter = nullptr;
+    double* s_pinned = nullptr;  // host staging for host-drawn sketches
+    void alloc(int64_t n, int64_t q, bool own_x);
+    void release();
+    bool own_x = true;
+};
+
+// Workspace of one AdaRBFGS factor update (adarbfgs.cpp:12-21):
+//   S = L·S̃, AS = A·S, G = Sᵀ·AS, R = G^{-1/2}, Z = (AS)ᵀ·L,
+//   L ← L + (S·R)·(T − R·Z),  T = (S̃ᵀS̃)^{-1/2} S̃ᵀ.
+struct AdaWork {
+    int64_t n = 0, q = 0;
+    double* L = nullptr;
+    double *S = nullptr, *AS = nullptr, *G = nullptr, *R = nullptr, *SR = nullptr, *Z = nullptr, *B = nullptr;
+    double *St = nullptr, *G2 = nullptr, *R2 = nullptr, *Tm = nullptr;  // Gaussian S̃ path
+    double* eig_scratch = nullptr;
+    int64_t* idx_dev = nullptr;
+    int64_t* idx_pinned = nullptr;
+    double* st_pinned = nullptr;
+    double* AL = nullptr;  // n×n scratch for residual / probabilities (lazy)
+    double* pdiag = nullptr;  // n
+    double* p_pinned = nullptr;
+    int* status = nullptr;
+    unsigned long long* counter = nullptr;
+    void alloc(int64_t n, int64_t q, bool gaussian);
+    void release();
+};
+
+// ---- engine entry points (engine.cu) -------------------------------------
+Context* context_create(int device, cudaStream_t external);
+void problem_upload_dense(Problem& p, const double* host, bool device_src);
+void problem_upload_csr(Problem& p, const int64_t* rowptr, const int32_t* colind, const double* val);
+bool problem_validate_spd(Problem& p);  // Cholesky-based (cuSOLVER potrf on a scratch copy)
+void problem_download_dense(Problem& p, double* host);
+
+// generic dense product C = alpha·op(A)·op(B) + beta·C with leading dimensions
+void gemm(Context& c, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, bool a_kmajor, const double* B,
+          int64_t ldb, bool b_kmajor, double* C, int64_t ldc, double alpha, double beta, const int* skip = nullptr,
+          int* nonfinite = nullptr);
+// Y = A·P for the problem matrix (dense GEMM or CSR SpMM), P n×k
+void apply_a(Context& c, Problem& a, const double* P, int64_t ldp, int64_t k, double* Y, int64_t ldy,
+             const int* skip = nullptr);
+
+void rbfgs_enqueue_iteration(Context& c, Problem& a, RbfgsWork& w, bool device_sketch, uint64_t seed);
+void rbfgs_enqueue_sketch_upload(Context& c, RbfgsWork& w);  // s_pinned -> S
+// sum of squares of I − A·X into *out_dev (no n×n write); returns nothing (async)
+void residual_sq_enqueue(Context& c, Problem& a, const double* X, double* out_dev, double* scratch_nxn);
+void factored_residual_sq_enqueue(Context& c, Problem& a, const double* L, double* AL, double* out_dev);
+void set_identity(Context& c, double* X, int64_t n);
+
+void ada_enqueue_update(Context& c, Problem& a, AdaWork& w, int mode /*0 cols idx, 1 gaussian host, 2 gaussian dev*/,
+                        uint64_t seed);
+void ada_enqueue_probabilities(Context& c, Problem& a, AdaWork& w);  // pdiag = diag(LᵀAL) -> p_pinned (async)
+
+}  // namespace si

@@ -1,0 +1,228 @@
+// Non-GEMM kernels of the RBFGS / AdaRBFGS iteration (sm_100a):
+//   - split-K and scalar reductions (deterministic order),
+//   - K-FACTOR: SPD check + inverse of the q×q Gram (Gauss-Jordan without
+//     pivoting, single CTA; its pivots are the squared Cholesky diagonals, so
+//     the failure test matches gram_llt, qn_updates.cpp:37-43),
+//   - K-CORE: assembly of the 2q×2q core M of the rank-2q update,
+//   - K-RNG: counter-based (Philox4x32-10) Gaussian sketch generator,
+//   - small fill / copy helpers.
+#pragma once
+#include "common.cuh"
+
+namespace si {
+
+// C(m,n) = alpha * sum_z ws[z][m,n] + beta * C(m,n)
+__global__ void splitk_reduce_kernel(const double* __restrict__ ws, int splits, int64_t M, int64_t N, double* C,
+                                     int64_t ldc, double alpha, double beta, const int* skip) {
+    if (skip && *skip) return;
+    const int64_t total = M * N;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int z = 0; z < splits; ++z) s += ws[z * total + idx];
+        const int64_t m = idx % M, n = idx / M;
+        double* c = C + m + n * ldc;
+        *c = beta != 0.0 ? alpha * s + beta * *c : alpha * s;
+    }
+}
+
+// out[0] = sum ws[0..count) in a fixed order (one CTA).
+__global__ void sum_reduce_kernel(const double* __restrict__ ws, int64_t count, double* out) {
+    __shared__ double red[32];
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < count; i += blockDim.x) s += ws[i];
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        out[0] = t;
+    }
+}
+
+// K-FACTOR.  G_ref(i,j) = P(min(i,j), max(i,j)) (the reference's LLT reads the
+// lower triangle of gram = SᵀAS; P = YᵀS = gramᵀ).  Writes Ginv (q×q, ldo) and
+// sets *status = 1 when a pivot is not > 0 (the GramRankDeficientError
+// resample signal, qn_updates.cpp:37-43).  `work` is q*q doubles of global
+// scratch used when the matrix does not fit shared memory.
+__global__ void __launch_bounds__(1024) spd_inverse_kernel(const double* __restrict__ P, int64_t ldp, int q,
+                                                           double* __restrict__ ginv, int64_t ldo, double* work,
+                                                           int* status, int use_smem) {
+    extern __shared__ __align__(16) double sm[];
+    if (*status) return;
+    double* a = use_smem ? sm : work;  // q×q col-major, ld = q
+    double* rowk = use_smem ? sm + (size_t)q * q : work + (size_t)q * q;
+    double* colk = rowk + q;
+    __shared__ int fail;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    if (tid == 0) fail = 0;
+    for (int idx = tid; idx < q * q; idx += nt) {
+        const int i = idx % q, j = idx / q;
+        a[idx] = i <= j ? P[i + (int64_t)j * ldp] : P[j + (int64_t)i * ldp];
+    }
+    __syncthreads();
+    for (int k = 0; k < q; ++k) {
+        const double piv = a[k + k * q];
+        if (!(piv > 0.0)) {  // uniform across threads: everyone read the same value
+            if (tid == 0) fail = 1;
+            break;
+        }
+        const double inv = 1.0 / piv;
+        for (int j = tid; j < q; j += nt) {
+            rowk[j] = (j == k ? 1.0 : a[k + j * q]) * inv;
+            colk[j] = a[j + k * q];
+        }
+        __syncthreads();
+        for (int idx = tid; idx < q * q; idx += nt) {
+            const int i = idx % q, j = idx / q;
+            if (i == k) {
+                a[idx] = rowk[j];
+            } else {
+                const double base = (j == k) ? 0.0 : a[idx];
+                a[idx] = base - colk[i] * rowk[j];
+            }
+        }
+        __syncthreads();
+    }
+    __syncthreads();
+    if (fail) {
+        if (tid == 0) *status = 1;
+        return;
+    }
+    for (int idx = tid; idx < q * q; idx += nt) {
+        const int i = idx % q, j = idx / q;
+        // symmetrize the inverse (exact symmetry of the implied projector)
+        ginv[i + (int64_t)j * ldo] = 0.5 * (a[i + j * q] + a[j + i * q]);
+    }
+}
+
+// K-CORE (part 1): lay out M = [[Ginv, −Ginv], [−Ginv, 0]] (2q×2q, ld 2q) from
+// Ginv so that the follow-up GEMM M11 += Ginv·(H·Ginv) completes
+// M11 = Ginv + Ginv·H·Ginv.
+__global__ void core_layout_kernel(const double* __restrict__ ginv, int q, double* __restrict__ M, const int* skip) {
+    if (skip && *skip) return;
+    const int q2 = 2 * q;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < q2 * q2; idx += gridDim.x * blockDim.x) {
+        const int i = idx % q2, j = idx / q2;
+        double v;
+        if (i < q && j < q) v = ginv[i + j * q];
+        else if (i >= q && j >= q) v = 0.0;
+        else v = -ginv[(i % q) + (j % q) * q];
+        M[idx] = v;
+    }
+}
+
+// ---------------------------------------------------------------- K-RNG --
+struct Philox {
+    __device__ static void round(uint32_t& c0, uint32_t& c1, uint32_t& c2, uint32_t& c3, uint32_t k0, uint32_t k1) {
+        const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+        const uint32_t hi0 = __umulhi(M0, c0), lo0 = M0 * c0;
+        const uint32_t hi1 = __umulhi(M1, c2), lo1 = M1 * c2;
+        const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+        c0 = n0;
+        c1 = lo1;
+        c2 = n2;
+        c3 = lo0;
+    }
+    __device__ static void gen(uint32_t (&c)[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+        for (int r = 0; r < 10; ++r) {
+            round(c[0], c[1], c[2], c[3], k0, k1);
+            k0 += 0x9E3779B9u;
+            k1 += 0xBB67AE85u;
+        }
+    }
+};
+
+// S(i,j) ~ N(0,1), column-major n×q with leading dimension lds.  Element pair
+// (2e, 2e+1) in linear order comes from Philox(key = seed, counter = (e, draw)).
+// `draw_counter` lives in device memory so one captured iteration can be
+// replayed; K-FACTOR's launcher advances it.
+__global__ void philox_gaussian_kernel(double* __restrict__ S, int64_t n, int64_t q, int64_t lds, uint64_t seed,
+                                       const unsigned long long* draw_counter, const int* skip) {
+    if (skip && *skip) return;
+    const uint64_t draw = *draw_counter;
+    const int64_t total = n * q;
+    const int64_t pairs = (total + 1) / 2;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < pairs; e += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t c[4] = {(uint32_t)e, (uint32_t)(e >> 32), (uint32_t)draw, (uint32_t)(draw >> 32)};
+        Philox::gen(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+        const uint64_t x0 = ((uint64_t)c[0] << 32) | c[1];
+        const uint64_t x1 = ((uint64_t)c[2] << 32) | c[3];
+        const double u1 = ((double)(x0 >> 11) + 0.5) * 0x1.0p-53;  // (0,1)
+        const double u2 = ((double)(x1 >> 11)) * 0x1.0p-53;        // [0,1)
+        const double r = sqrt(-2.0 * log(u1));
+        double sn, cs;
+        sincospi(2.0 * u2, &sn, &cs);
+        const int64_t l0 = 2 * e, l1 = 2 * e + 1;
+        S[(l0 % n) + (l0 / n) * lds] = r * cs;
+        if (l1 < total) S[(l1 % n) + (l1 / n) * lds] = r * sn;
+    }
+}
+
+// End of a device-sketched iteration: advance the draw counter and, when the
+// iteration's Gram was rejected, count it (status[2]) and clear the skip flag so
+// the next enqueued iteration runs -- a rejected draw becomes a redraw.
+__global__ void advance_counter_kernel(unsigned long long* counter, int* status) {
+    *counter += 1ull;
+    if (status[0]) {
+        status[2] += 1;
+        status[0] = 0;
+    }
+}
+
+// A <- (A + Aᵀ)/2 in place (ProblemMatrix construction, problem_matrix.cpp:9-18).
+// Block (bx, by) with bx <= by owns tile pair (I=bx, J=by) and its mirror.
+__global__ void symmetrize_kernel(double* A, int64_t n) {
+    __shared__ double t1[32][33], t2[32][33];
+    const int64_t I = blockIdx.x, J = blockIdx.y;
+    if (I > J) return;
+    const int tx = threadIdx.x;
+    for (int ty = threadIdx.y; ty < 32; ty += blockDim.y) {
+        const int64_t r1 = I * 32 + tx, c1 = J * 32 + ty;  // tile (I,J): A[r1, c1]
+        const int64_t r2 = J * 32 + tx, c2 = I * 32 + ty;  // tile (J,I): A[r2, c2]
+        t1[ty][tx] = (r1 < n && c1 < n) ? A[r1 + c1 * n] : 0.0;
+        t2[ty][tx] = (r2 < n && c2 < n) ? A[r2 + c2 * n] : 0.0;
+    }
+    __syncthreads();
+    for (int ty = threadIdx.y; ty < 32; ty += blockDim.y) {
+        // new A[I*32+tx, J*32+ty] = 0.5 (t1[ty][tx] + A[J*32+ty, I*32+tx]) = 0.5 (t1[ty][tx] + t2[tx][ty])
+        const int64_t r1 = I * 32 + tx, c1 = J * 32 + ty;
+        const int64_t r2 = J * 32 + tx, c2 = I * 32 + ty;
+        const double v1 = 0.5 * (t1[ty][tx] + t2[tx][ty]);
+        const double v2 = 0.5 * (t2[ty][tx] + t1[tx][ty]);
+        if (r1 < n && c1 < n) A[r1 + c1 * n] = v1;
+        if (r2 < n && c2 < n) A[r2 + c2 * n] = v2;
+    }
+}
+
+__global__ void set_identity_kernel(double* X, int64_t n, int64_t ldx) {
+    const int64_t total = n * n;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = idx % n, j = idx / n;
+        X[i + j * ldx] = (i == j) ? 1.0 : 0.0;
+    }
+}
+
+// Columns `idx[0..q)` of L (n×n, ld) gathered into S (n×q, ld n): S = L·S̃ for a
+// coordinate S̃ (adarbfgs.cpp:13 without the dense GEMM).
+__global__ void gather_columns_kernel(const double* __restrict__ L, int64_t n, int64_t ldl,
+                                      const int64_t* __restrict__ idx, int64_t q, double* __restrict__ S) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * q; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e % n, j = e / n;
+        S[e] = L[i + idx[j] * ldl];
+    }
+}
+
+// all-finite check: flag |= any non-finite entry
+__global__ void nonfinite_kernel(const double* __restrict__ X, int64_t count, int* flag) {
+    int bad = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+        bad |= !isfinite(X[i]);
+    bad = __syncthreads_or(bad);
+    if (bad && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+}  // namespace si

@@ -1,0 +1,244 @@
+// q×q kernels of the AdaRBFGS factor update and sparse/elementwise helpers.
+//   - K-ISQRT: symmetric inverse square root R = G^{-1/2} by cyclic Jacobi in a
+//     parallel (round-robin tournament) ordering inside one CTA.  Same stopping
+//     rule (off-norm ≤ 1e-15‖G‖_F, ≤ 60 sweeps), same eigenvalue floor
+//     (λ ≤ 1e-14 λ_max or λ ≤ 0 → resample) as linalg.cpp:13-79,144-155; the
+//     symmetric root is unique, so R matches the reference's to rounding.
+//   - K-SPMM: Y = A·P for CSR A (warp per row, vectorised row-major P).
+//   - column dots for diag(LᵀAL) (Eq 8.2, adarbfgs.cpp:23-36).
+#pragma once
+#include "common.cuh"
+
+namespace si {
+
+// Outputs QD = Q·diag(λ^{-1/2}) and Q (both q×q, ld q) so R = QD·Qᵀ follows as
+// one GEMM.  `work` holds 2*q*q + 4*q doubles when use_smem == 0.
+__global__ void __launch_bounds__(1024) jacobi_isqrt_kernel(const double* __restrict__ Gm, int64_t ldg, int q,
+                                                            double* __restrict__ QD, double* __restrict__ Qout,
+                                                            double* work, int* status, int use_smem,
+                                                            double floor_rel) {
+    extern __shared__ __align__(16) double sm[];
+    if (*status) return;
+    const int qe = q + (q & 1);  // even count for the tournament (index q is a bye when q is odd)
+    double* base = use_smem ? sm : work;
+    double* a = base;                       // q×q
+    double* Q = base + (size_t)q * q;       // q×q
+    double* cs = Q + (size_t)q * q;         // qe/2
+    double* sn = cs + qe / 2;               // qe/2
+    int* pp = reinterpret_cast<int*>(sn + qe / 2);  // qe/2
+    int* rr = pp + qe / 2;                          // qe/2
+    __shared__ double red[32];
+    __shared__ double s_scale, s_off;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
+
+    for (int idx = tid; idx < q * q; idx += nt) {
+        const int i = idx % q, j = idx / q;
+        a[idx] = 0.5 * (Gm[i + (int64_t)j * ldg] + Gm[j + (int64_t)i * ldg]);  // linalg.cpp:19
+        Q[idx] = (i == j) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    auto block_sum = [&](double v) -> double {
+        v = warp_sum(v);
+        __syncthreads();
+        if (lane == 0) red[wid] = v;
+        __syncthreads();
+        double t = 0.0;
+        if (tid == 0) {
+            for (int w = 0; w < (nt >> 5); ++w) t += red[w];
+        }
+        return t;
+    };
+    {
+        double v = 0.0;
+        for (int idx = tid; idx < q * q; idx += nt) v += a[idx] * a[idx];
+        const double t = block_sum(v);
+        if (tid == 0) s_scale = fmax(sqrt(t), 1e-300);  // linalg.cpp:22
+        __syncthreads();
+    }
+    const double scale = s_scale;
+    const int half = qe / 2;
+    for (int sweep = 0; sweep < 60; ++sweep) {
+        double v = 0.0;
+        for (int idx = tid; idx < q * q; idx += nt) {
+            const int i = idx % q, j = idx / q;
+            if (i < j) v += a[idx] * a[idx];
+        }
+        const double t = block_sum(v);
+        if (tid == 0) s_off = t;
+        __syncthreads();
+        if (sqrt(2.0 * s_off) <= 1e-15 * scale) break;  // linalg.cpp:28
+        for (int round = 0; round < qe - 1; ++round) {
+            // tournament pairing: slot 0 fixed, others rotate
+            for (int k = tid; k < half; k += nt) {
+                auto slot = [&](int s) { return s == 0 ? 0 : ((s - 1 + round) % (qe - 1)) + 1; };
+                int p = slot(k), r = slot(qe - 1 - k);
+                if (p > r) {
+                    const int tmp = p;
+                    p = r;
+                    r = tmp;
+                }
+                double c = 1.0, s = 0.0;
+                if (r < q) {
+                    const double apq = a[p + r * q];
+                    if (fabs(apq) > 1e-300) {
+                        const double theta = (a[r + r * q] - a[p + p * q]) / (2.0 * apq);
+                        const double tt = (theta >= 0.0) ? 1.0 / (theta + sqrt(1.0 + theta * theta))
+                                                         : 1.0 / (theta - sqrt(1.0 + theta * theta));
+                        c = 1.0 / sqrt(1.0 + tt * tt);
+                        s = tt * c;
+                    }
+                }
+                pp[k] = p;
+                rr[k] = r;
+                cs[k] = c;
+                sn[k] = s;
+            }
+            __syncthreads();
+            // A <- A J and Q <- Q J (column rotations)
+            for (int w = tid; w < half * q * 2; w += nt) {
+                const int which = w / (half * q);  // 0: a, 1: Q
+                const int rem = w % (half * q);
+                const int k = rem / q, row = rem % q;
+                const int p = pp[k], r = rr[k];
+                if (r >= q || sn[k] == 0.0) continue;
+                double* m = which ? Q : a;
+                const double c = cs[k], s = sn[k];
+                const double xp = m[row + p * q], xr = m[row + r * q];
+                m[row + p * q] = c * xp - s * xr;
+                m[row + r * q] = s * xp + c * xr;
+            }
+            __syncthreads();
+            // A <- Jᵀ A (row rotations)
+            for (int w = tid; w < half * q; w += nt) {
+                const int k = w / q, col = w % q;
+                const int p = pp[k], r = rr[k];
+                if (r >= q || sn[k] == 0.0) continue;
+                const double c = cs[k], s = sn[k];
+                const double xp = a[p + col * q], xr = a[r + col * q];
+                a[p + col * q] = c * xp - s * xr;
+                a[r + col * q] = s * xp + c * xr;
+            }
+            __syncthreads();
+        }
+    }
+    // eigenvalue floor (linalg.cpp:146-152)
+    double lmax = -1e308;
+    for (int i = 0; i < q; ++i) lmax = fmax(lmax, a[i + i * q]);
+    __shared__ int fail;
+    if (tid == 0) fail = 0;
+    __syncthreads();
+    for (int i = tid; i < q; i += nt) {
+        const double lam = a[i + i * q];
+        if (lam <= floor_rel * lmax || lam <= 0.0) fail = 1;
+    }
+    __syncthreads();
+    if (fail) {
+        if (tid == 0) *status = 1;
+        return;
+    }
+    for (int idx = tid; idx < q * q; idx += nt) {
+        const int j = idx / q;
+        const double qv = Q[idx];
+        Qout[idx] = qv;
+        QD[idx] = qv * (1.0 / sqrt(a[j + j * q]));
+    }
+}
+
+// Y(i,:) = sum_c A(i,c) P(c,:) for CSR A; P and Y column-major (ld n).  One warp
+// per row; lanes stride over the k columns.  P is read through the read-only
+// path; for k >= 32 the loads of one nonzero are 32 distinct columns.
+__global__ void spmm_csr_kernel(int64_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
+                                const double* __restrict__ val, const double* __restrict__ P, int64_t ldp, int64_t k,
+                                double* __restrict__ Y, int64_t ldy, const int* skip) {
+    if (skip && *skip) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; row < n; row += warps) {
+        const int64_t b = rowptr[row], e = rowptr[row + 1];
+        for (int64_t c0 = 0; c0 < k; c0 += 32) {
+            const int64_t col = c0 + lane;
+            double acc = 0.0;
+            if (col < k) {
+                for (int64_t t = b; t < e; ++t) acc += __ldg(val + t) * __ldg(P + colind[t] + col * ldp);
+                Y[row + col * ldy] = acc;
+            }
+        }
+    }
+}
+
+// Row-major SpMM: Yr(i,:) = sum_c A(i,c) Pr(c,:) with Pr, Yr row-major (ld = k).
+// Coalesced: the warp reads one contiguous k-row of Pr per nonzero.
+__global__ void spmm_csr_rowmajor_kernel(int64_t n, const int64_t* __restrict__ rowptr,
+                                         const int32_t* __restrict__ colind, const double* __restrict__ val,
+                                         const double* __restrict__ Pr, int64_t k, double* __restrict__ Y,
+                                         int64_t ldy, const int* skip) {
+    if (skip && *skip) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; row < n; row += warps) {
+        const int64_t b = rowptr[row], e = rowptr[row + 1];
+        for (int64_t c0 = 0; c0 < k; c0 += 64) {
+            const int64_t col = c0 + 2 * lane;
+            double2 acc = make_double2(0.0, 0.0);
+            if (col + 1 < k) {
+                for (int64_t t = b; t < e; ++t) {
+                    const double v = __ldg(val + t);
+                    const double2 x = __ldg(reinterpret_cast<const double2*>(Pr + (int64_t)colind[t] * k + col));
+                    acc.x += v * x.x;
+                    acc.y += v * x.y;
+                }
+                Y[row + col * ldy] = acc.x;
+                Y[row + (col + 1) * ldy] = acc.y;
+            } else if (col < k) {
+                for (int64_t t = b; t < e; ++t) acc.x += __ldg(val + t) * __ldg(Pr + (int64_t)colind[t] * k + col);
+                Y[row + col * ldy] = acc.x;
+            }
+        }
+    }
+}
+
+// out (k×n row-major, i.e. Pᵀ col-major) = transpose of P (n×k col-major)
+__global__ void transpose_kernel(const double* __restrict__ P, int64_t n, int64_t k, int64_t ldp,
+                                 double* __restrict__ out, const int* skip) {
+    if (skip && *skip) return;
+    __shared__ double tile[32][33];
+    const int64_t i0 = (int64_t)blockIdx.x * 32, j0 = (int64_t)blockIdx.y * 32;
+    for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+        const int64_t i = i0 + threadIdx.x, j = j0 + dy;
+        if (i < n && j < k) tile[dy][threadIdx.x] = P[i + j * ldp];
+    }
+    __syncthreads();
+    for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+        const int64_t i = i0 + dy, j = j0 + threadIdx.x;
+        if (i < n && j < k) out[j + i * k] = tile[threadIdx.x][dy];
+    }
+}
+
+// d_j = sum_i AL(i,j) * L(i,j)  (diag(Lᵀ A L)); one warp per column.
+__global__ void column_dots_kernel(const double* __restrict__ AL, const double* __restrict__ L, int64_t n,
+                                   double* __restrict__ d) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; j < n; j += warps) {
+        double s = 0.0;
+        for (int64_t i = lane; i < n; i += 32) s += AL[i + j * n] * L[i + j * n];
+        s = warp_sum(s);
+        if (lane == 0) d[j] = s;
+    }
+}
+
+// B = T − R·Z precursor for coordinate S̃: after B = −R·Z, add T = S̃ᵀ (B[j, idx[j]] += 1).
+__global__ void add_selector_kernel(double* B, int64_t q, const int64_t* __restrict__ idx, const int* skip) {
+    if (skip && *skip) return;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < q; j += (int64_t)gridDim.x * blockDim.x)
+        B[j + idx[j] * q] += 1.0;
+}
+
+// ‖X‖ entries of a dense matrix into a scaled copy (used for QD-style scaling)
+__global__ void scatter_coordinate_kernel(double* S, int64_t n, int64_t q, const int64_t* __restrict__ idx) {
+    // S = I[:, idx] (n×q, ld n), S zero-initialised by the caller
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < q; j += (int64_t)gridDim.x * blockDim.x)
+        S[idx[j] + j * n] = 1.0;
+}
+
+}  // namespace si
