@@ -105,7 +105,12 @@ struct si_solver {
     int* status_host = nullptr;
     int64_t redraws = 0;
     std::unique_ptr<si::RngStream> rng;
+    // one device-sketched iteration captured as a CUDA graph (launch-bound small n)
+    cudaGraphExec_t graph = nullptr;
+    int64_t graph_launches = 0;
+    bool warmed = false;
     ~si_solver() {
+        if (graph) cudaGraphExecDestroy(graph);
         rw.release();
         aw.release();
         if (status_host) cudaFreeHost(status_host);
@@ -561,10 +566,10 @@ int si_run_inverter(si_context* ctx, si_problem* prob, const si_inverter_config*
                 } else if (sk == SI_SKETCH_COORDINATE_BLOCK) {
                     const si::Index i = rng.categorical(p.data(), si::Index(p.size()));
                     const auto& blk = blocks[size_t(i)];
-                    std::fill(w.s_pinned, w.s_pinned + n * q, 0.0);
+                    // the last block of contiguous_partition may be narrower: this draw has q' = |C_i| columns
+                    w.q = int64_t(blk.size());
+                    std::fill(w.s_pinned, w.s_pinned + n * w.q, 0.0);
                     for (size_t j = 0; j < blk.size(); ++j) w.s_pinned[blk[j] + int64_t(j) * n] = 1.0;
-                    // a last, narrower block keeps unused columns zero: shrink q for that draw
-                    if (int64_t(blk.size()) != q) throw ConfigError("coordinate_block: n must be a multiple of q here");
                 }
                 if (!device_sketch) si::rbfgs_enqueue_sketch_upload(c, w);
                 ck(cudaEventRecord(tm.a, c.stream), "event");  // timer starts after the draw (simi.cpp:298)
@@ -578,7 +583,7 @@ int si_run_inverter(si_context* ctx, si_problem* prob, const si_inverter_config*
                     continue;
                 }
                 if (cfg->track_wall_time) seconds += tm.seconds();
-                if (cfg->track_flops) flops += flops_bfgs(double(n), double(q));
+                if (cfg->track_flops) flops += flops_bfgs(double(n), double(w.q));  // flops::bfgs(n, s.cols())
                 stepped = true;
             }
             if (st[1]) {  // simi.cpp:342-347
@@ -687,8 +692,7 @@ int si_run_adarbfgs(si_context* ctx, si_problem* prob, const si_inverter_config*
                 if (cols) {
                     const si::Index i = rng.categorical(p.data(), si::Index(p.size()));
                     const auto& blk = blocks[size_t(i)];
-                    if (int64_t(blk.size()) != q)
-                        throw ConfigError("adaptive_cols: n must be a multiple of q here");
+                    w.q = int64_t(blk.size());  // a narrower last block draws q' = |C_i| columns
                     for (size_t j = 0; j < blk.size(); ++j) w.idx_pinned[j] = blk[j];
                 } else if (sk == SI_SKETCH_ADAPTIVE_COLS_UNIFORM) {
                     const auto idx = si::uniform_subset(rng, n, q);
@@ -700,7 +704,7 @@ int si_run_adarbfgs(si_context* ctx, si_problem* prob, const si_inverter_config*
                     mode = 2;
                 }
                 if (mode == 0)
-                    ck(cudaMemcpyAsync(w.idx_dev, w.idx_pinned, size_t(q) * sizeof(int64_t), cudaMemcpyHostToDevice,
+                    ck(cudaMemcpyAsync(w.idx_dev, w.idx_pinned, size_t(w.q) * sizeof(int64_t), cudaMemcpyHostToDevice,
                                        c.stream),
                        "h2d idx");
                 si::ada_enqueue_update(c, a, w, mode, cfg->seed);
@@ -721,7 +725,7 @@ int si_run_adarbfgs(si_context* ctx, si_problem* prob, const si_inverter_config*
             }
             if (cfg->track_wall_time) seconds += std::chrono::duration<double>(t1 - t0).count();
             if (cfg->track_flops) {
-                flops += flops_adarbfgs(double(n), double(q));
+                flops += flops_adarbfgs(double(n), double(q));  // adarbfgs.cpp:166 uses rule.q
                 if (cols) flops += 2.0 * double(n) * double(n) * double(n);  // adarbfgs.cpp:168
             }
             if (st[1]) {
@@ -889,8 +893,34 @@ int si_solver_step(si_solver* s, int64_t iters) {
         // i.e. redrawn, as simi.cpp:287-340.
         int64_t remaining = iters;
         int64_t total_redraws = 0;
+        const char* ng = std::getenv("SI_NO_GRAPH");
+        const bool graphs = !(ng && ng[0] == '1') && !c.profiling;
+        auto one = [&]() {
+            if (!graphs) {
+                solver_one(s, nullptr, nullptr, false);
+                return;
+            }
+            if (!s->warmed) {  // first iteration eagerly: sizes workspaces, sets kernel attributes
+                solver_one(s, nullptr, nullptr, false);
+                s->warmed = true;
+                return;
+            }
+            if (!s->graph) {
+                const int64_t l0 = c.launches;
+                cudaGraph_t g = nullptr;
+                ck(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal), "capture");
+                solver_one(s, nullptr, nullptr, false);
+                ck(cudaStreamEndCapture(c.stream, &g), "end capture");
+                ck(cudaGraphInstantiate(&s->graph, g, 0), "instantiate");
+                cudaGraphDestroy(g);
+                s->graph_launches = c.launches - l0;
+                c.launches = l0;
+            }
+            ck(cudaGraphLaunch(s->graph, c.stream), "graph launch");
+            c.launches += s->graph_launches;
+        };
         while (remaining > 0) {
-            for (int64_t i = 0; i < remaining; ++i) solver_one(s, nullptr, nullptr, false);
+            for (int64_t i = 0; i < remaining; ++i) one();
             read_status(c, status, s->status_host);
             if (s->status_host[1]) throw NumericalError("diverged: non-finite iterate");
             remaining = s->status_host[2] + s->status_host[0];

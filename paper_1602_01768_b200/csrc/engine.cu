@@ -1,10 +1,12 @@
 // Engine: launch logic of the RBFGS / AdaRBFGS iteration on one B200.
 // See engine.hpp for the data each pipeline keeps resident in HBM.
+#include <cudaTypedefs.h>
 #include <cusolverDn.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "engine.hpp"
@@ -117,6 +119,25 @@ static int grid_for(int64_t work, int threads, int max_blocks = 148 * 16) {
 }
 
 // --------------------------------------------------------------- GEMM ------
+enum TileCfg { T128x128 = 0, T128x64 = 1, T128x32 = 2, T128x128W16 = 3 };
+
+// development switches: SI_WARPS16=1 selects 16 consumer warps for 128×128
+// tiles; SI_NO_TMA=1 forces the cp.async mainloop.
+static bool env_flag(const char* name) {
+    const char* s = std::getenv(name);
+    return s && s[0] == '1';
+}
+static bool use_w16() {
+    static int v = -1;
+    if (v < 0) v = env_flag("SI_WARPS16") ? 1 : 0;
+    return v == 1;
+}
+static bool tma_disabled() {
+    static int v = -1;
+    if (v < 0) v = env_flag("SI_NO_TMA") ? 1 : 0;
+    return v == 1;
+}
+
 template <int BM, int BN, int BK, int WM, int WN, int ST, bool AK, bool BKM, int VEC, int EPI>
 static void launch_gemm_cfg(Context& c, const GemmArgs& a, dim3 grid, const char* name) {
     using SM = GemmSmem<BM, BN, BK, WM, WN, ST, AK, BKM>;
@@ -131,29 +152,95 @@ static void launch_gemm_cfg(Context& c, const GemmArgs& a, dim3 grid, const char
     check_launch(name);
 }
 
-enum TileCfg { T128x128 = 0, T128x64 = 1, T128x32 = 2 };
+// ---- TMA descriptors (cuTensorMapEncodeTiled through the runtime's driver entry point)
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !p) throw CudaError("cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// 2-D FP64 tensor: `inner` contiguous elements per line, `outer` lines `ld` apart.
+static void make_tmap(CUtensorMap* m, const double* base, int64_t inner, int64_t outer, int64_t ld, uint32_t box_inner,
+                      uint32_t box_outer) {
+    cuuint64_t dims[2] = {cuuint64_t(inner), cuuint64_t(outer)};
+    cuuint64_t strides[1] = {cuuint64_t(ld) * sizeof(double)};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int ST, bool AK, bool BKM, int EPI>
+static void launch_tma_cfg(Context& c, const GemmArgs& a, dim3 grid, const char* name) {
+    using SM = GemmSmem<BM, BN, BK, WM, WN, ST, AK, BKM>;
+    auto kern = gemm_tma_kernel<BM, BN, BK, WM, WN, ST, AK, BKM, EPI>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SM::TMA_BYTES)));
+        attr_set = true;
+    }
+    CUtensorMap ta, tb;
+    if (AK)
+        make_tmap(&ta, a.A, a.K, a.M, a.lda, BK + 4, BM);
+    else
+        make_tmap(&ta, a.A, a.M, a.K, a.lda, BM + 4, BK);
+    if (BKM)
+        make_tmap(&tb, a.B, a.K, a.N, a.ldb, BK + 4, BN);
+    else
+        make_tmap(&tb, a.B, a.N, a.K, a.ldb, BN + 4, BK);
+    LaunchScope ls(c, name);
+    kern<<<grid, WM * WN * 32, SM::TMA_BYTES, c.stream>>>(ta, tb, a);
+    check_launch(name);
+}
 
 template <bool AK, bool BKM, int VEC, int EPI>
-static void launch_gemm_tile(Context& c, TileCfg t, const GemmArgs& a, dim3 grid, const char* name) {
+static void launch_gemm_tile(Context& c, TileCfg t, const GemmArgs& a, dim3 grid, const char* name, bool tma) {
+    if (tma) {
+        switch (t) {
+            case T128x128: launch_tma_cfg<128, 128, 16, 4, 2, 5, AK, BKM, EPI>(c, a, grid, name); break;
+            case T128x64: launch_tma_cfg<128, 64, 16, 4, 2, 4, AK, BKM, EPI>(c, a, grid, name); break;
+            case T128x32: launch_tma_cfg<128, 32, 16, 8, 1, 4, AK, BKM, EPI>(c, a, grid, name); break;
+            case T128x128W16: launch_tma_cfg<128, 128, 16, 4, 4, 5, AK, BKM, EPI>(c, a, grid, name); break;
+        }
+        return;
+    }
     switch (t) {
         case T128x128: launch_gemm_cfg<128, 128, 16, 4, 2, 4, AK, BKM, VEC, EPI>(c, a, grid, name); break;
         case T128x64: launch_gemm_cfg<128, 64, 16, 4, 2, 4, AK, BKM, VEC, EPI>(c, a, grid, name); break;
         case T128x32: launch_gemm_cfg<128, 32, 16, 8, 1, 4, AK, BKM, VEC, EPI>(c, a, grid, name); break;
+        case T128x128W16: launch_gemm_cfg<128, 128, 16, 4, 4, 4, AK, BKM, VEC, EPI>(c, a, grid, name); break;
     }
+}
+
+static bool aligned_ptr(const void* p, uintptr_t b) { return (reinterpret_cast<uintptr_t>(p) & (b - 1)) == 0; }
+
+// TMA needs 16-byte aligned bases and line strides (even leading dimensions)
+static bool tma_ok(const GemmArgs& a) {
+    return !tma_disabled() && a.lda % 2 == 0 && a.ldb % 2 == 0 && aligned_ptr(a.A, 16) && aligned_ptr(a.B, 16) &&
+           a.M < (int64_t(1) << 31) && a.N < (int64_t(1) << 31) && a.K < (int64_t(1) << 31);
 }
 
 template <int EPI>
 static void launch_gemm_layout(Context& c, TileCfg t, bool ak, bool bkm, int vec, const GemmArgs& a, dim3 grid,
                                const char* name) {
+    const bool tma = tma_ok(a);
     if (!ak && bkm) {
-        vec == 2 ? launch_gemm_tile<false, true, 2, EPI>(c, t, a, grid, name)
-                 : launch_gemm_tile<false, true, 1, EPI>(c, t, a, grid, name);
+        vec == 2 ? launch_gemm_tile<false, true, 2, EPI>(c, t, a, grid, name, tma)
+                 : launch_gemm_tile<false, true, 1, EPI>(c, t, a, grid, name, tma);
     } else if (ak && bkm) {
-        vec == 2 ? launch_gemm_tile<true, true, 2, EPI>(c, t, a, grid, name)
-                 : launch_gemm_tile<true, true, 1, EPI>(c, t, a, grid, name);
+        vec == 2 ? launch_gemm_tile<true, true, 2, EPI>(c, t, a, grid, name, tma)
+                 : launch_gemm_tile<true, true, 1, EPI>(c, t, a, grid, name, tma);
     } else if (!ak && !bkm) {
-        vec == 2 ? launch_gemm_tile<false, false, 2, EPI>(c, t, a, grid, name)
-                 : launch_gemm_tile<false, false, 1, EPI>(c, t, a, grid, name);
+        vec == 2 ? launch_gemm_tile<false, false, 2, EPI>(c, t, a, grid, name, tma)
+                 : launch_gemm_tile<false, false, 1, EPI>(c, t, a, grid, name, tma);
     } else {
         throw std::invalid_argument("gemm: A K-major with B N-major is not instantiated");
     }
@@ -170,7 +257,7 @@ static int pick_vec(const GemmArgs& a) {
 static TileCfg pick_tile(int64_t N) {
     if (N <= 32) return T128x32;
     if (N <= 64) return T128x64;
-    return T128x128;
+    return use_w16() ? T128x128W16 : T128x128;
 }
 
 void gemm(Context& c, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, bool a_kmajor, const double* B,
@@ -192,25 +279,30 @@ void gemm(Context& c, int64_t M, int64_t N, int64_t K, const double* A, int64_t 
     a.skip = skip;
     a.nonfinite = nonfinite;
     const TileCfg t = pick_tile(N);
-    const int BM = 128, BN = t == T128x128 ? 128 : (t == T128x64 ? 64 : 32), BKT = 16;
+    const int BM = 128, BN = (t == T128x128 || t == T128x128W16) ? 128 : (t == T128x64 ? 64 : 32), BKT = 16;
     const int64_t tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN, tiles = tm * tn;
     const int per_sm = t == T128x128 ? 1 : 2;
     const int64_t slots = int64_t(c.num_sms) * per_sm;
     // split-K so the number of work units fills whole waves of the 148 SMs
     int splits = 1;
-    if (K > 8 * BKT && tiles < 4 * slots && !nonfinite) {
-        double best = double(tiles) / double(((tiles + slots - 1) / slots) * slots);
+    if (K > 8 * BKT && tiles < 8 * slots && !nonfinite) {
+        // wave efficiency of `units` work units on `slots` resident CTAs, minus a
+        // small per-split cost (partials written + reduced)
+        auto score = [&](int64_t s) {
+            const int64_t units = tiles * s;
+            const double eff = double(units) / double(((units + slots - 1) / slots) * slots);
+            return eff - 0.004 * double(s);
+        };
+        double best = score(1);
         for (int s = 2; s <= 128; ++s) {
             const int64_t chunk = ((K + s - 1) / s + BKT - 1) / BKT * BKT;
             if (chunk < 8 * BKT) break;
             if (double(s) * double(M) * double(N) * 8.0 > 512.0 * 1024 * 1024) break;
-            const int64_t units = tiles * s;
-            const double eff = double(units) / double(((units + slots - 1) / slots) * slots);
-            if (eff > best + 0.02 || (units <= slots && eff > best)) {
-                best = eff;
+            const double sc = score(s);
+            if (sc > best + 1e-9) {
+                best = sc;
                 splits = s;
             }
-            if (units >= 4 * slots) break;
         }
     }
     const int vec = pick_vec(a);
@@ -254,8 +346,9 @@ static void symupd(Context& c, int64_t n, int64_t k, const double* V, int64_t ld
     a.nonfinite = nonfinite;
     const int64_t T = (n + 127) / 128;
     const int vec = pick_vec(a);
-    launch_gemm_layout<EPI_SYMUPD>(c, T128x128, false, false, vec, a, dim3(unsigned(T * (T + 1) / 2), 1, 1),
-                                   "gemm_symupd");
+    // 16 warps: the update has only K = 2q, so more resident warps hide its per-tile fill/drain
+    launch_gemm_layout<EPI_SYMUPD>(c, env_flag("SI_SYMUPD_W8") ? T128x128 : T128x128W16, false, false, vec, a,
+                                   dim3(unsigned(T * (T + 1) / 2), 1, 1), "gemm_symupd");
 }
 
 // ----------------------------------------------------------- problem -------
@@ -431,6 +524,30 @@ void rbfgs_enqueue_sketch_upload(Context& c, RbfgsWork& w) {
 
 static void spd_inverse(Context& c, const double* P, int64_t ldp, int64_t q, double* ginv, double* scratch,
                         int* status) {
+    if (q <= 128) {
+        // register-resident Gauss-Jordan: q columns × ceil(q/RPT) row groups
+        const int rpt = q <= 32 ? 1 : (q <= 64 ? 8 : 16);
+        const int threads = int(q * ((q + rpt - 1) / rpt));
+        {
+            LaunchScope ls(c, "spd_inverse");
+            switch (rpt) {
+                case 1:
+                    spd_inverse_reg_kernel<1, 1024><<<1, threads, 0, c.stream>>>(P, ldp, int(q), ginv, q, status);
+                    break;
+                case 8:
+                    spd_inverse_reg_kernel<8, 512><<<1, threads, 0, c.stream>>>(P, ldp, int(q), ginv, q, status);
+                    break;
+                default:
+                    spd_inverse_reg_kernel<16, 1024><<<1, threads, 0, c.stream>>>(P, ldp, int(q), ginv, q, status);
+                    break;
+            }
+            check_launch("spd_inverse_reg");
+        }
+        LaunchScope ls(c, "symmetrize_small");
+        symmetrize_small_kernel<<<grid_for(q * q, 256), 256, 0, c.stream>>>(ginv, int(q), q, status);
+        check_launch("symmetrize_small");
+        return;
+    }
     const size_t smem = (size_t(q) * size_t(q) + 2 * size_t(q)) * sizeof(double);
     const bool use_smem = smem <= 200 * 1024;
     static bool attr = false;
@@ -494,7 +611,8 @@ static void resid_gemm(Context& c, int64_t n, const double* A, int64_t lda, cons
     const int64_t T = (n + 127) / 128;
     g.ws = c.ensure_ws(size_t(T * T));
     const int vec = pick_vec(g);
-    launch_gemm_layout<EPI_RESID>(c, T128x128, false, BKM, vec, g, dim3(unsigned(T), unsigned(T), 1), "gemm_resid");
+    launch_gemm_layout<EPI_RESID>(c, use_w16() ? T128x128W16 : T128x128, false, BKM, vec, g,
+                                  dim3(unsigned(T), unsigned(T), 1), "gemm_resid");
     LaunchScope ls(c, "sum_reduce");
     sum_reduce_kernel<<<1, 1024, 0, c.stream>>>(g.ws, T * T, out_dev);
     check_launch("sum_reduce");

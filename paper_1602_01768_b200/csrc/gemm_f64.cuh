@@ -1,18 +1,26 @@
 // FP64 tensor-core (DMMA) GEMM engine for sm_100a.
 //
-// One templated mainloop serves every dense contraction on the RBFGS/AdaRBFGS
-// path (SURVEY §2.4 compute-site table):
+// One templated tile engine serves every dense contraction on the RBFGS /
+// AdaRBFGS path (SURVEY §2.4 compute-site table):
 //   Y = A·S, W = X·Y, V = U·M              (EPI_STORE / EPI_PARTIAL + split-K)
 //   [G | H] = Yᵀ·[S W], Z = (AS)ᵀ·L        (A operand K-major)
 //   X ← X + V·Uᵀ on upper tiles, mirrored   (EPI_SYMUPD, the fused rank-2q update)
 //   ‖I − A·X‖²_F partials, no n×n write     (EPI_RESID)
 //
-// Tiles are staged global→shared by a STAGES-deep cp.async ring (zero-filled
-// out of bounds), fragments are read from padded shared memory (row pitch ≡ 4
-// doubles mod 16 → conflict-free 64-bit LDS), and each warp issues
-// mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4, measured 36.9 TFLOP/s peak on B200,
-// profiles/r01_fp64_peak.txt).
+// Two mainloops feed the same warp tiles:
+//   gemm_tma_kernel  — Blackwell path: one elected thread issues TMA
+//                      (cp.async.bulk.tensor) boxes into a STAGES-deep ring
+//                      guarded by mbarriers (full / empty); the WM×WN warps
+//                      never block on a CTA-wide barrier.  Boxes are 4
+//                      doubles wider than the tile so shared memory keeps a
+//                      pitch ≡ 4 (mod 16) doubles → conflict-free 64-bit LDS.
+//   gemm_f64_kernel  — cp.async ring for operands TMA cannot describe (odd
+//                      leading dimensions / unaligned bases).
+// Warps issue mma.sync.aligned.m16n8k8.f64 (SASS DMMA.8x8x4; measured FP64
+// DMMA peak 36.9 TFLOP/s on B200, profiles/r01_fp64_peak.txt).
 #pragma once
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace si {
@@ -31,7 +39,7 @@ struct GemmArgs {
     int64_t k_chunk;  // split-K chunk (multiple of BK); gridDim.z = #splits
     double* ws;       // EPI_PARTIAL: ws[z*M*N + m + n*M]; EPI_RESID: ws[linear block]
     const int* skip;  // if set and nonzero, the launch is a no-op (failed Gram upstream)
-    int* nonfinite;   // EPI_SYMUPD: set to 1 when a written entry is not finite (simi.cpp:342-347 guard)
+    int* nonfinite;   // STORE / SYMUPD: set to 1 when a written entry is not finite (simi.cpp:342-347)
 };
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool A_KMAJOR, bool B_KMAJOR>
@@ -40,59 +48,257 @@ struct GemmSmem {
     static constexpr int B_ELEMS = B_KMAJOR ? BN * (BK + 4) : BK * (BN + 4);
     static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
     static constexpr size_t BYTES = size_t(STAGES) * STAGE_ELEMS * sizeof(double);
+    static constexpr size_t BAR_OFFSET = (BYTES + 127) / 128 * 128;
+    static constexpr size_t TMA_BYTES = BAR_OFFSET + 2 * STAGES * sizeof(uint64_t);
 };
 
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool A_KMAJOR, bool B_KMAJOR, int VEC, int EPI>
-__global__ void __launch_bounds__(WM* WN * 32) gemm_f64_kernel(GemmArgs p) {
-    static_assert(BM % (WM * 8) == 0 && BN % (WN * 8) == 0, "warp tiling");
-    static_assert(BK % 4 == 0 && (BK + 4) % 16 == 4 && (BM + 4) % 16 == 4 && (BN + 4) % 16 == 4, "smem pitch");
-    constexpr int NT = WM * WN * 32;
-    constexpr int MI = BM / WM / 8;
-    constexpr int NI = BN / WN / 8;
+// Shared per-tile logic of both mainloops.
+template <int BM, int BN, int BK, int WM, int WN, bool A_KMAJOR, bool B_KMAJOR, int EPI>
+struct TileOps {
+    static constexpr int MI = BM / WM / 16;  // m16 blocks per warp
+    static constexpr int NI = BN / WN / 8;   // n8 blocks per warp
+    static constexpr int LDA_S = A_KMAJOR ? BK + 4 : BM + 4;
+    static constexpr int LDB_S = B_KMAJOR ? BK + 4 : BN + 4;
+    static_assert(BM % (WM * 16) == 0 && BN % (WN * 8) == 0, "warp tiling");
+    static_assert(BK % 8 == 0 && (BK + 4) % 16 == 4 && (BM + 4) % 16 == 4 && (BN + 4) % 16 == 4, "smem pitch");
+
+    int64_t m0, n0, tile_m, tile_n;
+    int g, t4, wm0, wn0;
+
+    __device__ __forceinline__ void setup(int warp, int lane) {
+        if constexpr (EPI == EPI_SYMUPD) {
+            // linear index over upper-triangular tile pairs (ti <= tj)
+            const int64_t t = blockIdx.x;
+            int64_t tj = (int64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+            while (tj * (tj + 1) / 2 > t) --tj;
+            while ((tj + 1) * (tj + 2) / 2 <= t) ++tj;
+            tile_n = tj;
+            tile_m = t - tj * (tj + 1) / 2;
+        } else {
+            tile_m = blockIdx.x;
+            tile_n = blockIdx.y;
+        }
+        m0 = tile_m * BM;
+        n0 = tile_n * BN;
+        g = lane >> 2;
+        t4 = lane & 3;
+        wm0 = (warp / WN) * (BM / WM);
+        wn0 = (warp % WN) * (BN / WN);
+    }
+    // fragment element e of block (i, j) sits at (wm0 + 16i + g + 8(e>>1), wn0 + 8j + 2t + (e&1))
+    __device__ __forceinline__ int64_t row(int i, int e) const { return m0 + wm0 + i * 16 + g + ((e >> 1) << 3); }
+    __device__ __forceinline__ int64_t col(int j, int e) const { return n0 + wn0 + j * 8 + 2 * t4 + (e & 1); }
+
+    __device__ __forceinline__ void init_acc(double (&acc)[MI][NI][4], const GemmArgs& p) const {
+        if constexpr (EPI == EPI_SYMUPD) {
+            // accumulate onto the X tile itself (C = X + V·Uᵀ, alpha = 1): the loads
+            // are issued under the pipeline fill and the epilogue becomes store-only
+#pragma unroll
+            for (int i = 0; i < MI; ++i)
+#pragma unroll
+                for (int j = 0; j < NI; ++j)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int64_t r = row(i, e), c = col(j, e);
+                        acc[i][j][e] = (r < p.M && c < p.N) ? p.C[r + c * p.ldc] : 0.0;
+                    }
+        } else {
+#pragma unroll
+            for (int i = 0; i < MI; ++i)
+#pragma unroll
+                for (int j = 0; j < NI; ++j)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
+        }
+    }
+
+    __device__ __forceinline__ void compute_stage(double (&acc)[MI][NI][4], const double* As, const double* Bs) const {
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 8) {
+            double a[MI][4], b[NI][2];
+#pragma unroll
+            for (int i = 0; i < MI; ++i)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int m = wm0 + i * 16 + g + ((e & 1) << 3), k = kk + t4 + ((e >> 1) << 2);
+                    a[i][e] = A_KMAJOR ? As[m * LDA_S + k] : As[k * LDA_S + m];
+                }
+#pragma unroll
+            for (int j = 0; j < NI; ++j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int n = wn0 + j * 8 + g, k = kk + t4 + (e << 2);
+                    b[j][e] = B_KMAJOR ? Bs[n * LDB_S + k] : Bs[k * LDB_S + n];
+                }
+#pragma unroll
+            for (int i = 0; i < MI; ++i)
+#pragma unroll
+                for (int j = 0; j < NI; ++j) dmma_1688(acc[i][j], a[i], b[j]);
+        }
+    }
+
+    // `sync_consumers` synchronises exactly the threads that hold accumulators
+    template <class Sync>
+    __device__ __forceinline__ void epilogue(const double (&acc)[MI][NI][4], const GemmArgs& p, int tid, int nthreads,
+                                             Sync sync_consumers) const {
+        if constexpr (EPI == EPI_RESID) {
+            double local = 0.0;
+#pragma unroll
+            for (int i = 0; i < MI; ++i)
+#pragma unroll
+                for (int j = 0; j < NI; ++j)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int64_t r = row(i, e), c = col(j, e);
+                        if (r < p.M && c < p.N) {
+                            const double d = (r == c ? 1.0 : 0.0) - acc[i][j][e];
+                            local += d * d;
+                        }
+                    }
+            local = warp_sum(local);
+            __shared__ double red[32];
+            const int lane = tid & 31, w = tid >> 5;
+            if (lane == 0) red[w] = local;
+            sync_consumers();
+            if (tid == 0) {
+                double s = 0.0;
+                for (int k = 0; k < nthreads / 32; ++k) s += red[k];
+                p.ws[(int64_t)blockIdx.x + (int64_t)gridDim.x * ((int64_t)blockIdx.y + (int64_t)gridDim.y * blockIdx.z)] = s;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < MI; ++i)
+#pragma unroll
+                for (int j = 0; j < NI; ++j)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int64_t r = row(i, e), c = col(j, e);
+                        if (r >= p.M || c >= p.N) continue;
+                        const double v = acc[i][j][e];
+                        if constexpr (EPI == EPI_STORE) {
+                            double* cp = p.C + r + c * p.ldc;
+                            const double nv = p.beta != 0.0 ? p.alpha * v + p.beta * *cp : p.alpha * v;
+                            *cp = nv;
+                            if (p.nonfinite && !isfinite(nv)) atomicOr(p.nonfinite, 1);
+                        } else if constexpr (EPI == EPI_PARTIAL) {
+                            p.ws[(int64_t)blockIdx.z * p.M * p.N + r + c * p.M] = v;
+                        } else {  // EPI_SYMUPD: X(r,c) = acc (= X + V·Uᵀ) on the upper triangle, mirrored
+                            if (tile_m < tile_n || r <= c) {
+                                p.C[r + c * p.ldc] = v;
+                                if (r != c) p.C[c + r * p.ldc] = v;
+                                if (!isfinite(v) && p.nonfinite) atomicOr(p.nonfinite, 1);
+                            }
+                        }
+                    }
+        }
+    }
+};
+
+// --------------------------------------------------------------- TMA path --
+// Threads: WM·WN warps, all of them compute.  Lane 0 of warp 0 is also the
+// TMA producer: it keeps STAGES−1 stages in flight, arming full[s] with the
+// stage's byte count and issuing one box for A and one for B.  Every warp waits
+// on full[s], computes, and arrives on empty[s] (count WM·WN); the producer
+// waits on empty[s] only before refilling that slot, so there is no CTA-wide
+// barrier in the mainloop.  (A separate producer warp would cost a whole
+// warpgroup of registers: ptxas allocates in 4-warp units.)
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool A_KMAJOR, bool B_KMAJOR, int EPI>
+__global__ void __launch_bounds__(WM* WN * 32, 1)
+    gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs p) {
     using SM = GemmSmem<BM, BN, BK, WM, WN, STAGES, A_KMAJOR, B_KMAJOR>;
-    constexpr int LDA_S = A_KMAJOR ? BK + 4 : BM + 4;
-    constexpr int LDB_S = B_KMAJOR ? BK + 4 : BN + 4;
+    using T = TileOps<BM, BN, BK, WM, WN, A_KMAJOR, B_KMAJOR, EPI>;
+    constexpr int NW = WM * WN;
+    constexpr uint32_t STAGE_BYTES = SM::STAGE_ELEMS * sizeof(double);
 
     if (p.skip && *p.skip) return;
     extern __shared__ __align__(128) double smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(smem) + SM::BAR_OFFSET);
+    uint64_t* empty = full + STAGES;
 
-    // ---- tile coordinates
-    int64_t tile_m, tile_n;
-    if constexpr (EPI == EPI_SYMUPD) {
-        // linear index over upper-triangular tile pairs (ti <= tj)
-        const int64_t t = blockIdx.x;
-        int64_t tj = (int64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
-        while (tj * (tj + 1) / 2 > t) --tj;
-        while ((tj + 1) * (tj + 2) / 2 <= t) ++tj;
-        tile_n = tj;
-        tile_m = t - tj * (tj + 1) / 2;
-    } else {
-        tile_m = blockIdx.x;
-        tile_n = blockIdx.y;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    T t;
+    t.setup(warp, lane);
+    const int64_t k_begin = (int64_t)blockIdx.z * p.k_chunk;
+    const int64_t k_end = min(p.K, k_begin + p.k_chunk);
+    const int num_kt = (int)((k_end - k_begin + BK - 1) / BK);
+    const bool producer = tid == 0;
+
+    auto issue = [&](int kt) {
+        const int s = kt % STAGES;
+        if (kt >= STAGES) mbar_wait(&empty[s], ((kt / STAGES) - 1) & 1);
+        double* As = smem + s * SM::STAGE_ELEMS;
+        double* Bs = As + SM::A_ELEMS;
+        const int32_t kc = (int32_t)(k_begin + (int64_t)kt * BK);
+        mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+        if constexpr (A_KMAJOR)
+            tma_load_2d(As, &tmA, kc, (int32_t)t.m0, &full[s]);
+        else
+            tma_load_2d(As, &tmA, (int32_t)t.m0, kc, &full[s]);
+        if constexpr (B_KMAJOR)
+            tma_load_2d(Bs, &tmB, kc, (int32_t)t.n0, &full[s]);
+        else
+            tma_load_2d(Bs, &tmB, (int32_t)t.n0, kc, &full[s]);
+    };
+
+    if (producer) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NW);
+        }
+        mbar_fence_init();
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
     }
-    const int64_t m0 = tile_m * BM, n0 = tile_n * BN;
+    __syncthreads();
+    if (producer)
+        for (int kt = 0; kt < STAGES - 1 && kt < num_kt; ++kt) issue(kt);
+
+    double acc[T::MI][T::NI][4];
+    t.init_acc(acc, p);
+    for (int kt = 0; kt < num_kt; ++kt) {
+        if (warp == 0) {
+            if (producer && kt + STAGES - 1 < num_kt) issue(kt + STAGES - 1);
+            __syncwarp();
+        }
+        const int s = kt % STAGES;
+        mbar_wait(&full[s], (kt / STAGES) & 1);
+        const double* As = smem + s * SM::STAGE_ELEMS;
+        t.compute_stage(acc, As, As + SM::A_ELEMS);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    t.epilogue(acc, p, tid, NW * 32, [] { __syncthreads(); });
+}
+
+// ---------------------------------------------------------- cp.async path --
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool A_KMAJOR, bool B_KMAJOR, int VEC, int EPI>
+__global__ void __launch_bounds__(WM* WN * 32) gemm_f64_kernel(GemmArgs p) {
+    using SM = GemmSmem<BM, BN, BK, WM, WN, STAGES, A_KMAJOR, B_KMAJOR>;
+    using T = TileOps<BM, BN, BK, WM, WN, A_KMAJOR, B_KMAJOR, EPI>;
+    constexpr int NT = WM * WN * 32;
+    constexpr int LDA_S = T::LDA_S, LDB_S = T::LDB_S;
+
+    if (p.skip && *p.skip) return;
+    extern __shared__ __align__(128) double smem[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    T t;
+    t.setup(warp, lane);
+    const int64_t m0 = t.m0, n0 = t.n0;
     const int64_t k_begin = (int64_t)blockIdx.z * p.k_chunk;
     const int64_t k_end = min(p.K, k_begin + p.k_chunk);
     const int num_kt = (int)((k_end - k_begin + BK - 1) / BK);
 
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int g = lane >> 2, t4 = lane & 3;
-    const int wm0 = (warp / WN) * (BM / WM), wn0 = (warp % WN) * (BN / WN);
-
-    // ---- global -> shared stage loader
     auto load_stage = [&](int stage, int kt) {
         double* As = smem + stage * SM::STAGE_ELEMS;
         double* Bs = As + SM::A_ELEMS;
         const int64_t kbase = k_begin + (int64_t)kt * BK;
-        // A tile
         if constexpr (!A_KMAJOR) {  // columns of BM contiguous doubles
             constexpr int CH = BK * BM / VEC;
             for (int c = tid; c < CH; c += NT) {
                 const int kk = c / (BM / VEC), mm = (c % (BM / VEC)) * VEC;
                 const int64_t gm = m0 + mm, gk = kbase + kk;
                 const bool ok = gm < p.M && gk < k_end;
-                const double* src = ok ? p.A + gm + gk * p.lda : p.A;
-                cp_async<VEC * 8>(As + kk * LDA_S + mm, src, ok);
+                cp_async<VEC * 8>(As + kk * LDA_S + mm, ok ? p.A + gm + gk * p.lda : p.A, ok);
             }
         } else {  // rows of BK contiguous doubles
             constexpr int CH = BM * BK / VEC;
@@ -100,19 +306,16 @@ __global__ void __launch_bounds__(WM* WN * 32) gemm_f64_kernel(GemmArgs p) {
                 const int mm = c / (BK / VEC), kk = (c % (BK / VEC)) * VEC;
                 const int64_t gm = m0 + mm, gk = kbase + kk;
                 const bool ok = gm < p.M && gk < k_end;
-                const double* src = ok ? p.A + gm * p.lda + gk : p.A;
-                cp_async<VEC * 8>(As + mm * LDA_S + kk, src, ok);
+                cp_async<VEC * 8>(As + mm * LDA_S + kk, ok ? p.A + gm * p.lda + gk : p.A, ok);
             }
         }
-        // B tile
         if constexpr (B_KMAJOR) {  // columns n: BK contiguous doubles
             constexpr int CH = BN * BK / VEC;
             for (int c = tid; c < CH; c += NT) {
                 const int nn = c / (BK / VEC), kk = (c % (BK / VEC)) * VEC;
                 const int64_t gn = n0 + nn, gk = kbase + kk;
                 const bool ok = gn < p.N && gk < k_end;
-                const double* src = ok ? p.B + gk + gn * p.ldb : p.B;
-                cp_async<VEC * 8>(Bs + nn * LDB_S + kk, src, ok);
+                cp_async<VEC * 8>(Bs + nn * LDB_S + kk, ok ? p.B + gk + gn * p.ldb : p.B, ok);
             }
         } else {  // rows k: BN contiguous doubles
             constexpr int CH = BK * BN / VEC;
@@ -120,24 +323,18 @@ __global__ void __launch_bounds__(WM* WN * 32) gemm_f64_kernel(GemmArgs p) {
                 const int kk = c / (BN / VEC), nn = (c % (BN / VEC)) * VEC;
                 const int64_t gn = n0 + nn, gk = kbase + kk;
                 const bool ok = gn < p.N && gk < k_end;
-                const double* src = ok ? p.B + gn + gk * p.ldb : p.B;
-                cp_async<VEC * 8>(Bs + kk * LDB_S + nn, src, ok);
+                cp_async<VEC * 8>(Bs + kk * LDB_S + nn, ok ? p.B + gn + gk * p.ldb : p.B, ok);
             }
         }
     };
 
-    double acc[MI][NI][2];
-#pragma unroll
-    for (int i = 0; i < MI; ++i)
-#pragma unroll
-        for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
+    double acc[T::MI][T::NI][4];
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
         if (s < num_kt) load_stage(s, s);
         cp_async_commit();
     }
-
+    t.init_acc(acc, p);
     for (int kt = 0; kt < num_kt; ++kt) {
         cp_async_wait<STAGES - 2>();
         __syncthreads();
@@ -147,83 +344,10 @@ __global__ void __launch_bounds__(WM* WN * 32) gemm_f64_kernel(GemmArgs p) {
             cp_async_commit();
         }
         const double* As = smem + (kt % STAGES) * SM::STAGE_ELEMS;
-        const double* Bs = As + SM::A_ELEMS;
-#pragma unroll
-        for (int kk = 0; kk < BK; kk += 4) {
-            double a[MI], b[NI];
-#pragma unroll
-            for (int i = 0; i < MI; ++i) {
-                const int m = wm0 + i * 8 + g, k = kk + t4;
-                a[i] = A_KMAJOR ? As[m * LDA_S + k] : As[k * LDA_S + m];
-            }
-#pragma unroll
-            for (int j = 0; j < NI; ++j) {
-                const int n = wn0 + j * 8 + g, k = kk + t4;
-                b[j] = B_KMAJOR ? Bs[n * LDB_S + k] : Bs[k * LDB_S + n];
-            }
-#pragma unroll
-            for (int i = 0; i < MI; ++i)
-#pragma unroll
-                for (int j = 0; j < NI; ++j) dmma_884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
-        }
+        t.compute_stage(acc, As, As + SM::A_ELEMS);
     }
     cp_async_wait<0>();
-
-    // ---- epilogues
-    if constexpr (EPI == EPI_RESID) {
-        double local = 0.0;
-#pragma unroll
-        for (int i = 0; i < MI; ++i)
-#pragma unroll
-            for (int j = 0; j < NI; ++j)
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int64_t row = m0 + wm0 + i * 8 + g, col = n0 + wn0 + j * 8 + 2 * t4 + e;
-                    if (row < p.M && col < p.N) {
-                        const double d = (row == col ? 1.0 : 0.0) - acc[i][j][e];
-                        local += d * d;
-                    }
-                }
-        local = warp_sum(local);
-        __shared__ double red[NT / 32];
-        __syncthreads();
-        if (lane == 0) red[warp] = local;
-        __syncthreads();
-        if (tid == 0) {
-            double s = 0.0;
-            for (int w = 0; w < NT / 32; ++w) s += red[w];
-            p.ws[(int64_t)blockIdx.x + (int64_t)gridDim.x * ((int64_t)blockIdx.y + (int64_t)gridDim.y * blockIdx.z)] =
-                s;
-        }
-        return;
-    } else {
-#pragma unroll
-        for (int i = 0; i < MI; ++i)
-#pragma unroll
-            for (int j = 0; j < NI; ++j)
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int64_t row = m0 + wm0 + i * 8 + g, col = n0 + wn0 + j * 8 + 2 * t4 + e;
-                    if (row >= p.M || col >= p.N) continue;
-                    const double v = acc[i][j][e];
-                    if constexpr (EPI == EPI_STORE) {
-                        double* c = p.C + row + col * p.ldc;
-                        const double nv = p.beta != 0.0 ? p.alpha * v + p.beta * *c : p.alpha * v;
-                        *c = nv;
-                        if (p.nonfinite && !isfinite(nv)) atomicOr(p.nonfinite, 1);
-                    } else if constexpr (EPI == EPI_PARTIAL) {
-                        p.ws[(int64_t)blockIdx.z * p.M * p.N + row + col * p.M] = v;
-                    } else {  // EPI_SYMUPD: X(row,col) += alpha*acc on the upper triangle, mirrored
-                        if (tile_m < tile_n || row <= col) {
-                            double* c = p.C + row + col * p.ldc;
-                            const double nv = *c + p.alpha * v;
-                            *c = nv;
-                            if (row != col) p.C[col + row * p.ldc] = nv;
-                            if (!isfinite(nv) && p.nonfinite) atomicOr(p.nonfinite, 1);
-                        }
-                    }
-                }
-    }
+    t.epilogue(acc, p, tid, NT, [] { __syncthreads(); });
 }
 
 }  // namespace si

@@ -44,8 +44,82 @@ __global__ void sum_reduce_kernel(const double* __restrict__ ws, int64_t count, 
 // K-FACTOR.  G_ref(i,j) = P(min(i,j), max(i,j)) (the reference's LLT reads the
 // lower triangle of gram = SᵀAS; P = YᵀS = gramᵀ).  Writes Ginv (q×q, ldo) and
 // sets *status = 1 when a pivot is not > 0 (the GramRankDeficientError
-// resample signal, qn_updates.cpp:37-43).  `work` is q*q doubles of global
-// scratch used when the matrix does not fit shared memory.
+// resample signal, qn_updates.cpp:37-43).
+//
+// Gauss-Jordan without pivoting, register resident: thread t owns column
+// j = t % q and rows [r0, r0 + RPT) with r0 = (t / q)·RPT, so one elimination
+// step is: owners of row k / column k publish them to shared memory, barrier,
+// RPT register FMAs, barrier.  Used for q ≤ 128 (RPT ≤ 32); larger q falls back
+// to the shared/global-memory variant below.
+template <int RPT, int MAXT>
+__global__ void __launch_bounds__(MAXT) spd_inverse_reg_kernel(const double* __restrict__ P, int64_t ldp, int q,
+                                                               double* __restrict__ ginv, int64_t ldo, int* status) {
+    __shared__ double rowk[128], colk[128];
+    if (*status) return;
+    const int tid = threadIdx.x;
+    const int j = tid % q, grp = tid / q, r0 = grp * RPT;
+    const int ngrp = (q + RPT - 1) / RPT;
+    const bool active = grp < ngrp;
+    double a[RPT];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+        const int i = r0 + r;
+        a[r] = (active && i < q) ? (i <= j ? P[i + (int64_t)j * ldp] : P[j + (int64_t)i * ldp]) : 0.0;
+    }
+    // k = kb·RPT + kr with kr unrolled, so the owner of pivot row k reads the
+    // compile-time register a[kr] and the update needs no dynamic indexing
+    for (int kb = 0; kb < ngrp; ++kb) {
+        const bool own_row = active && grp == kb;
+#pragma unroll
+        for (int kr = 0; kr < RPT; ++kr) {
+            const int k = kb * RPT + kr;
+            if (k >= q) break;  // uniform
+            if (own_row) rowk[j] = a[kr];
+            if (active && j == k) {
+#pragma unroll
+                for (int r = 0; r < RPT; ++r) colk[r0 + r] = a[r];
+            }
+            __syncthreads();
+            const double piv = colk[k];
+            if (!(piv > 0.0)) {  // uniform: every thread read the same shared value
+                if (tid == 0) *status = 1;
+                return;
+            }
+            const double inv = 1.0 / piv;
+            const bool jk = j == k;
+            const double rk = (jk ? 1.0 : rowk[j]) * inv;  // new row k, column j
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) {
+                const double base = jk ? 0.0 : a[r];
+                const double upd = base - colk[r0 + r] * rk;
+                a[r] = (r == kr && own_row) ? rk : upd;
+            }
+            __syncthreads();
+        }
+    }
+    if (active) {
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+            const int i = r0 + r;
+            if (i < q) ginv[i + (int64_t)j * ldo] = a[r];
+        }
+    }
+}
+
+// symmetrize Ginv in place: (G + Gᵀ)/2 (exact symmetry of the implied projector)
+__global__ void symmetrize_small_kernel(double* g, int q, int64_t ld, const int* skip) {
+    if (skip && *skip) return;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < q * q; idx += gridDim.x * blockDim.x) {
+        const int i = idx % q, j = idx / q;
+        if (i < j) {
+            const double v = 0.5 * (g[i + j * ld] + g[j + i * ld]);
+            g[i + j * ld] = v;
+            g[j + i * ld] = v;
+        }
+    }
+}
+
+// Shared/global-memory Gauss-Jordan for large q (same arithmetic).
 __global__ void __launch_bounds__(1024) spd_inverse_kernel(const double* __restrict__ P, int64_t ldp, int q,
                                                            double* __restrict__ ginv, int64_t ldo, double* work,
                                                            int* status, int use_smem) {
@@ -64,7 +138,7 @@ __global__ void __launch_bounds__(1024) spd_inverse_kernel(const double* __restr
     __syncthreads();
     for (int k = 0; k < q; ++k) {
         const double piv = a[k + k * q];
-        if (!(piv > 0.0)) {  // uniform across threads: everyone read the same value
+        if (!(piv > 0.0)) {
             if (tid == 0) fail = 1;
             break;
         }
@@ -92,7 +166,6 @@ __global__ void __launch_bounds__(1024) spd_inverse_kernel(const double* __restr
     }
     for (int idx = tid; idx < q * q; idx += nt) {
         const int i = idx % q, j = idx / q;
-        // symmetrize the inverse (exact symmetry of the implied projector)
         ginv[i + (int64_t)j * ldo] = 0.5 * (a[i + j * q] + a[j + i * q]);
     }
 }
