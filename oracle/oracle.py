@@ -53,6 +53,8 @@ def _load():
     lib.or_rng_uniform_matrix.argtypes = [C.c_void_p, _i64, _i64, _pd]
     lib.or_uniform_subset.argtypes = [C.c_void_p, _i64, _i64, _pi64]
     lib.or_bfgs_step.argtypes = [_i64, _i64, _pd, _pd, _pd, _pd]
+    lib.or_symmetrize.restype = _d
+    lib.or_symmetrize.argtypes = [_i64, _pd]
     lib.or_adarbfgs_update_factor.argtypes = [_i64, _i64, _pd, _pd, _pd, _pd]
     lib.or_adaptive_block_probabilities.argtypes = [_i64, _i64, _pd, _pd, _pd]
     lib.or_sym_inv_sqrt.argtypes = [_i64, _pd, _pd]
@@ -169,6 +171,12 @@ def bfgs_step(x, a, s) -> np.ndarray:
     out = np.empty((n, n), order="F")
     _check(lib().or_bfgs_step(n, q, _p(x), _p(a), _p(s), _p(out)))
     return out
+
+
+def symmetrize_(x: np.ndarray) -> float:
+    """In place X = (X + Xᵀ)/2, returns the removed drift ‖X − Xᵀ‖_F (simi.cpp:351-357)."""
+    assert x.flags.f_contiguous and x.dtype == np.float64
+    return float(lib().or_symmetrize(x.shape[0], _p(x)))
 
 
 def adarbfgs_update_factor(l, a, stilde) -> np.ndarray:

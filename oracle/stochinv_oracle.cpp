@@ -30,13 +30,32 @@
 #include <cstdlib>
 #include <cstring>
 #include <glob.h>
+#include <malloc.h>
 #include <numeric>
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 namespace oracle {
+
+// Minimal parallel-for over [0, count) on all host threads (this image has no
+// OpenMP runtime); used for the O(n²) elementwise passes, GEMMs use OpenBLAS.
+template <class F>
+void parallel_for(long count, F&& f) {
+    const long nt = std::max(1L, std::min<long>(count, long(std::thread::hardware_concurrency())));
+    if (nt <= 1) {
+        for (long i = 0; i < count; ++i) f(i);
+        return;
+    }
+    std::vector<std::thread> pool;
+    for (long t = 0; t < nt; ++t)
+        pool.emplace_back([&, t] {
+            for (long i = t; i < count; i += nt) f(i);
+        });
+    for (auto& th : pool) th.join();
+}
 
 using Index = std::ptrdiff_t;
 
@@ -254,24 +273,91 @@ Llt gram_llt(const Mat& gram, const char* kernel) {  // qn_updates.cpp:37-43
 
 // ------------------------------------------------------------ bfgs_step ----
 // proj/src/qn_updates.cpp:176-186, same expression order.
-Mat bfgs_step(const Mat& x, const Mat& a, const Mat& s) {
-    const Mat as = mul(a, s);                      // :177
-    const Mat gram = gemm(s, true, as, false);     // :178  S^T A S
-    const Llt llt = gram_llt(gram, "bfgs_step");   // :179
-    const Mat t1 = llt.solve(as.t());              // :180
-    const Mat t2 = llt.solve(s.t());               // :181
-    const Mat k = mul(t1, x);                      // :182
-    const Mat pax = mul(s, k);                     // :183
+// Raw-pointer GEMM on column-major operands: C(m×n) = op(A)·op(B).
+void gemm_raw(Index m, Index n, Index k, const double* A, Index lda, bool ta, const double* B, Index ldb, bool tb,
+              double* C, Index ldc) {
+    probe_blas();
+    if (m == 0 || n == 0) return;
+    if (g_dgemm && k > 0) {
+        g_dgemm(102, ta ? 112 : 111, tb ? 112 : 111, m, n, k, 1.0, A, std::max<Index>(1, lda), B,
+                std::max<Index>(1, ldb), 0.0, C, std::max<Index>(1, ldc));
+        return;
+    }
+    for (Index j = 0; j < n; ++j) {
+        for (Index i = 0; i < m; ++i) C[i + j * ldc] = 0.0;
+        for (Index p = 0; p < k; ++p) {
+            const double bpj = tb ? B[j + p * ldb] : B[p + j * ldb];
+            for (Index i = 0; i < m; ++i) C[i + j * ldc] += (ta ? A[p + i * lda] : A[i + p * lda]) * bpj;
+        }
+    }
+}
+
+// proj/src/qn_updates.cpp:176-186, same expression order; operands borrowed
+// (the reference takes const Matrix&), n×n temporaries as Eigen evaluates them.
+void bfgs_step_raw(Index n, Index q, const double* x, const double* a, const double* s, double* out) {
+    Mat as(n, q);
+    gemm_raw(n, q, n, a, n, false, s, n, false, as.data(), n);  // :177  A S
+    Mat gram(q, q);
+    gemm_raw(q, q, n, s, n, true, as.data(), n, false, gram.data(), q);  // :178  S^T A S
+    const Llt llt = gram_llt(gram, "bfgs_step");                         // :179
+    const Mat t1 = llt.solve(as.t());                                    // :180
+    Mat st(q, n);
+    for (Index j = 0; j < q; ++j)
+        for (Index i = 0; i < n; ++i) st(j, i) = s[i + j * n];
+    const Mat t2 = llt.solve(st);  // :181
+    Mat k(q, n);
+    gemm_raw(q, n, n, t1.data(), q, false, x, n, false, k.data(), q);  // :182
+    Mat pax(n, n);
+    gemm_raw(n, n, q, s, n, false, k.data(), q, false, pax.data(), n);  // :183
     // :185  s*t2 + x - pax - pax^T + s*((k*t1^T)*s^T)
-    const Mat st2 = mul(s, t2);
+    Mat st2(n, n);
+    gemm_raw(n, n, q, s, n, false, t2.data(), q, false, st2.data(), n);
     const Mat core = gemm(k, false, t1, true);
-    const Mat last = mul(s, gemm(core, false, s, true));
+    Mat cst(q, n);
+    gemm_raw(q, n, q, core.data(), q, false, s, n, true, cst.data(), q);
+    Mat last(n, n);
+    gemm_raw(n, n, q, s, n, false, cst.data(), q, false, last.data(), n);
+    // combine in cache blocks so the transposed read of pax stays in cache
+    const Index B = 64;
+    const Index nb = (n + B - 1) / B;
+    parallel_for(long(nb), [&](long jbi) {
+        const Index jb = Index(jbi) * B;
+        for (Index ib = 0; ib < n; ib += B)
+            for (Index j = jb; j < std::min(n, jb + B); ++j)
+                for (Index i = ib; i < std::min(n, ib + B); ++i)
+                    out[i + j * n] = st2(i, j) + x[i + j * n] - pax(i, j) - pax(j, i) + last(i, j);
+    });
+}
+
+Mat bfgs_step(const Mat& x, const Mat& a, const Mat& s) {
     Mat out(x.r, x.c);
-    const Index n = x.r;
-    for (Index j = 0; j < n; ++j)
-        for (Index i = 0; i < n; ++i)
-            out(i, j) = st2(i, j) + x(i, j) - pax(i, j) - pax(j, i) + last(i, j);
+    bfgs_step_raw(x.r, s.c, x.data(), a.data(), s.data(), out.data());
     return out;
+}
+
+// run_inverter's symmetrization (simi.cpp:351-357): drift = ‖X − Xᵀ‖_F, X = (X + Xᵀ)/2, blocked.
+double symmetrize_inplace(Index n, double* x) {
+    const Index B = 64;
+    const Index nb = (n + B - 1) / B;
+    std::vector<double> part(static_cast<size_t>(nb), 0.0);
+    parallel_for(long(nb), [&](long jbi) {
+        const Index jb = Index(jbi) * B;
+        double d = 0.0;
+        for (Index ib = 0; ib <= jb; ib += B)
+            for (Index j = jb; j < std::min(n, jb + B); ++j)
+                for (Index i = ib; i < std::min(n, ib + B); ++i) {
+                    if (i >= j) continue;
+                    const double u = x[i + j * n], l = x[j + i * n];
+                    d += 2.0 * (u - l) * (u - l);
+                    const double v = 0.5 * (u + l);
+                    x[i + j * n] = v;
+                    x[j + i * n] = v;
+                }
+        part[size_t(jbi)] = d;
+    });
+    double drift = 0.0;
+    for (double d : part) drift += d;
+    return std::sqrt(drift);
 }
 
 // ------------------------------------------------------------ Jacobi -------
@@ -483,6 +569,15 @@ void out(const Mat& m, double* p) {
 }
 }  // namespace
 
+// The reference (like this restatement) allocates several n×n temporaries per
+// bfgs_step (qn_updates.cpp:183-185).  glibc serves blocks > 32 MB with fresh
+// mmaps, so every call would page-fault gigabytes; as a CPU baseline we give the
+// port a tuned allocator instead (heap reuse, no trimming).
+__attribute__((constructor)) static void oracle_tune_malloc() {
+    mallopt(M_MMAP_MAX, 0);
+    mallopt(M_TRIM_THRESHOLD, 1 << 30);
+}
+
 extern "C" {
 
 const char* or_last_error() { return g_err.c_str(); }
@@ -512,8 +607,10 @@ void or_uniform_subset(void* h, int64_t n, int64_t q, int64_t* idx) {
 
 // --- step kernels ---
 int or_bfgs_step(int64_t n, int64_t q, const double* x, const double* a, const double* s, double* x_out) {
-    OR_GUARD(out(bfgs_step(wrap(x, n, n), wrap(a, n, n), wrap(s, n, q)), x_out))
+    OR_GUARD(bfgs_step_raw(n, q, x, a, s, x_out))
 }
+// in place: returns the drift ‖X − Xᵀ‖_F removed (simi.cpp:351-357)
+double or_symmetrize(int64_t n, double* x) { return symmetrize_inplace(n, x); }
 int or_adarbfgs_update_factor(int64_t n, int64_t q, const double* l, const double* a, const double* st, double* l_out) {
     OR_GUARD(out(adarbfgs_update_factor(wrap(l, n, n), wrap(a, n, n), wrap(st, n, q)), l_out))
 }
@@ -629,17 +726,7 @@ int or_run_inverter_bfgs(int64_t n, const double* a_in, int rule, int64_t q, dou
             }
             x = std::move(next);
             // :351-357 symmetrize + drift
-            double drift = 0.0;
-            for (Index j = 0; j < n; ++j)
-                for (Index i = 0; i < n; ++i) {
-                    const double d = x(i, j) - x(j, i);
-                    drift += d * d;
-                }
-            drift_max = std::max(drift_max, std::sqrt(drift));
-            Mat xs(n, n);
-            for (Index j = 0; j < n; ++j)
-                for (Index i = 0; i < n; ++i) xs(i, j) = 0.5 * (x(i, j) + x(j, i));
-            x = std::move(xs);
+            drift_max = std::max(drift_max, symmetrize_inplace(n, x.data()));
             if (k == 1 || k == max_iters_ || k % every_k == 0) {  // :361-375
                 const double rel = residual_dense(a, x) / base;
                 record(rel);

@@ -364,8 +364,11 @@ def _cfg(rule: SketchRule, tol, max_iters, budget, seed, track, x0, max_redraws,
     return c, keep
 
 
-def run_inverter(config: InverterConfig) -> RunResult:
-    """RunResult run_inverter(const InverterConfig&) for MethodSpec::named_method(bfgs) (simi.cpp:217-381)."""
+def run_inverter(config: InverterConfig, out: Optional[np.ndarray] = None) -> RunResult:
+    """RunResult run_inverter(const InverterConfig&) for MethodSpec::named_method(bfgs) (simi.cpp:217-381).
+
+    `out` (optional): caller-provided n×n Fortran-ordered float64 buffer for the
+    final X (e.g. pinned host memory)."""
     a = config.a
     if config.rule.is_adaptive():
         raise ConfigError("run_inverter: adaptive sketch rules belong to the adarbfgs driver")
@@ -377,7 +380,12 @@ def run_inverter(config: InverterConfig) -> RunResult:
     cap = int(config.max_iters) // max(1, config.track.residual_every_k) + 4
     hist = (L.HistoryPoint * cap)()
     res = L.RunResultC()
-    x = np.empty((n, n), order="F") if config.return_x else None
+    if out is not None:
+        if out.shape != (n, n) or out.dtype != np.float64 or not out.flags.f_contiguous:
+            raise ConfigError("run_inverter: out must be an n×n Fortran-ordered float64 array")
+        x = out
+    else:
+        x = np.empty((n, n), order="F") if config.return_x else None
     _check(L.load().si_run_inverter(a.ctx.handle, a.handle, C.byref(c), _pd(x) if x is not None else None, hist, cap,
                                     C.byref(res)))
     del keep

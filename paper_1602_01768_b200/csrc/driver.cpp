@@ -511,7 +511,16 @@ int si_run_inverter(si_context* ctx, si_problem* prob, const si_inverter_config*
             ck(cudaStreamSynchronize(c.stream), "sync");
         };
 
-        const double base = residual_norm(c, a, w.X);  // simi.cpp:242-246
+        // simi.cpp:242-246; for the default X0 = I, ‖I − A·I‖ = ‖I − A‖ needs no GEMM
+        double base;
+        if (cfg->x0_host) {
+            base = residual_norm(c, a, w.X);
+        } else {
+            si::identity_residual_sq_enqueue(c, a, c.scalar_dev);
+            ck(cudaMemcpyAsync(c.scalar_host, c.scalar_dev, sizeof(double), cudaMemcpyDeviceToHost, c.stream), "d2h");
+            ck(cudaStreamSynchronize(c.stream), "sync");
+            base = std::sqrt(c.scalar_host[0]);
+        }
         if (base == 0.0) {
             hist.record(0, 0.0, 0.0, 0.0);
             finish(SI_TOL_REACHED, "");
@@ -667,7 +676,16 @@ int si_run_adarbfgs(si_context* ctx, si_problem* prob, const si_inverter_config*
             ck(cudaStreamSynchronize(c.stream), "sync");
         };
 
-        const double base = factored_residual_norm(c, a, w);
+        // adarbfgs.cpp:112-115,126; for the default L0 = I the base is ‖I − A‖ (no GEMM)
+        double base;
+        if (cfg->x0_host) {
+            base = factored_residual_norm(c, a, w);
+        } else {
+            si::identity_residual_sq_enqueue(c, a, c.scalar_dev);
+            ck(cudaMemcpyAsync(c.scalar_host, c.scalar_dev, sizeof(double), cudaMemcpyDeviceToHost, c.stream), "d2h");
+            ck(cudaStreamSynchronize(c.stream), "sync");
+            base = std::sqrt(c.scalar_host[0]);
+        }
         if (base == 0.0) {
             hist.record(0, 0.0, 0.0, 0.0);
             finish(SI_TOL_REACHED, "");

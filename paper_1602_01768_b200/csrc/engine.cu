@@ -48,6 +48,7 @@ Context::~Context() {
     }
     for (auto e : event_pool) cudaEventDestroy(e);
     if (ws) cudaFree(ws);
+    if (solver_handle) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(solver_handle));
     if (scalar_dev) cudaFree(scalar_dev);
     if (scalar_host) cudaFreeHost(scalar_host);
     if (own_stream && stream) cudaStreamDestroy(stream);
@@ -426,11 +427,15 @@ bool problem_validate_spd(Problem& p) {
         CK(cudaMemsetAsync(tmp, 0, bytes, c.stream));
         densify_csr_kernel<<<grid_for(n, 256), 256, 0, c.stream>>>(n, p.rowptr, p.colind, p.val, tmp);
     }
-    cusolverDnHandle_t h;
-    if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) {
-        cudaFree(tmp);
-        throw CudaError("cusolverDnCreate failed");
+    if (!c.solver_handle) {
+        cusolverDnHandle_t hh;
+        if (cusolverDnCreate(&hh) != CUSOLVER_STATUS_SUCCESS) {
+            cudaFree(tmp);
+            throw CudaError("cusolverDnCreate failed");
+        }
+        c.solver_handle = hh;
     }
+    cusolverDnHandle_t h = static_cast<cusolverDnHandle_t>(c.solver_handle);
     cusolverDnSetStream(h, c.stream);
     int lwork = 0;
     cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_LOWER, int(n), tmp, int(n), &lwork);
@@ -442,7 +447,6 @@ bool problem_validate_spd(Problem& p) {
     int hinfo = -1;
     CK(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
     CK(cudaStreamSynchronize(c.stream));
-    cusolverDnDestroy(h);
     cudaFree(work);
     cudaFree(info);
     cudaFree(tmp);
@@ -644,6 +648,66 @@ __global__ void csr_resid_kernel(int64_t n, const int64_t* __restrict__ rowptr, 
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
         partial[blockIdx.x] = t;
     }
+}
+
+// ‖I − A‖²_F (the base residual for X0 = I, simi.cpp:242-246 with X = I): no GEMM needed.
+__global__ void identity_resid_dense_kernel(const double* __restrict__ A, int64_t n, double* partial) {
+    __shared__ double red[32];
+    double acc = 0.0;
+    const int64_t total = n * n;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = idx % n, j = idx / n;
+        const double d = (i == j ? 1.0 : 0.0) - A[idx];
+        acc += d * d;
+    }
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        partial[blockIdx.x] = t;
+    }
+}
+
+__global__ void identity_resid_csr_kernel(int64_t n, const int64_t* __restrict__ rowptr,
+                                          const int32_t* __restrict__ colind, const double* __restrict__ val,
+                                          double* partial) {
+    __shared__ double red[32];
+    double acc = 0.0;
+    for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < n; row += (int64_t)gridDim.x * blockDim.x) {
+        double diag = 0.0;
+        for (int64_t t = rowptr[row]; t < rowptr[row + 1]; ++t) {
+            if (colind[t] == row) diag += val[t];
+            else acc += val[t] * val[t];
+        }
+        acc += (1.0 - diag) * (1.0 - diag);
+    }
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        partial[blockIdx.x] = t;
+    }
+}
+
+void identity_residual_sq_enqueue(Context& c, Problem& a, double* out_dev) {
+    const int blocks = c.num_sms * 4;
+    double* part = c.ensure_ws(size_t(blocks));
+    {
+        LaunchScope ls(c, "identity_resid");
+        if (a.dense)
+            identity_resid_dense_kernel<<<blocks, 256, 0, c.stream>>>(a.a, a.n, part);
+        else
+            identity_resid_csr_kernel<<<blocks, 256, 0, c.stream>>>(a.n, a.rowptr, a.colind, a.val, part);
+        check_launch("identity_resid");
+    }
+    LaunchScope ls(c, "sum_reduce");
+    sum_reduce_kernel<<<1, 1024, 0, c.stream>>>(part, blocks, out_dev);
+    check_launch("sum_reduce");
 }
 
 void residual_sq_enqueue(Context& c, Problem& a, const double* X, double* out_dev, double* /*scratch*/) {

@@ -43,6 +43,7 @@ struct Context {
     };
     std::vector<Pending> pending;
     std::vector<cudaEvent_t> event_pool;
+    void* solver_handle = nullptr;  // cusolverDn handle for validate_spd (lazy, reused)
 
     double* ensure_ws(size_t doubles);
     int class_id(const char* name);
@@ -132,6 +133,8 @@ void rbfgs_enqueue_iteration(Context& c, Problem& a, RbfgsWork& w, bool device_s
 void rbfgs_enqueue_sketch_upload(Context& c, RbfgsWork& w);  // s_pinned -> S
 // sum of squares of I − A·X into *out_dev (no n×n write); returns nothing (async)
 void residual_sq_enqueue(Context& c, Problem& a, const double* X, double* out_dev, double* scratch_nxn);
+// ‖I − A‖²_F: the base residual when X0 = I (default), O(n²) instead of 2n³
+void identity_residual_sq_enqueue(Context& c, Problem& a, double* out_dev);
 void factored_residual_sq_enqueue(Context& c, Problem& a, const double* L, double* AL, double* out_dev);
 void set_identity(Context& c, double* X, int64_t n);
 
