@@ -184,6 +184,28 @@ int si_solver_step_with_sketch(si_solver* s, const double* s_host, const int64_t
 int si_solver_residual(si_solver* s, double* out); /* absolute ||I - A X||_F */
 int64_t si_solver_redraws(si_solver* s);
 
+/* ---- device-pointer operations ---------------------------------------
+ * The row-sharded multi-GPU driver (paper_1602_01768_b200/dist.py) composes an
+ * RBFGS iteration from these on each rank's panels; pointers are device memory
+ * of the context's GPU, column-major.  All are asynchronous on the context
+ * stream except si_rbfgs_core_device (reads the PD status) and
+ * si_residual_rows_device (returns a host scalar). */
+/* C = alpha·op(A)·op(B) + beta·C.  A is M×K (a_kmajor: A(m,k) = A[m*lda + k], else A[m + k*lda]);
+ * B is K×N (b_kmajor: B(k,n) = B[k + n*ldb], else B[n + k*ldb]); FP64 DMMA. */
+int si_gemm_device(si_context* ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, int a_kmajor,
+                   const double* B, int64_t ldb, int b_kmajor, double* C, int64_t ldc, double alpha, double beta);
+/* S (n×q, ld lds) ~ N(0,1) from Philox4x32-10(seed, draw): identical bytes on every rank. */
+int si_sketch_gaussian_device(si_context* ctx, double* S, int64_t n, int64_t q, int64_t lds, uint64_t seed,
+                              uint64_t draw);
+/* From P = [SᵀY | YᵀW] (q×2q, ld ldp) build M = [[G⁻¹ + G⁻¹HG⁻¹, −G⁻¹], [−G⁻¹, 0]] (2q×2q, ld 2q).
+ * scratch: 2q² + 2q + 16 doubles.  Returns SI_ERR_RESAMPLE when G = SᵀAS is not positive definite. */
+int si_rbfgs_core_device(si_context* ctx, const double* P, int64_t ldp, int64_t q, double* M, double* scratch);
+/* Σ_{i<m, j<n} (δ(r0+i, j) − (X_rows·A)(i, j))², X_rows = rows [r0, r0+m) of X (ld ldx), dense A. */
+int si_residual_rows_device(si_context* ctx, si_problem* prob, int64_t m, int64_t r0, const double* x_rows,
+                            int64_t ldx, double* out_host);
+/* Device pointer to the problem's dense A (column-major, ld n); NULL for CSR. */
+const double* si_problem_dense_device(si_problem* prob);
+
 /* ---- host RngStream (rng.hpp:13-71), exposed for input generation and tests */
 typedef struct si_rng si_rng;
 int si_rng_create(uint64_t seed, si_rng** out);

@@ -75,6 +75,11 @@ _SIGS = {
     "si_solver_step_with_sketch": (ci, [vp, pd, pi64]),
     "si_solver_residual": (ci, [vp, pd]),
     "si_solver_redraws": (i64, [vp]),
+    "si_gemm_device": (ci, [vp, i64, i64, i64, vp, i64, ci, vp, i64, ci, vp, i64, d, d]),
+    "si_sketch_gaussian_device": (ci, [vp, vp, i64, i64, i64, u64, u64]),
+    "si_rbfgs_core_device": (ci, [vp, vp, i64, i64, vp, vp]),
+    "si_residual_rows_device": (ci, [vp, vp, i64, i64, vp, i64, pd]),
+    "si_problem_dense_device": (vp, [vp]),
     "si_rng_create": (ci, [u64, C.POINTER(vp)]),
     "si_rng_substream": (ci, [vp, u64, C.POINTER(vp)]),
     "si_rng_destroy": (ci, [vp]),

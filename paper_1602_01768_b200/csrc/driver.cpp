@@ -966,6 +966,52 @@ int si_solver_residual(si_solver* s, double* out) {
     });
 }
 
+// ------------------------------------------------------- device pointers --
+int si_gemm_device(si_context* ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, int a_kmajor,
+                   const double* B, int64_t ldb, int b_kmajor, double* C, int64_t ldc, double alpha, double beta) {
+    return guard([&] {
+        require(M >= 0 && N >= 0 && K >= 0, "gemm: negative dimension");
+        si::gemm(*ctx->c, M, N, K, A, lda, a_kmajor != 0, B, ldb, b_kmajor != 0, C, ldc, alpha, beta);
+    });
+}
+
+int si_sketch_gaussian_device(si_context* ctx, double* S, int64_t n, int64_t q, int64_t lds, uint64_t seed,
+                              uint64_t draw) {
+    return guard([&] {
+        require(n >= 1 && q >= 1 && lds >= n, "sketch: bad shape");
+        si::philox_sketch(*ctx->c, S, n, q, lds, seed, nullptr, draw, nullptr);
+    });
+}
+
+int si_rbfgs_core_device(si_context* ctx, const double* P, int64_t ldp, int64_t q, double* M, double* scratch) {
+    return guard([&] {
+        auto& c = *ctx->c;
+        require(q >= 1 && ldp >= q, "rbfgs_core: bad shape");
+        if (!c.aux_status) ck(cudaMalloc(&c.aux_status, 4 * sizeof(int)), "malloc");
+        ck(cudaMemsetAsync(c.aux_status, 0, 4 * sizeof(int), c.stream), "memset");
+        double* ginv = scratch;
+        double* t = scratch + q * q;
+        double* fs = scratch + 2 * q * q;
+        si::rbfgs_core_enqueue(c, P, ldp, q, ginv, t, M, fs, c.aux_status);
+        int st[4];
+        read_status(c, c.aux_status, st);
+        if (st[0]) throw ResampleError("bfgs_step: sketched Gram matrix is not positive definite");
+    });
+}
+
+int si_residual_rows_device(si_context* ctx, si_problem* prob, int64_t m, int64_t r0, const double* x_rows,
+                            int64_t ldx, double* out_host) {
+    return guard([&] {
+        auto& c = *ctx->c;
+        si::residual_rows_sq_enqueue(c, *prob->p, m, r0, x_rows, ldx, c.scalar_dev);
+        ck(cudaMemcpyAsync(c.scalar_host, c.scalar_dev, sizeof(double), cudaMemcpyDeviceToHost, c.stream), "d2h");
+        ck(cudaStreamSynchronize(c.stream), "sync");
+        *out_host = c.scalar_host[0];
+    });
+}
+
+const double* si_problem_dense_device(si_problem* prob) { return prob->p->dense ? prob->p->a : nullptr; }
+
 // ---------------------------------------------------------------- rng ------
 struct si_rng {
     si::RngStream r;

@@ -48,6 +48,7 @@ Context::~Context() {
     }
     for (auto e : event_pool) cudaEventDestroy(e);
     if (ws) cudaFree(ws);
+    if (aux_status) cudaFree(aux_status);
     if (solver_handle) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(solver_handle));
     if (scalar_dev) cudaFree(scalar_dev);
     if (scalar_host) cudaFreeHost(scalar_host);
@@ -565,6 +566,29 @@ static void spd_inverse(Context& c, const double* P, int64_t ldp, int64_t q, dou
     check_launch("spd_inverse");
 }
 
+// K-FACTOR + K-CORE: from P = [G | H] (q×2q, ld ldp) build
+// M = [[Ginv + Ginv·H·Ginv, −Ginv], [−Ginv, 0]] (2q×2q, ld 2q).  status[0] is
+// set (and every later launch skipped) when G is not positive definite.
+void rbfgs_core_enqueue(Context& c, const double* P, int64_t ldp, int64_t q, double* Ginv, double* T, double* M,
+                        double* scratch, int* status) {
+    spd_inverse(c, P, ldp, q, Ginv, scratch, status);
+    {
+        LaunchScope ls(c, "core_layout");
+        core_layout_kernel<<<grid_for(4 * q * q, 256), 256, 0, c.stream>>>(Ginv, int(q), M, status);
+        check_launch("core_layout");
+    }
+    gemm(c, q, q, q, P + q * ldp, ldp, false, Ginv, q, true, T, q, 1.0, 0.0, status);  // T = H·Ginv
+    gemm(c, q, q, q, Ginv, q, false, T, q, true, M, 2 * q, 1.0, 1.0, status);          // M11 = Ginv + Ginv·T
+}
+
+void philox_sketch(Context& c, double* S, int64_t n, int64_t q, int64_t lds, uint64_t seed,
+                   const unsigned long long* counter_dev, uint64_t draw, const int* skip) {
+    LaunchScope ls(c, "sketch_philox");
+    philox_gaussian_kernel<<<grid_for((n * q + 1) / 2, 256), 256, 0, c.stream>>>(S, n, q, lds, seed, counter_dev, skip,
+                                                                               draw);
+    check_launch("philox");
+}
+
 // One RBFGS iteration:  X⁺ = X + [S W]·M·[S W]ᵀ.  Every launch
 // is skipped on the device once K-FACTOR flags a non-PD Gram (status[0]).
 void rbfgs_enqueue_iteration(Context& c, Problem& a, RbfgsWork& w, bool device_sketch, uint64_t seed) {
@@ -581,14 +605,7 @@ void rbfgs_enqueue_iteration(Context& c, Problem& a, RbfgsWork& w, bool device_s
     apply_a(c, a, S, n, q, w.Y, n, skip);                                    // Y = A·S
     gemm(c, n, q, n, w.X, n, false, w.Y, n, true, W, n, 1.0, 0.0, skip);     // W = X·Y
     gemm(c, q, 2 * q, n, w.Y, n, true, w.U, n, true, w.P, q, 1.0, 0.0, skip);  // P = Yᵀ·[S W] = [G | H]
-    spd_inverse(c, w.P, q, q, w.Ginv, w.factor_scratch, w.status);          // Ginv, PD check
-    {
-        LaunchScope ls(c, "core_layout");
-        core_layout_kernel<<<grid_for(4 * q * q, 256), 256, 0, c.stream>>>(w.Ginv, int(q), w.M, skip);
-        check_launch("core_layout");
-    }
-    gemm(c, q, q, q, w.P + q * q, q, false, w.Ginv, q, true, w.T, q, 1.0, 0.0, skip);  // T = H·Ginv
-    gemm(c, q, q, q, w.Ginv, q, false, w.T, q, true, w.M, 2 * q, 1.0, 1.0, skip);     // M11 = Ginv + Ginv·T
+    rbfgs_core_enqueue(c, w.P, q, q, w.Ginv, w.T, w.M, w.factor_scratch, w.status);  // Ginv, PD check, M
     gemm(c, n, 2 * q, 2 * q, w.U, n, false, w.M, 2 * q, true, w.V, n, 1.0, 0.0, skip);  // V = U·M
     symupd(c, n, 2 * q, w.V, n, w.U, n, w.X, n, 1.0, skip, w.status + 1);            // X += V·Uᵀ
     if (device_sketch) {
@@ -599,27 +616,44 @@ void rbfgs_enqueue_iteration(Context& c, Problem& a, RbfgsWork& w, bool device_s
 }
 
 // ----------------------------------------------------------- residual ------
+// Σ (δ(r + diag_off, c) − (A·B)(r, c))² over an M×N product with K = n, no
+// M×N write; partial per CTA then a fixed-order reduction into *out_dev.
 template <bool BKM>
-static void resid_gemm(Context& c, int64_t n, const double* A, int64_t lda, const double* B, int64_t ldb,
-                       double* out_dev) {
+static void resid_gemm_rect(Context& c, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                            const double* B, int64_t ldb, int64_t diag_off, double* out_dev) {
     GemmArgs g{};
-    g.M = n;
-    g.N = n;
-    g.K = n;
+    g.M = M;
+    g.N = N;
+    g.K = K;
     g.A = A;
     g.lda = lda;
     g.B = B;
     g.ldb = ldb;
     g.alpha = 1.0;
-    g.k_chunk = n;
-    const int64_t T = (n + 127) / 128;
-    g.ws = c.ensure_ws(size_t(T * T));
+    g.k_chunk = K;
+    g.diag_off = diag_off;
+    const int64_t TM = (M + 127) / 128, TN = (N + 127) / 128;
+    g.ws = c.ensure_ws(size_t(TM * TN));
     const int vec = pick_vec(g);
     launch_gemm_layout<EPI_RESID>(c, use_w16() ? T128x128W16 : T128x128, false, BKM, vec, g,
-                                  dim3(unsigned(T), unsigned(T), 1), "gemm_resid");
+                                  dim3(unsigned(TM), unsigned(TN), 1), "gemm_resid");
     LaunchScope ls(c, "sum_reduce");
-    sum_reduce_kernel<<<1, 1024, 0, c.stream>>>(g.ws, T * T, out_dev);
+    sum_reduce_kernel<<<1, 1024, 0, c.stream>>>(g.ws, TM * TN, out_dev);
     check_launch("sum_reduce");
+}
+
+template <bool BKM>
+static void resid_gemm(Context& c, int64_t n, const double* A, int64_t lda, const double* B, int64_t ldb,
+                       double* out_dev) {
+    resid_gemm_rect<BKM>(c, n, n, n, A, lda, B, ldb, 0, out_dev);
+}
+
+// Row panel of a row-sharded X: Σ over rows [r0, r0+m) of ‖I − X·A‖² (= ‖I − A·X‖²
+// for symmetric A and X), dense A.
+void residual_rows_sq_enqueue(Context& c, Problem& a, int64_t m, int64_t r0, const double* Xrows, int64_t ldx,
+                              double* out_dev) {
+    if (!a.dense) throw std::invalid_argument("residual_rows: sparse A is not supported for row panels yet");
+    resid_gemm_rect<true>(c, m, a.n, a.n, Xrows, ldx, a.a, a.n, r0, out_dev);
 }
 
 __global__ void csr_resid_kernel(int64_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colind,

@@ -44,6 +44,7 @@ struct Context {
     std::vector<Pending> pending;
     std::vector<cudaEvent_t> event_pool;
     void* solver_handle = nullptr;  // cusolverDn handle for validate_spd (lazy, reused)
+    int* aux_status = nullptr;      // status words of device-pointer entry points
 
     double* ensure_ws(size_t doubles);
     int class_id(const char* name);
@@ -130,6 +131,14 @@ void apply_a(Context& c, Problem& a, const double* P, int64_t ldp, int64_t k, do
              const int* skip = nullptr);
 
 void rbfgs_enqueue_iteration(Context& c, Problem& a, RbfgsWork& w, bool device_sketch, uint64_t seed);
+// the q×q stage: Gram inverse (PD check into status[0]) and the 2q×2q core M
+void rbfgs_core_enqueue(Context& c, const double* P, int64_t ldp, int64_t q, double* Ginv, double* T, double* M,
+                        double* scratch, int* status);
+// Gaussian sketch from Philox(seed, draw): draw read from counter_dev if non-null
+void philox_sketch(Context& c, double* S, int64_t n, int64_t q, int64_t lds, uint64_t seed,
+                   const unsigned long long* counter_dev, uint64_t draw, const int* skip);
+void residual_rows_sq_enqueue(Context& c, Problem& a, int64_t m, int64_t r0, const double* Xrows, int64_t ldx,
+                              double* out_dev);
 void rbfgs_enqueue_sketch_upload(Context& c, RbfgsWork& w);  // s_pinned -> S
 // sum of squares of I − A·X into *out_dev (no n×n write); returns nothing (async)
 void residual_sq_enqueue(Context& c, Problem& a, const double* X, double* out_dev, double* scratch_nxn);

@@ -40,6 +40,7 @@ struct GemmArgs {
     double* ws;       // EPI_PARTIAL: ws[z*M*N + m + n*M]; EPI_RESID: ws[linear block]
     const int* skip;  // if set and nonzero, the launch is a no-op (failed Gram upstream)
     int* nonfinite;   // STORE / SYMUPD: set to 1 when a written entry is not finite (simi.cpp:342-347)
+    int64_t diag_off; // RESID: the identity's diagonal is at (r, r + diag_off) (row panels of a sharded X)
 };
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool A_KMAJOR, bool B_KMAJOR>
@@ -151,7 +152,7 @@ struct TileOps {
                     for (int e = 0; e < 4; ++e) {
                         const int64_t r = row(i, e), c = col(j, e);
                         if (r < p.M && c < p.N) {
-                            const double d = (r == c ? 1.0 : 0.0) - acc[i][j][e];
+                            const double d = (r + p.diag_off == c ? 1.0 : 0.0) - acc[i][j][e];
                             local += d * d;
                         }
                     }

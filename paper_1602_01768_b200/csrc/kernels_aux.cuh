@@ -213,9 +213,10 @@ struct Philox {
 // `draw_counter` lives in device memory so one captured iteration can be
 // replayed; K-FACTOR's launcher advances it.
 __global__ void philox_gaussian_kernel(double* __restrict__ S, int64_t n, int64_t q, int64_t lds, uint64_t seed,
-                                       const unsigned long long* draw_counter, const int* skip) {
+                                       const unsigned long long* draw_counter, const int* skip,
+                                       unsigned long long draw_value = 0) {
     if (skip && *skip) return;
-    const uint64_t draw = *draw_counter;
+    const uint64_t draw = draw_counter ? *draw_counter : draw_value;
     const int64_t total = n * q;
     const int64_t pairs = (total + 1) / 2;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < pairs; e += (int64_t)gridDim.x * blockDim.x) {

@@ -1,0 +1,61 @@
+"""CPU test double for the sharded driver's panel ops (TEST INFRASTRUCTURE).
+
+Implements the same contract as paper_1602_01768_b200.dist.CudaPanelOps on CPU
+torch tensors with numpy arithmetic, and draws sketches from the oracle's
+RngStream(seed).substream(draw), so the gloo tests exercise the row
+decomposition, the collectives and the packing, against a single-process oracle
+run on the same sketch sequence.
+"""
+import numpy as np
+from numpy.lib.stride_tricks import as_strided
+
+from oracle import oracle as O
+
+
+def _view(t, rows, cols, ld, kmajor=False):
+    a = t.numpy()
+    if kmajor:  # element (r, c) at r*ld + c
+        return as_strided(a, shape=(rows, cols), strides=(8 * ld, 8))
+    return as_strided(a, shape=(rows, cols), strides=(8, 8 * ld))
+
+
+class NumpyPanelOps:
+    def __init__(self, a_dense=None):
+        self.a = a_dense
+
+    def gemm(self, M, N, K, A, lda, a_kmajor, B, ldb, b_kmajor, Cm, ldc, alpha=1.0, beta=0.0):
+        a = _view(A, M, K, lda, a_kmajor)
+        b = _view(B, K, N, ldb, not b_kmajor)  # b_kmajor: B(k,n) = B[k + n*ldb] -> column-major K×N
+        c = _view(Cm, M, N, ldc)
+        res = alpha * (a @ b)
+        if beta != 0.0:
+            res = res + beta * c
+        c[...] = res
+
+    def sketch(self, S, n, q, lds, seed, draw):
+        s = O.RngStream(seed).substream(draw).gaussian_matrix(n, q)
+        _view(S, n, q, lds)[...] = s
+
+    def core(self, P, ldp, q, M, scratch):
+        from paper_1602_01768_b200.api import GramRankDeficientError
+
+        p = _view(P, q, 2 * q, ldp).copy()
+        g = np.triu(p[:, :q]) + np.triu(p[:, :q], 1).T
+        try:
+            np.linalg.cholesky(g)
+        except np.linalg.LinAlgError:
+            raise GramRankDeficientError("bfgs_step: sketched Gram matrix is not positive definite")
+        gi = np.linalg.inv(g)
+        gi = 0.5 * (gi + gi.T)
+        h = p[:, q:]
+        m = np.zeros((2 * q, 2 * q))
+        m[:q, :q] = gi + gi @ h @ gi
+        m[:q, q:] = -gi
+        m[q:, :q] = -gi
+        _view(M, 2 * q, 2 * q, 2 * q)[...] = m
+
+    def residual_rows_sq(self, prob, m, r0, X, ldx):
+        x = _view(X, m, self.a.shape[0], ldx)
+        r = x @ self.a
+        r[np.arange(m), r0 + np.arange(m)] -= 1.0
+        return float((r * r).sum())

@@ -1,0 +1,87 @@
+"""Row-sharded RBFGS host logic on CPU: world_size 1 and 2 over gloo, against a
+single-process oracle run on the same sketch sequence."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import oracle as O
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _problem(n, seed=3):
+    rng = O.RngStream(seed)
+    b = rng.gaussian_matrix(n, n)
+    return np.asfortranarray(b @ b.T / n + np.eye(n))
+
+
+def _oracle_run(a, q, iters, seed):
+    n = a.shape[0]
+    x = np.asfortranarray(np.eye(n))
+    for draw in range(iters):
+        s = O.RngStream(seed).substream(draw).gaussian_matrix(n, q)
+        x = O.bfgs_step(x, a, s)
+    return x
+
+
+def _worker(rank, world, port, n, q, iters, seed, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+
+        sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+        from dist_test_ops import NumpyPanelOps
+        from paper_1602_01768_b200.dist import RowShardedRBFGS, row_partition
+
+        a = _problem(n)
+        starts = row_partition(n, world)
+        r0, r1 = starts[rank], starts[rank + 1]
+        a_rows = torch.from_numpy(np.asfortranarray(a[r0:r1, :]).reshape(-1, order="F").copy())
+        solver = RowShardedRBFGS(NumpyPanelOps(a), n, q, a_rows, seed=seed)
+        for _ in range(iters):
+            solver.step()
+        x = solver.gather_x().numpy().reshape((n, n), order="F")
+        res = solver.residual()
+        if rank == 0:
+            out_q.put((x, res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n,q", [(1, 24, 4), (2, 37, 3), (2, 64, 8)])
+def test_row_sharded_matches_oracle(world, n, q):
+    iters, seed = 12, 5
+    ctx = mp.get_context("spawn")
+    out_q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, q, iters, seed, out_q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    x, res = out_q.get(timeout=180)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    a = _problem(n)
+    ref = _oracle_run(a, q, iters, seed)
+    assert np.linalg.norm(x - ref) / np.linalg.norm(ref) <= 1e-9
+    assert res == pytest.approx(np.linalg.norm(np.eye(n) - a @ x), rel=1e-9)
+
+
+def test_row_partition():
+    from paper_1602_01768_b200.dist import row_partition
+
+    assert row_partition(10, 3) == [0, 4, 7, 10]
+    assert row_partition(8, 8) == list(range(9))

@@ -1,0 +1,71 @@
+"""GPU checks of the device-pointer C ABI and the row-sharded driver at world
+size 1 (the only GPU count available to this run; N > 1 is covered on CPU by
+tests/test_dist_cpu.py with the same driver code)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+
+    import paper_1602_01768_b200 as si
+    from paper_1602_01768_b200.dist import CudaPanelOps
+
+    ctx = si.Context(0, stream=torch.cuda.current_stream().cuda_stream)
+    return si, torch, ctx, CudaPanelOps(ctx)
+
+
+@pytest.mark.parametrize("ak,bk", [(False, True), (True, True), (False, False)])
+@pytest.mark.parametrize("M,N,K", [(33, 17, 65), (256, 128, 512), (130, 256, 2048)])
+def test_gemm_device_layouts(env, ak, bk, M, N, K):
+    si, torch, ctx, ops = env
+    rng = np.random.default_rng(M + N + K)
+    a = rng.standard_normal((M, K))
+    b = rng.standard_normal((K, N))
+    c0 = rng.standard_normal((M, N))
+    A = torch.from_numpy((a if ak else a.T).copy().reshape(-1)).cuda()  # kmajor: row-major M×K
+    B = torch.from_numpy((b.T if bk else b).copy().reshape(-1)).cuda()  # kmajor: col-major K×N
+    Cm = torch.from_numpy(c0.T.copy().reshape(-1)).cuda()
+    ops.gemm(M, N, K, A, K if ak else M, ak, B, K if bk else N, bk, Cm, M, 0.5, 2.0)
+    torch.cuda.synchronize()
+    got = Cm.cpu().numpy().reshape((N, M)).T
+    ref = 0.5 * a @ b + 2.0 * c0
+    assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max() * K
+
+
+def test_sketch_deterministic_and_gaussian(env):
+    si, torch, ctx, ops = env
+    n, q = 4096, 64
+    s1 = torch.empty(n * q, dtype=torch.float64, device="cuda")
+    s2 = torch.empty_like(s1)
+    ops.sketch(s1, n, q, n, 11, 3)
+    ops.sketch(s2, n, q, n, 11, 3)
+    torch.cuda.synchronize()
+    assert torch.equal(s1, s2)
+    ops.sketch(s2, n, q, n, 11, 4)
+    v = s2.cpu().numpy()
+    assert abs(v.mean()) < 5e-3 and abs(v.std() - 1.0) < 5e-3
+    assert not torch.equal(s1, s2)
+
+
+def test_row_sharded_world1_matches_solver(env):
+    si, torch, ctx, ops = env
+    from paper_1602_01768_b200 import generators as G
+    from paper_1602_01768_b200.dist import RowShardedRBFGS
+
+    n, q, iters, seed = 512, 16, 15, 7
+    a = G.config1_dense(n, seed=2)
+    prob = si.ProblemMatrix(a, si.Symmetry.spd, context=ctx)
+    a_rows = torch.from_numpy(a.reshape(-1, order="F").copy()).cuda()
+    sh = RowShardedRBFGS(ops, n, q, a_rows, seed=seed, prob=prob)
+    for _ in range(iters):
+        sh.step()
+    x_sh = sh.gather_x().cpu().numpy().reshape((n, n), order="F")
+    sol = si.Solver(prob, si.Method.rbfgs, si.SketchRule.gaussian_device(q), seed=seed)
+    sol.step(iters)
+    x_so = sol.iterate()
+    assert np.linalg.norm(x_sh - x_so) / np.linalg.norm(x_so) <= 1e-9
+    assert sh.residual() == pytest.approx(sol.residual(), rel=1e-9)
