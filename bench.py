@@ -204,10 +204,88 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def run_sharded(args, cfg):
+    """N > 1: X and A row-sharded over the ranks (paper_1602_01768_b200/dist.py),
+    NCCL all-gathers of Y and W and one packed all-reduce per iteration; the
+    workload (config 3) is fixed, so scaling is strong."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29531")
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local), rank=rank, world_size=world)
+    import paper_1602_01768_b200 as si
+    from paper_1602_01768_b200 import generators as G
+    from paper_1602_01768_b200.dist import CudaPanelOps, RowShardedRBFGS, row_partition
+
+    n, q = cfg["n"], cfg["q"]
+    stream = torch.cuda.current_stream()
+    ctx = si.Context(local, stream=stream.cuda_stream)
+    a_full = G.config3_dense_device(n, seed=0) if cfg["gen"] == "config3" else \
+        torch.from_numpy(make_dense(cfg)).cuda()
+    starts = row_partition(n, world)
+    r0, r1 = starts[rank], starts[rank + 1]
+    # A symmetric: the row-major tensor is Aᵀ = A, so columns r0..r1 of it are the
+    # column-major m×n row panel A[R_p, :]
+    a_rows = a_full[r0:r1, :].contiguous().reshape(-1)
+    prob = None  # the timed loop needs no residual
+    del a_full
+    torch.cuda.empty_cache()
+    sh = RowShardedRBFGS(CudaPanelOps(ctx), n, q, a_rows, seed=0, prob=prob)
+    for _ in range(args.warmup):
+        sh.step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    launches0 = ctx.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            sh.step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    launches = ctx.launch_count() - launches0
+    t = torch.tensor([ms], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    m = r1 - r0
+    rank_flops = 2.0 * m * n * q * 2 + 4.0 * m * n * q + 2.0 * m * q * 2 * q + 2.0 * m * 2 * q * 2 * q
+    achieved = rank_flops * args.steps / (ms * 1e-3) / 1e12
+    if rank == 0:
+        alg = 6.0 * n * n * q + 12.0 * n * q * q
+        line = {
+            "metric": "rbfgs_iterations_per_s", "value": args.steps / (ms * 1e-3), "unit": "iter/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": cfg["name"], "n": n, "q": q, "sketch": "gaussian, device Philox4x32-10",
+                       "l2": "inputs larger than L2; no flush", "parallelism": f"row-sharded X and A over {world} GPUs",
+                       "algorithmic_gflop_per_step": alg / 1e9},
+            "roofline": {"bound": "tensor", "kernel": "row-panel iteration (all DMMA GEMMs of one rank)",
+                         "achieved": achieved, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": achieved / FP64_DMMA_PEAK_TFLOPS, "traffic": None,
+                         "peak_source": "measured FP64 DMMA peak, profiles/r01_fp64_peak.txt"},
+            "cpu_baseline": None,
+            "e2e": None,
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def run_ours(args, cfg):
     import torch
 
     rank, world, local = dist_env()
+    if world > 1 or args.sharded:
+        return run_sharded(args, cfg)
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
@@ -331,6 +409,7 @@ def main():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", type=int, default=3, choices=sorted(CONFIGS))
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--sharded", action="store_true", help="use the row-sharded driver even at N=1")
     args = p.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]

@@ -280,10 +280,11 @@ void gemm(Context& c, int64_t M, int64_t N, int64_t K, const double* A, int64_t 
     a.beta = beta;
     a.skip = skip;
     a.nonfinite = nonfinite;
-    const TileCfg t = pick_tile(N);
+    // short-K, wide-output products (the rank-2q panel update) keep 16 warps resident
+    const TileCfg t = (K <= 512 && N > 64 && M > 64) ? T128x128W16 : pick_tile(N);
     const int BM = 128, BN = (t == T128x128 || t == T128x128W16) ? 128 : (t == T128x64 ? 64 : 32), BKT = 16;
     const int64_t tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN, tiles = tm * tn;
-    const int per_sm = t == T128x128 ? 1 : 2;
+    const int per_sm = (t == T128x128 || t == T128x128W16) ? 1 : 2;
     const int64_t slots = int64_t(c.num_sms) * per_sm;
     // split-K so the number of work units fills whole waves of the 148 SMs
     int splits = 1;
@@ -313,6 +314,7 @@ void gemm(Context& c, int64_t M, int64_t N, int64_t K, const double* A, int64_t 
     }
     if (splits == 1) {
         a.k_chunk = std::max<int64_t>(K, 1);
+        a.c_in_acc = (alpha == 1.0 && beta != 0.0) ? 1 : 0;
         launch_gemm_layout<EPI_STORE>(c, t, a_kmajor, b_kmajor, vec, a, dim3(unsigned(tm), unsigned(tn), 1),
                                       "gemm_store");
         return;

@@ -41,6 +41,7 @@ struct GemmArgs {
     const int* skip;  // if set and nonzero, the launch is a no-op (failed Gram upstream)
     int* nonfinite;   // STORE / SYMUPD: set to 1 when a written entry is not finite (simi.cpp:342-347)
     int64_t diag_off; // RESID: the identity's diagonal is at (r, r + diag_off) (row panels of a sharded X)
+    int c_in_acc;     // STORE: accumulators start from beta·C (set by the host when alpha == 1, beta != 0)
 };
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool A_KMAJOR, bool B_KMAJOR>
@@ -90,10 +91,19 @@ struct TileOps {
     __device__ __forceinline__ int64_t row(int i, int e) const { return m0 + wm0 + i * 16 + g + ((e >> 1) << 3); }
     __device__ __forceinline__ int64_t col(int j, int e) const { return n0 + wn0 + j * 8 + 2 * t4 + (e & 1); }
 
+    // STORE with alpha = 1 and beta ≠ 0 also starts from C (p.c_in_acc)
+    __device__ __forceinline__ bool c_in_acc(const GemmArgs& p) const {
+        if constexpr (EPI == EPI_SYMUPD) return true;
+        if constexpr (EPI == EPI_STORE) return p.c_in_acc != 0;
+        return false;
+    }
+
     __device__ __forceinline__ void init_acc(double (&acc)[MI][NI][4], const GemmArgs& p) const {
-        if constexpr (EPI == EPI_SYMUPD) {
-            // accumulate onto the X tile itself (C = X + V·Uᵀ, alpha = 1): the loads
-            // are issued under the pipeline fill and the epilogue becomes store-only
+        if (c_in_acc(p)) {
+            // accumulate onto the C tile itself (C = beta·C + A·B with alpha = 1; for
+            // SYMUPD X + V·Uᵀ): the loads are issued under the pipeline fill and the
+            // epilogue becomes store-only
+            const double b = EPI == EPI_SYMUPD ? 1.0 : p.beta;
 #pragma unroll
             for (int i = 0; i < MI; ++i)
 #pragma unroll
@@ -101,7 +111,7 @@ struct TileOps {
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const int64_t r = row(i, e), c = col(j, e);
-                        acc[i][j][e] = (r < p.M && c < p.N) ? p.C[r + c * p.ldc] : 0.0;
+                        acc[i][j][e] = (r < p.M && c < p.N) ? b * p.C[r + c * p.ldc] : 0.0;
                     }
         } else {
 #pragma unroll
@@ -178,7 +188,7 @@ struct TileOps {
                         const double v = acc[i][j][e];
                         if constexpr (EPI == EPI_STORE) {
                             double* cp = p.C + r + c * p.ldc;
-                            const double nv = p.beta != 0.0 ? p.alpha * v + p.beta * *cp : p.alpha * v;
+                            const double nv = p.c_in_acc ? v : (p.beta != 0.0 ? p.alpha * v + p.beta * *cp : p.alpha * v);
                             *cp = nv;
                             if (p.nonfinite && !isfinite(nv)) atomicOr(p.nonfinite, 1);
                         } else if constexpr (EPI == EPI_PARTIAL) {
