@@ -465,6 +465,13 @@ void apply_a(Context& c, Problem& a, const double* P, int64_t ldp, int64_t k, do
         gemm(c, n, k, n, a.a, n, false, P, ldp, true, Y, ldy, 1.0, 0.0, skip);
         return;
     }
+    if (k > 4096) {  // very wide operand (A·L): thread per (row, column), CSR stays in L2
+        LaunchScope ls(c, "spmm_csr_cols");
+        dim3 grid(unsigned(std::min<int64_t>((n + 255) / 256, 1024)), unsigned(std::min<int64_t>(k, 65535)));
+        spmm_csr_colmajor_kernel<<<grid, 256, 0, c.stream>>>(n, a.rowptr, a.colind, a.val, P, ldp, k, Y, ldy, skip);
+        check_launch("spmm_csr_cols");
+        return;
+    }
     // row-major copy of P so each nonzero reads one contiguous k-row
     double* Pr = c.ensure_ws(size_t(n) * size_t(k));
     {
@@ -784,7 +791,7 @@ void AdaWork::alloc(int64_t n_, int64_t q_, bool gaussian) {
     dmalloc(&R, size_t(q) * size_t(q));
     dmalloc(&Z, size_t(q) * size_t(n));
     dmalloc(&B, size_t(q) * size_t(n));
-    dmalloc(&eig_scratch, 2 * size_t(q) * size_t(q) + 8 * size_t(q) + 16);
+    dmalloc(&eig_scratch, 6 * size_t(q) * size_t(q) + 8 * size_t(q) + 32);
     dmalloc(&idx_dev, size_t(q));
     dmalloc(&pdiag, size_t(n));
     dmalloc(&status, 4);
@@ -821,23 +828,57 @@ void AdaWork::release() {
 }
 
 // R = M^{-1/2} (q×q, ld q) via K-ISQRT + one GEMM; sets status on floor hit.
+// R = M^{-1/2} (q×q, ld q); sets status on a floor hit / non-convergence.
+//   q ≤ 96: K-ISQRT Jacobi in one CTA's shared memory + one GEMM;
+//   q > 96: coupled Newton–Schulz on the DMMA GEMM engine (no host round trip:
+//           converged iterations are skipped on the device).
+// scratch: 6q² + 8q + 32 doubles; status[3] is used as the NS stop flag.
 static void inv_sqrt(Context& c, const double* Mq, int64_t q, double* R, double* scratch, int* status) {
+    if (q > 96) {
+        double* Y = scratch;
+        double* Z = Y + q * q;
+        double* T = Z + q * q;
+        double* ZY = T + q * q;
+        double* Yn = ZY + q * q;
+        double* Zn = Yn + q * q;
+        double* scal = Zn + q * q;
+        int* conv = status + 3;
+        {
+            LaunchScope ls(c, "ns_init");
+            ns_init_kernel<<<1, 1024, 0, c.stream>>>(Mq, q, int(q), Y, Z, scal, status, conv);
+            check_launch("ns_init");
+        }
+        const double tol = 1e-14 * std::sqrt(double(q));
+        for (int it = 0; it < 48; ++it) {
+            gemm(c, q, q, q, Z, q, false, Y, q, true, ZY, q, 1.0, 0.0, conv);  // Z·Y
+            {
+                LaunchScope ls(c, "ns_step");
+                ns_step_kernel<<<1, 1024, 0, c.stream>>>(ZY, int(q), T, scal, conv, tol);
+                check_launch("ns_step");
+            }
+            gemm(c, q, q, q, Y, q, false, T, q, true, Yn, q, 1.0, 0.0, conv);  // Y·T
+            gemm(c, q, q, q, T, q, false, Z, q, true, Zn, q, 1.0, 0.0, conv);  // T·Z
+            LaunchScope ls(c, "ns_copy");
+            ns_copy2_kernel<<<grid_for(q * q, 256), 256, 0, c.stream>>>(Y, Yn, Z, Zn, int(q), conv);
+            check_launch("ns_copy");
+        }
+        LaunchScope ls(c, "ns_finish");
+        ns_finish_kernel<<<grid_for(q * q, 256), 256, 0, c.stream>>>(Z, int(q), scal, R, status, conv);
+        check_launch("ns_finish");
+        return;
+    }
     double* QD = scratch;
     double* Qm = scratch + q * q;
     double* work = scratch + 2 * q * q;
     const size_t smem = (2 * size_t(q) * size_t(q) + 4 * size_t(q)) * sizeof(double);
-    const bool use_smem = smem <= 200 * 1024;
     static bool attr = false;
     if (!attr) {
         CK(cudaFuncSetAttribute(jacobi_isqrt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr = true;
     }
-    double* gwork = nullptr;
-    if (!use_smem) gwork = c.ensure_ws(2 * size_t(q) * size_t(q) + 4 * size_t(q));
     {
         LaunchScope ls(c, "jacobi_isqrt");
-        jacobi_isqrt_kernel<<<1, 1024, use_smem ? smem : 0, c.stream>>>(Mq, q, int(q), QD, Qm, use_smem ? work : gwork,
-                                                                        status, use_smem ? 1 : 0, 1e-14);
+        jacobi_isqrt_kernel<<<1, 1024, smem, c.stream>>>(Mq, q, int(q), QD, Qm, work, status, 1, 1e-14);
         check_launch("jacobi_isqrt");
     }
     gemm(c, q, q, q, QD, q, false, Qm, q, false, R, q, 1.0, 0.0, status);  // R = QD·Qᵀ

@@ -197,6 +197,24 @@ __global__ void spmm_csr_rowmajor_kernel(int64_t n, const int64_t* __restrict__ 
     }
 }
 
+// Column-major SpMM for very wide dense operands (k ≫ 1, e.g. A·L with k = n):
+// thread per (row i, column j); consecutive rows of a banded / stencil A touch
+// consecutive rows of P, so the P loads of a warp coalesce.
+__global__ void spmm_csr_colmajor_kernel(int64_t n, const int64_t* __restrict__ rowptr,
+                                         const int32_t* __restrict__ colind, const double* __restrict__ val,
+                                         const double* __restrict__ P, int64_t ldp, int64_t k, double* __restrict__ Y,
+                                         int64_t ldy, const int* skip) {
+    if (skip && *skip) return;
+    for (int64_t j = blockIdx.y; j < k; j += gridDim.y) {
+        const double* pj = P + j * ldp;
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+            double acc = 0.0;
+            for (int64_t t = rowptr[i]; t < rowptr[i + 1]; ++t) acc += __ldg(val + t) * __ldg(pj + colind[t]);
+            Y[i + j * ldy] = acc;
+        }
+    }
+}
+
 // out (k×n row-major, i.e. Pᵀ col-major) = transpose of P (n×k col-major)
 __global__ void transpose_kernel(const double* __restrict__ P, int64_t n, int64_t k, int64_t ldp,
                                  double* __restrict__ out, const int* skip) {
@@ -239,6 +257,101 @@ __global__ void scatter_coordinate_kernel(double* S, int64_t n, int64_t q, const
     // S = I[:, idx] (n×q, ld n), S zero-initialised by the caller
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < q; j += (int64_t)gridDim.x * blockDim.x)
         S[idx[j] + j * n] = 1.0;
+}
+
+}  // namespace si
+
+namespace si {
+
+// ---- K-ISQRT for larger q: coupled Newton–Schulz iteration (one CTA per small
+// kernel, GEMMs on the DMMA engine in between).  With c = ‖G‖_F:
+//   Y0 = G/c, Z0 = I;  T = (3I − Z·Y)/2;  Y ← Y·T;  Z ← T·Z
+// Y → (G/c)^{1/2}, Z → (G/c)^{-1/2} quadratically; R = Z/√c is the unique
+// symmetric root the reference's Jacobi produces (linalg.cpp:144-155), so L⁺
+// matches it to rounding.  Flags: conv (int) skips the remaining GEMMs once
+// ‖Z·Y − I‖_F ≤ tol; a non-converged or non-finite result sets status (the
+// reference's floor / resample signal).
+__global__ void ns_init_kernel(const double* __restrict__ G, int64_t ldg, int q, double* Y, double* Z, double* scal,
+                               int* status, int* conv) {
+    __shared__ double red[32];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    double s = 0.0;
+    for (int idx = tid; idx < q * q; idx += nt) {
+        const int i = idx % q, j = idx / q;
+        const double v = 0.5 * (G[i + (int64_t)j * ldg] + G[j + (int64_t)i * ldg]);
+        s += v * v;
+    }
+    s = warp_sum(s);
+    if ((tid & 31) == 0) red[tid >> 5] = s;
+    __syncthreads();
+    if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < nt / 32; ++w) t += red[w];
+        scal[0] = sqrt(t);
+        scal[1] = 1e300;  // previous error
+    }
+    __syncthreads();
+    const double c = scal[0];
+    const bool bad = !(c > 0.0) || !isfinite(c) || *status;
+    for (int idx = tid; idx < q * q; idx += nt) {
+        const int i = idx % q, j = idx / q;
+        Y[idx] = bad ? 0.0 : 0.5 * (G[i + (int64_t)j * ldg] + G[j + (int64_t)i * ldg]) / c;
+        Z[idx] = (i == j) ? 1.0 : 0.0;
+    }
+    if (tid == 0) {
+        *conv = bad ? 1 : 0;
+        if (bad) *status = 1;
+    }
+}
+
+// T = (3I − ZY)/2 from Tmp = Z·Y; err = ‖ZY − I‖_F; stop once err ≤ tol or it stagnates
+__global__ void ns_step_kernel(const double* __restrict__ ZY, int q, double* T, double* scal, int* conv, double tol) {
+    __shared__ double red[32];
+    if (*conv) return;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    double s = 0.0;
+    for (int idx = tid; idx < q * q; idx += nt) {
+        const int i = idx % q, j = idx / q;
+        const double d = ZY[idx] - (i == j ? 1.0 : 0.0);
+        s += d * d;
+        T[idx] = (i == j ? 1.5 : 0.0) - 0.5 * ZY[idx];
+    }
+    s = warp_sum(s);
+    if ((tid & 31) == 0) red[tid >> 5] = s;
+    __syncthreads();
+    if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < nt / 32; ++w) t += red[w];
+        const double err = sqrt(t);
+        if (err <= tol || (err < 1e-8 && err >= scal[1])) *conv = 2;  // converged (2: stop after this check)
+        scal[1] = err;
+    }
+}
+
+__global__ void ns_copy2_kernel(double* Y, const double* Yn, double* Z, const double* Zn, int q, const int* conv) {
+    if (*conv) return;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < q * q; idx += gridDim.x * blockDim.x) {
+        Y[idx] = Yn[idx];
+        Z[idx] = Zn[idx];
+    }
+}
+
+// R = Z/√c (symmetrized); failure when the iteration did not converge
+__global__ void ns_finish_kernel(const double* __restrict__ Z, int q, const double* scal, double* R, int* status,
+                                 const int* conv) {
+    if (*status) return;
+    const bool ok = *conv == 2 && scal[1] < 1e-6;
+    if (!ok) {
+        if (threadIdx.x == 0 && blockIdx.x == 0) *status = 1;
+        return;
+    }
+    const double rc = 1.0 / sqrt(scal[0]);
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < q * q; idx += gridDim.x * blockDim.x) {
+        const int i = idx % q, j = idx / q;
+        const double v = 0.5 * (Z[i + j * q] + Z[j + i * q]) * rc;
+        if (!isfinite(v)) *status = 1;
+        R[idx] = v;
+    }
 }
 
 }  // namespace si

@@ -109,7 +109,8 @@ def test_adarbfgs_scalar_fixture_gpu(si):  # test_adarbfgs.cpp:15-23
     assert nxt[0, 0] == pytest.approx(0.5, rel=1e-12)
 
 
-@pytest.mark.parametrize("n,q,gauss", [(6, 2, True), (40, 5, True), (128, 16, False), (200, 64, False)])
+@pytest.mark.parametrize("n,q,gauss", [(6, 2, True), (40, 5, True), (128, 16, False), (200, 64, False),
+                                       (300, 96, False), (320, 128, False), (400, 160, True), (600, 256, False)])
 def test_adarbfgs_update_matches_oracle(si, n, q, gauss):  # test_adarbfgs.cpp:25-35 + oracle
     rng = O.RngStream(73 + n)
     a = random_spd(n, rng)
@@ -300,3 +301,14 @@ def test_csr_problem_matches_dense(si, cfg):
                                         track=si.TrackOptions(residual_every_k=10)))
     ref2 = O.run_adarbfgs(dense, 12, rule=O.ADA_COLS_UNIFORM, tol=0.0, max_iters=30, every_k=10, seed=1)
     assert rel(res2.state.l, ref2.x) <= ITER_TOL
+
+
+def test_adarbfgs_large_q_run_parity(si):
+    """q > 96 takes the Newton–Schulz inverse square root; the run must still match."""
+    rng = O.RngStream(91)
+    n, q = 512, 128
+    a = random_spd(n, rng)
+    ref = O.run_adarbfgs(a, q, rule=O.ADA_COLS_UNIFORM, tol=0.0, max_iters=12, every_k=4, seed=2)
+    res = si.run_adarbfgs(si.AdaConfig(si.ProblemMatrix(a, si.Symmetry.spd), si.SketchRule.adaptive_cols_uniform(q),
+                                       tol=0.0, max_iters=12, seed=2, track=si.TrackOptions(residual_every_k=4)))
+    assert rel(res.state.l, ref.x) <= ITER_TOL
