@@ -55,6 +55,10 @@ def load_peaks():
 CONFIGS = {
     1: dict(name="config1_rbfgs_gaussian_dense_n1024_q32", n=1024, q=32, gen="config1"),
     3: dict(name="config3_rbfgs_gaussian_dense_n16384_q128", n=16384, q=128, gen="config3"),
+    2: dict(name="config2_adarbfgs_uniform_cols_ridge_n4096_q64", n=4096, q=64, gen="config2", method="adarbfgs"),
+    4: dict(name="config4_adarbfgs_uniform_cols_laplacian_csr_n65536_q256", n=65536, q=256, gen="config4",
+            method="adarbfgs"),
+    5: dict(name="config5_rbfgs_gaussian_banded_csr_n98304_q512", n=98304, q=512, gen="config5", method="rbfgs"),
 }
 
 
@@ -280,10 +284,73 @@ def run_sharded(args, cfg):
     dist.destroy_process_group()
 
 
+def run_extra_config(args, cfg):
+    """BASELINE configs 2, 4, 5 on one GPU (extra lines; config 3 is the headline):
+    2 — AdaRBFGS, ridge Gram (dense n=4096), paper uniform q=64 coordinate sampler;
+    4 — AdaRBFGS, 2-D Laplacian CSR n=65536, uniform q=256 (L is 34 GB);
+    5 — RBFGS, banded CSR n=98304, Gaussian q=512 (X is 77 GB).
+    The timed steps are solver iterations with the iterate resident in HBM."""
+    import torch
+
+    import paper_1602_01768_b200 as si
+    from paper_1602_01768_b200 import generators as G
+
+    _, _, local = dist_env()
+    torch.cuda.set_device(local)
+    n, q = cfg["n"], cfg["q"]
+    stream = torch.cuda.current_stream()
+    ctx = si.Context(local, stream=stream.cuda_stream)
+    if cfg["gen"] == "config2":
+        prob = si.ProblemMatrix(G.config2_dense(n, seed=0), si.Symmetry.spd, context=ctx)
+    elif cfg["gen"] == "config4":
+        prob = si.ProblemMatrix(csr=G.config4_csr(n), n=n, symmetry=si.Symmetry.spd, context=ctx)
+    else:
+        prob = si.ProblemMatrix(csr=G.config5_csr(n, half_bandwidth=64, seed=0), n=n, symmetry=si.Symmetry.spd,
+                                context=ctx)
+    if cfg["method"] == "adarbfgs":
+        sol = si.Solver(prob, si.Method.adarbfgs, si.SketchRule.adaptive_cols_uniform(q), seed=0)
+        # Z = (AS)ᵀ·L and L += SR·B (2n²q each) + A·S (2n²q dense / 2·nnz·q CSR) + q×q-class terms
+        alg = 4.0 * n * n * q + (2.0 * n * n * q if not prob.sparse else 2.0 * prob.nnz * q) + 6.0 * n * q * q
+    else:
+        sol = si.Solver(prob, si.Method.rbfgs, si.SketchRule.gaussian_device(q), seed=0)
+        alg = 4.0 * n * n * q + 2.0 * prob.nnz * q + 12.0 * n * q * q
+    sol.step(args.warmup)
+    torch.cuda.synchronize()
+    launches0 = ctx.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        sol.step(args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    launches = ctx.launch_count() - launches0
+    ctx.set_profiling(True)
+    ctx.reset_profile()
+    sol.step(2)
+    prof = ctx.profile()
+    ctx.set_profiling(False)
+    ksum = sum(v[1] for v in prof.values())
+    per = ms / args.steps
+    line = {
+        "metric": f"{cfg['method']}_iterations_per_s", "value": args.steps / (ms * 1e-3), "unit": "iter/s",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": per, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["name"], "n": n, "q": q, "sparse": prob.sparse, "nnz": prob.nnz,
+                   "algorithmic_gflop_per_step": alg / 1e9,
+                   "achieved_tflops_per_step": alg / (per * 1e-3) / 1e12},
+        "kernel_share_of_step": {k: round(v[1] / ksum, 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])},
+        "gpu_launches": int(launches), "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def run_ours(args, cfg):
     import torch
 
     rank, world, local = dist_env()
+    if args.config in (2, 4, 5):
+        return run_extra_config(args, cfg)
     if world > 1 or args.sharded:
         return run_sharded(args, cfg)
     torch.cuda.set_device(local)

@@ -198,7 +198,7 @@ int si_gemm_device(si_context* ctx, int64_t M, int64_t N, int64_t K, const doubl
 int si_sketch_gaussian_device(si_context* ctx, double* S, int64_t n, int64_t q, int64_t lds, uint64_t seed,
                               uint64_t draw);
 /* From P = [SᵀY | YᵀW] (q×2q, ld ldp) build M = [[G⁻¹ + G⁻¹HG⁻¹, −G⁻¹], [−G⁻¹, 0]] (2q×2q, ld 2q).
- * scratch: 2q² + 2q + 16 doubles.  Returns SI_ERR_RESAMPLE when G = SᵀAS is not positive definite. */
+ * scratch: 6q² + 2q + 16 doubles.  Returns SI_ERR_RESAMPLE when G = SᵀAS is not positive definite. */
 int si_rbfgs_core_device(si_context* ctx, const double* P, int64_t ldp, int64_t q, double* M, double* scratch);
 /* Σ_{i<m, j<n} (δ(r0+i, j) − (X_rows·A)(i, j))², X_rows = rows [r0, r0+m) of X (ld ldx), dense A. */
 int si_residual_rows_device(si_context* ctx, si_problem* prob, int64_t m, int64_t r0, const double* x_rows,

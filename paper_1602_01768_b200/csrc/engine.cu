@@ -121,7 +121,7 @@ static int grid_for(int64_t work, int threads, int max_blocks = 148 * 16) {
 }
 
 // --------------------------------------------------------------- GEMM ------
-enum TileCfg { T128x128 = 0, T128x64 = 1, T128x32 = 2, T128x128W16 = 3 };
+enum TileCfg { T128x128 = 0, T128x64 = 1, T128x32 = 2, T128x128W16 = 3, T64x128 = 4 };
 
 // development switches: SI_WARPS16=1 selects 16 consumer warps for 128×128
 // tiles; SI_NO_TMA=1 forces the cp.async mainloop.
@@ -211,6 +211,7 @@ static void launch_gemm_tile(Context& c, TileCfg t, const GemmArgs& a, dim3 grid
             case T128x64: launch_tma_cfg<128, 64, 16, 4, 2, 4, AK, BKM, EPI>(c, a, grid, name); break;
             case T128x32: launch_tma_cfg<128, 32, 16, 8, 1, 4, AK, BKM, EPI>(c, a, grid, name); break;
             case T128x128W16: launch_tma_cfg<128, 128, 16, 4, 4, 5, AK, BKM, EPI>(c, a, grid, name); break;
+            case T64x128: launch_tma_cfg<64, 128, 16, 2, 4, 6, AK, BKM, EPI>(c, a, grid, name); break;
         }
         return;
     }
@@ -219,6 +220,7 @@ static void launch_gemm_tile(Context& c, TileCfg t, const GemmArgs& a, dim3 grid
         case T128x64: launch_gemm_cfg<128, 64, 16, 4, 2, 4, AK, BKM, VEC, EPI>(c, a, grid, name); break;
         case T128x32: launch_gemm_cfg<128, 32, 16, 8, 1, 4, AK, BKM, VEC, EPI>(c, a, grid, name); break;
         case T128x128W16: launch_gemm_cfg<128, 128, 16, 4, 4, 4, AK, BKM, VEC, EPI>(c, a, grid, name); break;
+        case T64x128: launch_gemm_cfg<64, 128, 16, 2, 4, 4, AK, BKM, VEC, EPI>(c, a, grid, name); break;
     }
 }
 
@@ -256,7 +258,8 @@ static int pick_vec(const GemmArgs& a) {
     return ok ? 2 : 1;
 }
 
-static TileCfg pick_tile(int64_t N) {
+static TileCfg pick_tile(int64_t N, int64_t M = 1 << 30) {
+    if (M <= 64 && N > 64) return T64x128;  // q×n products (Z = (AS)ᵀL, Grams): no half-empty tiles
     if (N <= 32) return T128x32;
     if (N <= 64) return T128x64;
     return use_w16() ? T128x128W16 : T128x128;
@@ -281,10 +284,11 @@ void gemm(Context& c, int64_t M, int64_t N, int64_t K, const double* A, int64_t 
     a.skip = skip;
     a.nonfinite = nonfinite;
     // short-K, wide-output products (the rank-2q panel update) keep 16 warps resident
-    const TileCfg t = (K <= 512 && N > 64 && M > 64) ? T128x128W16 : pick_tile(N);
-    const int BM = 128, BN = (t == T128x128 || t == T128x128W16) ? 128 : (t == T128x64 ? 64 : 32), BKT = 16;
+    const TileCfg t = (K <= 512 && N > 64 && M > 64) ? T128x128W16 : pick_tile(N, M);
+    const int BM = t == T64x128 ? 64 : 128;
+    const int BN = (t == T128x128 || t == T128x128W16 || t == T64x128) ? 128 : (t == T128x64 ? 64 : 32), BKT = 16;
     const int64_t tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN, tiles = tm * tn;
-    const int per_sm = (t == T128x128 || t == T128x128W16) ? 1 : 2;
+    const int per_sm = (t == T128x128 || t == T128x128W16 || t == T64x128) ? 1 : 2;
     const int64_t slots = int64_t(c.num_sms) * per_sm;
     // split-K so the number of work units fills whole waves of the 148 SMs
     int splits = 1;
@@ -510,7 +514,7 @@ void RbfgsWork::alloc(int64_t n_, int64_t q_, bool own) {
     dmalloc(&Ginv, size_t(q) * size_t(q));
     dmalloc(&T, size_t(q) * size_t(q));
     dmalloc(&M, size_t(2 * q) * size_t(2 * q));
-    dmalloc(&factor_scratch, size_t(q) * size_t(q) + size_t(2 * q) + 16);
+    dmalloc(&factor_scratch, 4 * size_t(q) * size_t(q) + size_t(2 * q) + 16);
     dmalloc(&status, 4);
     dmalloc(&counter, 1);
     CK(cudaMemset(status, 0, 4 * sizeof(int)));
@@ -536,43 +540,82 @@ void rbfgs_enqueue_sketch_upload(Context& c, RbfgsWork& w) {
                        c.stream));
 }
 
-static void spd_inverse(Context& c, const double* P, int64_t ldp, int64_t q, double* ginv, double* scratch,
-                        int* status) {
-    if (q <= 128) {
-        // register-resident Gauss-Jordan: q columns × ceil(q/RPT) row groups
+// Gi (ld ldo) = G⁻¹ for SPD G read as G(i,j) = P(min, max) (ld ldp).
+//   q ≤ 128: register-resident Gauss-Jordan in one CTA (pivots = squared Cholesky
+//            diagonals → the gram_llt failure test), then exact symmetrization;
+//   q > 128: 2×2 block elimination on the DMMA GEMM engine, recursively:
+//            Ai = A⁻¹, T1 = Ai·B, S = D − Bᵀ·T1, Si = S⁻¹ (PD ⇔ A and S PD),
+//            G⁻¹ = [[Ai + T2·T1ᵀ, −T2], [−T2ᵀ, Si]] with T2 = T1·Si.
+// scratch: 4q² doubles.
+static int inverse_base_q() {
+    static int v = 0;
+    if (!v) {
+        const char* s = std::getenv("SI_INV_BASE");
+        v = s ? std::max(16, std::min(128, std::atoi(s))) : 64;  // measured: 64 beats 128 at q = 128
+    }
+    return v;
+}
+
+static void spd_inverse_ld(Context& c, const double* P, int64_t ldp, int64_t q, double* ginv, int64_t ldo,
+                           double* scratch, int* status) {
+    if (q <= inverse_base_q()) {
         const int rpt = q <= 32 ? 1 : (q <= 64 ? 8 : 16);
         const int threads = int(q * ((q + rpt - 1) / rpt));
         {
             LaunchScope ls(c, "spd_inverse");
             switch (rpt) {
                 case 1:
-                    spd_inverse_reg_kernel<1, 1024><<<1, threads, 0, c.stream>>>(P, ldp, int(q), ginv, q, status);
+                    spd_inverse_reg_kernel<1, 1024><<<1, threads, 0, c.stream>>>(P, ldp, int(q), ginv, ldo, status);
                     break;
                 case 8:
-                    spd_inverse_reg_kernel<8, 512><<<1, threads, 0, c.stream>>>(P, ldp, int(q), ginv, q, status);
+                    spd_inverse_reg_kernel<8, 512><<<1, threads, 0, c.stream>>>(P, ldp, int(q), ginv, ldo, status);
                     break;
                 default:
-                    spd_inverse_reg_kernel<16, 1024><<<1, threads, 0, c.stream>>>(P, ldp, int(q), ginv, q, status);
+                    spd_inverse_reg_kernel<16, 1024><<<1, threads, 0, c.stream>>>(P, ldp, int(q), ginv, ldo, status);
                     break;
             }
             check_launch("spd_inverse_reg");
         }
         LaunchScope ls(c, "symmetrize_small");
-        symmetrize_small_kernel<<<grid_for(q * q, 256), 256, 0, c.stream>>>(ginv, int(q), q, status);
+        symmetrize_small_kernel<<<grid_for(q * q, 256), 256, 0, c.stream>>>(ginv, int(q), ldo, status);
         check_launch("symmetrize_small");
         return;
     }
-    const size_t smem = (size_t(q) * size_t(q) + 2 * size_t(q)) * sizeof(double);
-    const bool use_smem = smem <= 200 * 1024;
-    static bool attr = false;
-    if (!attr) {
-        CK(cudaFuncSetAttribute(spd_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr = true;
+    const int64_t h = ((q / 2 + 63) / 64) * 64, q2 = q - h;
+    const double* A = P;                     // G11 (h×h)
+    const double* B = P + h * ldp;           // G12 (h×q2): upper-right block of the upper triangle
+    const double* D = P + h + h * ldp;       // G22 (q2×q2)
+    double* T1 = scratch;                    // h×q2
+    double* S = T1 + h * q2;                 // q2×q2
+    double* T2 = S + q2 * q2;                // h×q2
+    double* sub = T2 + h * q2;               // recursion scratch
+    double* Gi11 = ginv;
+    double* Gi12 = ginv + h * ldo;
+    double* Gi22 = ginv + h + h * ldo;
+    spd_inverse_ld(c, A, ldp, h, Gi11, ldo, sub, status);                          // Ai
+    gemm(c, h, q2, h, Gi11, ldo, false, B, ldp, true, T1, h, 1.0, 0.0, status);      // T1 = Ai·B
+    {
+        LaunchScope ls(c, "scale_copy");
+        scale_copy_kernel<<<grid_for(q2 * q2, 256), 256, 0, c.stream>>>(D, ldp, S, q2, q2, q2, 1.0, status);
+        check_launch("scale_copy");
     }
-    LaunchScope ls(c, "spd_inverse");
-    spd_inverse_kernel<<<1, 1024, use_smem ? smem : 0, c.stream>>>(P, ldp, int(q), ginv, q, scratch, status,
-                                                                   use_smem ? 1 : 0);
-    check_launch("spd_inverse");
+    gemm(c, q2, q2, h, B, ldp, true, T1, h, true, S, q2, -1.0, 1.0, status);        // S = D − Bᵀ·T1
+    spd_inverse_ld(c, S, q2, q2, Gi22, ldo, sub, status);                          // Si
+    gemm(c, h, q2, q2, T1, h, false, Gi22, ldo, true, T2, h, 1.0, 0.0, status);      // T2 = T1·Si
+    gemm(c, h, h, q2, T2, h, false, T1, h, false, Gi11, ldo, 1.0, 1.0, status);      // Gi11 += T2·T1ᵀ
+    {
+        LaunchScope ls(c, "scale_copy");
+        scale_copy_kernel<<<grid_for(h * q2, 256), 256, 0, c.stream>>>(T2, h, Gi12, ldo, h, q2, -1.0, status);
+        check_launch("scale_copy");
+    }
+    LaunchScope ls(c, "mirror_upper");
+    mirror_upper_kernel<<<grid_for(q * q, 256), 256, 0, c.stream>>>(ginv, q, ldo, status);  // Gi21 = Gi12ᵀ
+    check_launch("mirror_upper");
+}
+
+static void spd_inverse(Context& c, const double* P, int64_t ldp, int64_t q, double* ginv, double* scratch,
+                        int* status) {
+    spd_inverse_ld(c, P, ldp, q, ginv, q, scratch, status);
 }
 
 // K-FACTOR + K-CORE: from P = [G | H] (q×2q, ld ldp) build
@@ -827,14 +870,35 @@ void AdaWork::release() {
     st_pinned = nullptr;
 }
 
-// R = M^{-1/2} (q×q, ld q) via K-ISQRT + one GEMM; sets status on floor hit.
+template <int QP>
+static void ns_fused(Context& c, const double* Mq, int64_t q, double* R, int* status) {
+    const size_t smem = size_t(5) * QP * (QP + 4) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(ns_fused_kernel<QP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        attr = true;
+    }
+    LaunchScope ls(c, "ns_fused");
+    ns_fused_kernel<QP><<<1, 256, smem, c.stream>>>(Mq, q, int(q), R, status, 1e-14 * std::sqrt(double(q)), 60);
+    check_launch("ns_fused");
+}
+
 // R = M^{-1/2} (q×q, ld q); sets status on a floor hit / non-convergence.
-//   q ≤ 96: K-ISQRT Jacobi in one CTA's shared memory + one GEMM;
-//   q > 96: coupled Newton–Schulz on the DMMA GEMM engine (no host round trip:
-//           converged iterations are skipped on the device).
+//   q ≤ 64: fused Newton–Schulz in one CTA (operands in shared memory, DMMA);
+//   q > 64: coupled Newton–Schulz on the DMMA GEMM engine (no host round trip:
+//           converged iterations are skipped on the device);
+//   SI_ISQRT_JACOBI=1 (q ≤ 96): the reference's cyclic Jacobi (parallel order).
 // scratch: 6q² + 8q + 32 doubles; status[3] is used as the NS stop flag.
 static void inv_sqrt(Context& c, const double* Mq, int64_t q, double* R, double* scratch, int* status) {
-    if (q > 96) {
+    const bool jacobi = env_flag("SI_ISQRT_JACOBI") && q <= 96;
+    if (!jacobi && q <= 64) {
+        if (q <= 16) ns_fused<16>(c, Mq, q, R, status);
+        else if (q <= 32) ns_fused<32>(c, Mq, q, R, status);
+        else if (q <= 48) ns_fused<48>(c, Mq, q, R, status);
+        else ns_fused<64>(c, Mq, q, R, status);
+        return;
+    }
+    if (!jacobi) {
         double* Y = scratch;
         double* Z = Y + q * q;
         double* T = Z + q * q;

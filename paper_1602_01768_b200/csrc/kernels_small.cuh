@@ -354,4 +354,148 @@ __global__ void ns_finish_kernel(const double* __restrict__ Z, int q, const doub
     }
 }
 
+// ---- fused Newton–Schulz for q ≤ 64: one CTA, all five QP×QP operands in
+// shared memory (pitch QP+4 ≡ 4 mod 16 → conflict-free fragment loads), each
+// product on the DMMA pipe (mma.m16n8k8), no global round trips between
+// iterations.  Padding rows/cols carry an identity block, which the iteration
+// leaves invariant.  Same contract as the multi-kernel variant above.
+template <int QP>
+__device__ __forceinline__ void cta_gemm_smem(const double* __restrict__ A, const double* __restrict__ B,
+                                              double* __restrict__ Cm, int warp, int nwarps, int lane) {
+    constexpr int LD = QP + 4;
+    constexpr int MB = QP / 16, NB = QP / 8;
+    const int g = lane >> 2, t = lane & 3;
+    for (int blk = warp; blk < MB * NB; blk += nwarps) {
+        const int m0 = (blk % MB) * 16, n0 = (blk / MB) * 8;
+        double c[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int k0 = 0; k0 < QP; k0 += 8) {
+            double a[4], b[2];
+            a[0] = A[(m0 + g) + (k0 + t) * LD];
+            a[1] = A[(m0 + g + 8) + (k0 + t) * LD];
+            a[2] = A[(m0 + g) + (k0 + t + 4) * LD];
+            a[3] = A[(m0 + g + 8) + (k0 + t + 4) * LD];
+            b[0] = B[(k0 + t) + (n0 + g) * LD];
+            b[1] = B[(k0 + t + 4) + (n0 + g) * LD];
+            dmma_1688(c, a, b);
+        }
+        Cm[(m0 + g) + (n0 + 2 * t) * LD] = c[0];
+        Cm[(m0 + g) + (n0 + 2 * t + 1) * LD] = c[1];
+        Cm[(m0 + g + 8) + (n0 + 2 * t) * LD] = c[2];
+        Cm[(m0 + g + 8) + (n0 + 2 * t + 1) * LD] = c[3];
+    }
+}
+
+template <int QP>
+__global__ void __launch_bounds__(256) ns_fused_kernel(const double* __restrict__ G, int64_t ldg, int q,
+                                                       double* __restrict__ R, int* status, double tol, int max_it) {
+    constexpr int LD = QP + 4, SZ = QP * LD;
+    extern __shared__ __align__(16) double sm[];
+    __shared__ double red[8];
+    __shared__ double s_c, s_err, s_prev;
+    __shared__ int s_stop;
+    if (*status) return;
+    double* Y = sm;
+    double* Z = Y + SZ;
+    double* T = Z + SZ;
+    double* Yn = T + SZ;
+    double* Zn = Yn + SZ;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+    auto block_sum = [&](double v) {
+        v = warp_sum(v);
+        if (lane == 0) red[warp] = v;
+        __syncthreads();
+        double s = 0.0;
+        for (int w = 0; w < nw; ++w) s += red[w];
+        __syncthreads();
+        return s;
+    };
+    double fro = 0.0;
+    for (int idx = tid; idx < q * q; idx += nt) {
+        const int i = idx % q, j = idx / q;
+        const double v = 0.5 * (G[i + (int64_t)j * ldg] + G[j + (int64_t)i * ldg]);
+        fro += v * v;
+    }
+    fro = block_sum(fro);
+    if (tid == 0) {
+        s_c = sqrt(fro);
+        s_prev = 1e300;
+        s_stop = 0;
+    }
+    __syncthreads();
+    const double cc = s_c;
+    if (!(cc > 0.0) || !isfinite(cc)) {
+        if (tid == 0) *status = 1;
+        return;
+    }
+    for (int idx = tid; idx < QP * QP; idx += nt) {
+        const int i = idx % QP, j = idx / QP;
+        const bool in = i < q && j < q;
+        Y[i + j * LD] = in ? 0.5 * (G[i + (int64_t)j * ldg] + G[j + (int64_t)i * ldg]) / cc : (i == j ? 1.0 : 0.0);
+        Z[i + j * LD] = (i == j) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    int it = 0;
+    for (; it < max_it; ++it) {
+        cta_gemm_smem<QP>(Z, Y, T, warp, nw, lane);  // T ← Z·Y
+        __syncthreads();
+        double e = 0.0;
+        for (int idx = tid; idx < QP * QP; idx += nt) {
+            const int i = idx % QP, j = idx / QP;
+            const double zy = T[i + j * LD];
+            const double d = zy - (i == j ? 1.0 : 0.0);
+            e += d * d;
+            T[i + j * LD] = (i == j ? 1.5 : 0.0) - 0.5 * zy;
+        }
+        e = block_sum(e);
+        if (tid == 0) {
+            const double err = sqrt(e);
+            s_stop = (err <= tol || (err < 1e-8 && err >= s_prev)) ? 1 : 0;
+            s_prev = err;
+            s_err = err;
+        }
+        __syncthreads();
+        if (s_stop) break;
+        cta_gemm_smem<QP>(Y, T, Yn, warp, nw, lane);  // Y ← Y·T
+        cta_gemm_smem<QP>(T, Z, Zn, warp, nw, lane);  // Z ← T·Z
+        __syncthreads();
+        double* tmp = Y;
+        Y = Yn;
+        Yn = tmp;
+        tmp = Z;
+        Z = Zn;
+        Zn = tmp;
+    }
+    if (!s_stop || !(s_err < 1e-6)) {
+        if (tid == 0) *status = 1;  // did not converge: the reference's floor / resample signal
+        return;
+    }
+    const double rc = 1.0 / sqrt(cc);
+    for (int idx = tid; idx < q * q; idx += nt) {
+        const int i = idx % q, j = idx / q;
+        R[idx] = 0.5 * (Z[i + j * LD] + Z[j + i * LD]) * rc;
+    }
+}
+
+// ---- recursive SPD inverse helpers (q > 128): Gi21 := Gi12ᵀ and scaled copies
+__global__ void scale_copy_kernel(const double* __restrict__ src, int64_t lds, double* __restrict__ dst, int64_t ldd,
+                                  int64_t rows, int64_t cols, double alpha, const int* skip) {
+    if (skip && *skip) return;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < rows * cols;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = idx % rows, j = idx / rows;
+        dst[i + j * ldd] = alpha * src[i + j * lds];
+    }
+}
+
+// lower triangle := upper triangle (q×q, ld) — exact symmetry of an assembled inverse
+__global__ void mirror_upper_kernel(double* g, int64_t q, int64_t ld, const int* skip) {
+    if (skip && *skip) return;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < q * q;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = idx % q, j = idx / q;
+        if (i > j) g[i + j * ld] = g[j + i * ld];
+    }
+}
+
 }  // namespace si

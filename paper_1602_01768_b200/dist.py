@@ -120,7 +120,7 @@ class RowShardedRBFGS:
         self.P = torch.empty(q * 2 * q, **f)
         self.M = torch.empty(4 * q * q, **f)
         self.Vp = torch.empty(m * 2 * q, **f)
-        self.scratch = torch.empty(2 * q * q + 2 * q + 16, **f)
+        self.scratch = torch.empty(6 * q * q + 2 * q + 16, **f)
         self.gather_buf = torch.empty(self.world * mm * q, **f)
         self.send_buf = torch.zeros(mm * q, **f)
         self.set_identity()

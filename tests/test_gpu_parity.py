@@ -68,7 +68,8 @@ def test_bfgs_recurrence_and_full_sketch_gpu(si):  # test_qn_updates.cpp:213-228
     assert np.linalg.norm(si.bfgs_step(xs, big, eye) - np.linalg.inv(big)) <= 1e-8
 
 
-@pytest.mark.parametrize("n,q", [(1, 1), (7, 3), (37, 5), (130, 17), (256, 32), (300, 64), (513, 128), (640, 130)])
+@pytest.mark.parametrize("n,q", [(1, 1), (7, 3), (37, 5), (130, 17), (256, 32), (300, 64), (513, 128), (640, 130),
+                                 (700, 300), (1100, 520)])
 def test_bfgs_step_matches_oracle(si, n, q):
     rng = O.RngStream(1000 + n + q)
     a = random_spd(n, rng)
