@@ -134,6 +134,24 @@ int64_t si_problem_n(si_problem* prob);
 int si_problem_validate_spd(si_problem* prob);
 /* Copy A (dense or densified CSR) to host, n×n column-major. */
 int si_problem_get_dense(si_problem* prob, double* a_host);
+/* ProblemMatrix load_matrix_market(path), io.hpp:14 / io.cpp:28-121 (same checks and messages,
+ * SI_ERR_IO on parse errors).  symmetry < 0 takes the header's (general / symmetric); coordinate
+ * files stay sparse (CSR) when keep_sparse != 0 instead of being densified (io.cpp:72). */
+int si_problem_load_matrix_market(si_context* ctx, const char* path, int symmetry, int keep_sparse,
+                                  si_problem** out);
+/* ProblemMatrix build_ridge_hessian(path, lambda), io.hpp:19 / io.cpp:123-166: A = BᵀB + λI from a
+ * LIBSVM file, the product on the GPU; SPD-flagged when λ > 0. */
+int si_problem_ridge_hessian(si_context* ctx, const char* libsvm_path, double lambda, si_problem** out);
+/* ProblemMatrix gen_synthetic(n, seed), io.hpp:23 / io.cpp:168-171: A = ĀᵀĀ, Ā ~ U(0,1) from RngStream(seed). */
+int si_problem_synthetic(si_context* ctx, int64_t n, uint64_t seed, si_problem** out);
+/* Host-side parse only (no device work): the same reader and error texts as
+ * si_problem_load_matrix_market.  info: n, header symmetry, stored entries after
+ * mirroring/deduplication.  dense: the n×n column-major matrix the reference's
+ * load_matrix_market(path).data() holds. */
+int si_io_matrix_market_info(const char* path, int64_t* n, int* symmetric, int64_t* stored);
+int si_io_matrix_market_dense(const char* path, double* out_colmajor);
+/* LIBSVM scan (io.cpp:128-161): sample and feature counts, SI_ERR_IO on the reference's errors. */
+int si_io_libsvm_info(const char* path, int64_t* samples, int64_t* features);
 
 /* ---- step-level drop-ins (host buffers, reference semantics) ----------- */
 /* Matrix bfgs_step(const Matrix& x, const Matrix& a, const Matrix& s), qn_updates.hpp:70.

@@ -35,10 +35,15 @@ from .api import (  # noqa: E402
     adaptive_block_probabilities,
     adarbfgs_update_factor,
     bfgs_step,
+    build_ridge_hessian,
     contiguous_partition,
     default_context,
     flops_adarbfgs,
     flops_bfgs,
+    gen_synthetic,
+    libsvm_shape,
+    load_matrix_market,
+    read_matrix_market,
     residual,
     run_adarbfgs,
     run_inverter,

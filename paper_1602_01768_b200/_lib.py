@@ -56,6 +56,12 @@ _SIGS = {
     "si_problem_n": (i64, [vp]),
     "si_problem_validate_spd": (ci, [vp]),
     "si_problem_get_dense": (ci, [vp, pd]),
+    "si_problem_load_matrix_market": (ci, [vp, C.c_char_p, ci, ci, C.POINTER(vp)]),
+    "si_problem_ridge_hessian": (ci, [vp, C.c_char_p, d, C.POINTER(vp)]),
+    "si_problem_synthetic": (ci, [vp, i64, u64, C.POINTER(vp)]),
+    "si_io_matrix_market_info": (ci, [C.c_char_p, pi64, C.POINTER(ci), pi64]),
+    "si_io_matrix_market_dense": (ci, [C.c_char_p, pd]),
+    "si_io_libsvm_info": (ci, [C.c_char_p, pi64, pi64]),
     "si_bfgs_step": (ci, [vp, i64, i64, pd, pd, pd, pd]),
     "si_bfgs_step_problem": (ci, [vp, vp, i64, pd, pd, pd]),
     "si_adarbfgs_update_factor": (ci, [vp, i64, i64, pd, pd, pd, pd]),

@@ -219,6 +219,67 @@ class ProblemMatrix:
             pass
 
 
+def _problem_from_handle(h, ctx, symmetry) -> ProblemMatrix:
+    pm = ProblemMatrix.__new__(ProblemMatrix)
+    pm.ctx = ctx
+    pm._h = h
+    pm._n = int(L.load().si_problem_n(h))
+    pm.symmetry = Symmetry(symmetry)
+    pm.sparse = L.load().si_problem_dense_device(h) is None
+    pm.nnz = pm._n * pm._n if not pm.sparse else -1
+    return pm
+
+
+def load_matrix_market(path: str, symmetry: Optional[Symmetry] = None, keep_sparse: bool = True,
+                       context: Optional[Context] = None) -> ProblemMatrix:
+    """ProblemMatrix load_matrix_market(path) (io.hpp:14): header checks, line-numbered
+    IoError; coordinate files stay CSR when keep_sparse (the reference densifies)."""
+    ctx = context or default_context()
+    h = C.c_void_p()
+    sym = -1 if symmetry is None else int(symmetry)
+    _check(L.load().si_problem_load_matrix_market(ctx.handle, str(path).encode(), sym, 1 if keep_sparse else 0,
+                                                  C.byref(h)))
+    if symmetry is None:
+        # the header decides (general / symmetric); read it back from the file banner
+        with open(path) as f:
+            symmetry = Symmetry.symmetric if "symmetric" in f.readline().lower() else Symmetry.general
+    return _problem_from_handle(h, ctx, symmetry)
+
+
+def build_ridge_hessian(path: str, lam: float, context: Optional[Context] = None) -> ProblemMatrix:
+    """ProblemMatrix build_ridge_hessian(path, lambda) (io.hpp:19): BᵀB + λI on the GPU."""
+    ctx = context or default_context()
+    h = C.c_void_p()
+    _check(L.load().si_problem_ridge_hessian(ctx.handle, str(path).encode(), float(lam), C.byref(h)))
+    return _problem_from_handle(h, ctx, Symmetry.spd if lam > 0 else Symmetry.symmetric)
+
+
+def gen_synthetic(n: int, seed: int = 0, context: Optional[Context] = None) -> ProblemMatrix:
+    """ProblemMatrix gen_synthetic(n, seed) (io.hpp:23): ĀᵀĀ with Ā ~ U(0,1) from RngStream(seed)."""
+    ctx = context or default_context()
+    h = C.c_void_p()
+    _check(L.load().si_problem_synthetic(ctx.handle, int(n), C.c_uint64(seed), C.byref(h)))
+    return _problem_from_handle(h, ctx, Symmetry.spd)
+
+
+def read_matrix_market(path: str) -> tuple[np.ndarray, bool]:
+    """Host parse of a MatrixMarket file: (dense n×n, header-symmetric) — what the
+    reference's load_matrix_market(path).data() holds (io.cpp:28-121), no device work."""
+    lib = L.load()
+    n, sym, stored = C.c_int64(), C.c_int(), C.c_int64()
+    _check(lib.si_io_matrix_market_info(str(path).encode(), C.byref(n), C.byref(sym), C.byref(stored)))
+    out = np.zeros((n.value, n.value), dtype=np.float64, order="F")
+    _check(lib.si_io_matrix_market_dense(str(path).encode(), _pd(out)))
+    return out, bool(sym.value)
+
+
+def libsvm_shape(path: str) -> tuple[int, int]:
+    """(samples, features) of a LIBSVM file, with the reference's parse errors (io.cpp:128-161)."""
+    m, n = C.c_int64(), C.c_int64()
+    _check(L.load().si_io_libsvm_info(str(path).encode(), C.byref(m), C.byref(n)))
+    return m.value, n.value
+
+
 def contiguous_partition(n: int, q: int) -> list[list[int]]:  # sketching.cpp:106-115
     if q < 1 or q > n:
         raise ConfigError("contiguous_partition: need 1 <= q <= n")

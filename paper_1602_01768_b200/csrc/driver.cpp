@@ -44,6 +44,9 @@ int guard(F&& f) {
     } catch (const NumericalError& e) {
         g_err = e.what();
         return SI_ERR_NUMERICAL;
+    } catch (const si::IoError& e) {  // errors.hpp:24-26 (CLI exit 4)
+        g_err = e.what();
+        return SI_ERR_IO;
     } catch (const si::CudaError& e) {
         g_err = e.what();
         return SI_ERR_CUDA;
@@ -1011,6 +1014,76 @@ int si_residual_rows_device(si_context* ctx, si_problem* prob, int64_t m, int64_
 }
 
 const double* si_problem_dense_device(si_problem* prob) { return prob->p->dense ? prob->p->a : nullptr; }
+
+// ------------------------------------------------------------ ingestion ---
+int si_problem_load_matrix_market(si_context* ctx, const char* path, int symmetry, int keep_sparse,
+                                  si_problem** out) {
+    return guard([&] {
+        const si::LoadedMatrix m = si::load_matrix_market(path, keep_sparse != 0);
+        const int sym = symmetry >= 0 ? symmetry : (m.symmetric ? SI_SYMMETRIC : SI_GENERAL);
+        std::unique_ptr<si_problem> h(new_problem(ctx, m.n, sym));
+        if (m.sparse) {
+            h->p->nnz = int64_t(m.val.size());
+            si::problem_upload_csr(*h->p, m.rowptr.data(), m.colind.data(), m.val.data());
+        } else {
+            si::problem_upload_dense(*h->p, m.dense.data(), false);
+        }
+        *out = h.release();
+    });
+}
+
+int si_problem_ridge_hessian(si_context* ctx, const char* libsvm_path, double lambda, si_problem** out) {
+    return guard([&] {
+        require(lambda >= 0.0, "build_ridge_hessian: lambda must be >= 0");
+        const si::LibsvmRows rows = si::read_libsvm(libsvm_path);
+        double* a = si::ridge_hessian_device(*ctx->c, rows, lambda);
+        struct Free {
+            double* p;
+            ~Free() { cudaFree(p); }
+        } f{a};
+        std::unique_ptr<si_problem> h(new_problem(ctx, rows.n, lambda > 0.0 ? SI_SPD : SI_SYMMETRIC));
+        si::problem_upload_dense(*h->p, a, true);
+        *out = h.release();
+    });
+}
+
+int si_problem_synthetic(si_context* ctx, int64_t n, uint64_t seed, si_problem** out) {
+    return guard([&] {
+        if (n < 2) throw ConfigError("gen_synthetic: n must be >= 2");
+        double* a = si::synthetic_device(*ctx->c, n, seed);
+        struct Free {
+            double* p;
+            ~Free() { cudaFree(p); }
+        } f{a};
+        std::unique_ptr<si_problem> h(new_problem(ctx, n, SI_SPD));
+        si::problem_upload_dense(*h->p, a, true);
+        *out = h.release();
+    });
+}
+
+int si_io_matrix_market_info(const char* path, int64_t* n, int* symmetric, int64_t* stored) {
+    return guard([&] {
+        const si::LoadedMatrix m = si::load_matrix_market(path, true);
+        if (n) *n = m.n;
+        if (symmetric) *symmetric = m.symmetric ? 1 : 0;
+        if (stored) *stored = m.sparse ? int64_t(m.val.size()) : m.n * m.n;
+    });
+}
+
+int si_io_matrix_market_dense(const char* path, double* out_colmajor) {
+    return guard([&] {
+        const si::LoadedMatrix m = si::load_matrix_market(path, false);
+        std::copy(m.dense.begin(), m.dense.end(), out_colmajor);
+    });
+}
+
+int si_io_libsvm_info(const char* path, int64_t* samples, int64_t* features) {
+    return guard([&] {
+        const si::LibsvmRows r = si::read_libsvm(path);
+        if (samples) *samples = r.m;
+        if (features) *features = r.n;
+    });
+}
 
 // ---------------------------------------------------------------- rng ------
 struct si_rng {

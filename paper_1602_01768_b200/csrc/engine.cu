@@ -183,12 +183,23 @@ static void make_tmap(CUtensorMap* m, const double* base, int64_t inner, int64_t
 template <int BM, int BN, int BK, int WM, int WN, int ST, bool AK, bool BKM, int EPI>
 static void launch_tma_cfg(Context& c, const GemmArgs& a, dim3 grid, const char* name) {
     using SM = GemmSmem<BM, BN, BK, WM, WN, ST, AK, BKM>;
-    auto kern = gemm_tma_kernel<BM, BN, BK, WM, WN, ST, AK, BKM, EPI>;
+    // Short-K products (the rank-2q updates) run persistent — one CTA per resident
+    // slot striding over the work items, so the next tile's TMA stages stream in
+    // under the current tile's epilogue; long-K products keep one CTA per item
+    // (measured faster: their fill is amortised over >= 100 k-stages).
+    const bool persist = EPI == EPI_SYMUPD || a.K <= 1024;
+    auto kern_p = gemm_tma_persistent_kernel<BM, BN, BK, WM, WN, ST, AK, BKM, EPI>;
+    auto kern_g = gemm_tma_kernel<BM, BN, BK, WM, WN, ST, AK, BKM, EPI>;
     static bool attr_set = false;
+    static int per_sm = 1;
     if (!attr_set) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SM::TMA_BYTES)));
+        CK(cudaFuncSetAttribute(kern_p, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SM::TMA_BYTES)));
+        CK(cudaFuncSetAttribute(kern_g, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SM::TMA_BYTES)));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern_p, WM * WN * 32, SM::TMA_BYTES));
+        per_sm = std::max(per_sm, 1);
         attr_set = true;
     }
+    const int64_t work = int64_t(grid.x) * grid.y * grid.z;
     CUtensorMap ta, tb;
     if (AK)
         make_tmap(&ta, a.A, a.K, a.M, a.lda, BK + 4, BM);
@@ -199,7 +210,11 @@ static void launch_tma_cfg(Context& c, const GemmArgs& a, dim3 grid, const char*
     else
         make_tmap(&tb, a.B, a.N, a.K, a.ldb, BN + 4, BK);
     LaunchScope ls(c, name);
-    kern<<<grid, WM * WN * 32, SM::TMA_BYTES, c.stream>>>(ta, tb, a);
+    if (persist)
+        kern_p<<<unsigned(std::min<int64_t>(work, int64_t(c.num_sms) * per_sm)), WM * WN * 32, SM::TMA_BYTES,
+                 c.stream>>>(ta, tb, a);
+    else
+        kern_g<<<grid, WM * WN * 32, SM::TMA_BYTES, c.stream>>>(ta, tb, a);
     check_launch(name);
 }
 

@@ -151,4 +151,26 @@ void ada_enqueue_update(Context& c, Problem& a, AdaWork& w, int mode /*0 cols id
                         uint64_t seed);
 void ada_enqueue_probabilities(Context& c, Problem& a, AdaWork& w);  // pdiag = diag(LᵀAL) -> p_pinned (async)
 
+// ---- ingestion (io.cpp) --------------------------------
+struct IoError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct LoadedMatrix {
+    int64_t n = 0;
+    bool symmetric = false;
+    bool sparse = false;
+    std::vector<double> dense;  // column-major n×n (array format, or coordinate with keep_sparse = false)
+    std::vector<int64_t> rowptr;
+    std::vector<int32_t> colind;
+    std::vector<double> val;
+};
+LoadedMatrix load_matrix_market(const std::string& path, bool keep_sparse);  // io.cpp:28-121
+struct LibsvmRows {
+    int64_t n = 0, m = 0;
+    std::vector<std::vector<std::pair<int64_t, double>>> samples;
+};
+LibsvmRows read_libsvm(const std::string& path);                          // io.cpp:123-157
+double* ridge_hessian_device(Context& c, const LibsvmRows& r, double lambda);  // BᵀB + λI, n×n device
+double* synthetic_device(Context& c, int64_t n, uint64_t seed);           // ĀᵀĀ (io.cpp:168-176)
+
 }  // namespace si

@@ -64,8 +64,48 @@ struct TileOps {
     static_assert(BM % (WM * 16) == 0 && BN % (WN * 8) == 0, "warp tiling");
     static_assert(BK % 8 == 0 && (BK + 4) % 16 == 4 && (BM + 4) % 16 == 4 && (BN + 4) % 16 == 4, "smem pitch");
 
-    int64_t m0, n0, tile_m, tile_n;
+    int64_t m0, n0, tile_m, tile_n, split;
     int g, t4, wm0, wn0;
+
+    // Work item w of a launch: SYMUPD enumerates upper-triangular tile pairs
+    // (ti <= tj); otherwise w = tile_m + tm·(tile_n + tn·split).
+    struct Work {
+        int64_t tile_m, tile_n, split;
+    };
+    __device__ __forceinline__ static Work decode(int64_t w, const GemmArgs& p) {
+        Work r;
+        if constexpr (EPI == EPI_SYMUPD) {
+            int64_t tj = (int64_t)((sqrt(8.0 * (double)w + 1.0) - 1.0) * 0.5);
+            while (tj * (tj + 1) / 2 > w) --tj;
+            while ((tj + 1) * (tj + 2) / 2 <= w) ++tj;
+            r.tile_n = tj;
+            r.tile_m = w - tj * (tj + 1) / 2;
+            r.split = 0;
+        } else {
+            const int64_t tm = (p.M + BM - 1) / BM, tn = (p.N + BN - 1) / BN;
+            r.tile_m = w % tm;
+            r.tile_n = (w / tm) % tn;
+            r.split = w / (tm * tn);
+        }
+        return r;
+    }
+    __device__ __forceinline__ static int64_t work_count(const GemmArgs& p) {
+        const int64_t tm = (p.M + BM - 1) / BM, tn = (p.N + BN - 1) / BN;
+        if constexpr (EPI == EPI_SYMUPD) return tm * (tm + 1) / 2;
+        return tm * tn * ((p.K + p.k_chunk - 1) / p.k_chunk > 0 ? (p.K + p.k_chunk - 1) / p.k_chunk : 1);
+    }
+    __device__ __forceinline__ void setup_work(int64_t w, const GemmArgs& p, int warp, int lane) {
+        const Work r = decode(w, p);
+        tile_m = r.tile_m;
+        tile_n = r.tile_n;
+        split = r.split;
+        m0 = tile_m * BM;
+        n0 = tile_n * BN;
+        g = lane >> 2;
+        t4 = lane & 3;
+        wm0 = (warp / WN) * (BM / WM);
+        wn0 = (warp % WN) * (BN / WN);
+    }
 
     __device__ __forceinline__ void setup(int warp, int lane) {
         if constexpr (EPI == EPI_SYMUPD) {
@@ -80,12 +120,26 @@ struct TileOps {
             tile_m = blockIdx.x;
             tile_n = blockIdx.y;
         }
+        split = blockIdx.z;
         m0 = tile_m * BM;
         n0 = tile_n * BN;
         g = lane >> 2;
         t4 = lane & 3;
         wm0 = (warp / WN) * (BM / WM);
         wn0 = (warp % WN) * (BN / WN);
+    }
+
+    // L2 prefetch of this thread's part of a C tile (the next work item's X block)
+    __device__ __forceinline__ void prefetch_c(const GemmArgs& p) const {
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+            for (int j = 0; j < NI; ++j) {
+                const int64_t r = row(i, 0), c = col(j, 0);
+                if (r < p.M && c < p.N) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p.C + r + c * p.ldc));
+                if (r < p.M && c + 1 < p.N)
+                    asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p.C + r + (c + 1) * p.ldc));
+            }
     }
     // fragment element e of block (i, j) sits at (wm0 + 16i + g + 8(e>>1), wn0 + 8j + 2t + (e&1))
     __device__ __forceinline__ int64_t row(int i, int e) const { return m0 + wm0 + i * 16 + g + ((e >> 1) << 3); }
@@ -174,9 +228,34 @@ struct TileOps {
             if (tid == 0) {
                 double s = 0.0;
                 for (int k = 0; k < nthreads / 32; ++k) s += red[k];
-                p.ws[(int64_t)blockIdx.x + (int64_t)gridDim.x * ((int64_t)blockIdx.y + (int64_t)gridDim.y * blockIdx.z)] = s;
+                p.ws[tile_m + ((p.M + BM - 1) / BM) * (tile_n + ((p.N + BN - 1) / BN) * split)] = s;
             }
+            sync_consumers();  // `red` is reused by the next work item of a persistent CTA
         } else {
+            if constexpr (EPI == EPI_SYMUPD) {
+                // off-diagonal full tiles: the mirror X(c, r), X(c+1, r) of the fragment
+                // pair (r, c), (r, c+1) is one aligned 16-byte store
+                const bool fast = tile_m < tile_n && m0 + BM <= p.M && n0 + BN <= p.N && (p.ldc & 1) == 0 &&
+                                  (reinterpret_cast<uintptr_t>(p.C) & 15) == 0;
+                if (fast) {
+                    bool bad = false;
+#pragma unroll
+                    for (int i = 0; i < MI; ++i)
+#pragma unroll
+                        for (int j = 0; j < NI; ++j)
+#pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                const int64_t r = row(i, 2 * h), c = col(j, 2 * h);
+                                const double v0 = acc[i][j][2 * h], v1 = acc[i][j][2 * h + 1];
+                                p.C[r + c * p.ldc] = v0;
+                                p.C[r + (c + 1) * p.ldc] = v1;
+                                *reinterpret_cast<double2*>(p.C + c + r * p.ldc) = make_double2(v0, v1);
+                                bad |= !isfinite(v0) || !isfinite(v1);
+                            }
+                    if (bad && p.nonfinite) atomicOr(p.nonfinite, 1);
+                    return;
+                }
+            }
 #pragma unroll
             for (int i = 0; i < MI; ++i)
 #pragma unroll
@@ -192,7 +271,7 @@ struct TileOps {
                             *cp = nv;
                             if (p.nonfinite && !isfinite(nv)) atomicOr(p.nonfinite, 1);
                         } else if constexpr (EPI == EPI_PARTIAL) {
-                            p.ws[(int64_t)blockIdx.z * p.M * p.N + r + c * p.M] = v;
+                            p.ws[split * p.M * p.N + r + c * p.M] = v;
                         } else {  // EPI_SYMUPD: X(r,c) = acc (= X + V·Uᵀ) on the upper triangle, mirrored
                             if (tile_m < tile_n || r <= c) {
                                 p.C[r + c * p.ldc] = v;
@@ -206,13 +285,131 @@ struct TileOps {
 };
 
 // --------------------------------------------------------------- TMA path --
-// Threads: WM·WN warps, all of them compute.  Lane 0 of warp 0 is also the
-// TMA producer: it keeps STAGES−1 stages in flight, arming full[s] with the
-// stage's byte count and issuing one box for A and one for B.  Every warp waits
-// on full[s], computes, and arrives on empty[s] (count WM·WN); the producer
-// waits on empty[s] only before refilling that slot, so there is no CTA-wide
-// barrier in the mainloop.  (A separate producer warp would cost a whole
-// warpgroup of registers: ptxas allocates in 4-warp units.)
+// Persistent: gridDim.x CTAs stride over the launch's work items (tiles ×
+// split-K chunks; upper-triangular tile pairs for SYMUPD).  Threads: WM·WN
+// warps, all of them compute.  Lane 0 of warp 0 is also the TMA producer: it
+// keeps STAGES−1 k-stages in flight *across work-item boundaries*, so the next
+// tile's operands stream in while the current tile finishes and stores, arming
+// full[s] with the stage's byte count and issuing one box for A and one for B.
+// Every warp waits on full[s], computes, and arrives on empty[s] (count WM·WN);
+// the producer waits on empty[s] only before refilling that slot — no CTA-wide
+// barrier in the mainloop.  Each CTA also prefetches the next tile's C block to
+// L2 when the epilogue will read it.  (A separate producer warp would cost a
+// whole warpgroup of registers: ptxas allocates in 4-warp units.)
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool A_KMAJOR, bool B_KMAJOR, int EPI>
+__global__ void __launch_bounds__(WM* WN * 32, 1)
+    gemm_tma_persistent_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                               GemmArgs p) {
+    using SM = GemmSmem<BM, BN, BK, WM, WN, STAGES, A_KMAJOR, B_KMAJOR>;
+    using T = TileOps<BM, BN, BK, WM, WN, A_KMAJOR, B_KMAJOR, EPI>;
+    constexpr int NW = WM * WN;
+    constexpr uint32_t STAGE_BYTES = SM::STAGE_ELEMS * sizeof(double);
+
+    if (p.skip && *p.skip) return;
+    extern __shared__ __align__(128) double smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(smem) + SM::BAR_OFFSET);
+    uint64_t* empty = full + STAGES;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool producer = tid == 0;
+    const int64_t W = T::work_count(p);
+    auto chunk_kt = [&](int64_t split) {
+        const int64_t kb = split * p.k_chunk;
+        return (int)((min(p.K, kb + p.k_chunk) - kb + BK - 1) / BK);
+    };
+
+    // producer cursor: work item pw, k-stage pk within it, ring slot ps with its
+    // use count (parity) — 32-bit incremental counters keep the issue path short
+    int64_t pw = blockIdx.x;
+    int pk = 0, ps = 0, pround = 0, pissued = 0;
+    typename T::Work pwork{};
+    int pnk = 0;
+    if (producer && pw < W) {
+        pwork = T::decode(pw, p);
+        pnk = chunk_kt(pwork.split);
+    }
+    auto issue_next = [&]() {  // issue the next stage for (pw, pk) and advance the cursor
+        const int s = ps;
+        if (pround > 0) mbar_wait(&empty[s], (uint32_t)((pround - 1) & 1));
+        double* As = smem + s * SM::STAGE_ELEMS;
+        double* Bs = As + SM::A_ELEMS;
+        const int32_t kc = (int32_t)(pwork.split * p.k_chunk + (int64_t)pk * BK);
+        const int32_t mc = (int32_t)(pwork.tile_m * BM), nc = (int32_t)(pwork.tile_n * BN);
+        mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+        if constexpr (A_KMAJOR)
+            tma_load_2d(As, &tmA, kc, mc, &full[s]);
+        else
+            tma_load_2d(As, &tmA, mc, kc, &full[s]);
+        if constexpr (B_KMAJOR)
+            tma_load_2d(Bs, &tmB, kc, nc, &full[s]);
+        else
+            tma_load_2d(Bs, &tmB, nc, kc, &full[s]);
+        ++pissued;
+        if (++ps == STAGES) {
+            ps = 0;
+            ++pround;
+        }
+        if (++pk == pnk) {
+            pk = 0;
+            pw += gridDim.x;
+            if (pw < W) {
+                pwork = T::decode(pw, p);
+                pnk = chunk_kt(pwork.split);
+            }
+        }
+    };
+    // keep the producer STAGES−1 stages ahead of consumer stage cg
+    auto pump = [&](int cg) {
+        while (pw < W && pissued < cg + STAGES - 1) issue_next();
+    };
+
+    if (producer) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NW);
+        }
+        mbar_fence_init();
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+    }
+    __syncthreads();
+    if (producer) pump(0);
+
+    T t;
+    int cg = 0, cs = 0;
+    uint32_t cphase = 0;
+    for (int64_t w = blockIdx.x; w < W; w += gridDim.x) {
+        t.setup_work(w, p, warp, lane);
+        const int nk = chunk_kt(t.split);
+        double acc[T::MI][T::NI][4];
+        t.init_acc(acc, p);
+        for (int kt = 0; kt < nk; ++kt, ++cg) {
+            if (warp == 0) {
+                if (producer) pump(cg);
+                __syncwarp();
+            }
+            const int s = cs;
+            mbar_wait(&full[s], cphase);
+            if (++cs == STAGES) {
+                cs = 0;
+                cphase ^= 1u;
+            }
+            const double* As = smem + s * SM::STAGE_ELEMS;
+            t.compute_stage(acc, As, As + SM::A_ELEMS);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            if (kt == nk - 1 && w + gridDim.x < W && t.c_in_acc(p)) {
+                T nt = t;  // warm L2 with the next tile's C block before its init_acc
+                nt.setup_work(w + gridDim.x, p, warp, lane);
+                nt.prefetch_c(p);
+            }
+        }
+        t.epilogue(acc, p, tid, NW * 32, [] { __syncthreads(); });
+    }
+}
+
+// One CTA per work item (grid = tiles × splits): the long-K products (Y = A·S,
+// W = X·Y), whose pipeline fill is amortised over ≥ 100 k-stages.
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool A_KMAJOR, bool B_KMAJOR, int EPI>
 __global__ void __launch_bounds__(WM* WN * 32, 1)
     gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs p) {
