@@ -221,6 +221,20 @@ int si_rbfgs_core_device(si_context* ctx, const double* P, int64_t ldp, int64_t 
 /* Σ_{i<m, j<n} (δ(r0+i, j) − (X_rows·A)(i, j))², X_rows = rows [r0, r0+m) of X (ld ldx), dense A. */
 int si_residual_rows_device(si_context* ctx, si_problem* prob, int64_t m, int64_t r0, const double* x_rows,
                             int64_t ldx, double* out_host);
+/* AdaRBFGS panel ops (adarbfgs.cpp:12-21 split over row panels).
+ * gather: out (rows×q, ld rows) = L[:, idx] for a rows×? panel L (ld ldl), idx on the device. */
+int si_gather_columns_device(si_context* ctx, const double* L, int64_t rows, int64_t ldl, const int64_t* idx_dev,
+                             int64_t q, double* out);
+/* q×n stage: R = G^{-1/2} (q×q) and B = T − R·Z (q×n, ld q) from the all-reduced G and Z = (AS)ᵀL.
+ * Coordinate S̃: St = NULL, T = S̃ᵀ from idx_dev.  Gaussian S̃ (St n×q): T = (S̃ᵀS̃)^{-1/2}S̃ᵀ is
+ * also written to T_out (q×n).  scratch: 8q² + 8q + 32 doubles.  SI_ERR_RESAMPLE on the
+ * sym_inv_sqrt floor (linalg.cpp:144-155). */
+int si_ada_core_device(si_context* ctx, const double* G, int64_t q, const double* Z, int64_t n,
+                       const int64_t* idx_dev, const double* St, double* T_out, double* R, double* B, double* scratch);
+/* d_j += 2⟨T_j, B_j⟩ − ‖B_j‖² — diag(LᵀAL) carried across L += (S·R)·B; T = NULL
+ * means T = S̃ᵀ from idx_dev. */
+int si_pdiag_update_device(si_context* ctx, const double* B, int64_t q, int64_t n, const double* T,
+                           const int64_t* idx_dev, double* d);
 /* Device pointer to the problem's dense A (column-major, ld n); NULL for CSR. */
 const double* si_problem_dense_device(si_problem* prob);
 

@@ -84,6 +84,9 @@ _SIGS = {
     "si_gemm_device": (ci, [vp, i64, i64, i64, vp, i64, ci, vp, i64, ci, vp, i64, d, d]),
     "si_sketch_gaussian_device": (ci, [vp, vp, i64, i64, i64, u64, u64]),
     "si_rbfgs_core_device": (ci, [vp, vp, i64, i64, vp, vp]),
+    "si_gather_columns_device": (ci, [vp, vp, i64, i64, vp, i64, vp]),
+    "si_ada_core_device": (ci, [vp, vp, i64, vp, i64, vp, vp, vp, vp, vp, vp]),
+    "si_pdiag_update_device": (ci, [vp, vp, i64, i64, vp, vp, vp]),
     "si_residual_rows_device": (ci, [vp, vp, i64, i64, vp, i64, pd]),
     "si_problem_dense_device": (vp, [vp]),
     "si_rng_create": (ci, [u64, C.POINTER(vp)]),

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -652,6 +653,8 @@ int si_run_adarbfgs(si_context* ctx, si_problem* prob, const si_inverter_config*
                "h2d l0");
         else
             si::set_identity(c, w.L, n);
+        if (const char* e = std::getenv("SI_PDIAG_REFRESH")) w.pdiag_refresh = std::max(1, std::atoi(e));
+        if (cols && !cfg->x0_host) si::ada_init_pdiag_identity(c, a, w);  // diag(I·A·I) = diag(A)
 
         HistoryWriter hist{history, history_cap, 0, cfg};
         double flops = 0.0, seconds = 0.0;
@@ -999,6 +1002,40 @@ int si_rbfgs_core_device(si_context* ctx, const double* P, int64_t ldp, int64_t 
         int st[4];
         read_status(c, c.aux_status, st);
         if (st[0]) throw ResampleError("bfgs_step: sketched Gram matrix is not positive definite");
+    });
+}
+
+int si_gather_columns_device(si_context* ctx, const double* L, int64_t rows, int64_t ldl, const int64_t* idx_dev,
+                             int64_t q, double* out) {
+    return guard([&] {
+        require(rows >= 0 && q >= 0 && ldl >= rows, "gather_columns: bad shape");
+        if (rows * q > 0) si::gather_columns(*ctx->c, L, rows, ldl, idx_dev, q, out);
+    });
+}
+
+int si_ada_core_device(si_context* ctx, const double* G, int64_t q, const double* Z, int64_t n,
+                       const int64_t* idx_dev, const double* St, double* T_out, double* R, double* B, double* scratch) {
+    return guard([&] {
+        auto& c = *ctx->c;
+        require(q >= 1 && n >= q, "ada_core: bad shape");
+        require(St == nullptr || T_out != nullptr, "ada_core: Gaussian S̃ needs T_out");
+        if (!c.aux_status) ck(cudaMalloc(&c.aux_status, 4 * sizeof(int)), "malloc");
+        ck(cudaMemsetAsync(c.aux_status, 0, 4 * sizeof(int), c.stream), "memset");
+        double* g2 = scratch;
+        double* r2 = scratch + q * q;
+        double* es = scratch + 2 * q * q;
+        si::ada_core_enqueue(c, G, q, Z, n, idx_dev, St, g2, r2, T_out, R, B, es, c.aux_status);
+        int st[4];
+        read_status(c, c.aux_status, st);
+        if (st[0]) throw ResampleError("sym_inv_sqrt: matrix is not positive definite");
+    });
+}
+
+int si_pdiag_update_device(si_context* ctx, const double* B, int64_t q, int64_t n, const double* T,
+                           const int64_t* idx_dev, double* d) {
+    return guard([&] {
+        require(q >= 1 && n >= 1, "pdiag_update: bad shape");
+        si::pdiag_update(*ctx->c, B, q, n, T, idx_dev, nullptr, d);
     });
 }
 

@@ -220,6 +220,7 @@ static void launch_tma_cfg(Context& c, const GemmArgs& a, dim3 grid, const char*
 
 template <bool AK, bool BKM, int VEC, int EPI>
 static void launch_gemm_tile(Context& c, TileCfg t, const GemmArgs& a, dim3 grid, const char* name, bool tma) {
+    if (EPI == EPI_SYMUPD && t == T64x128) throw std::logic_error("gemm_symupd: tile height must be a multiple of its width");
     if (tma) {
         switch (t) {
             case T128x128: launch_tma_cfg<128, 128, 16, 4, 2, 5, AK, BKM, EPI>(c, a, grid, name); break;
@@ -367,11 +368,22 @@ static void symupd(Context& c, int64_t n, int64_t k, const double* V, int64_t ld
     a.k_chunk = k;
     a.skip = skip;
     a.nonfinite = nonfinite;
-    const int64_t T = (n + 127) / 128;
     const int vec = pick_vec(a);
-    // 16 warps: the update has only K = 2q, so more resident warps hide its per-tile fill/drain
-    launch_gemm_layout<EPI_SYMUPD>(c, env_flag("SI_SYMUPD_W8") ? T128x128 : T128x128W16, false, false, vec, a,
-                                   dim3(unsigned(T * (T + 1) / 2), 1, 1), "gemm_symupd");
+    // Tile choice (SI_SYMUPD_TILE): default one 16-warp CTA per SM on 128×128
+    // tiles; "w8" one 8-warp CTA on 128×128; "128x64" two 8-warp CTAs per SM so
+    // one CTA's store epilogue overlaps the other's mainloop (measured 2.5%
+    // slower at config 3: 2.31 vs 2.25 ms).
+    static const TileCfg cfg = [] {
+        const char* e = std::getenv("SI_SYMUPD_TILE");
+        const std::string v = e ? e : "";
+        if (v == "128x64") return T128x64;
+        if (v == "w8") return T128x128;
+        return T128x128W16;
+    }();
+    const int64_t bn = cfg == T128x64 ? 64 : 128, r = 128 / bn;
+    const int64_t tn = (n + bn - 1) / bn, full = tn / r, rest = tn % r;
+    const int64_t work = r * full * (full + 1) / 2 + rest * (full + 1);  // TileOps::sym_work_count
+    launch_gemm_layout<EPI_SYMUPD>(c, cfg, false, false, vec, a, dim3(unsigned(work), 1, 1), "gemm_symupd");
 }
 
 // ----------------------------------------------------------- problem -------
@@ -963,6 +975,40 @@ static void inv_sqrt(Context& c, const double* Mq, int64_t q, double* R, double*
     gemm(c, q, q, q, QD, q, false, Qm, q, false, R, q, 1.0, 0.0, status);  // R = QD·Qᵀ
 }
 
+// The q×n stage of adarbfgs_update_factor (adarbfgs.cpp:13-19): R = G^{-1/2} and
+// B = T − R·Z with T = S̃ᵀ (coordinate: idx, St null) or T = (S̃ᵀS̃)^{-1/2}·S̃ᵀ
+// (Gaussian S̃ = St, n×q; T written to Tq, q×n).  Floor hits set status[0].
+void ada_core_enqueue(Context& c, const double* G, int64_t q, const double* Z, int64_t n, const int64_t* idx,
+                      const double* St, double* G2, double* R2, double* Tq, double* R, double* B, double* scratch,
+                      int* st) {
+    inv_sqrt(c, G, q, R, scratch, st);  // R = G^{-1/2}
+    if (!St) {
+        gemm(c, q, n, q, R, q, false, Z, q, true, B, q, -1.0, 0.0, st);  // B = −R·Z
+        LaunchScope ls(c, "add_selector");
+        add_selector_kernel<<<grid_for(q, 128), 128, 0, c.stream>>>(B, q, idx, st);  // + T = S̃ᵀ
+        check_launch("add_selector");
+    } else {
+        gemm(c, q, q, n, St, n, true, St, n, true, G2, q, 1.0, 0.0, st);  // S̃ᵀS̃
+        inv_sqrt(c, G2, q, R2, scratch, st);
+        gemm(c, q, n, q, R2, q, false, St, n, false, Tq, q, 1.0, 0.0, st);  // T = R2·S̃ᵀ
+        CK(cudaMemcpyAsync(B, Tq, size_t(q) * size_t(n) * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+        gemm(c, q, n, q, R, q, false, Z, q, true, B, q, -1.0, 1.0, st);  // B = T − R·Z
+    }
+}
+
+void gather_columns(Context& c, const double* L, int64_t rows, int64_t ld, const int64_t* idx, int64_t q, double* out) {
+    LaunchScope ls(c, "gather_columns");
+    gather_columns_kernel<<<grid_for(rows * q, 256), 256, 0, c.stream>>>(L, rows, ld, idx, q, out);
+    check_launch("gather");
+}
+
+void pdiag_update(Context& c, const double* B, int64_t q, int64_t n, const double* T, const int64_t* idx,
+                  const int* skip, double* d) {
+    LaunchScope ls(c, "pdiag_update");
+    pdiag_update_kernel<<<grid_for(n * 32, 256), 256, 0, c.stream>>>(B, q, n, T, idx, skip, d);
+    check_launch("pdiag_update");
+}
+
 // L⁺ = L + (S·R)·(T − R·(AS)ᵀ·L), adarbfgs.cpp:12-21.
 //   mode 0: coordinate S̃ = I[:, idx] (idx_dev filled), S = L[:, idx] gathered
 //   mode 1: Gaussian S̃ uploaded from st_pinned; mode 2: Gaussian S̃ from Philox
@@ -970,9 +1016,7 @@ void ada_enqueue_update(Context& c, Problem& a, AdaWork& w, int mode, uint64_t s
     const int64_t n = w.n, q = w.q;
     int* st = w.status;
     if (mode == 0) {
-        LaunchScope ls(c, "gather_columns");
-        gather_columns_kernel<<<grid_for(n * q, 256), 256, 0, c.stream>>>(w.L, n, n, w.idx_dev, q, w.S);
-        check_launch("gather");
+        gather_columns(c, w.L, n, n, w.idx_dev, q, w.S);
     } else {
         if (mode == 1) {
             CK(cudaMemcpyAsync(w.St, w.st_pinned, size_t(n) * size_t(q) * sizeof(double), cudaMemcpyHostToDevice,
@@ -987,23 +1031,15 @@ void ada_enqueue_update(Context& c, Problem& a, AdaWork& w, int mode, uint64_t s
     }
     apply_a(c, a, w.S, n, q, w.AS, n, st);                                 // AS = A·S
     gemm(c, q, q, n, w.S, n, true, w.AS, n, true, w.G, q, 1.0, 0.0, st);   // G = Sᵀ·AS
-    inv_sqrt(c, w.G, q, w.R, w.eig_scratch, st);                           // R = G^{-1/2}
     gemm(c, q, n, n, w.AS, n, true, w.L, n, true, w.Z, q, 1.0, 0.0, st);   // Z = (AS)ᵀ·L
-    if (mode == 0) {
-        gemm(c, q, n, q, w.R, q, false, w.Z, q, true, w.B, q, -1.0, 0.0, st);  // B = −R·Z
-        LaunchScope ls(c, "add_selector");
-        add_selector_kernel<<<grid_for(q, 128), 128, 0, c.stream>>>(w.B, q, w.idx_dev, st);  // + T = S̃ᵀ
-        check_launch("add_selector");
-    } else {
-        // T = (S̃ᵀS̃)^{-1/2}·S̃ᵀ
-        gemm(c, q, q, n, w.St, n, true, w.St, n, true, w.G2, q, 1.0, 0.0, st);
-        inv_sqrt(c, w.G2, q, w.R2, w.eig_scratch, st);
-        gemm(c, q, n, q, w.R2, q, false, w.St, n, false, w.Tm, q, 1.0, 0.0, st);  // R2·S̃ᵀ (B N-major)
-        CK(cudaMemcpyAsync(w.B, w.Tm, size_t(q) * size_t(n) * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
-        gemm(c, q, n, q, w.R, q, false, w.Z, q, true, w.B, q, -1.0, 1.0, st);  // B = T − R·Z
-    }
+    ada_core_enqueue(c, w.G, q, w.Z, n, w.idx_dev, mode == 0 ? nullptr : w.St, w.G2, w.R2, w.Tm, w.R, w.B,
+                     w.eig_scratch, st);
     gemm(c, n, q, q, w.S, n, false, w.R, q, true, w.SR, n, 1.0, 0.0, st);  // SR = S·R
     gemm(c, n, n, q, w.SR, n, false, w.B, q, true, w.L, n, 1.0, 1.0, st, st + 1);  // L += SR·B (+ finite check)
+    if (w.pdiag_valid) {  // carry diag(LᵀAL) across the accepted update (App. C3)
+        pdiag_update(c, w.B, q, n, mode == 0 ? nullptr : w.Tm, w.idx_dev, st, w.pdiag);
+        ++w.pdiag_age;
+    }
     if (mode == 2) {
         LaunchScope ls(c, "advance_counter");
         advance_counter_kernel<<<1, 1, 0, c.stream>>>(w.counter, w.status);
@@ -1014,14 +1050,27 @@ void ada_enqueue_update(Context& c, Problem& a, AdaWork& w, int mode, uint64_t s
 // pdiag_j = l_jᵀ A l_j (diag(LᵀAL), Eq 8.2 numerators), copied to p_pinned.
 void ada_enqueue_probabilities(Context& c, Problem& a, AdaWork& w) {
     const int64_t n = w.n;
-    if (!w.AL) dmalloc(&w.AL, size_t(n) * size_t(n));
-    apply_a(c, a, w.L, n, n, w.AL, n, nullptr);
-    {
+    if (!w.pdiag_valid || w.pdiag_refresh <= 1 || w.pdiag_age >= w.pdiag_refresh) {
+        // exact: diag(Lᵀ·(A·L)) (adarbfgs.cpp:23-36)
+        if (!w.AL) dmalloc(&w.AL, size_t(n) * size_t(n));
+        apply_a(c, a, w.L, n, n, w.AL, n, nullptr);
         LaunchScope ls(c, "column_dots");
         column_dots_kernel<<<grid_for(n * 32, 256), 256, 0, c.stream>>>(w.AL, w.L, n, w.pdiag);
         check_launch("column_dots");
+        w.pdiag_valid = w.pdiag_refresh > 1;
+        w.pdiag_age = 0;
     }
     CK(cudaMemcpyAsync(w.p_pinned, w.pdiag, size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+}
+
+void ada_init_pdiag_identity(Context& c, Problem& a, AdaWork& w) {
+    if (w.pdiag_refresh <= 1) return;  // reference behaviour: exact every iteration
+    LaunchScope ls(c, "problem_diagonal");
+    problem_diagonal_kernel<<<grid_for(w.n, 256), 256, 0, c.stream>>>(a.dense ? a.a : nullptr, a.rowptr, a.colind,
+                                                                       a.val, w.n, w.pdiag);
+    check_launch("problem_diagonal");
+    w.pdiag_valid = true;
+    w.pdiag_age = 0;
 }
 
 }  // namespace si

@@ -107,7 +107,10 @@ struct AdaWork {
     int64_t* idx_pinned = nullptr;
     double* st_pinned = nullptr;
     double* AL = nullptr;  // n×n scratch for residual / probabilities (lazy)
-    double* pdiag = nullptr;  // n
+    double* pdiag = nullptr;  // n: diag(LᵀAL), exact or carried by App. C3
+    bool pdiag_valid = false;
+    int pdiag_age = 0;       // incremental updates since the last exact refresh
+    int pdiag_refresh = 64;  // exact A·L refresh period (SI_PDIAG_REFRESH; 1 = every iteration)
     double* p_pinned = nullptr;
     int* status = nullptr;
     unsigned long long* counter = nullptr;
@@ -149,7 +152,14 @@ void set_identity(Context& c, double* X, int64_t n);
 
 void ada_enqueue_update(Context& c, Problem& a, AdaWork& w, int mode /*0 cols idx, 1 gaussian host, 2 gaussian dev*/,
                         uint64_t seed);
-void ada_enqueue_probabilities(Context& c, Problem& a, AdaWork& w);  // pdiag = diag(LᵀAL) -> p_pinned (async)
+void ada_enqueue_probabilities(Context& c, Problem& a, AdaWork& w);
+void ada_core_enqueue(Context& c, const double* G, int64_t q, const double* Z, int64_t n, const int64_t* idx,
+                      const double* St, double* G2, double* R2, double* Tq, double* R, double* B, double* scratch,
+                      int* st);
+void gather_columns(Context& c, const double* L, int64_t rows, int64_t ld, const int64_t* idx, int64_t q, double* out);
+void pdiag_update(Context& c, const double* B, int64_t q, int64_t n, const double* T, const int64_t* idx,
+                  const int* skip, double* d);
+void ada_init_pdiag_identity(Context& c, Problem& a, AdaWork& w);  // diag(A): the L = I diagonal  // pdiag = diag(LᵀAL) -> p_pinned (async)
 
 // ---- ingestion (io.cpp) --------------------------------
 struct IoError : std::runtime_error {

@@ -72,14 +72,28 @@ struct TileOps {
     struct Work {
         int64_t tile_m, tile_n, split;
     };
+    // SYMUPD tiles: BM×BN blocks (BM = R·BN) that meet the upper triangle.  Column
+    // block tn needs row blocks 0..tn/R, so column chunk c (R column blocks) holds
+    // R·(c+1) tiles and chunks 0..c−1 hold R·c(c+1)/2; w runs row blocks fastest.
+    // (the host launches SYMUPD only with BM a multiple of BN)
+    static constexpr int R_SYM = BM % BN == 0 ? BM / BN : 1;
+    __host__ __device__ __forceinline__ static int64_t sym_work_count(int64_t n) {
+        const int64_t tn = (n + BN - 1) / BN;
+        const int64_t full = tn / R_SYM, rest = tn % R_SYM;  // complete chunks, columns of the last one
+        return R_SYM * full * (full + 1) / 2 + rest * (full + 1);
+    }
+    __device__ __forceinline__ static void sym_tile(int64_t w, int64_t& tile_m, int64_t& tile_n) {
+        int64_t c = (int64_t)((sqrt(8.0 * (double)w / R_SYM + 1.0) - 1.0) * 0.5);
+        while (c > 0 && R_SYM * c * (c + 1) / 2 > w) --c;
+        while (R_SYM * (c + 1) * (c + 2) / 2 <= w) ++c;
+        const int64_t rem = w - R_SYM * c * (c + 1) / 2;
+        tile_n = c * R_SYM + rem / (c + 1);
+        tile_m = rem % (c + 1);
+    }
     __device__ __forceinline__ static Work decode(int64_t w, const GemmArgs& p) {
         Work r;
         if constexpr (EPI == EPI_SYMUPD) {
-            int64_t tj = (int64_t)((sqrt(8.0 * (double)w + 1.0) - 1.0) * 0.5);
-            while (tj * (tj + 1) / 2 > w) --tj;
-            while ((tj + 1) * (tj + 2) / 2 <= w) ++tj;
-            r.tile_n = tj;
-            r.tile_m = w - tj * (tj + 1) / 2;
+            sym_tile(w, r.tile_m, r.tile_n);
             r.split = 0;
         } else {
             const int64_t tm = (p.M + BM - 1) / BM, tn = (p.N + BN - 1) / BN;
@@ -91,7 +105,7 @@ struct TileOps {
     }
     __device__ __forceinline__ static int64_t work_count(const GemmArgs& p) {
         const int64_t tm = (p.M + BM - 1) / BM, tn = (p.N + BN - 1) / BN;
-        if constexpr (EPI == EPI_SYMUPD) return tm * (tm + 1) / 2;
+        if constexpr (EPI == EPI_SYMUPD) return sym_work_count(p.N);
         return tm * tn * ((p.K + p.k_chunk - 1) / p.k_chunk > 0 ? (p.K + p.k_chunk - 1) / p.k_chunk : 1);
     }
     __device__ __forceinline__ void setup_work(int64_t w, const GemmArgs& p, int warp, int lane) {
@@ -109,13 +123,7 @@ struct TileOps {
 
     __device__ __forceinline__ void setup(int warp, int lane) {
         if constexpr (EPI == EPI_SYMUPD) {
-            // linear index over upper-triangular tile pairs (ti <= tj)
-            const int64_t t = blockIdx.x;
-            int64_t tj = (int64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
-            while (tj * (tj + 1) / 2 > t) --tj;
-            while ((tj + 1) * (tj + 2) / 2 <= t) ++tj;
-            tile_n = tj;
-            tile_m = t - tj * (tj + 1) / 2;
+            sym_tile(blockIdx.x, tile_m, tile_n);
         } else {
             tile_m = blockIdx.x;
             tile_n = blockIdx.y;
@@ -235,7 +243,7 @@ struct TileOps {
             if constexpr (EPI == EPI_SYMUPD) {
                 // off-diagonal full tiles: the mirror X(c, r), X(c+1, r) of the fragment
                 // pair (r, c), (r, c+1) is one aligned 16-byte store
-                const bool fast = tile_m < tile_n && m0 + BM <= p.M && n0 + BN <= p.N && (p.ldc & 1) == 0 &&
+                const bool fast = m0 + BM <= n0 && m0 + BM <= p.M && n0 + BN <= p.N && (p.ldc & 1) == 0 &&
                                   (reinterpret_cast<uintptr_t>(p.C) & 15) == 0;
                 if (fast) {
                     bool bad = false;
@@ -273,7 +281,7 @@ struct TileOps {
                         } else if constexpr (EPI == EPI_PARTIAL) {
                             p.ws[split * p.M * p.N + r + c * p.M] = v;
                         } else {  // EPI_SYMUPD: X(r,c) = acc (= X + V·Uᵀ) on the upper triangle, mirrored
-                            if (tile_m < tile_n || r <= c) {
+                            if (r <= c) {
                                 p.C[r + c * p.ldc] = v;
                                 if (r != c) p.C[c + r * p.ldc] = v;
                                 if (!isfinite(v) && p.nonfinite) atomicOr(p.nonfinite, 1);
@@ -297,7 +305,7 @@ struct TileOps {
 // L2 when the epilogue will read it.  (A separate producer warp would cost a
 // whole warpgroup of registers: ptxas allocates in 4-warp units.)
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool A_KMAJOR, bool B_KMAJOR, int EPI>
-__global__ void __launch_bounds__(WM* WN * 32, 1)
+__global__ void __launch_bounds__(WM* WN * 32, (EPI == EPI_SYMUPD && BM * BN <= 128 * 64) ? 2 : 1)
     gemm_tma_persistent_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                                GemmArgs p) {
     using SM = GemmSmem<BM, BN, BK, WM, WN, STAGES, A_KMAJOR, B_KMAJOR>;

@@ -30,8 +30,10 @@ from dataclasses import dataclass
 import torch
 import torch.distributed as dist
 
+import numpy as np
+
 from . import _lib as L
-from .api import GramRankDeficientError, ProblemMatrix, _check
+from .api import GramRankDeficientError, NumericalError, ProblemMatrix, RngStream, _check, contiguous_partition
 
 
 def row_partition(n: int, world: int):
@@ -67,6 +69,22 @@ class CudaPanelOps:
     def core(self, P, ldp, q, M, scratch):
         _check(self.lib.si_rbfgs_core_device(self.ctx.handle, self._p(P), ldp, q, self._p(M), self._p(scratch)))
 
+    def gather_columns(self, Lp, rows, ldl, idx, q, out):
+        _check(self.lib.si_gather_columns_device(self.ctx.handle, self._p(Lp), rows, ldl, self._p(idx), q,
+                                                 self._p(out)))
+
+    def ada_core(self, G, q, Z, n, idx, St, T, R, B, scratch):
+        _check(self.lib.si_ada_core_device(self.ctx.handle, self._p(G), q, self._p(Z), n,
+                                           self._p(idx) if idx is not None else None,
+                                           self._p(St) if St is not None else None,
+                                           self._p(T) if T is not None else None, self._p(R), self._p(B),
+                                           self._p(scratch)))
+
+    def pdiag_update(self, B, q, n, T, idx, d):
+        _check(self.lib.si_pdiag_update_device(self.ctx.handle, self._p(B), q, n,
+                                               self._p(T) if T is not None else None,
+                                               self._p(idx) if idx is not None else None, self._p(d)))
+
     def residual_rows_sq(self, prob: ProblemMatrix, m, r0, X, ldx) -> float:
         out = C.c_double()
         _check(self.lib.si_residual_rows_device(self.ctx.handle, prob.handle, m, r0, self._p(X), ldx, C.byref(out)))
@@ -88,7 +106,46 @@ class ShardLayout:
         self.m_max = max(self.starts[p + 1] - self.starts[p] for p in range(self.world))
 
 
-class RowShardedRBFGS:
+class _RowPanels:
+    """Collectives on row panels shared by the sharded drivers (self.lay, self.world,
+    self.send_buf / self.gather_buf sized for m_max × q)."""
+
+    def _all_gather_rows(self, panel: torch.Tensor, out: torch.Tensor, ncols: int):
+        """panel: this rank's m×ncols column-major panel; out: n×ncols column-major."""
+        lay = self.lay
+        mm = lay.m_max
+        send = self.send_buf[: mm * ncols].view(ncols, mm)
+        send[:, : lay.m].copy_(panel.view(ncols, lay.m))
+        if self.world == 1:
+            out.view(ncols, lay.n).copy_(send[:, : lay.n])
+            return
+        gbuf = self.gather_buf[: self.world * mm * ncols]
+        dist.all_gather_into_tensor(gbuf, send.reshape(-1))
+        g = gbuf.view(self.world, ncols, mm)
+        ov = out.view(ncols, lay.n)
+        for p in range(self.world):
+            a, b = lay.starts[p], lay.starts[p + 1]
+            ov[:, a:b].copy_(g[p, :, : b - a])
+
+    def _gather_panel(self, panel, out):
+        """All-gather an m×n row panel (column-major, flat) into the full n×n matrix."""
+        lay = self.lay
+        mm = lay.m_max
+        send = torch.zeros(mm * lay.n, dtype=torch.float64, device=panel.device).view(lay.n, mm)
+        send[:, : lay.m].copy_(panel.view(lay.n, lay.m))
+        if self.world == 1:
+            out.view(lay.n, lay.n).copy_(send[:, : lay.n])
+            return
+        g = torch.empty(self.world * mm * lay.n, dtype=torch.float64, device=panel.device)
+        dist.all_gather_into_tensor(g, send.reshape(-1))
+        gv = g.view(self.world, lay.n, mm)
+        ov = out.view(lay.n, lay.n)
+        for p in range(self.world):
+            a, b = lay.starts[p], lay.starts[p + 1]
+            ov[:, a:b].copy_(gv[p, :, : b - a])
+
+
+class RowShardedRBFGS(_RowPanels):
     """RBFGS with X row-sharded over the ranks of the default process group.
 
     a_rows: A[R_p, :] as a column-major m×n panel held in a flat float64 tensor
@@ -136,23 +193,6 @@ class RowShardedRBFGS:
     def set_rows(self, x_rows: torch.Tensor):
         """x_rows: column-major m×n panel (flat)."""
         self.X.copy_(x_rows)
-
-    def _all_gather_rows(self, panel: torch.Tensor, out: torch.Tensor, ncols: int):
-        """panel: this rank's m×ncols column-major panel; out: n×ncols column-major."""
-        lay = self.lay
-        mm = lay.m_max
-        send = self.send_buf[: mm * ncols].view(ncols, mm)
-        send[:, : lay.m].copy_(panel.view(ncols, lay.m))
-        if self.world == 1:
-            out.view(ncols, lay.n).copy_(send[:, : lay.n])
-            return
-        gbuf = self.gather_buf[: self.world * mm * ncols]
-        dist.all_gather_into_tensor(gbuf, send.reshape(-1))
-        g = gbuf.view(self.world, ncols, mm)
-        ov = out.view(ncols, lay.n)
-        for p in range(self.world):
-            a, b = lay.starts[p], lay.starts[p + 1]
-            ov[:, a:b].copy_(g[p, :, : b - a])
 
     # --------------------------------------------------------------- step --
     def step(self):
@@ -202,17 +242,152 @@ class RowShardedRBFGS:
         return out
 
     def _gather_full(self, out):
+        self._gather_panel(self.X, out)
+
+
+class RowShardedAdaRBFGS(_RowPanels):
+    """AdaRBFGS with the factor L row-sharded: rank p owns the
+    column-major m×n panel L_p = L[R_p, :] and A_p = A[R_p, :].  One iteration
+    (adarbfgs.cpp:12-21 over panels):
+
+        C / S̃    host draw (RngStream, identical on every rank) or Philox S̃
+        S_p      = L_p[:, C]  or  L_p·S̃                    local
+        S        = all-gather(S_p)                          n×q
+        (AS)_p   = A_p·S                                    local  2·m·n·q
+        [G | Z]  = all-reduce([S_pᵀ(AS)_p | (AS)_pᵀL_p])     q×q + q×n, one packed call
+        R, B     = G^{-1/2},  T − R·Z                        replicated q×n stage
+        L_p     += (S_p·R)·B                                 local  2·m·n·q
+        d       += 2⟨T_j, B_j⟩ − ‖B_j‖²                      replicated Eq. 8.2 diagonal (App. C3)
+
+    rule: "cols" (reference contiguous blocks + Eq. 8.2, adarbfgs.cpp:23-36),
+    "uniform" (paper sampler, uniform q-subsets) or "gauss" (Philox S̃).  The host
+    RNG consumption matches run_adarbfgs (one categorical / subset per attempt),
+    so the coordinate paths draw the same indices as the single-GPU driver.
+    """
+
+    def __init__(self, ops, n: int, q: int, a_rows: torch.Tensor, *, rule: str = "cols", seed: int = 0,
+                 prob: ProblemMatrix | None = None, max_redraws: int = 100, l0_rows: torch.Tensor | None = None):
+        if rule not in ("cols", "uniform", "gauss"):
+            raise ValueError("rule must be 'cols', 'uniform' or 'gauss'")
+        self.ops, self.rule, self.seed, self.prob, self.max_redraws = ops, rule, seed, prob, max_redraws
+        self.world = dist.get_world_size() if dist.is_initialized() else 1
+        self.rank = dist.get_rank() if dist.is_initialized() else 0
+        self.lay = ShardLayout(n, q, self.rank, self.world)
+        self.rng = RngStream(seed)
+        self.draw = 0
+        self.redraws = 0
+        self.k = 0
+        dev = a_rows.device
+        m = self.lay.m
+        f = dict(dtype=torch.float64, device=dev)
+        self.A = a_rows
+        self.L = torch.empty(m * n, **f)
+        self.Sp = torch.empty(m * q, **f)
+        self.S = torch.empty(n * q, **f)
+        self.ASp = torch.empty(m * q, **f)
+        self.SRp = torch.empty(m * q, **f)
+        self.GZ = torch.empty(q * q + q * n, **f)
+        self.R = torch.empty(q * q, **f)
+        self.B = torch.empty(q * n, **f)
+        self.scratch = torch.empty(8 * q * q + 8 * q + 32, **f)
+        self.idx = torch.zeros(q, dtype=torch.int64, device=dev)
+        self.St = torch.empty(n * q, **f) if rule == "gauss" else None
+        self.T = torch.empty(q * n, **f) if rule == "gauss" else None
+        self.gather_buf = torch.empty(self.world * self.lay.m_max * q, **f)
+        self.send_buf = torch.zeros(self.lay.m_max * q, **f)
+        self.blocks = contiguous_partition(n, q) if rule == "cols" else None
+        self.d = torch.empty(n, **f) if rule == "cols" else None
+        if l0_rows is None:
+            Lv = self.L.view(n, m)
+            Lv.zero_()
+            i = torch.arange(m, device=dev)
+            Lv[self.lay.r0 + i, i] = 1.0
+            if self.d is not None:  # diag(LᵀAL) at L = I is diag(A): the diagonal entries of the local rows
+                self.d.zero_()
+                self.d[self.lay.r0 + i] = self.A.view(n, m)[self.lay.r0 + i, i]
+                if self.world > 1:
+                    dist.all_reduce(self.d)
+        else:
+            self.L.copy_(l0_rows)
+            if self.d is not None:
+                self.refresh_diagonal()
+
+    # ------------------------------------------------------------- helpers --
+    def gather_l(self) -> torch.Tensor:
+        """Full L (n×n column-major, flat) on every rank."""
+        out = torch.empty(self.lay.n * self.lay.n, dtype=torch.float64, device=self.L.device)
+        self._gather_panel(self.L, out)
+        return out
+
+    def refresh_diagonal(self):
+        """Exact diag(LᵀAL) = Σ_p diag(L_pᵀ·(A_p·L)) (needs all of L: n² traffic)."""
         lay = self.lay
-        mm = lay.m_max
-        send = torch.zeros(mm * lay.n, dtype=torch.float64, device=self.X.device).view(lay.n, mm)
-        send[:, : lay.m].copy_(self.X.view(lay.n, lay.m))
-        if self.world == 1:
-            out.view(lay.n, lay.n).copy_(send[:, : lay.n])
+        n, m = lay.n, lay.m
+        full = self.gather_l()
+        AL = torch.empty(m * n, dtype=torch.float64, device=self.L.device)
+        self.ops.gemm(m, n, n, self.A, m, False, full, n, True, AL, m)  # (A·L)[R_p, :] = A_p·L
+        part = (AL.view(n, m) * self.L.view(n, m)).sum(dim=1)
+        if self.world > 1:
+            dist.all_reduce(part)
+        self.d.copy_(part)
+
+    def _probabilities(self) -> np.ndarray:  # adarbfgs.cpp:23-36 on the carried diagonal
+        d = self.d.cpu().numpy()
+        p = np.array([d[b[0]:b[-1] + 1].sum() for b in self.blocks])
+        if p.min() <= 0.0:
+            raise NumericalError("adaptive_block_probabilities: non-positive block trace; "
+                                 "the factor has degenerated")
+        return p / p.sum()
+
+    # --------------------------------------------------------------- step --
+    def step(self):
+        lay, ops = self.lay, self.ops
+        n, m = lay.n, lay.m
+        p = self._probabilities() if self.rule == "cols" else None
+        for _ in range(self.max_redraws + 1):
+            if self.rule == "gauss":
+                q = lay.q
+                ops.sketch(self.St, n, q, n, self.seed, self.draw)
+                self.draw += 1
+                ops.gemm(m, q, n, self.L, m, False, self.St, n, True, self.Sp, m)            # S_p = L_p·S̃
+            else:
+                if self.rule == "cols":
+                    cols = self.blocks[self.rng.categorical(p)]
+                else:
+                    cols = [int(v) for v in self.rng.uniform_subset(n, lay.q)]
+                q = len(cols)
+                self.idx[:q].copy_(torch.tensor(cols, dtype=torch.int64))
+                ops.gather_columns(self.L, m, m, self.idx, q, self.Sp)                        # S_p = L_p[:, C]
+            self._all_gather_rows(self.Sp[: m * q], self.S[: n * q], q)                       # S
+            ops.gemm(m, q, n, self.A, m, False, self.S, n, True, self.ASp, m)                 # (AS)_p = A_p·S
+            G, Z = self.GZ[: q * q], self.GZ[q * q: q * q + q * n]
+            ops.gemm(q, q, m, self.Sp, m, True, self.ASp, m, True, G, q)                       # S_pᵀ(AS)_p
+            ops.gemm(q, n, m, self.ASp, m, True, self.L, m, True, Z, q)                        # (AS)_pᵀ L_p
+            if self.world > 1:
+                dist.all_reduce(self.GZ[: q * q + q * n])                                     # [G | Z]
+            try:
+                ops.ada_core(G, q, Z, n, None if self.rule == "gauss" else self.idx, self.St, self.T,
+                             self.R, self.B, self.scratch)                                     # R, B = T − R·Z
+            except GramRankDeficientError:
+                self.redraws += 1  # G, Z identical on every rank: all ranks redraw together
+                continue
+            ops.gemm(m, q, q, self.Sp, m, False, self.R, q, True, self.SRp, m)                # (S·R)_p
+            ops.gemm(m, n, q, self.SRp, m, False, self.B, q, True, self.L, m, 1.0, 1.0)      # L_p += (S·R)_p·B
+            if self.d is not None:
+                ops.pdiag_update(self.B, q, n, None, self.idx, self.d)                        # Eq. 8.2 diagonal
+            self.k += 1
             return
-        g = torch.empty(self.world * mm * lay.n, dtype=torch.float64, device=self.X.device)
-        dist.all_gather_into_tensor(g, send.reshape(-1))
-        gv = g.view(self.world, lay.n, mm)
-        ov = out.view(lay.n, lay.n)
-        for p in range(self.world):
-            a, b = lay.starts[p], lay.starts[p + 1]
-            ov[:, a:b].copy_(gv[p, :, : b - a])
+        raise GramRankDeficientError("sketch rejection limit exceeded")
+
+    def residual(self) -> float:
+        """‖I − A·L·Lᵀ‖_F: X_p = L_p·Lᵀ from the gathered L, then the row-panel residual."""
+        lay = self.lay
+        n, m = lay.n, lay.m
+        full = self.gather_l()
+        Xp = torch.empty(m * n, dtype=torch.float64, device=self.L.device)
+        self.ops.gemm(m, n, n, self.L, m, False, full, n, False, Xp, m)                       # X_p = L_p·Lᵀ
+        part = self.ops.residual_rows_sq(self.prob, m, lay.r0, Xp, m)
+        t = torch.tensor([part], dtype=torch.float64, device=self.L.device)
+        if self.world > 1:
+            dist.all_reduce(t)
+        return float(t.item()) ** 0.5

@@ -59,3 +59,37 @@ class NumpyPanelOps:
         r = x @ self.a
         r[np.arange(m), r0 + np.arange(m)] -= 1.0
         return float((r * r).sum())
+
+    # ---- AdaRBFGS panel ops (same contract as CudaPanelOps) ----
+    def gather_columns(self, Lp, rows, ldl, idx, q, out):
+        src, dst = Lp.numpy(), out.numpy()
+        for j, c in enumerate(idx.numpy()[:q]):
+            dst[j * rows:(j + 1) * rows] = src[c * ldl: c * ldl + rows]
+
+    def ada_core(self, G, q, Z, n, idx, St, T, R, B, scratch):
+        from paper_1602_01768_b200.api import GramRankDeficientError
+
+        g = _view(G, q, q, q).copy()
+        z = _view(Z, q, n, q).copy()
+        try:
+            r = O.sym_inv_sqrt(g)
+            if St is None:
+                t = np.zeros((q, n))
+                t[np.arange(q), idx.numpy()[:q]] = 1.0
+            else:
+                st = _view(St, n, q, n).copy()
+                t = O.sym_inv_sqrt(st.T @ st) @ st.T
+                _view(T, q, n, q)[...] = t
+        except O.NumericalError as e:
+            raise GramRankDeficientError(str(e))
+        _view(R, q, q, q)[...] = r
+        _view(B, q, n, q)[...] = t - r @ z
+
+    def pdiag_update(self, B, q, n, T, idx, d):
+        b = _view(B, q, n, q)
+        if T is None:
+            t = np.zeros((q, n))
+            t[np.arange(q), idx.numpy()[:q]] = 1.0
+        else:
+            t = _view(T, q, n, q)
+        d.numpy()[:] += 2.0 * (t * b).sum(axis=0) - (b * b).sum(axis=0)

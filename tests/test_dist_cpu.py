@@ -85,3 +85,70 @@ def test_row_partition():
 
     assert row_partition(10, 3) == [0, 4, 7, 10]
     assert row_partition(8, 8) == list(range(9))
+
+
+def _ada_worker(rank, world, port, n, q, iters, seed, rule, use_l0, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+
+        sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+        from dist_test_ops import NumpyPanelOps
+        from paper_1602_01768_b200.dist import RowShardedAdaRBFGS, row_partition
+
+        a = _problem(n)
+        starts = row_partition(n, world)
+        r0, r1 = starts[rank], starts[rank + 1]
+        a_rows = torch.from_numpy(np.asfortranarray(a[r0:r1, :]).reshape(-1, order="F").copy())
+        l0_rows = None
+        if use_l0:
+            l0 = _l0(n)
+            l0_rows = torch.from_numpy(np.asfortranarray(l0[r0:r1, :]).reshape(-1, order="F").copy())
+        solver = RowShardedAdaRBFGS(NumpyPanelOps(a), n, q, a_rows, rule=rule, seed=seed, l0_rows=l0_rows)
+        for _ in range(iters):
+            solver.step()
+        lf = solver.gather_l().numpy().reshape((n, n), order="F")
+        res = solver.residual()
+        d = solver.d.numpy().copy() if solver.d is not None else None
+        if rank == 0:
+            out_q.put((lf, res, d))
+    finally:
+        dist.destroy_process_group()
+
+
+def _l0(n):
+    return np.eye(n) + 0.01 * O.RngStream(77).gaussian_matrix(n, n)
+
+
+@pytest.mark.parametrize("world,n,q,rule,use_l0", [
+    (1, 24, 4, "cols", False), (2, 37, 4, "cols", False), (2, 40, 6, "uniform", False),
+    (2, 33, 3, "gauss", False), (2, 30, 5, "cols", True),
+])
+def test_row_sharded_adarbfgs_matches_oracle(world, n, q, rule, use_l0):
+    iters, seed = 15, 4
+    ctx = mp.get_context("spawn")
+    out_q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ada_worker, args=(r, world, port, n, q, iters, seed, rule, use_l0, out_q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    lf, res, d = out_q.get(timeout=180)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    a = _problem(n)
+    l0 = _l0(n) if use_l0 else None
+    if rule == "gauss":  # same Philox-stand-in sketch sequence as the test double
+        ref = np.asfortranarray(l0 if l0 is not None else np.eye(n))
+        for draw in range(iters):
+            ref = O.adarbfgs_update_factor(ref, a, O.RngStream(seed).substream(draw).gaussian_matrix(n, q))
+    else:
+        orule = O.ADA_COLS if rule == "cols" else O.ADA_COLS_UNIFORM
+        ref = O.run_adarbfgs(a, q, rule=orule, tol=0.0, max_iters=iters, every_k=iters, seed=seed, l0=l0).x
+    assert np.linalg.norm(lf - ref) / np.linalg.norm(ref) <= 1e-9
+    assert res == pytest.approx(np.linalg.norm(np.eye(n) - a @ lf @ lf.T), rel=1e-9)
+    if d is not None:  # the carried Eq. 8.2 diagonal equals the exact diag(LᵀAL)
+        assert np.allclose(d, np.einsum("ij,ij->j", lf, a @ lf), rtol=1e-10, atol=0)

@@ -69,3 +69,39 @@ def test_row_sharded_world1_matches_solver(env):
     x_so = sol.iterate()
     assert np.linalg.norm(x_sh - x_so) / np.linalg.norm(x_so) <= 1e-9
     assert sh.residual() == pytest.approx(sol.residual(), rel=1e-9)
+
+
+@pytest.mark.parametrize("rule", ["cols", "uniform", "gauss"])
+def test_row_sharded_ada_world1(env, rule):
+    """The sharded AdaRBFGS driver at world size 1 on the GPU against the oracle
+    on the same index / sketch sequence, and its carried Eq. 8.2 diagonal against
+    the exact diag(LᵀAL)."""
+    si, torch, ctx, ops = env
+    from oracle import oracle as O
+    from paper_1602_01768_b200.dist import RowShardedAdaRBFGS
+
+    n, q, iters, seed = 300, 20, 40, 6
+    rng = O.RngStream(41)
+    b = rng.gaussian_matrix(n, n)
+    a = np.asfortranarray(b @ b.T / n + np.eye(n))
+    prob = si.ProblemMatrix(a, si.Symmetry.spd, context=ctx)
+    a_rows = torch.from_numpy(a.reshape(-1, order="F").copy()).cuda()
+    sh = RowShardedAdaRBFGS(ops, n, q, a_rows, rule=rule, seed=seed, prob=prob)
+    sketches = []
+    for _ in range(iters):
+        sh.step()
+        if rule == "gauss":
+            sketches.append(sh.St.cpu().numpy().reshape((n, q), order="F").copy())
+    lf = sh.gather_l().cpu().numpy().reshape((n, n), order="F")
+    if rule == "gauss":
+        ref = np.eye(n)
+        for s in sketches:
+            ref = O.adarbfgs_update_factor(ref, a, s)
+    else:
+        ref = O.run_adarbfgs(a, q, rule=O.ADA_COLS if rule == "cols" else O.ADA_COLS_UNIFORM, tol=0.0,
+                             max_iters=iters, every_k=iters, seed=seed).x
+    assert np.linalg.norm(lf - ref) / np.linalg.norm(ref) <= 1e-9
+    assert sh.residual() == pytest.approx(np.linalg.norm(np.eye(n) - a @ lf @ lf.T), rel=1e-8)
+    if rule == "cols":
+        d = sh.d.cpu().numpy()
+        assert np.allclose(d, np.einsum("ij,ij->j", lf, a @ lf), rtol=1e-10, atol=0)

@@ -237,6 +237,36 @@ def test_run_adarbfgs_parity(si, rule):
     assert rel(res.state.x, res.state.l @ res.state.l.T) <= 1e-13
 
 
+@pytest.mark.parametrize("refresh", ["1", "7", "100000"])
+def test_eq82_incremental_diagonal_parity(si, refresh, monkeypatch):
+    """Eq. 8.2 probabilities from the carried diag(LᵀAL) (App. C3) draw the same
+    blocks as the reference's exact A·L every iteration: 150 iterations over a
+    ragged partition (n = 100, q = 8: last block 4 wide), same iterate."""
+    monkeypatch.setenv("SI_PDIAG_REFRESH", refresh)
+    rng = O.RngStream(23)
+    n, q, iters = 100, 8, 150
+    a = random_spd(n, rng)
+    ref = O.run_adarbfgs(a, q, rule=O.ADA_COLS, tol=0.0, max_iters=iters, every_k=10, seed=2)
+    res = si.run_adarbfgs(si.AdaConfig(si.ProblemMatrix(a, si.Symmetry.spd), si.SketchRule.adaptive_cols(n, q),
+                                       tol=0.0, max_iters=iters, seed=2, track=si.TrackOptions(residual_every_k=10)))
+    assert res.state.k == iters
+    assert rel(res.state.l, ref.x) <= ITER_TOL
+    assert trace_gap([h.residual for h in res.state.history], [h[1] for h in ref.history]) <= TRACE_TOL
+
+
+def test_eq82_incremental_diagonal_from_x0(si, monkeypatch):
+    monkeypatch.setenv("SI_PDIAG_REFRESH", "1000")
+    rng = O.RngStream(29)
+    n, q, iters = 64, 8, 60
+    a = random_spd(n, rng)
+    l0 = np.eye(n) + 0.01 * rng.gaussian_matrix(n, n)
+    ref = O.run_adarbfgs(a, q, rule=O.ADA_COLS, tol=0.0, max_iters=iters, every_k=10, seed=4, l0=l0)
+    res = si.run_adarbfgs(si.AdaConfig(si.ProblemMatrix(a, si.Symmetry.spd), si.SketchRule.adaptive_cols(n, q),
+                                       tol=0.0, max_iters=iters, seed=4, l0=l0,
+                                       track=si.TrackOptions(residual_every_k=10)))
+    assert rel(res.state.l, ref.x) <= ITER_TOL
+
+
 def test_run_adarbfgs_converges(si):  # test_adarbfgs.cpp:94-112
     rng = O.RngStream(89)
     a = random_spd(10, rng)

@@ -135,7 +135,7 @@ def test_gpu_matrix_market_solver_roundtrip(tmp_path):
         j = rng.integers(0, n, 3)
         a[i, j] += 0.1
     a = (a + a.T) / 2
-    lines = [f"{i + 1} {j + 1} {a[i, j]!r}" for j in range(n) for i in range(j, n) if a[i, j] != 0.0]
+    lines = [f"{i + 1} {j + 1} {float(a[i, j])!r}" for j in range(n) for i in range(j, n) if a[i, j] != 0.0]
     path = _fixture(tmp_path, "spd.mtx", "%%MatrixMarket matrix coordinate real symmetric\n"
                     f"{n} {n} {len(lines)}\n" + "\n".join(lines) + "\n")
     sparse = si.load_matrix_market(path, symmetry=si.Symmetry.spd)
@@ -166,7 +166,7 @@ def test_gpu_ridge_hessian_random_rows(tmp_path):
     for s in range(m):
         idx = rng.choice(n, size=int(rng.integers(0, 9)), replace=False) + 1
         vals = np.round(rng.normal(size=idx.size), 6)
-        toks = [f"{k}:{v!r}" for k, v in zip(idx, vals)]
+        toks = [f"{int(k)}:{float(v)!r}" for k, v in zip(idx, vals)]
         if idx.size and s % 50 == 0:  # duplicated feature: contributes (v1 + v2)² like the reference's pair loop
             toks.append(f"{idx[0]}:0.25")
             dense[s, idx[0] - 1] += 0.25
