@@ -73,6 +73,23 @@ def _load():
     lib.or_run_adarbfgs.argtypes = [
         _i64, _pd, C.c_int, _i64, _d, _i64, _i64, C.c_uint64, C.c_int, _pd, _pd,
         C.POINTER(C.c_int), _pi64, _pi64, _pd, _pd, _pd, _i64, _pi64, _pi64, _i64]
+    lib.or_psb_step.argtypes = [_i64, _i64, _pd, _pd, _pd, _pd]
+    lib.or_aip_step.argtypes = [_i64, _i64, _pd, _pd, _pd, _pd]
+    lib.or_dfp_step.argtypes = [_i64, _i64, _pd, _pd, _pd, _pd, _pd, _pd]
+    lib.or_lu_inverse.argtypes = [_i64, _pd, _pd]
+    lib.or_flops_named.restype = _d
+    lib.or_flops_named.argtypes = [C.c_int, _i64, _i64]
+    lib.or_newton_schulz_step.argtypes = [_i64, _pd, _pd, _pd]
+    lib.or_newton_schulz_init.argtypes = [_i64, _pd, C.c_uint64, _pd]
+    lib.or_spectral_norm_estimate.argtypes = [_i64, _i64, _pd, C.c_int, C.c_uint64, _pd]
+    lib.or_mr_step_cached.argtypes = [_i64, _pd, _pd, _pd, _pd, _pd, _pd, C.POINTER(C.c_int)]
+    lib.or_mr_init.argtypes = [_i64, _pd, _pd]
+    lib.or_run_baseline.argtypes = [
+        _i64, _pd, C.c_int, _d, _i64, _i64, C.c_uint64, _pd, _pd, C.POINTER(C.c_int), _pi64, _pi64, _pd, _pd,
+        _pd, _i64, _pi64]
+    lib.or_run_inverter.argtypes = [
+        C.c_int, _i64, _pd, C.c_int, C.c_int, _i64, _d, _i64, _i64, C.c_uint64, C.c_int, _pd, _pd, _pd,
+        C.POINTER(C.c_int), _pi64, _pi64, _pd, _pd, _pd, _i64, _pi64, _pd, _pi64]
     return lib
 
 
@@ -292,3 +309,122 @@ def run_adarbfgs(a, q, *, rule=ADA_COLS, tol=1e-2, max_iters=1000, every_k=10, s
     m = min(hc.value, cap)
     hist = [(int(hk[i]), float(hr[i]), float(hf[i]), float(hs[i])) for i in range(m)]
     return RunResult(lo, term.value, k.value, hist, outcomes=outc)
+
+
+# ------------------------------------------------ row f3: other updates --
+UPDATE_BFGS, UPDATE_PSB, UPDATE_AIP, UPDATE_DFP = 0, 1, 2, 3
+PROB_UNIFORM, PROB_CONVENIENT = 0, 1
+
+
+def psb_step(x, a, s) -> np.ndarray:  # qn_updates.cpp:121-129
+    x, a, s = _f(x), _f(a), _f(s)
+    o = np.empty_like(x, order="F")
+    _check(lib().or_psb_step(x.shape[0], s.shape[1], _p(x), _p(a), _p(s), _p(o)))
+    return o
+
+
+def aip_step(x, a, s) -> np.ndarray:  # qn_updates.cpp:147-152
+    x, a, s = _f(x), _f(a), _f(s)
+    o = np.empty_like(x, order="F")
+    _check(lib().or_aip_step(x.shape[0], s.shape[1], _p(x), _p(a), _p(s), _p(o)))
+    return o
+
+
+def dfp_step(x, x_inv, a, s):  # qn_updates.cpp:154-174 -> (primal, inverse)
+    x, xi, a, s = _f(x), _f(x_inv), _f(a), _f(s)
+    o, oi = np.empty_like(x, order="F"), np.empty_like(x, order="F")
+    _check(lib().or_dfp_step(x.shape[0], s.shape[1], _p(x), _p(xi), _p(a), _p(s), _p(o), _p(oi)))
+    return o, oi
+
+
+def lu_inverse(m) -> np.ndarray:  # linalg.cpp:157-160
+    m = _f(m)
+    o = np.empty_like(m, order="F")
+    _check(lib().or_lu_inverse(m.shape[0], _p(m), _p(o)))
+    return o
+
+
+def flops_named(update: int, n: int, q: int) -> float:
+    return float(lib().or_flops_named(update, n, q))
+
+
+def run_inverter(a, q, *, update=UPDATE_BFGS, rule=RULE_GAUSSIAN, prob=PROB_UNIFORM, tol=1e-2, max_iters=1000,
+                 every_k=10, seed=0, max_redraws=100, x0=None):
+    """run_inverter for MethodSpec::named_method(bfgs|psb|aip|dfp) (simi.cpp:217-381).
+    Returns (RunResult, x_inv) with x_inv the tracked inverse for dfp (else None)."""
+    a = _f(a)
+    n = a.shape[0]
+    xo = np.empty((n, n), order="F")
+    xio = np.empty((n, n), order="F") if update == UPDATE_DFP else None
+    x0f = _f(x0) if x0 is not None else None
+    cap = max_iters + 2
+    hk = np.zeros(cap, dtype=np.int64)
+    hr, hf, hs = np.zeros(cap), np.zeros(cap), np.zeros(cap)
+    term, k, hc, red = C.c_int(), C.c_int64(), C.c_int64(), C.c_int64()
+    drift = C.c_double()
+    _check(lib().or_run_inverter(update, n, _p(a), rule, prob, q, tol, max_iters, every_k, seed, max_redraws,
+                                 _p(x0f) if x0f is not None else None, _p(xo),
+                                 _p(xio) if xio is not None else None, C.byref(term), C.byref(k),
+                                 hk.ctypes.data_as(_pi64), _p(hr), _p(hf), _p(hs), cap, C.byref(hc), C.byref(drift),
+                                 C.byref(red)))
+    m = min(hc.value, cap)
+    hist = [(int(hk[i]), float(hr[i]), float(hf[i]), float(hs[i])) for i in range(m)]
+    return RunResult(xo, term.value, k.value, hist, drift.value, red.value), xio
+
+
+# ------------------------------------------------ row f4: baselines --
+BASELINE_NS, BASELINE_MR = 0, 1
+
+
+def newton_schulz_step(x, a) -> np.ndarray:  # baselines.cpp:12-14
+    x, a = _f(x), _f(a)
+    o = np.empty_like(x, order="F")
+    _check(lib().or_newton_schulz_step(x.shape[0], _p(x), _p(a), _p(o)))
+    return o
+
+
+def newton_schulz_init(a, seed=0) -> np.ndarray:  # baselines.cpp:16-20
+    a = _f(a)
+    o = np.empty_like(a, order="F")
+    _check(lib().or_newton_schulz_init(a.shape[0], _p(a), seed, _p(o)))
+    return o
+
+
+def spectral_norm_estimate(m, iters=100, seed=0) -> float:  # linalg.cpp:106-129
+    m = _f(m)
+    est = C.c_double()
+    _check(lib().or_spectral_norm_estimate(m.shape[0], m.shape[1], _p(m), iters, seed, C.byref(est)))
+    return est.value
+
+
+def mr_step_cached(x, r, a):  # baselines.cpp:22-37 -> (x, r, alpha, stagnated)
+    x, r, a = _f(x), _f(r), _f(a)
+    xo, ro = np.empty_like(x, order="F"), np.empty_like(x, order="F")
+    al, stg = C.c_double(), C.c_int()
+    _check(lib().or_mr_step_cached(x.shape[0], _p(x), _p(r), _p(a), _p(xo), _p(ro), C.byref(al), C.byref(stg)))
+    return xo, ro, al.value, bool(stg.value)
+
+
+def mr_init(a) -> np.ndarray:  # baselines.cpp:45-50
+    a = _f(a)
+    o = np.empty_like(a, order="F")
+    _check(lib().or_mr_init(a.shape[0], _p(a), _p(o)))
+    return o
+
+
+def run_baseline(a, *, method=BASELINE_NS, tol=1e-2, max_iters=1000, every_k=10, seed=0, x0=None) -> RunResult:
+    """run_baseline (baselines.cpp:52-151)."""
+    a = _f(a)
+    n = a.shape[0]
+    xo = np.empty((n, n), order="F")
+    x0f = _f(x0) if x0 is not None else None
+    cap = max_iters + 2
+    hk = np.zeros(cap, dtype=np.int64)
+    hr, hf, hs = np.zeros(cap), np.zeros(cap), np.zeros(cap)
+    term, k, hc = C.c_int(), C.c_int64(), C.c_int64()
+    _check(lib().or_run_baseline(n, _p(a), method, tol, max_iters, every_k, seed,
+                                 _p(x0f) if x0f is not None else None, _p(xo), C.byref(term), C.byref(k),
+                                 hk.ctypes.data_as(_pi64), _p(hr), _p(hf), _p(hs), cap, C.byref(hc)))
+    m = min(hc.value, cap)
+    hist = [(int(hk[i]), float(hr[i]), float(hf[i]), float(hs[i])) for i in range(m)]
+    return RunResult(xo, term.value, k.value, hist)

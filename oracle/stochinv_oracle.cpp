@@ -537,6 +537,171 @@ double residual_dense(const Mat& a, const Mat& x) {  // simi.cpp:242-244
     return std::sqrt(s);
 }
 
+// ------------------------------------------- other rank-q updates (row f3) --
+// proj/src/qn_updates.cpp:121-129
+Mat psb_step(const Mat& x, const Mat& a, const Mat& s) {
+    const Mat as = mul(a, s);
+    const Mat gram = gemm(as, true, as, false);                    // SᵀAAS
+    const Mat t = gram_llt(gram, "psb_step").solve(as.t());        // q×n
+    const Mat u = mul(x, as) - s;                                  // (XA − I)S
+    const Mat mtheta = mul(u, t);
+    const Mat c = gemm(as, true, u, false);                        // q×q
+    return x - mtheta - mtheta.t() + gemm(t, true, mul(c, t), false);
+}
+
+// proj/src/qn_updates.cpp:147-152
+Mat aip_step(const Mat& x, const Mat& a, const Mat& s) {
+    const Mat as = mul(a, s);
+    const Mat gram = gemm(s, true, as, false);                     // SᵀAS
+    const Mat rhs = s.t() - gemm(as, true, x, false);              // Sᵀ − (AS)ᵀX
+    return x + mul(s, gram_llt(gram, "aip_step").solve(rhs));
+}
+
+struct IteratePair {
+    Mat primal, inverse;
+};
+
+// proj/src/qn_updates.cpp:154-174 (primal DFP update and the BFGS-form update of its inverse)
+IteratePair dfp_step(const Mat& x, const Mat& x_inv, const Mat& a, const Mat& s) {
+    const Mat as = mul(a, s);
+    const Mat gram = gemm(s, true, as, false);
+    const Llt llt = gram_llt(gram, "dfp_step");
+    const Mat t1 = llt.solve(as.t());
+    const Mat t2 = llt.solve(s.t());
+    const Mat k = mul(t2, x);
+    const Mat aox = mul(as, k);
+    const Mat aoa = mul(as, t1);
+    IteratePair next;
+    next.primal = x + aoa - aox - aox.t() + mul(as, mul(gemm(k, false, t2, true), as.t()));
+    const Mat hy = mul(x_inv, as);
+    const Mat gram2 = gemm(as, true, hy, false);
+    next.inverse = x_inv + mul(s, t2) - mul(hy, gram_llt(gram2, "dfp_step (inverse)").solve(hy.t()));
+    return next;
+}
+
+// Eigen::PartialPivLU(m).inverse() (linalg.cpp:157-160): row-pivoted LU, then solve against I
+Mat lu_inverse(const Mat& m) {
+    const Index n = m.r;
+    Mat lu = m;
+    std::vector<Index> piv(static_cast<size_t>(n));
+    for (Index i = 0; i < n; ++i) piv[size_t(i)] = i;
+    for (Index k = 0; k < n; ++k) {
+        Index p = k;
+        for (Index i = k + 1; i < n; ++i)
+            if (std::fabs(lu(i, k)) > std::fabs(lu(p, k))) p = i;
+        if (p != k) {
+            for (Index j = 0; j < n; ++j) std::swap(lu(k, j), lu(p, j));
+            std::swap(piv[size_t(k)], piv[size_t(p)]);
+        }
+        const double d = lu(k, k);
+        for (Index i = k + 1; i < n; ++i) {
+            lu(i, k) /= d;
+            const double l = lu(i, k);
+            for (Index j = k + 1; j < n; ++j) lu(i, j) -= l * lu(k, j);
+        }
+    }
+    Mat inv(n, n);
+    for (Index c = 0; c < n; ++c) {
+        std::vector<double> y(static_cast<size_t>(n));
+        for (Index i = 0; i < n; ++i) {
+            double v = piv[size_t(i)] == c ? 1.0 : 0.0;
+            for (Index j = 0; j < i; ++j) v -= lu(i, j) * y[size_t(j)];
+            y[size_t(i)] = v;
+        }
+        for (Index i = n - 1; i >= 0; --i) {
+            double v = y[size_t(i)];
+            for (Index j = i + 1; j < n; ++j) v -= lu(i, j) * inv(j, c);
+            inv(i, c) = v / lu(i, i);
+        }
+    }
+    return inv;
+}
+
+// flops.cpp:22-25, 32-35, 37-41
+double flops_psb(double n, double q) { return 8 * n * n * q + 8 * n * q * q + 2 * q * q * q + n * q + 3 * n * n; }
+double flops_aip(double n, double q) { return 6 * n * n * q + 4 * n * q * q + 2 * q * q * q + n * q + n * n; }
+double flops_dfp(double n, double q) { return 14 * n * n * q + 14 * n * q * q + 4 * q * q * q + 6 * n * n; }
+double flops_newton_schulz(double n) { return 4 * n * n * n + 2 * n * n; }   // flops.cpp:76-79
+double flops_minimal_residual(double n) { return 4 * n * n * n + 8 * n * n; }  // flops.cpp:81-85
+
+// --------------------------------------------------- baselines (row f4) ------
+// proj/src/baselines.cpp:12-14
+Mat newton_schulz_step(const Mat& x, const Mat& a) { return 2.0 * x - mul(x, mul(a, x)); }
+
+// proj/src/linalg.cpp:106-129 (power iteration on MᵀM from a seeded Gaussian start)
+double spectral_norm_estimate(const Mat& m, int iters, uint64_t seed) {
+    if (iters < 1) throw std::invalid_argument("spectral_norm_estimate: iters must be >= 1");
+    if (m.v.empty() || m.norm() == 0.0) return 0.0;
+    RngStream rng(seed);
+    Mat v = rng.gaussian_matrix(m.c, 1);
+    if (v.norm() == 0.0)
+        for (double& e : v.v) e = 1.0;
+    v = (1.0 / v.norm()) * v;
+    double est = 0.0;
+    for (int it = 0; it < iters; ++it) {
+        const Mat w = mul(m, v);
+        est = w.norm();
+        if (est == 0.0) {
+            v = rng.gaussian_matrix(m.c, 1);
+            v = (1.0 / v.norm()) * v;
+            continue;
+        }
+        v = gemm(m, true, w, false);
+        const double nv = v.norm();
+        if (nv == 0.0) break;
+        for (double& e : v.v) e /= nv;
+    }
+    return est;
+}
+
+// proj/src/baselines.cpp:16-20
+Mat newton_schulz_init(const Mat& a, uint64_t seed) {
+    const double s = spectral_norm_estimate(a, 100, seed);
+    if (s <= 0.0) throw ConfigError("newton_schulz_init: zero matrix");
+    return (0.99 / (s * s)) * a.t();
+}
+
+struct MrStep {
+    Mat x, r;
+    double alpha = 0.0;
+    bool stagnated = false;
+};
+
+// proj/src/baselines.cpp:22-37
+MrStep mr_step_cached(const Mat& x, const Mat& r, const Mat& a) {
+    MrStep out;
+    const Mat xr = mul(x, r);
+    const Mat axr = mul(a, xr);
+    const double denom = axr.squared_norm();
+    if (denom == 0.0) {
+        out.x = x;
+        out.r = r;
+        out.stagnated = true;
+        return out;
+    }
+    double num = 0.0;
+    for (size_t i = 0; i < r.v.size(); ++i) num += r.v[i] * axr.v[i];
+    out.alpha = num / denom;
+    out.x = x + out.alpha * xr;
+    out.r = r - out.alpha * axr;
+    return out;
+}
+
+// proj/src/baselines.cpp:45-50
+Mat mr_init(const Mat& a) {
+    const double denom = gemm(a, false, a, true).v.empty() ? 0.0 : a.squared_norm();  // Tr(AAᵀ) = ‖A‖_F²
+    if (denom == 0.0) throw ConfigError("mr_init: zero matrix");
+    double tr = 0.0;
+    for (Index i = 0; i < a.r; ++i) tr += a(i, i);
+    return (tr / denom) * Mat::identity(a.r);
+}
+
+Mat identity_minus(const Mat& m) {
+    Mat o = (-1.0) * m;
+    for (Index i = 0; i < o.r; ++i) o(i, i) += 1.0;
+    return o;
+}
+
 }  // namespace oracle
 
 // =================================================================== C ABI ==
@@ -857,6 +1022,292 @@ int or_run_adarbfgs(int64_t n, const double* a_in, int rule, int64_t q, double t
         *k_out = kfinal;
         *hcount = hc;
         out(l, l_out);
+    })
+}
+
+// --- row f3: psb / aip / dfp steps ---
+int or_psb_step(int64_t n, int64_t q, const double* x, const double* a, const double* s, double* x_out) {
+    OR_GUARD(out(psb_step(wrap(x, n, n), wrap(a, n, n), wrap(s, n, q)), x_out))
+}
+int or_aip_step(int64_t n, int64_t q, const double* x, const double* a, const double* s, double* x_out) {
+    OR_GUARD(out(aip_step(wrap(x, n, n), wrap(a, n, n), wrap(s, n, q)), x_out))
+}
+int or_dfp_step(int64_t n, int64_t q, const double* x, const double* x_inv, const double* a, const double* s,
+                double* x_out, double* x_inv_out) {
+    OR_GUARD({
+        const IteratePair p = dfp_step(wrap(x, n, n), wrap(x_inv, n, n), wrap(a, n, n), wrap(s, n, q));
+        out(p.primal, x_out);
+        out(p.inverse, x_inv_out);
+    })
+}
+int or_lu_inverse(int64_t n, const double* m, double* o) { OR_GUARD(out(lu_inverse(wrap(m, n, n)), o)) }
+double or_flops_named(int update, int64_t n, int64_t q) {
+    const double nn = double(n), qq = double(q);
+    switch (update) {
+        case 0: return flops_bfgs(nn, qq);
+        case 1: return flops_psb(nn, qq);
+        case 2: return flops_aip(nn, qq);
+        case 3: return flops_dfp(nn, qq);
+    }
+    return 0.0;
+}
+
+// --- row f4: Newton-Schulz / minimal residual ---
+int or_newton_schulz_step(int64_t n, const double* x, const double* a, double* x_out) {
+    OR_GUARD(out(newton_schulz_step(wrap(x, n, n), wrap(a, n, n)), x_out))
+}
+int or_newton_schulz_init(int64_t n, const double* a, uint64_t seed, double* x_out) {
+    OR_GUARD(out(newton_schulz_init(wrap(a, n, n), seed), x_out))
+}
+int or_spectral_norm_estimate(int64_t r, int64_t c, const double* m, int iters, uint64_t seed, double* est) {
+    OR_GUARD(*est = spectral_norm_estimate(wrap(m, r, c), iters, seed))
+}
+int or_mr_step_cached(int64_t n, const double* x, const double* r, const double* a, double* x_out, double* r_out,
+                      double* alpha, int* stagnated) {
+    OR_GUARD({
+        const MrStep st = mr_step_cached(wrap(x, n, n), wrap(r, n, n), wrap(a, n, n));
+        out(st.x, x_out);
+        out(st.r, r_out);
+        *alpha = st.alpha;
+        *stagnated = st.stagnated ? 1 : 0;
+    })
+}
+int or_mr_init(int64_t n, const double* a, double* x_out) { OR_GUARD(out(mr_init(wrap(a, n, n)), x_out)) }
+
+// run_baseline (baselines.cpp:52-151); method 0 = newton-schulz, 1 = minimal residual.
+int or_run_baseline(int64_t n, const double* a_in, int method, double tol, int64_t max_iters_, int64_t every_k,
+                    uint64_t seed, const double* x0, double* x_out, int* term, int64_t* k_out, int64_t* hk,
+                    double* hres, double* hflops, double* hsec, int64_t hcap, int64_t* hcount) {
+    OR_GUARD({
+        if (tol < 0.0) throw ConfigError("run_baseline: tol must be >= 0");
+        if (max_iters_ < 1) throw ConfigError("run_baseline: max_iters must be >= 1");
+        const bool ns = method == 0;
+        const Mat a = wrap(a_in, n, n);
+        Mat x = x0 ? wrap(x0, n, n) : (ns ? newton_schulz_init(a, seed) : mr_init(a));
+        Mat r = identity_minus(mul(a, x));
+        const double base = r.norm();
+        int64_t hc = 0;
+        double flops_total = 0.0, seconds = 0.0;
+        long k = 0;
+        auto record = [&](double rel) {
+            if (hc < hcap) {
+                hk[hc] = k;
+                hres[hc] = rel;
+                hflops[hc] = flops_total;
+                hsec[hc] = seconds;
+            }
+            ++hc;
+        };
+        *term = max_iters;
+        long kfinal = max_iters_;
+        g_err.clear();
+        if (base == 0.0) {
+            record(0.0);
+            *term = tol_reached;
+            kfinal = 0;
+        } else {
+            record(1.0);
+            for (k = 1; k <= max_iters_; ++k) {
+                const auto start = std::chrono::steady_clock::now();
+                bool stagnated = false;
+                Mat next;
+                if (ns) {
+                    next = newton_schulz_step(x, a);
+                } else {
+                    MrStep st = mr_step_cached(x, r, a);
+                    stagnated = st.stagnated;
+                    next = std::move(st.x);
+                    r = std::move(st.r);
+                }
+                seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count();
+                flops_total += ns ? flops_newton_schulz(double(n)) : flops_minimal_residual(double(n));
+                if (!next.all_finite()) {
+                    *term = error;
+                    g_err = "diverged: non-finite entries at iteration " + std::to_string(k);
+                    kfinal = k;
+                    break;
+                }
+                x = std::move(next);
+                if (stagnated) {
+                    const double rel = r.norm() / base;
+                    record(rel);
+                    *term = rel <= tol ? tol_reached : error;
+                    if (*term == error)
+                        g_err = "minimal residual stagnated (zero step denominator) at iteration " + std::to_string(k);
+                    kfinal = k;
+                    break;
+                }
+                if (k == 1 || k == max_iters_ || k % every_k == 0) {
+                    r = identity_minus(mul(a, x));
+                    const double rel = r.norm() / base;
+                    record(rel);
+                    if (!std::isfinite(rel)) {
+                        *term = error;
+                        g_err = "diverged: residual overflow at iteration " + std::to_string(k);
+                        kfinal = k;
+                        break;
+                    }
+                    if (rel <= tol) {
+                        *term = tol_reached;
+                        kfinal = k;
+                        break;
+                    }
+                }
+            }
+        }
+        *k_out = kfinal;
+        *hcount = hc;
+        out(x, x_out);
+    })
+}
+
+// run_inverter for the named updates on the GPU path (simi.cpp:217-381):
+// update 0 bfgs, 1 psb, 2 aip, 3 dfp.  rule 0 = gaussian(q), 1 = coordinate_block(n, q)
+// with probabilities prob (0 uniform, 1 convenient: simi.cpp:121-150 per update).
+// x_inv_out receives the tracked inverse for dfp (may be NULL otherwise).
+int or_run_inverter(int update, int64_t n, const double* a_in, int rule, int prob, int64_t q, double tol,
+                    int64_t max_iters_, int64_t every_k, uint64_t seed, int max_redraws, const double* x0,
+                    double* x_out, double* x_inv_out, int* term, int64_t* k_out, int64_t* hk, double* hres,
+                    double* hflops, double* hsec, int64_t hcap, int64_t* hcount, double* max_drift,
+                    int64_t* redraws_out) {
+    OR_GUARD({
+        if (tol < 0.0) throw ConfigError("run_inverter: tol must be >= 0");
+        if (max_iters_ < 1) throw ConfigError("run_inverter: max_iters must be >= 1");
+        if (max_redraws < 0) throw ConfigError("run_inverter: max_redraws must be >= 0");
+        if (every_k < 1) throw ConfigError("run_inverter: residual_every_k must be >= 1");
+        if (q < 1 || q > n) throw ConfigError("SketchRule: q must satisfy 1 <= q <= n");
+        const Mat a = wrap(a_in, n, n);
+        const bool dfp = update == 3, symmetric = update != 2;
+        Mat x = x0 ? wrap(x0, n, n) : Mat::identity(n);
+        Mat x_inv = dfp ? (x0 ? lu_inverse(x) : Mat::identity(n)) : Mat();
+        std::vector<std::vector<Index>> blocks;
+        std::vector<double> p;
+        if (rule == 1) {
+            blocks = contiguous_partition(n, q);
+            p.assign(blocks.size(), 1.0 / double(blocks.size()));
+            if (prob == 1) {  // convenient (simi.cpp:121-150)
+                std::vector<double> w(static_cast<size_t>(n));
+                if (update == 0 || update == 2) {  // Tr(SᵢᵀASᵢ)
+                    for (Index j = 0; j < n; ++j) w[size_t(j)] = a(j, j);
+                } else if (update == 1) {  // ‖A Sᵢ‖_F² (col side, identity weight)
+                    for (Index j = 0; j < n; ++j) {
+                        double t = 0.0;
+                        for (Index i = 0; i < n; ++i) t += a(i, j) * a(i, j);
+                        w[size_t(j)] = t;
+                    }
+                } else {  // Tr(SᵢᵀA⁻¹Sᵢ)
+                    const Llt llt(a);
+                    const Mat ai = llt.solve(Mat::identity(n));
+                    for (Index j = 0; j < n; ++j) w[size_t(j)] = ai(j, j);
+                }
+                double sum = 0.0;
+                for (size_t i = 0; i < blocks.size(); ++i) {
+                    double t = 0.0;
+                    for (Index j : blocks[i]) t += w[size_t(j)];
+                    if (!(t > 0.0))
+                        throw ConfigError(update == 1 ? "convenient_probabilities: family member with zero sketched norm"
+                                                      : "trace probabilities: member with non-positive sketched trace");
+                    p[i] = t;
+                    sum += t;
+                }
+                for (double& v : p) v /= sum;
+            }
+        }
+        auto residual = [&]() { return residual_dense(a, dfp ? x_inv : x); };
+        int64_t hc = 0;
+        double flops_total = 0.0, seconds = 0.0, drift_max = 0.0;
+        int64_t redraws = 0;
+        long k = 0;
+        long kfinal = max_iters_;
+        auto record = [&](double rel) {
+            if (hc < hcap) {
+                hk[hc] = k;
+                hres[hc] = rel;
+                hflops[hc] = flops_total;
+                hsec[hc] = seconds;
+            }
+            ++hc;
+        };
+        const double base = residual();
+        *term = max_iters;
+        bool done = false;
+        g_err.clear();
+        if (base == 0.0) {
+            record(0.0);
+            *term = tol_reached;
+            done = true;
+            kfinal = 0;
+        } else {
+            record(1.0);
+        }
+        RngStream rng(seed);
+        for (k = 1; !done && k <= max_iters_; ++k) {
+            Mat next, next_inv;
+            bool stepped = false;
+            for (int failures = 0; !stepped; ++failures) {
+                if (failures > max_redraws) {
+                    *term = error;
+                    g_err = "sketch rejection limit exceeded";
+                    done = true;
+                    kfinal = k;
+                    break;
+                }
+                Mat s;
+                if (rule == 0) {
+                    s = rng.gaussian_matrix(n, q);
+                } else {
+                    const Index i = rng.categorical(p.data(), Index(p.size()));
+                    s = coordinate_block_member(n, blocks[size_t(i)]);
+                }
+                const auto start = std::chrono::steady_clock::now();
+                try {
+                    switch (update) {
+                        case 0: next = bfgs_step(x, a, s); break;
+                        case 1: next = psb_step(x, a, s); break;
+                        case 2: next = aip_step(x, a, s); break;
+                        default: {
+                            IteratePair pr = dfp_step(x, x_inv, a, s);
+                            next = std::move(pr.primal);
+                            next_inv = std::move(pr.inverse);
+                        }
+                    }
+                } catch (const NumericalError&) {
+                    ++redraws;
+                    continue;
+                }
+                seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count();
+                flops_total += or_flops_named(update, n, s.c);
+                stepped = true;
+            }
+            if (done) break;
+            if (!next.all_finite() || (dfp && !next_inv.all_finite())) {
+                *term = error;
+                g_err = "diverged: non-finite entries at iteration " + std::to_string(k);
+                kfinal = k;
+                break;
+            }
+            x = std::move(next);
+            if (dfp) x_inv = std::move(next_inv);
+            if (symmetric) {
+                drift_max = std::max(drift_max, symmetrize_inplace(n, x.data()));
+                if (dfp) symmetrize_inplace(n, x_inv.data());
+            }
+            if (k == 1 || k == max_iters_ || k % every_k == 0) {
+                const double rel = residual() / base;
+                record(rel);
+                if (rel <= tol) {
+                    *term = tol_reached;
+                    kfinal = k;
+                    break;
+                }
+            }
+        }
+        *k_out = kfinal;
+        *hcount = hc;
+        *max_drift = drift_max;
+        *redraws_out = redraws;
+        out(x, x_out);
+        if (dfp && x_inv_out) out(x_inv, x_inv_out);
     })
 }
 

@@ -278,3 +278,176 @@ def test_uniform_subset_distinct():
     for _ in range(50):
         idx = rng.uniform_subset(64, 16)
         assert len(set(idx.tolist())) == 16 and idx.min() >= 0 and idx.max() < 64
+
+
+# ------------------------------------------------- row f3: psb / aip / dfp --
+def random_symmetric(n, rng):  # tests/helpers.hpp:24-27
+    b = rng.gaussian_matrix(n, n)
+    return 0.5 * (b + b.T)
+
+
+def row_oracle(x, a, s, w):  # tests/helpers.hpp:69-75
+    n = x.shape[0]
+    sa = s.T @ a
+    return kkt_projection(x, w, kron(np.eye(n), sa), (s.T - sa @ x).reshape(-1, order="F"))
+
+
+def test_psb_matches_symmetric_oracle():  # test_qn_updates.cpp:119-132
+    rng = O.RngStream(23)
+    a = random_symmetric(4, rng)
+    x = random_symmetric(4, rng)
+    s = coordinate_sketch(4, [1, 2])
+    stepped = O.psb_step(x, a, s)
+    oracle = sym_oracle(x, a, s, np.eye(4))
+    assert np.linalg.norm(stepped - oracle) <= 1e-8 * max(1.0, np.linalg.norm(oracle))
+    assert np.linalg.norm(stepped - stepped.T) <= 1e-10
+    assert np.linalg.norm(stepped @ a @ s - s) <= 1e-9
+
+
+def test_aip_equals_row_update_with_inverse_weight():  # test_qn_updates.cpp:160-174
+    rng = O.RngStream(31)
+    a = random_spd(4, rng)
+    x = random_symmetric(4, rng)
+    s = coordinate_sketch(4, [0, 3])
+    stepped = O.aip_step(x, a, s)
+    a_inv = O.lu_inverse(a)
+    oracle = row_oracle(x, a, s, a_inv)
+    assert np.linalg.norm(stepped - oracle) <= 1e-7 * max(1.0, np.linalg.norm(oracle))
+    assert np.linalg.norm(s.T @ a @ stepped - s.T) <= 1e-9
+
+
+def test_dfp_full_sketch_recurrence_and_woodbury_pair():  # test_qn_updates.cpp:176-197
+    rng = O.RngStream(37)
+    a = random_spd(4, rng)
+    x, x_inv = np.eye(4), np.eye(4)
+    full_p, full_i = O.dfp_step(x, x_inv, a, np.eye(4))
+    assert np.linalg.norm(full_p - a) <= 1e-9 * np.linalg.norm(a)
+    assert np.linalg.norm(full_i @ a - np.eye(4)) <= 1e-8
+    s = coordinate_sketch(4, [1, 2])
+    nxt_p, nxt_i = O.dfp_step(x, x_inv, a, s)
+    omega = s @ O.lu_inverse(s.T @ a @ s) @ s.T
+    eye = np.eye(4)
+    expected = a + (eye - a @ omega) @ (x - a) @ (eye - omega @ a)
+    assert np.linalg.norm(nxt_p - expected) <= 1e-9 * max(1.0, np.linalg.norm(expected))
+    assert np.linalg.norm(nxt_p - nxt_p.T) <= 1e-10
+    assert np.linalg.norm(nxt_i - O.lu_inverse(nxt_p)) <= 1e-8
+
+
+def test_rank_deficient_grams_raise_for_psb():  # test_qn_updates.cpp:253-261
+    rng = O.RngStream(47)
+    a = rng.gaussian_matrix(3, 3)
+    with pytest.raises(O.NumericalError):
+        O.psb_step(np.eye(3), a, np.zeros((3, 1)))
+    with pytest.raises(O.NumericalError):
+        O.aip_step(np.eye(3), random_spd(3, rng), np.ones((3, 2)))
+
+
+def test_lu_inverse_general():
+    rng = O.RngStream(5)
+    m = rng.gaussian_matrix(7, 7) + 3 * np.eye(7)
+    assert np.allclose(O.lu_inverse(m) @ m, np.eye(7), atol=1e-12)
+
+
+@pytest.mark.parametrize("update", [O.UPDATE_PSB, O.UPDATE_AIP, O.UPDATE_DFP, O.UPDATE_BFGS])
+def test_run_inverter_named_updates_converge(update):  # test_simi.cpp convergence contract, per update
+    rng = O.RngStream(53)
+    a = random_spd(12, rng)
+    res, xi = O.run_inverter(a, 3, update=update, rule=O.RULE_COORDINATE_BLOCK, tol=1e-8, max_iters=4000,
+                             every_k=10, seed=2)
+    assert res.termination == 0
+    tracked = xi if update == O.UPDATE_DFP else res.x
+    assert np.linalg.norm(np.eye(12) - a @ tracked) <= 1e-7 * np.linalg.norm(np.eye(12) - a)
+    assert res.history[0][1] == 1.0
+    if update != O.UPDATE_AIP:
+        assert np.array_equal(res.x, res.x.T)
+
+
+def test_run_inverter_bfgs_general_equals_bfgs_driver():
+    rng = O.RngStream(59)
+    a = random_spd(16, rng)
+    r1, _ = O.run_inverter(a, 4, update=O.UPDATE_BFGS, rule=O.RULE_GAUSSIAN, tol=0.0, max_iters=25, every_k=5, seed=9)
+    r2 = O.run_inverter_bfgs(a, 4, rule=O.RULE_GAUSSIAN, tol=0.0, max_iters=25, every_k=5, seed=9)
+    assert np.array_equal(r1.x, r2.x)
+    assert r1.history == [(k, r, f, r1.history[i][3]) for i, (k, r, f, _) in enumerate(r2.history)]
+
+
+def test_flop_polynomials():  # flops.cpp:22-46
+    assert O.flops_named(O.UPDATE_PSB, 3, 2) == 8 * 18 + 8 * 12 + 16 + 6 + 27
+    assert O.flops_named(O.UPDATE_AIP, 3, 2) == 6 * 18 + 4 * 12 + 16 + 6 + 9
+    assert O.flops_named(O.UPDATE_DFP, 3, 2) == 14 * 18 + 14 * 12 + 32 + 54
+
+
+# ---------------------------------------------------- row f4: baselines --
+def test_newton_schulz_scalar_and_quadratic_identity():  # test_baselines.cpp:14-33
+    a = np.array([[2.0]])
+    x = O.newton_schulz_step(np.array([[0.4]]), a)
+    assert x[0, 0] == pytest.approx(0.48, rel=1e-14)
+    x = O.newton_schulz_step(x, a)
+    assert x[0, 0] == pytest.approx(0.4992, rel=1e-14)
+    assert O.newton_schulz_init(a)[0, 0] == pytest.approx(0.495, rel=1e-8)
+    rng = O.RngStream(91)
+    m = random_spd(6, rng)
+    x0 = O.newton_schulz_init(m, 3)
+    res = np.eye(6) - m @ x0
+    x1 = O.newton_schulz_step(x0, m)
+    assert np.linalg.norm(np.eye(6) - m @ x1 - res @ res) <= 1e-10 * max(1.0, np.linalg.norm(res))
+
+
+def test_minimal_residual_scalar_and_init():  # test_baselines.cpp:35-50
+    a = np.array([[2.0]])
+    xo, _, alpha, stg = O.mr_step_cached(np.array([[0.25]]), np.eye(1) - 0.25 * a, a)
+    assert xo[0, 0] == pytest.approx(0.5, rel=1e-14) and alpha == pytest.approx(2.0) and not stg
+    init = O.mr_init(np.diag([1.0, 3.0]))
+    assert np.linalg.norm(init - 0.4 * np.eye(2)) <= 1e-14
+    with pytest.raises(O.ConfigError):
+        O.mr_init(np.zeros((2, 2)))
+
+
+def test_minimal_residual_monotone():  # test_baselines.cpp:52-71
+    rng = O.RngStream(93)
+    a = random_spd(8, rng)
+    x = O.mr_init(a)
+    r = np.eye(8) - a @ x
+    prev = np.linalg.norm(r)
+    for _ in range(1000):
+        xn, rn, _, stg = O.mr_step_cached(x, r, a)
+        if stg:
+            break
+        x, r = xn, rn
+        cur = np.linalg.norm(r)
+        assert cur <= prev * (1.0 + 1e-12)
+        prev = cur
+    assert np.linalg.norm(r - (np.eye(8) - a @ x)) <= 1e-8 * max(1.0, prev)
+    assert prev <= 0.5 * np.linalg.norm(np.eye(8) - a @ O.mr_init(a))
+
+
+def test_mr_stagnates_at_exact_inverse():  # test_baselines.cpp:73-83
+    d = np.diag([2.0, 4.0])
+    xo, _, alpha, stg = O.mr_step_cached(np.diag([0.5, 0.25]), np.zeros((2, 2)), d)
+    assert stg and alpha == 0.0 and np.array_equal(xo, np.diag([0.5, 0.25]))
+
+
+def test_run_baseline_converges_and_contract():  # test_baselines.cpp:85-123, 125-146
+    rng = O.RngStream(97)
+    a = random_spd(12, rng)
+    ns = O.run_baseline(a, method=O.BASELINE_NS, tol=1e-8, max_iters=200, every_k=5)
+    assert ns.termination == 0
+    assert np.linalg.norm(a @ ns.x - np.eye(12)) <= 1e-6 * np.linalg.norm(a)
+    assert ns.history[0][1] == 1.0 and ns.history[-1][2] > 0.0
+    mr = O.run_baseline(a, method=O.BASELINE_MR, tol=1e-2, max_iters=5000, every_k=25)
+    assert mr.termination == 0 and mr.history[-1][1] <= 1e-2
+    stiff = random_spd(10, O.RngStream(101))
+    div = O.run_baseline(stiff, method=O.BASELINE_NS, max_iters=200, x0=np.eye(10))
+    assert div.termination == 2 and "diverged" in O.lib().or_last_error().decode()
+    with pytest.raises(O.ConfigError):
+        O.run_baseline(a, tol=-1.0)
+    exact = O.run_baseline(np.diag([2.0, 4.0]), x0=np.diag([0.5, 0.25]))
+    assert exact.termination == 0 and exact.history[0][1] == 0.0
+
+
+def test_spectral_norm_estimate():
+    rng = O.RngStream(3)
+    m = rng.gaussian_matrix(9, 6)
+    est = O.spectral_norm_estimate(m, 100, 1)
+    assert est <= np.linalg.norm(m, 2) * (1 + 1e-12)
+    assert est == pytest.approx(np.linalg.norm(m, 2), rel=1e-6)
