@@ -88,7 +88,13 @@ typedef struct si_inverter_config {
     const double* x0_host;    /* optional X0 (RBFGS) or L0 (AdaRBFGS), n×n; NULL = identity */
     si_checkpoint_fn on_checkpoint;
     void* user;
+    int update;               /* si_update: MethodSpec::named_method for run_inverter (default bfgs) */
 } si_inverter_config;
+
+/* The named updates on the B200 path (qn_updates.hpp UpdateName subset, SURVEY §8 a1 + f3). */
+typedef enum si_update { SI_UPDATE_BFGS = 0, SI_UPDATE_PSB = 1, SI_UPDATE_AIP = 2, SI_UPDATE_DFP = 3 } si_update;
+/* run_baseline methods (baselines.hpp:36). */
+typedef enum si_baseline { SI_BASELINE_NEWTON_SCHULZ = 0, SI_BASELINE_MINIMAL_RESIDUAL = 1 } si_baseline;
 
 /* RunResult + InverterState scalars (simi.hpp:82-96) */
 typedef struct si_run_result {
@@ -170,6 +176,21 @@ int si_adarbfgs_update_factor(si_context* ctx, int64_t n, int64_t q, const doubl
 int si_adaptive_block_probabilities(si_context* ctx, int64_t n, const double* l_host, const double* a_host,
                                     int64_t nblocks, const int64_t* block_offsets, const int64_t* block_indices,
                                     double* p_out_host);
+/* psb_step / aip_step (qn_updates.hpp, qn_updates.cpp:121-129, 147-152) and the dfp_step pair
+ * (:154-174), host buffers; SI_ERR_RESAMPLE on a non-PD sketched Gram. */
+int si_psb_step(si_context* ctx, int64_t n, int64_t q, const double* x_host, const double* a_host,
+                const double* s_host, double* x_out_host);
+int si_aip_step(si_context* ctx, int64_t n, int64_t q, const double* x_host, const double* a_host,
+                const double* s_host, double* x_out_host);
+int si_dfp_step(si_context* ctx, int64_t n, int64_t q, const double* x_host, const double* x_inv_host,
+                const double* a_host, const double* s_host, double* x_out_host, double* x_inv_out_host);
+/* Newton-Schulz / minimal-residual building blocks (baselines.hpp:13-33, linalg.cpp:106-129). */
+int si_newton_schulz_step(si_context* ctx, int64_t n, const double* x_host, const double* a_host, double* x_out_host);
+int si_newton_schulz_init(si_context* ctx, si_problem* prob, uint64_t seed, double* x_out_host);
+int si_spectral_norm_estimate(si_context* ctx, si_problem* prob, int iters, uint64_t seed, double* out);
+int si_mr_step_cached(si_context* ctx, int64_t n, const double* x_host, const double* r_host, const double* a_host,
+                      double* x_out_host, double* r_out_host, double* alpha, int* stagnated);
+int si_mr_init(si_context* ctx, si_problem* prob, double* x_out_host);
 /* ||I - A X||_F (simi.cpp:242-244). */
 int si_residual(si_context* ctx, si_problem* prob, const double* x_host, double* out);
 
@@ -178,6 +199,16 @@ int si_residual(si_context* ctx, si_problem* prob, const double* x_host, double*
  * simi.hpp:105 / simi.cpp:217-381.  x_out_host (n×n) receives the final X. */
 int si_run_inverter(si_context* ctx, si_problem* prob, const si_inverter_config* cfg, double* x_out_host,
                     si_history_point* history, int64_t history_cap, si_run_result* result);
+/* run_inverter for any si_update (cfg->update); x_inv_out_host (optional) receives the tracked
+ * inverse iterate of dfp (simi.cpp:227-229; tracks_inverse_iterate), ignored otherwise. */
+int si_run_inverter_pair(si_context* ctx, si_problem* prob, const si_inverter_config* cfg, double* x_out_host,
+                         double* x_inv_out_host, si_history_point* history, int64_t history_cap,
+                         si_run_result* result);
+/* RunResult run_baseline(const BaselineConfig&), baselines.hpp:68 / baselines.cpp:52-151: method
+ * si_baseline; uses cfg->tol, max_iters, time_budget_seconds, seed (spectral-norm start vector),
+ * residual_every_k, track_*, x0_host (NULL = the method's paper initialisation), on_checkpoint. */
+int si_run_baseline(si_context* ctx, si_problem* prob, int method, const si_inverter_config* cfg,
+                    double* x_out_host, si_history_point* history, int64_t history_cap, si_run_result* result);
 /* RunResult run_adarbfgs(const AdaConfig&), adarbfgs.hpp:59 / adarbfgs.cpp:91-200.
  * l_out_host (optional) receives L; x_out_host (optional) receives X = L Lᵀ. */
 int si_run_adarbfgs(si_context* ctx, si_problem* prob, const si_inverter_config* cfg, double* l_out_host,

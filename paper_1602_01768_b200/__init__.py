@@ -12,6 +12,8 @@ _lib.load()
 
 from .api import (  # noqa: E402
     AdaConfig,
+    BaselineConfig,
+    BaselineMethod,
     ConfigError,
     Context,
     CudaError,
@@ -32,7 +34,17 @@ from .api import (  # noqa: E402
     Symmetry,
     Termination,
     TrackOptions,
+    UpdateName,
     adaptive_block_probabilities,
+    aip_step,
+    dfp_step,
+    mr_init,
+    mr_step_cached,
+    newton_schulz_init,
+    newton_schulz_step,
+    psb_step,
+    run_baseline,
+    spectral_norm_estimate,
     adarbfgs_update_factor,
     bfgs_step,
     build_ridge_hessian,

@@ -26,7 +26,7 @@ class InverterConfigC(C.Structure):
         ("sketch", ci), ("probabilities", ci), ("q", i64), ("tol", d), ("max_iters", i64),
         ("time_budget_seconds", d), ("seed", u64), ("residual_every_k", i64), ("track_flops", ci),
         ("track_wall_time", ci), ("max_redraws", ci), ("x0_host", pd), ("on_checkpoint", CHECKPOINT_FN),
-        ("user", vp),
+        ("user", vp), ("update", ci),
     ]
 
 
@@ -69,6 +69,18 @@ _SIGS = {
     "si_residual": (ci, [vp, vp, pd, pd]),
     "si_run_inverter": (ci, [vp, vp, C.POINTER(InverterConfigC), pd, C.POINTER(HistoryPoint), i64,
                              C.POINTER(RunResultC)]),
+    "si_run_inverter_pair": (ci, [vp, vp, C.POINTER(InverterConfigC), pd, pd, C.POINTER(HistoryPoint), i64,
+                                  C.POINTER(RunResultC)]),
+    "si_run_baseline": (ci, [vp, vp, ci, C.POINTER(InverterConfigC), pd, C.POINTER(HistoryPoint), i64,
+                             C.POINTER(RunResultC)]),
+    "si_psb_step": (ci, [vp, i64, i64, pd, pd, pd, pd]),
+    "si_aip_step": (ci, [vp, i64, i64, pd, pd, pd, pd]),
+    "si_dfp_step": (ci, [vp, i64, i64, pd, pd, pd, pd, pd, pd]),
+    "si_newton_schulz_step": (ci, [vp, i64, pd, pd, pd]),
+    "si_newton_schulz_init": (ci, [vp, vp, u64, pd]),
+    "si_spectral_norm_estimate": (ci, [vp, vp, ci, u64, pd]),
+    "si_mr_step_cached": (ci, [vp, i64, pd, pd, pd, pd, pd, pd, C.POINTER(ci)]),
+    "si_mr_init": (ci, [vp, vp, pd]),
     "si_run_adarbfgs": (ci, [vp, vp, C.POINTER(InverterConfigC), pd, pd, C.POINTER(HistoryPoint), i64,
                              C.POINTER(RunResultC)]),
     "si_solver_create": (ci, [vp, vp, ci, ci, i64, u64, C.POINTER(vp)]),

@@ -152,6 +152,27 @@ class SketchKind(enum.IntEnum):  # si_sketch_kind
     adaptive_factor_gauss_device = 6
 
 
+class UpdateName(enum.IntEnum):  # qn_updates.hpp UpdateName, the members on the B200 path (si_update)
+    bfgs = 0
+    psb = 1
+    aip = 2
+    dfp = 3
+
+    @classmethod
+    def _missing_(cls, value):  # update_name_from_string (qn_updates.cpp:55-65) for the CLI vocabulary
+        if isinstance(value, str):
+            for m in cls:
+                if m.name == value:
+                    return m
+            raise ConfigError(f"unknown update name: {value}")
+        return None
+
+
+class BaselineMethod(enum.IntEnum):  # baselines.hpp:36
+    newton_schulz = 0
+    minimal_residual = 1
+
+
 class Termination(enum.IntEnum):  # simi.hpp:80
     tol_reached = 0
     max_iters = 1
@@ -355,6 +376,7 @@ class InverterState:  # simi.hpp:82-90
     flops: float = 0.0
     seconds: float = 0.0
     l: Optional[np.ndarray] = None  # AdaRBFGS factor (FactoredState::l)
+    x_inv: Optional[np.ndarray] = None  # dfp's tracked inverse iterate (simi.hpp:86)
     redraws: int = 0
 
 
@@ -377,6 +399,21 @@ class InverterConfig:  # simi.hpp:59-71 (named bfgs method)
     x0: Optional[np.ndarray] = None
     max_redraws: int = 100
     on_checkpoint: Optional[Callable[[HistoryPoint], None]] = None  # addition
+    return_x: bool = True
+    update: UpdateName = UpdateName.bfgs  # MethodSpec::named_method(update)
+
+
+@dataclass
+class BaselineConfig:  # baselines.hpp:55-64
+    a: ProblemMatrix
+    method: BaselineMethod = BaselineMethod.newton_schulz
+    tol: float = 1e-2
+    max_iters: int = 1000
+    time_budget_seconds: float = 0.0
+    seed: int = 0  # spectral-norm start vector for the paper init
+    track: TrackOptions = field(default_factory=TrackOptions)
+    x0: Optional[np.ndarray] = None  # default: the method's paper initialisation
+    on_checkpoint: Optional[Callable[[HistoryPoint], None]] = None
     return_x: bool = True
 
 
@@ -426,7 +463,8 @@ def _cfg(rule: SketchRule, tol, max_iters, budget, seed, track, x0, max_redraws,
 
 
 def run_inverter(config: InverterConfig, out: Optional[np.ndarray] = None) -> RunResult:
-    """RunResult run_inverter(const InverterConfig&) for MethodSpec::named_method(bfgs) (simi.cpp:217-381).
+    """RunResult run_inverter(const InverterConfig&) for MethodSpec::named_method(config.update)
+    (simi.cpp:217-381): bfgs, psb, aip or dfp; state.x_inv is dfp's tracked inverse.
 
     `out` (optional): caller-provided n×n Fortran-ordered float64 buffer for the
     final X (e.g. pinned host memory)."""
@@ -436,8 +474,10 @@ def run_inverter(config: InverterConfig, out: Optional[np.ndarray] = None) -> Ru
     n = a.n()
     if config.x0 is not None and np.shape(config.x0) != (n, n):
         raise ConfigError("run_inverter: x0 dimension mismatch")
+    update = UpdateName(config.update)
     c, keep = _cfg(config.rule, config.tol, config.max_iters, config.time_budget_seconds, config.seed, config.track,
                    config.x0, config.max_redraws, config.on_checkpoint)
+    c.update = int(update)
     cap = int(config.max_iters) // max(1, config.track.residual_every_k) + 4
     hist = (L.HistoryPoint * cap)()
     res = L.RunResultC()
@@ -447,14 +487,38 @@ def run_inverter(config: InverterConfig, out: Optional[np.ndarray] = None) -> Ru
         x = out
     else:
         x = np.empty((n, n), order="F") if config.return_x else None
-    _check(L.load().si_run_inverter(a.ctx.handle, a.handle, C.byref(c), _pd(x) if x is not None else None, hist, cap,
-                                    C.byref(res)))
+    xi = np.empty((n, n), order="F") if (update == UpdateName.dfp and config.return_x) else None
+    _check(L.load().si_run_inverter_pair(a.ctx.handle, a.handle, C.byref(c), _pd(x) if x is not None else None,
+                                         _pd(xi) if xi is not None else None, hist, cap, C.byref(res)))
     del keep
     m = min(int(res.history_count), cap)
     st = InverterState(x=x, k=int(res.k),
                        history=[HistoryPoint(int(h.k), h.residual, h.flops, h.seconds) for h in hist[:m]],
                        max_symmetry_drift=res.max_symmetry_drift, flops=res.flops, seconds=res.seconds,
-                       redraws=int(res.redraws))
+                       redraws=int(res.redraws), x_inv=xi)
+    return RunResult(st, Termination(res.termination), res.message.decode(errors="replace"))
+
+
+def run_baseline(config: BaselineConfig) -> RunResult:
+    """RunResult run_baseline(const BaselineConfig&) (baselines.cpp:52-151): Newton–Schulz
+    X⁺ = 2X − XAX or minimal residual with the carried residual, on the GPU."""
+    a = config.a
+    n = a.n()
+    if config.x0 is not None and np.shape(config.x0) != (n, n):
+        raise ConfigError("run_baseline: x0 dimension mismatch")
+    c, keep = _cfg(SketchRule.gaussian(1), config.tol, config.max_iters, config.time_budget_seconds, config.seed,
+                   config.track, config.x0, 0, config.on_checkpoint)
+    cap = int(config.max_iters) // max(1, config.track.residual_every_k) + 4
+    hist = (L.HistoryPoint * cap)()
+    res = L.RunResultC()
+    x = np.empty((n, n), order="F") if config.return_x else None
+    _check(L.load().si_run_baseline(a.ctx.handle, a.handle, int(BaselineMethod(config.method)), C.byref(c),
+                                    _pd(x) if x is not None else None, hist, cap, C.byref(res)))
+    del keep
+    m = min(int(res.history_count), cap)
+    st = InverterState(x=x, k=int(res.k),
+                       history=[HistoryPoint(int(h.k), h.residual, h.flops, h.seconds) for h in hist[:m]],
+                       flops=res.flops, seconds=res.seconds)
     return RunResult(st, Termination(res.termination), res.message.decode(errors="replace"))
 
 
@@ -497,6 +561,81 @@ def bfgs_step(x, a, s, *, context: Optional[Context] = None) -> np.ndarray:
         raise ConfigError("bfgs_step: dimension mismatch")
     out = np.empty((n, n), order="F")
     _check(L.load().si_bfgs_step(ctx.handle, n, q, _pd(x), _pd(a), _pd(s), _pd(out)))
+    return out
+
+
+def _named_step(fn, name, x, a, s, context):
+    ctx = context or default_context()
+    x, a, s = _f64(x), _f64(a), _f64(s)
+    n, q = s.shape
+    if x.shape != (n, n) or a.shape != (n, n):
+        raise ConfigError(f"{name}: dimension mismatch")
+    out = np.empty((n, n), order="F")
+    _check(fn(ctx.handle, n, q, _pd(x), _pd(a), _pd(s), _pd(out)))
+    return out
+
+
+def psb_step(x, a, s, *, context: Optional[Context] = None) -> np.ndarray:
+    """Matrix psb_step(x, a, s) (qn_updates.cpp:121-129) on the GPU."""
+    return _named_step(L.load().si_psb_step, "psb_step", x, a, s, context)
+
+
+def aip_step(x, a, s, *, context: Optional[Context] = None) -> np.ndarray:
+    """Matrix aip_step(x, a, s) (qn_updates.cpp:147-152) on the GPU."""
+    return _named_step(L.load().si_aip_step, "aip_step", x, a, s, context)
+
+
+def dfp_step(x, x_inv, a, s, *, context: Optional[Context] = None):
+    """IteratePair dfp_step(x, x_inv, a, s) (qn_updates.cpp:154-174) -> (primal, inverse)."""
+    ctx = context or default_context()
+    x, xi, a, s = _f64(x), _f64(x_inv), _f64(a), _f64(s)
+    n, q = s.shape
+    if x.shape != (n, n) or xi.shape != (n, n) or a.shape != (n, n):
+        raise ConfigError("dfp_step: dimension mismatch")
+    out, outi = np.empty((n, n), order="F"), np.empty((n, n), order="F")
+    _check(L.load().si_dfp_step(ctx.handle, n, q, _pd(x), _pd(xi), _pd(a), _pd(s), _pd(out), _pd(outi)))
+    return out, outi
+
+
+def newton_schulz_step(x, a, *, context: Optional[Context] = None) -> np.ndarray:
+    """Matrix newton_schulz_step(x, a) = 2X − X·A·X (baselines.cpp:12-14) on the GPU."""
+    ctx = context or default_context()
+    x, a = _f64(x), _f64(a)
+    out = np.empty_like(x, order="F")
+    _check(L.load().si_newton_schulz_step(ctx.handle, x.shape[0], _pd(x), _pd(a), _pd(out)))
+    return out
+
+
+def newton_schulz_init(a: ProblemMatrix, seed: int = 0) -> np.ndarray:
+    """Matrix newton_schulz_init(a, seed) = 0.99·Aᵀ/s² (baselines.cpp:16-20)."""
+    out = np.empty((a.n(), a.n()), order="F")
+    _check(L.load().si_newton_schulz_init(a.ctx.handle, a.handle, C.c_uint64(seed), _pd(out)))
+    return out
+
+
+def spectral_norm_estimate(a: ProblemMatrix, iters: int = 100, seed: int = 0) -> float:
+    """double spectral_norm_estimate(m, iters, seed) (linalg.cpp:106-129), products on the GPU."""
+    out = C.c_double()
+    _check(L.load().si_spectral_norm_estimate(a.ctx.handle, a.handle, int(iters), C.c_uint64(seed), C.byref(out)))
+    return out.value
+
+
+def mr_step_cached(x, r, a, *, context: Optional[Context] = None):
+    """MrStep mr_step_cached(x, r, a) (baselines.cpp:22-37) -> (x, r, alpha, stagnated)."""
+    ctx = context or default_context()
+    x, r, a = _f64(x), _f64(r), _f64(a)
+    n = x.shape[0]
+    xo, ro = np.empty((n, n), order="F"), np.empty((n, n), order="F")
+    al, stg = C.c_double(), C.c_int()
+    _check(L.load().si_mr_step_cached(ctx.handle, n, _pd(x), _pd(r), _pd(a), _pd(xo), _pd(ro), C.byref(al),
+                                      C.byref(stg)))
+    return xo, ro, al.value, bool(stg.value)
+
+
+def mr_init(a: ProblemMatrix) -> np.ndarray:
+    """Matrix mr_init(a) = Tr(A)/Tr(AAᵀ)·I (baselines.cpp:45-50)."""
+    out = np.empty((a.n(), a.n()), order="F")
+    _check(L.load().si_mr_init(a.ctx.handle, a.handle, _pd(out)))
     return out
 
 

@@ -24,12 +24,8 @@ namespace {
 
 thread_local std::string g_err;
 
-struct ConfigError : std::invalid_argument {
-    using std::invalid_argument::invalid_argument;
-};
-struct NumericalError : std::runtime_error {
-    using std::runtime_error::runtime_error;
-};
+using si::ConfigError;
+using si::NumericalError;
 struct ResampleError : NumericalError {
     using NumericalError::NumericalError;
 };
@@ -216,6 +212,7 @@ void si_default_config(si_inverter_config* cfg) {
     cfg->track_flops = 1;
     cfg->track_wall_time = 1;
     cfg->max_redraws = 100;   // simi.hpp:70
+    cfg->update = SI_UPDATE_BFGS;
 }
 
 int si_context_create(int device, si_context** out) {
@@ -458,44 +455,318 @@ int si_residual(si_context* ctx, si_problem* prob, const double* x_host, double*
 
 // ---------------------------------------------------------- run_inverter ---
 // simi.cpp:217-381 for MethodSpec::named_method(UpdateName::bfgs).
+static const char* update_name(int u) {
+    switch (u) {
+        case SI_UPDATE_BFGS: return "bfgs";
+        case SI_UPDATE_PSB: return "psb";
+        case SI_UPDATE_AIP: return "aip";
+        case SI_UPDATE_DFP: return "dfp";
+    }
+    return "?";
+}
+
+static double flops_named(int u, double n, double q) {  // flops.cpp:22-46
+    switch (u) {
+        case SI_UPDATE_PSB: return 8 * n * n * q + 8 * n * q * q + 2 * q * q * q + n * q + 3 * n * n;
+        case SI_UPDATE_AIP: return 6 * n * n * q + 4 * n * q * q + 2 * q * q * q + n * q + n * n;
+        case SI_UPDATE_DFP: return 14 * n * n * q + 14 * n * q * q + 4 * q * q * q + 6 * n * n;
+    }
+    return flops_bfgs(n, q);
+}
+
+// validate_update (qn_updates.cpp:79-92): psb needs a symmetric A, bfgs / aip / dfp an SPD one
+static void validate_update(int u, si_problem* prob) {
+    if (u == SI_UPDATE_PSB) {
+        if (prob->p->symmetry == SI_GENERAL) throw ConfigError("psb requires a symmetric matrix");
+        return;
+    }
+    validate_spd(prob);
+}
+
+// ---------------------------------------------------------- run_inverter ---
+// simi.cpp:217-381 for MethodSpec::named_method(bfgs | psb | aip | dfp).
+static void run_inverter_impl(si_context* ctx, si_problem* prob, const si_inverter_config* cfg, double* x_out,
+                              double* x_inv_out, si_history_point* history, int64_t history_cap,
+                              si_run_result* result) {
+    auto& c = *ctx->c;
+    si::Problem& a = *prob->p;
+    const int64_t n = a.n, q = cfg->q;
+    const int upd = cfg->update;
+    std::memset(result, 0, sizeof(*result));
+    // validate_config (simi.cpp:185-213)
+    require(upd >= SI_UPDATE_BFGS && upd <= SI_UPDATE_DFP, "unknown update name");
+    require(q >= 1 && q <= n, "SketchRule: q must satisfy 1 <= q <= n");
+    const int sk = cfg->sketch;
+    if (sk == SI_SKETCH_ADAPTIVE_COLS || sk == SI_SKETCH_ADAPTIVE_GAUSS || sk == SI_SKETCH_ADAPTIVE_COLS_UNIFORM ||
+        sk == SI_SKETCH_ADAPTIVE_GAUSS_DEVICE)
+        throw ConfigError("run_inverter: adaptive sketch rules belong to the adarbfgs driver");
+    require(sk == SI_SKETCH_GAUSSIAN || sk == SI_SKETCH_GAUSSIAN_DEVICE || sk == SI_SKETCH_COORDINATE_BLOCK,
+            "run_inverter: unknown sketch rule");
+    require(cfg->tol >= 0.0, "run_inverter: tol must be >= 0");
+    require(cfg->max_iters >= 1, "run_inverter: max_iters must be >= 1");
+    require(cfg->max_redraws >= 0, "run_inverter: max_redraws must be >= 0");
+    require(cfg->residual_every_k >= 1, "run_inverter: residual_every_k must be >= 1");
+    validate_update(upd, prob);
+    const bool symmetric_iterates = upd != SI_UPDATE_AIP;  // simi.cpp:77-81
+    const bool tracks_inverse = upd == SI_UPDATE_DFP;
+    if (cfg->x0_host && symmetric_iterates) {
+        double nrm = 0.0;
+        const double asym = host_frobenius_asym(cfg->x0_host, n, &nrm);
+        if (asym > 1e-10 * std::max(1.0, nrm)) throw ConfigError("run_inverter: this method requires a symmetric x0");
+    }
+
+    si::RbfgsWork w;
+    struct Rel {
+        si::RbfgsWork& w;
+        double* scratch = nullptr;
+        ~Rel() {
+            si::family_release(w);
+            w.release();
+            if (scratch) cudaFree(scratch);
+        }
+    } rel{w};
+    w.alloc(n, q, true);
+    si::family_alloc(w, upd);
+    if (cfg->x0_host)
+        ck(cudaMemcpyAsync(w.X, cfg->x0_host, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyHostToDevice,
+                           c.stream),
+           "h2d x0");
+    else
+        si::set_identity(c, w.X, n);
+    if (tracks_inverse) {  // simi.cpp:227-229: x_inv = lu_inverse(x0) or I
+        if (cfg->x0_host)
+            si::lu_inverse_device(c, w.X, n, w.H);
+        else
+            si::set_identity(c, w.H, n);
+    }
+    const double* tracked = tracks_inverse ? w.H : w.X;  // simi.cpp:236-238
+    auto residual = [&]() -> double {
+        if (upd == SI_UPDATE_AIP && !a.dense) {  // general X with a CSR A
+            if (!rel.scratch) ck(cudaMalloc(&rel.scratch, size_t(n) * size_t(n) * sizeof(double)), "malloc");
+            si::residual_general_sq_enqueue(c, a, w.X, rel.scratch, c.scalar_dev);
+            ck(cudaMemcpyAsync(c.scalar_host, c.scalar_dev, sizeof(double), cudaMemcpyDeviceToHost, c.stream), "d2h");
+            ck(cudaStreamSynchronize(c.stream), "sync");
+            return std::sqrt(c.scalar_host[0]);
+        }
+        return residual_norm(c, a, tracked);
+    };
+
+    HistoryWriter hist{history, history_cap, 0, cfg};
+    double flops = 0.0, seconds = 0.0;
+    int64_t k = 0;
+    auto finish = [&](int term, const std::string& msg) {
+        result->termination = term;
+        result->k = k;
+        result->flops = flops;
+        result->seconds = seconds;
+        result->history_count = hist.count;
+        result->max_symmetry_drift = 0.0;  // symmetric updates write X (and H) exactly symmetric (mirrored tiles)
+        set_message(result, msg);
+        if (x_out)
+            ck(cudaMemcpyAsync(x_out, w.X, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, c.stream),
+               "d2h x");
+        if (x_inv_out && tracks_inverse)
+            ck(cudaMemcpyAsync(x_inv_out, w.H, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyDeviceToHost,
+                               c.stream),
+               "d2h x_inv");
+        ck(cudaStreamSynchronize(c.stream), "sync");
+    };
+
+    // simi.cpp:242-246; for the default X0 = I (and H0 = I), ‖I − A·I‖ = ‖I − A‖ needs no GEMM
+    double base;
+    if (cfg->x0_host) {
+        base = residual();
+    } else {
+        si::identity_residual_sq_enqueue(c, a, c.scalar_dev);
+        ck(cudaMemcpyAsync(c.scalar_host, c.scalar_dev, sizeof(double), cudaMemcpyDeviceToHost, c.stream), "d2h");
+        ck(cudaStreamSynchronize(c.stream), "sync");
+        base = std::sqrt(c.scalar_host[0]);
+    }
+    if (base == 0.0) {
+        hist.record(0, 0.0, 0.0, 0.0);
+        finish(SI_TOL_REACHED, "");
+        return;
+    }
+    hist.record(0, 1.0, 0.0, 0.0);
+
+    // coordinate-block rule (sketching.cpp:20-28) with uniform or convenient p (simi.cpp:121-150)
+    std::vector<std::vector<si::Index>> blocks;
+    std::vector<double> p;
+    if (sk == SI_SKETCH_COORDINATE_BLOCK) {
+        blocks = si::contiguous_partition(n, q);
+        p.assign(blocks.size(), 1.0 / double(blocks.size()));
+        if (cfg->probabilities == SI_PROB_CONVENIENT) {
+            std::vector<double> wts;
+            if (upd == SI_UPDATE_DFP)
+                si::spd_inverse_diagonal(c, a, wts);  // Tr(SᵢᵀA⁻¹Sᵢ)
+            else
+                si::column_weights(c, a, upd == SI_UPDATE_PSB ? 1 : 0, wts);  // ‖ASᵢ‖² or Tr(SᵢᵀASᵢ)
+            double sum = 0.0;
+            for (size_t i = 0; i < blocks.size(); ++i) {
+                double t = 0.0;
+                for (auto j : blocks[i]) t += wts[size_t(j)];
+                if (!(t > 0.0))
+                    throw ConfigError(upd == SI_UPDATE_PSB
+                                          ? "convenient_probabilities: family member with zero sketched norm"
+                                          : "trace probabilities: member with non-positive sketched trace");
+                p[i] = t;
+                sum += t;
+            }
+            for (double& v : p) v /= sum;
+        }
+    }
+
+    si::RngStream rng(cfg->seed);  // simi.cpp:275
+    const bool device_sketch = sk == SI_SKETCH_GAUSSIAN_DEVICE;
+    DeviceTimer tm;
+    int st[4];
+    for (k = 1; k <= cfg->max_iters; ++k) {
+        bool stepped = false;
+        for (int failures = 0; !stepped; ++failures) {
+            if (failures > cfg->max_redraws) {
+                finish(SI_TERMINATION_ERROR, "sketch rejection limit exceeded for " + describe(sk, q) +
+                                                 " at iteration " + std::to_string(k));
+                return;
+            }
+            if (sk == SI_SKETCH_GAUSSIAN) {
+                rng.gaussian_fill(w.s_pinned, n, q, n);  // rng.hpp:42-49
+            } else if (sk == SI_SKETCH_COORDINATE_BLOCK) {
+                const si::Index i = rng.categorical(p.data(), si::Index(p.size()));
+                const auto& blk = blocks[size_t(i)];
+                // the last block of contiguous_partition may be narrower: this draw has q' = |C_i| columns
+                w.q = int64_t(blk.size());
+                std::fill(w.s_pinned, w.s_pinned + n * w.q, 0.0);
+                for (size_t j = 0; j < blk.size(); ++j) w.s_pinned[blk[j] + int64_t(j) * n] = 1.0;
+            }
+            if (!device_sketch) si::rbfgs_enqueue_sketch_upload(c, w);
+            ck(cudaEventRecord(tm.a, c.stream), "event");  // timer starts after the draw (simi.cpp:298)
+            si::family_enqueue_iteration(c, a, w, device_sketch, cfg->seed);
+            ck(cudaEventRecord(tm.b, c.stream), "event");
+            read_status(c, w.status, st);
+            if (st[0] || st[2]) {  // GramRankDeficientError -> redraw (simi.cpp:331-333)
+                st[0] = st[2] = 0;
+                ck(cudaMemsetAsync(w.status, 0, 4 * sizeof(int), c.stream), "reset");
+                result->redraws++;
+                continue;
+            }
+            if (cfg->track_wall_time) seconds += tm.seconds();
+            if (cfg->track_flops) flops += flops_named(upd, double(n), double(w.q));  // s.cols()
+            stepped = true;
+        }
+        if (st[1]) {  // simi.cpp:342-347
+            finish(SI_TERMINATION_ERROR, "diverged: non-finite entries at iteration " + std::to_string(k));
+            return;
+        }
+        if (k == 1 || k == cfg->max_iters || k % cfg->residual_every_k == 0) {  // simi.cpp:361-375
+            const double rel_res = residual() / base;
+            hist.record(k, rel_res, flops, seconds);
+            if (rel_res <= cfg->tol) {
+                finish(SI_TOL_REACHED, "");
+                return;
+            }
+            if (cfg->time_budget_seconds > 0.0 && seconds > cfg->time_budget_seconds) {
+                finish(SI_MAX_ITERS, "time budget exhausted");
+                return;
+            }
+        }
+    }
+    k = cfg->max_iters;
+    finish(SI_MAX_ITERS, "");
+}
+
 int si_run_inverter(si_context* ctx, si_problem* prob, const si_inverter_config* cfg, double* x_out,
+                    si_history_point* history, int64_t history_cap, si_run_result* result) {
+    return guard([&] { run_inverter_impl(ctx, prob, cfg, x_out, nullptr, history, history_cap, result); });
+}
+
+int si_run_inverter_pair(si_context* ctx, si_problem* prob, const si_inverter_config* cfg, double* x_out,
+                         double* x_inv_out, si_history_point* history, int64_t history_cap, si_run_result* result) {
+    return guard([&] { run_inverter_impl(ctx, prob, cfg, x_out, x_inv_out, history, history_cap, result); });
+}
+
+// ---------------------------------------------------------- run_baseline ---
+// spectral_norm_estimate (linalg.cpp:106-129) with the start vector drawn here
+// (host RngStream, the oracle's bytes); products on the device.
+static double spectral_norm_estimate(si::Context& c, si::Problem& a, int iters, uint64_t seed) {
+    const int64_t n = a.n;
+    require(iters >= 1, "spectral_norm_estimate: iters must be >= 1");
+    if (!a.dense && a.symmetry == SI_GENERAL)
+        throw ConfigError("spectral_norm_estimate: a general CSR A is not supported (needs Aᵀ)");
+    if (si::sumsq_device(c, a.dense ? a.a : a.val, a.dense ? n * n : a.nnz) == 0.0) return 0.0;
+    si::RngStream rng(seed);
+    std::vector<double> v(static_cast<size_t>(n)), wv(static_cast<size_t>(n));
+    auto nrm = [](const std::vector<double>& x) {
+        double t = 0.0;
+        for (double e : x) t += e * e;
+        return std::sqrt(t);
+    };
+    double *dv = nullptr, *dw = nullptr;
+    ck(cudaMalloc(&dv, size_t(n) * sizeof(double)), "malloc");
+    ck(cudaMalloc(&dw, size_t(n) * sizeof(double)), "malloc");
+    struct Free {
+        double *p1, *p2;
+        ~Free() {
+            cudaFree(p1);
+            cudaFree(p2);
+        }
+    } fr{dv, dw};
+    rng.gaussian_fill(v.data(), n, 1, n);
+    if (nrm(v) == 0.0) std::fill(v.begin(), v.end(), 1.0);
+    double s0 = nrm(v);
+    for (double& e : v) e /= s0;
+    double est = 0.0;
+    for (int it = 0; it < iters; ++it) {
+        ck(cudaMemcpyAsync(dv, v.data(), size_t(n) * sizeof(double), cudaMemcpyHostToDevice, c.stream), "h2d");
+        si::apply_a(c, a, dv, n, 1, dw, n, nullptr);  // w = A·v
+        ck(cudaMemcpyAsync(wv.data(), dw, size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, c.stream), "d2h");
+        ck(cudaStreamSynchronize(c.stream), "sync");
+        est = nrm(wv);
+        if (est == 0.0) {  // v in the null space: restart from a fresh direction
+            rng.gaussian_fill(v.data(), n, 1, n);
+            s0 = nrm(v);
+            for (double& e : v) e /= s0;
+            continue;
+        }
+        if (a.dense && a.symmetry == SI_GENERAL)
+            si::gemm(c, n, 1, n, a.a, n, true, dw, n, true, dv, n, 1.0, 0.0);  // v = Aᵀ·w
+        else
+            si::apply_a(c, a, dw, n, 1, dv, n, nullptr);  // symmetric A: Aᵀ·w = A·w
+        ck(cudaMemcpyAsync(v.data(), dv, size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, c.stream), "d2h");
+        ck(cudaStreamSynchronize(c.stream), "sync");
+        const double nv = nrm(v);
+        if (nv == 0.0) break;
+        for (double& e : v) e /= nv;
+    }
+    return est;
+}
+
+int si_run_baseline(si_context* ctx, si_problem* prob, int method, const si_inverter_config* cfg, double* x_out,
                     si_history_point* history, int64_t history_cap, si_run_result* result) {
     return guard([&] {
         auto& c = *ctx->c;
         si::Problem& a = *prob->p;
-        const int64_t n = a.n, q = cfg->q;
+        const int64_t n = a.n;
         std::memset(result, 0, sizeof(*result));
-        // validate_config (simi.cpp:185-213)
-        require(q >= 1 && q <= n, "SketchRule: q must satisfy 1 <= q <= n");
-        const int sk = cfg->sketch;
-        if (sk == SI_SKETCH_ADAPTIVE_COLS || sk == SI_SKETCH_ADAPTIVE_GAUSS || sk == SI_SKETCH_ADAPTIVE_COLS_UNIFORM ||
-            sk == SI_SKETCH_ADAPTIVE_GAUSS_DEVICE)
-            throw ConfigError("run_inverter: adaptive sketch rules belong to the adarbfgs driver");
-        require(sk == SI_SKETCH_GAUSSIAN || sk == SI_SKETCH_GAUSSIAN_DEVICE || sk == SI_SKETCH_COORDINATE_BLOCK,
-                "run_inverter: unknown sketch rule");
-        require(cfg->tol >= 0.0, "run_inverter: tol must be >= 0");
-        require(cfg->max_iters >= 1, "run_inverter: max_iters must be >= 1");
-        require(cfg->max_redraws >= 0, "run_inverter: max_redraws must be >= 0");
-        require(cfg->residual_every_k >= 1, "run_inverter: residual_every_k must be >= 1");
-        validate_spd(prob);  // validate_update(bfgs) -> a.validate_spd() (qn_updates.cpp:79-92)
-        if (cfg->x0_host) {
-            double nrm = 0.0;
-            const double asym = host_frobenius_asym(cfg->x0_host, n, &nrm);
-            if (asym > 1e-10 * std::max(1.0, nrm)) throw ConfigError("run_inverter: this method requires a symmetric x0");
-        }
-
-        si::RbfgsWork w;
+        require(method == SI_BASELINE_NEWTON_SCHULZ || method == SI_BASELINE_MINIMAL_RESIDUAL,
+                "run_baseline: unknown method");
+        require(cfg->tol >= 0.0, "run_baseline: tol must be >= 0");
+        require(cfg->max_iters >= 1, "run_baseline: max_iters must be >= 1");
+        require(cfg->residual_every_k >= 1, "run_baseline: residual_every_k must be >= 1");
+        const bool ns = method == SI_BASELINE_NEWTON_SCHULZ;
+        si::BaselineWork w;
         struct Rel {
-            si::RbfgsWork& w;
+            si::BaselineWork& w;
             ~Rel() { w.release(); }
         } rel{w};
-        w.alloc(n, q, true);
+        w.alloc(n);
         if (cfg->x0_host)
             ck(cudaMemcpyAsync(w.X, cfg->x0_host, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyHostToDevice,
                                c.stream),
                "h2d x0");
+        else if (ns)
+            si::newton_schulz_init_device(c, a, w, spectral_norm_estimate(c, a, 100, cfg->seed));
         else
-            si::set_identity(c, w.X, n);
+            si::mr_init_device(c, a, w);
 
         HistoryWriter hist{history, history_cap, 0, cfg};
         double flops = 0.0, seconds = 0.0;
@@ -506,7 +777,6 @@ int si_run_inverter(si_context* ctx, si_problem* prob, const si_inverter_config*
             result->flops = flops;
             result->seconds = seconds;
             result->history_count = hist.count;
-            result->max_symmetry_drift = 0.0;  // X is written exactly symmetric (mirrored upper tiles)
             set_message(result, msg);
             if (x_out)
                 ck(cudaMemcpyAsync(x_out, w.X, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyDeviceToHost,
@@ -514,99 +784,52 @@ int si_run_inverter(si_context* ctx, si_problem* prob, const si_inverter_config*
                    "d2h x");
             ck(cudaStreamSynchronize(c.stream), "sync");
         };
-
-        // simi.cpp:242-246; for the default X0 = I, ‖I − A·I‖ = ‖I − A‖ needs no GEMM
-        double base;
-        if (cfg->x0_host) {
-            base = residual_norm(c, a, w.X);
-        } else {
-            si::identity_residual_sq_enqueue(c, a, c.scalar_dev);
-            ck(cudaMemcpyAsync(c.scalar_host, c.scalar_dev, sizeof(double), cudaMemcpyDeviceToHost, c.stream), "d2h");
-            ck(cudaStreamSynchronize(c.stream), "sync");
-            base = std::sqrt(c.scalar_host[0]);
-        }
+        const double base = si::baseline_residual(c, a, w);  // R = I − A X0 (baselines.cpp:70-71)
         if (base == 0.0) {
             hist.record(0, 0.0, 0.0, 0.0);
             finish(SI_TOL_REACHED, "");
             return;
         }
         hist.record(0, 1.0, 0.0, 0.0);
-
-        // coordinate-block rule (sketching.cpp:20-28) with uniform or convenient p
-        std::vector<std::vector<si::Index>> blocks;
-        std::vector<double> p;
-        if (sk == SI_SKETCH_COORDINATE_BLOCK) {
-            blocks = si::contiguous_partition(n, q);
-            p.assign(blocks.size(), 1.0 / double(blocks.size()));
-            if (cfg->probabilities == SI_PROB_CONVENIENT) {
-                // bfgs convenient p_i ∝ Tr(S_iᵀ A S_i) = sum_{j in C_i} a_jj (simi.cpp:135-142)
-                std::vector<double> diag(static_cast<size_t>(n));
-                if (a.dense) {
-                    for (int64_t j = 0; j < n; ++j)
-                        ck(cudaMemcpy(&diag[size_t(j)], a.a + j + j * n, sizeof(double), cudaMemcpyDeviceToHost),
-                           "diag");
-                } else {
-                    std::vector<double> full(size_t(n) * size_t(n));
-                    si::problem_download_dense(a, full.data());
-                    for (int64_t j = 0; j < n; ++j) diag[size_t(j)] = full[size_t(j + j * n)];
-                }
-                double sum = 0.0;
-                for (size_t i = 0; i < blocks.size(); ++i) {
-                    double t = 0.0;
-                    for (auto j : blocks[i]) t += diag[size_t(j)];
-                    if (t <= 0.0) throw ConfigError("trace probabilities: member with non-positive sketched trace");
-                    p[i] = t;
-                    sum += t;
-                }
-                for (double& v : p) v /= sum;
-            }
-        }
-
-        si::RngStream rng(cfg->seed);  // simi.cpp:275
-        const bool device_sketch = sk == SI_SKETCH_GAUSSIAN_DEVICE;
-        DeviceTimer tm;
-        int st[4];
+        const double fl = ns ? 4.0 * double(n) * n * n + 2.0 * double(n) * n   // flops.cpp:76-79
+                             : 4.0 * double(n) * n * n + 8.0 * double(n) * n;  // flops.cpp:81-85
         for (k = 1; k <= cfg->max_iters; ++k) {
-            bool stepped = false;
-            for (int failures = 0; !stepped; ++failures) {
-                if (failures > cfg->max_redraws) {
-                    finish(SI_TERMINATION_ERROR, "sketch rejection limit exceeded for " + describe(sk, q) +
-                                                     " at iteration " + std::to_string(k));
-                    return;
-                }
-                if (sk == SI_SKETCH_GAUSSIAN) {
-                    rng.gaussian_fill(w.s_pinned, n, q, n);  // rng.hpp:42-49
-                } else if (sk == SI_SKETCH_COORDINATE_BLOCK) {
-                    const si::Index i = rng.categorical(p.data(), si::Index(p.size()));
-                    const auto& blk = blocks[size_t(i)];
-                    // the last block of contiguous_partition may be narrower: this draw has q' = |C_i| columns
-                    w.q = int64_t(blk.size());
-                    std::fill(w.s_pinned, w.s_pinned + n * w.q, 0.0);
-                    for (size_t j = 0; j < blk.size(); ++j) w.s_pinned[blk[j] + int64_t(j) * n] = 1.0;
-                }
-                if (!device_sketch) si::rbfgs_enqueue_sketch_upload(c, w);
-                ck(cudaEventRecord(tm.a, c.stream), "event");  // timer starts after the draw (simi.cpp:298)
-                si::rbfgs_enqueue_iteration(c, a, w, device_sketch, cfg->seed);
-                ck(cudaEventRecord(tm.b, c.stream), "event");
-                read_status(c, w.status, st);
-                if (st[0] || st[2]) {  // GramRankDeficientError -> redraw (simi.cpp:331-333)
-                    st[0] = st[2] = 0;
-                    ck(cudaMemsetAsync(w.status, 0, 4 * sizeof(int), c.stream), "reset");
-                    result->redraws++;
-                    continue;
-                }
-                if (cfg->track_wall_time) seconds += tm.seconds();
-                if (cfg->track_flops) flops += flops_bfgs(double(n), double(w.q));  // flops::bfgs(n, s.cols())
-                stepped = true;
+            const auto t0 = std::chrono::steady_clock::now();
+            bool finite = true, stagnated = false;
+            if (ns) {
+                finite = si::newton_schulz_enqueue(c, a, w);
+            } else {
+                double alpha = 0.0;
+                const int r = si::mr_enqueue(c, a, w, &alpha);
+                stagnated = r == 1;
+                finite = r != 2;
             }
-            if (st[1]) {  // simi.cpp:342-347
+            const auto t1 = std::chrono::steady_clock::now();
+            if (cfg->track_wall_time) seconds += std::chrono::duration<double>(t1 - t0).count();
+            if (cfg->track_flops) flops += fl;
+            if (!finite) {
                 finish(SI_TERMINATION_ERROR, "diverged: non-finite entries at iteration " + std::to_string(k));
                 return;
             }
-            if (k == 1 || k == cfg->max_iters || k % cfg->residual_every_k == 0) {  // simi.cpp:361-375
-                const double rel = residual_norm(c, a, w.X) / base;
-                hist.record(k, rel, flops, seconds);
-                if (rel <= cfg->tol) {
+            if (stagnated) {  // baselines.cpp:110-119: ‖R‖ of the carried residual
+                const double rel_res = std::sqrt(si::sumsq_device(c, w.R, n * n)) / base;
+                hist.record(k, rel_res, flops, seconds);
+                if (rel_res <= cfg->tol) {
+                    finish(SI_TOL_REACHED, "");
+                } else {
+                    finish(SI_TERMINATION_ERROR,
+                           "minimal residual stagnated (zero step denominator) at iteration " + std::to_string(k));
+                }
+                return;
+            }
+            if (k == 1 || k == cfg->max_iters || k % cfg->residual_every_k == 0) {  // baselines.cpp:121-146
+                const double rel_res = si::baseline_residual(c, a, w) / base;     // replaces the carried R
+                hist.record(k, rel_res, flops, seconds);
+                if (!std::isfinite(rel_res)) {
+                    finish(SI_TERMINATION_ERROR, "diverged: residual overflow at iteration " + std::to_string(k));
+                    return;
+                }
+                if (rel_res <= cfg->tol) {
                     finish(SI_TOL_REACHED, "");
                     return;
                 }
@@ -618,6 +841,138 @@ int si_run_inverter(si_context* ctx, si_problem* prob, const si_inverter_config*
         }
         k = cfg->max_iters;
         finish(SI_MAX_ITERS, "");
+    });
+}
+
+// ------------------------------------------------ step-level (f3 / f4) -----
+static void upload_general(si::Problem& a, si_context* ctx, int64_t n, const double* a_host) {
+    a.ctx = ctx->c.get();
+    a.n = n;
+    a.symmetry = SI_GENERAL;  // the step kernels take A as given
+    si::problem_upload_dense(a, a_host, false);
+}
+
+static void named_step_impl(si_context* ctx, int update, int64_t n, int64_t q, const double* x_host,
+                            const double* x_inv_host, const double* a_host, const double* s_host, double* x_out,
+                            double* x_inv_out) {
+    auto& c = *ctx->c;
+    require(q >= 1 && n >= 1, "named step: bad shape");
+    si::Problem a;
+    upload_general(a, ctx, n, a_host);
+    si::RbfgsWork w;
+    struct Rel {
+        si::RbfgsWork& w;
+        ~Rel() {
+            si::family_release(w);
+            w.release();
+        }
+    } rel{w};
+    w.alloc(n, q, true);
+    si::family_alloc(w, update);
+    const size_t nn = size_t(n) * size_t(n) * sizeof(double);
+    ck(cudaMemcpyAsync(w.X, x_host, nn, cudaMemcpyHostToDevice, c.stream), "h2d");
+    if (update == SI_UPDATE_DFP) ck(cudaMemcpyAsync(w.H, x_inv_host, nn, cudaMemcpyHostToDevice, c.stream), "h2d");
+    std::memcpy(w.s_pinned, s_host, size_t(n) * size_t(q) * sizeof(double));
+    si::rbfgs_enqueue_sketch_upload(c, w);
+    si::family_enqueue_iteration(c, a, w, false, 0);
+    int st[4];
+    read_status(c, w.status, st);
+    if (st[0])
+        throw ResampleError(std::string(update_name(update)) + "_step: sketched Gram matrix is not positive definite");
+    ck(cudaMemcpyAsync(x_out, w.X, nn, cudaMemcpyDeviceToHost, c.stream), "d2h");
+    if (update == SI_UPDATE_DFP) ck(cudaMemcpyAsync(x_inv_out, w.H, nn, cudaMemcpyDeviceToHost, c.stream), "d2h");
+    ck(cudaStreamSynchronize(c.stream), "sync");
+}
+
+int si_psb_step(si_context* ctx, int64_t n, int64_t q, const double* x, const double* a, const double* s, double* o) {
+    return guard([&] { named_step_impl(ctx, SI_UPDATE_PSB, n, q, x, nullptr, a, s, o, nullptr); });
+}
+int si_aip_step(si_context* ctx, int64_t n, int64_t q, const double* x, const double* a, const double* s, double* o) {
+    return guard([&] { named_step_impl(ctx, SI_UPDATE_AIP, n, q, x, nullptr, a, s, o, nullptr); });
+}
+int si_dfp_step(si_context* ctx, int64_t n, int64_t q, const double* x, const double* xi, const double* a,
+                const double* s, double* o, double* oi) {
+    return guard([&] { named_step_impl(ctx, SI_UPDATE_DFP, n, q, x, xi, a, s, o, oi); });
+}
+
+int si_newton_schulz_step(si_context* ctx, int64_t n, const double* x_host, const double* a_host, double* x_out) {
+    return guard([&] {
+        auto& c = *ctx->c;
+        si::Problem a;
+        upload_general(a, ctx, n, a_host);
+        si::BaselineWork w;
+        struct Rel {
+            si::BaselineWork& w;
+            ~Rel() { w.release(); }
+        } rel{w};
+        w.alloc(n);
+        ck(cudaMemcpyAsync(w.X, x_host, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyHostToDevice, c.stream),
+           "h2d");
+        si::newton_schulz_enqueue(c, a, w);
+        ck(cudaMemcpyAsync(x_out, w.X, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, c.stream),
+           "d2h");
+        ck(cudaStreamSynchronize(c.stream), "sync");
+    });
+}
+
+int si_spectral_norm_estimate(si_context* ctx, si_problem* prob, int iters, uint64_t seed, double* out) {
+    return guard([&] { *out = spectral_norm_estimate(*ctx->c, *prob->p, iters, seed); });
+}
+
+int si_newton_schulz_init(si_context* ctx, si_problem* prob, uint64_t seed, double* x_out) {
+    return guard([&] {
+        auto& c = *ctx->c;
+        const int64_t n = prob->p->n;
+        si::BaselineWork w;
+        struct Rel {
+            si::BaselineWork& w;
+            ~Rel() { w.release(); }
+        } rel{w};
+        w.alloc(n);
+        si::newton_schulz_init_device(c, *prob->p, w, spectral_norm_estimate(c, *prob->p, 100, seed));
+        ck(cudaMemcpyAsync(x_out, w.X, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, c.stream),
+           "d2h");
+        ck(cudaStreamSynchronize(c.stream), "sync");
+    });
+}
+
+int si_mr_init(si_context* ctx, si_problem* prob, double* x_out) {
+    return guard([&] {
+        auto& c = *ctx->c;
+        const int64_t n = prob->p->n;
+        si::BaselineWork w;
+        struct Rel {
+            si::BaselineWork& w;
+            ~Rel() { w.release(); }
+        } rel{w};
+        w.alloc(n);
+        si::mr_init_device(c, *prob->p, w);
+        ck(cudaMemcpyAsync(x_out, w.X, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, c.stream),
+           "d2h");
+        ck(cudaStreamSynchronize(c.stream), "sync");
+    });
+}
+
+int si_mr_step_cached(si_context* ctx, int64_t n, const double* x_host, const double* r_host, const double* a_host,
+                      double* x_out, double* r_out, double* alpha, int* stagnated) {
+    return guard([&] {
+        auto& c = *ctx->c;
+        si::Problem a;
+        upload_general(a, ctx, n, a_host);
+        si::BaselineWork w;
+        struct Rel {
+            si::BaselineWork& w;
+            ~Rel() { w.release(); }
+        } rel{w};
+        w.alloc(n);
+        const size_t nn = size_t(n) * size_t(n) * sizeof(double);
+        ck(cudaMemcpyAsync(w.X, x_host, nn, cudaMemcpyHostToDevice, c.stream), "h2d");
+        ck(cudaMemcpyAsync(w.R, r_host, nn, cudaMemcpyHostToDevice, c.stream), "h2d");
+        const int r = si::mr_enqueue(c, a, w, alpha);
+        *stagnated = r == 1 ? 1 : 0;
+        ck(cudaMemcpyAsync(x_out, w.X, nn, cudaMemcpyDeviceToHost, c.stream), "d2h");
+        ck(cudaMemcpyAsync(r_out, w.R, nn, cudaMemcpyDeviceToHost, c.stream), "d2h");
+        ck(cudaStreamSynchronize(c.stream), "sync");
     });
 }
 

@@ -1074,3 +1074,5 @@ void ada_init_pdiag_identity(Context& c, Problem& a, AdaWork& w) {
 }
 
 }  // namespace si
+
+#include "family.cuh"

@@ -16,6 +16,13 @@ namespace si {
 struct CudaError : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
+// errors.hpp:9-22 (ConfigError is a std::invalid_argument, NumericalError a std::runtime_error)
+struct ConfigError : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+struct NumericalError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
 
 void cuda_check(cudaError_t e, const char* what);
 
@@ -81,9 +88,14 @@ struct Problem {
 // Workspace of one RBFGS iterate (SURVEY App. C1 rank-2q form):
 //   U = [S W] (n×2q), Y = A·S, P = Yᵀ·U = [G | H], Ginv, T = H·Ginv,
 //   M = [[Ginv + Ginv H Ginv, −Ginv], [−Ginv, 0]], V = U·M, X ← X + V·Uᵀ.
+enum UpdateKind { UPD_BFGS = 0, UPD_PSB = 1, UPD_AIP = 2, UPD_DFP = 3 };  // si_update
+
 struct RbfgsWork {
     int64_t n = 0, q = 0;
+    int update = UPD_BFGS;
     double* X = nullptr;
+    // other named updates (family.cuh): basis buffers, second core, DFP inverse iterate H
+    double *Bs = nullptr, *Bs2 = nullptr, *V2 = nullptr, *M2 = nullptr, *H = nullptr, *Ginv2 = nullptr;
     double *Y = nullptr, *U = nullptr, *P = nullptr, *Ginv = nullptr, *T = nullptr, *M = nullptr, *V = nullptr;
     double* factor_scratch = nullptr;
     int* status = nullptr;  // [0] Gram not PD (skip), [1] non-finite iterate
@@ -153,6 +165,28 @@ void set_identity(Context& c, double* X, int64_t n);
 void ada_enqueue_update(Context& c, Problem& a, AdaWork& w, int mode /*0 cols idx, 1 gaussian host, 2 gaussian dev*/,
                         uint64_t seed);
 void ada_enqueue_probabilities(Context& c, Problem& a, AdaWork& w);
+// ---- family.cuh: psb / aip / dfp iterations and the NS / MR baselines ----
+void family_alloc(RbfgsWork& w, int update);
+void family_release(RbfgsWork& w);
+void family_enqueue_iteration(Context& c, Problem& a, RbfgsWork& w, bool device_sketch, uint64_t seed);
+void residual_general_sq_enqueue(Context& c, Problem& a, const double* X, double* scratch_nn, double* out_dev);
+void column_weights(Context& c, Problem& a, int mode, std::vector<double>& out);
+void lu_inverse_device(Context& c, const double* M, int64_t n, double* out);
+void spd_inverse_diagonal(Context& c, Problem& a, std::vector<double>& out);
+struct BaselineWork {
+    int64_t n = 0;
+    double *X = nullptr, *Xn = nullptr, *T = nullptr, *R = nullptr, *part = nullptr;
+    int* flag = nullptr;
+    void alloc(int64_t n);
+    void release();
+};
+double baseline_residual(Context& c, Problem& a, BaselineWork& w);
+bool newton_schulz_enqueue(Context& c, Problem& a, BaselineWork& w);
+int mr_enqueue(Context& c, Problem& a, BaselineWork& w, double* alpha_out);
+double sumsq_device(Context& c, const double* x, int64_t count);
+void newton_schulz_init_device(Context& c, Problem& a, BaselineWork& w, double spectral_norm);
+void mr_init_device(Context& c, Problem& a, BaselineWork& w);
+
 void ada_core_enqueue(Context& c, const double* G, int64_t q, const double* Z, int64_t n, const int64_t* idx,
                       const double* St, double* G2, double* R2, double* Tq, double* R, double* B, double* scratch,
                       int* st);
