@@ -28,6 +28,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -41,6 +42,14 @@ sys.path.insert(0, ROOT)
 
 FP64_DMMA_PEAK_TFLOPS = 36.94  # profiles/r01_fp64_peak.txt (mma.sync m16n8k8 .f64, 148 SMs)
 HBM_PEAK_GBS = None
+
+
+def load_traffic():
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
 
 
 def load_peaks():
@@ -92,51 +101,81 @@ def make_dense(cfg):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + clock-event (throttle) reasons sampled DURING the timed region:
+    NVML polled from a thread every ~2 ms (nvidia-smi as a fallback)."""
+
+    _REASONS = (("hw_slowdown", 0x8), ("sw_thermal_slowdown", 0x20), ("hw_thermal_slowdown", 0x40),
+                ("hw_power_brake_slowdown", 0x80), ("sw_power_cap", 0x4))
 
     def __init__(self, index: int):
         self.index = index
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, reasons mask)
         self._stop = threading.Event()
-        self._proc = None
+        self._t = None
+        self._nv = None
+        self._h = None
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = None
+            try:
+                import torch
+
+                pr = torch.cuda.get_device_properties(index)
+                bus = "%08x:%02x:%02x.0" % (pr.pci_domain_id, pr.pci_bus_id, pr.pci_device_id)
+                h = nv.nvmlDeviceGetHandleByPciBusId(bus.encode())
+            except Exception:
+                h = nv.nvmlDeviceGetHandleByIndex(index)
+            self._nv, self._h = nv, h
+            self._max = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+        except Exception:
+            self._nv = None
+
+    def _reasons(self):
+        nv = self._nv
+        fn = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons")
+        return int(fn(self._h))
+
+    def _poll(self):
+        nv = self._nv
+        while True:
+            try:
+                self.samples.append((float(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)), self._max,
+                                     self._reasons()))
+            except Exception:
+                pass
+            if self._stop.wait(0.002):
+                break
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
-        try:
-            self._proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                           "--format=csv,noheader,nounits", "-lms", "100"],
-                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._t = threading.Thread(target=self._read, daemon=True)
+        if self._nv is not None:
+            self._t = threading.Thread(target=self._poll, daemon=True)
             self._t.start()
-        except Exception:
-            self._proc = None
         return self
 
-    def _read(self):
-        for line in self._proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 7:
-                self.samples.append(parts)
-
     def __exit__(self, *exc):
-        if self._proc:
-            self._proc.terminate()
+        if self._t is not None:
+            self._stop.set()
+            self._t.join(timeout=2)
+        if not self.samples:  # fallback: one nvidia-smi reading right after the region
             try:
-                self._proc.wait(timeout=2)
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      "--query-gpu=clocks.sm,clocks.max.sm", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=10).stdout.strip().split(",")
+                self.samples.append((float(out[0]), float(out[1]), -1))
             except Exception:
-                self._proc.kill()
+                pass
 
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        sm = [s[0] for s in self.samples]
+        reasons = sorted({name for s in self.samples if s[2] >= 0 for name, bit in self._REASONS if s[2] & bit})
+        src = "nvml, during the timed region" if self.samples[0][2] >= 0 else "nvidia-smi after the timed region"
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(s[1] for s in self.samples), "reasons": reasons,
+                "samples": len(self.samples), "source": src}
 
 
 def dist_env():
@@ -436,18 +475,38 @@ def run_ours(args, cfg):
     prof = ctx.profile()
     ctx.set_profiling(False)
     ksum = sum(v[1] for v in prof.values())
-    dom = max(prof.items(), key=lambda kv: kv[1][1])
-    upd = prof.get("gemm_symupd", dom[1])
-    upd_ms = upd[1] / max(1, upd[0])
-    upd_flops = 2.0 * n * n * q  # upper-triangular half of X + V·Uᵀ with K = 2q
-    achieved = upd_flops / (upd_ms * 1e-3) / 1e12
     shares = {k: round(v[1] / ksum, 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])}
     alg_flops = 6.0 * n * n * q + 12.0 * n * q * q
+    prof_iters = max(2, min(args.steps, 5))
+    # algorithmic FLOPs per iteration of each GEMM class:
+    #   gemm_splitk: Y = A·S (2n²q), W = X·Y (2n²q), [G|H] = Yᵀ[S W] (4nq²) — 3 launches
+    #   gemm_symupd: X += V·Uᵀ on the upper tiles (2n²q) — 1 launch
+    class_flops = {"gemm_splitk": 4.0 * n * n * q + 4.0 * n * q * q, "gemm_symupd": 2.0 * n * n * q}
+    traffic = load_traffic()
+
+    def roof(kname):
+        launches, total_ms = prof[kname]
+        per_launch_flops = class_flops[kname] * prof_iters / launches
+        per_launch_ms = total_ms / launches
+        ach = per_launch_flops / (per_launch_ms * 1e-3) / 1e12
+        t = traffic.get(kname, {}).get("bytes_per_launch") if traffic.get("workload") == cfg["name"] else None
+        return {"bound": "tensor", "kernel": kname, "achieved": ach, "peak": FP64_DMMA_PEAK_TFLOPS,
+                "unit": "TFLOP/s", "frac": ach / FP64_DMMA_PEAK_TFLOPS, "traffic": t,
+                "algorithmic_tflop_per_launch": per_launch_flops / 1e12, "launches_per_step": launches / prof_iters,
+                "ms_per_launch": per_launch_ms}
+
+    dom_name = max((k for k in prof if k in class_flops), key=lambda k: prof[k][1])
+    roofline = roof(dom_name)
+    roofline.update({"peak_source": "measured FP64 DMMA peak, profiles/r01_fp64_peak.txt (MEASURED_PEAKS.json has "
+                                    "no FP64 entry; tcgen05 has no f64 kind)",
+                     "traffic_source": "profiles/r01_traffic.json (ncu --set full, bytes per launch)",
+                     "kernel_share_of_step": shares})
+    secondary = roof("gemm_symupd") if "gemm_symupd" in prof and dom_name != "gemm_symupd" else None
 
     # ---- e2e through the public driver with host buffers ----
     e2e = None
     if rank == 0:
-        k_e2e = args.steps
+        k_e2e = 100 if cfg["gen"] == "config3" else max(args.steps, 100)  # one full BASELINE config-3 run
         a_np = a_host  # pinned host buffer (config 3) / numpy (config 1)
         x_pinned = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
         x_out = x_pinned.numpy().T  # Fortran-ordered view of a pinned buffer
@@ -462,10 +521,32 @@ def run_ours(args, cfg):
         e2e_v = k_e2e / (t1 - t0)
         e2e = {"value": e2e_v, "unit": "iter/s", "h2d_bytes_per_step": int(8 * n * n / k_e2e),
                "d2h_bytes_per_step": int(16 + 8 * n * n / k_e2e + 8 * 2 / k_e2e),
-               "note": "si_run_inverter from host A (H2D inside timing), device sketches, status word read back "
-                       "each iteration, residual at the last iteration (2n^3, included), X returned to host; "
-                       "byte counts are per step, A/X transfers amortised over the steps"}
+               "run_iterations": k_e2e,
+               "note": "one run_inverter call (si_run_inverter) of the BASELINE run length from a host A: H2D of A, "
+                       "SPD validation, device sketches, status word read back each iteration, the reference's "
+                       "forced residual checkpoints at k=1 and k=max (2n^3 each), X returned to host, all inside "
+                       "the timer; byte counts per step with the A/X transfers amortised over the run"}
         del prob2
+
+    # ---- time to ε: config 1 only, both normalisations ----
+    tte = None
+    if rank == 0 and cfg["gen"] == "config1":
+        import numpy as np
+
+        base = float(np.linalg.norm(np.eye(n) - a_host))
+        tte = {}
+        for label, tol in (("sqrt_n_1e-2", 1e-2 * math.sqrt(n) / base), ("reference_rel_1e-2", 1e-2)):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = si.run_inverter(si.InverterConfig(prob, si.SketchRule.gaussian_device(q), tol=tol, max_iters=20000,
+                                                  seed=0, track=si.TrackOptions(residual_every_k=10),
+                                                  return_x=False))
+            t1 = time.perf_counter()
+            tte[label] = {"seconds": t1 - t0, "iterations": r.state.k, "reached": r.termination.name,
+                          "relative_residual": r.state.history[-1].residual,
+                          "target": "||I-AX||_F/sqrt(n) <= 1e-2" if label.startswith("sqrt") else
+                                    "||I-AX_k||_F/||I-AX_0||_F <= 1e-2",
+                          "checkpoints": "every 10 iterations (2n^3 residual each, included)"}
 
     # ---- CPU baseline (oracle on host cores, bounded sample) ----
     cpu = None
@@ -483,20 +564,20 @@ def run_ours(args, cfg):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step_ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["name"], "n": n, "q": q, "sketch": "gaussian, device Philox4x32-10",
-                       "l2": "inputs larger than L2 (A, X 2.1 GB each); no flush",
+                       "l2": ("inputs larger than L2 (A, X 2.1 GB each); no flush" if n * n * 8 > 126e6 else
+                              "inputs fit in L2 (A, X %.0f MB); no flush — latency-bound extra line" % (n * n * 8e-6)),
                        "parallelism": "replicas" if world > 1 else "single-gpu",
                        "algorithmic_gflop_per_step": alg_flops / 1e9,
                        "achieved_tflops_per_step": alg_flops / (per_step_ms * 1e-3) / 1e12},
-            "roofline": {"bound": "tensor", "kernel": "gemm_symupd (X += V·Uᵀ, mirrored)", "achieved": achieved,
-                         "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_DMMA_PEAK_TFLOPS,
-                         "peak_source": "measured FP64 DMMA peak, profiles/r01_fp64_peak.txt "
-                                        "(MEASURED_PEAKS.json has no FP64 entry)",
-                         "traffic": None, "kernel_share_of_step": shares},
+            "roofline": roofline,
+            "roofline_secondary": secondary,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }
+        if tte is not None:
+            line["time_to_eps"] = tte
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()

@@ -230,6 +230,7 @@ enum class Termination { tol_reached = SI_TOL_REACHED, max_iters = SI_MAX_ITERS,
 
 struct InverterState {
     Matrix x;
+    std::optional<Matrix> x_inv;  // dfp's tracked inverse (tracks_inverse_iterate)
     long k = 0;
     std::vector<HistoryPoint> history;
     double max_symmetry_drift = 0.0;
@@ -307,20 +308,37 @@ inline std::vector<HistoryPoint> history(const std::vector<si_history_point>& h,
 }
 }  // namespace detail
 
-/// RunResult run_inverter(const InverterConfig&), simi.hpp:105 (named bfgs only on this path).
+namespace detail {
+inline int update_code(const MethodSpec& m) {
+    if (m.kind == VariantKind::named) {
+        switch (m.name) {
+            case UpdateName::bfgs: return SI_UPDATE_BFGS;
+            case UpdateName::psb: return SI_UPDATE_PSB;
+            case UpdateName::aip: return SI_UPDATE_AIP;
+            case UpdateName::dfp: return SI_UPDATE_DFP;
+            default: break;
+        }
+    }
+    throw ConfigError("stochinv_b200: only the named bfgs / psb / aip / dfp updates are on the GPU path");
+}
+}  // namespace detail
+
+/// RunResult run_inverter(const InverterConfig&), simi.hpp:105 (named bfgs / psb / aip / dfp).
 inline RunResult run_inverter(const InverterConfig& config) {
-    if (config.method.kind != VariantKind::named || config.method.name != UpdateName::bfgs)
-        throw ConfigError("stochinv_b200: only MethodSpec::named_method(UpdateName::bfgs) is on the GPU path");
+    const int upd = detail::update_code(config.method);
     const Index n = config.a.n();
     if (config.x0 && (config.x0->rows() != n || config.x0->cols() != n))
         throw ConfigError("run_inverter: x0 dimension mismatch");
     si_inverter_config c = detail::to_c(config, config.x0, &config.on_checkpoint);
+    c.update = upd;
     std::vector<si_history_point> h(size_t(config.max_iters / std::max<Index>(1, config.track.residual_every_k) + 4));
     si_run_result r;
     RunResult out;
     out.state.x = detail::make<Matrix>(n, n);
-    detail::check(si_run_inverter(detail::context(), config.a.handle(), &c, out.state.x.data(), h.data(),
-                                  int64_t(h.size()), &r));
+    if (upd == SI_UPDATE_DFP) out.state.x_inv = detail::make<Matrix>(n, n);
+    detail::check(si_run_inverter_pair(detail::context(), config.a.handle(), &c, out.state.x.data(),
+                                       out.state.x_inv ? out.state.x_inv->data() : nullptr, h.data(),
+                                       int64_t(h.size()), &r));
     out.state.k = long(r.k);
     out.state.history = detail::history(h, r.history_count);
     out.state.max_symmetry_drift = r.max_symmetry_drift;
@@ -328,6 +346,62 @@ inline RunResult run_inverter(const InverterConfig& config) {
     out.state.seconds = r.seconds;
     out.termination = Termination(r.termination);
     out.message = r.message;
+    return out;
+}
+
+// ---------------------------------------------------------------- baselines.hpp:36-68
+enum class BaselineMethod { newton_schulz = SI_BASELINE_NEWTON_SCHULZ, minimal_residual = SI_BASELINE_MINIMAL_RESIDUAL };
+struct BaselineConfig {
+    ProblemMatrix a;
+    BaselineMethod method = BaselineMethod::newton_schulz;
+    double tol = 1e-2;
+    long max_iters = 1000;
+    double time_budget_seconds = 0.0;
+    std::uint64_t seed = 0;
+    TrackOptions track;
+    std::optional<Matrix> x0;
+    std::function<void(const HistoryPoint&)> on_checkpoint;
+};
+
+/// RunResult run_baseline(const BaselineConfig&), baselines.hpp:68.
+inline RunResult run_baseline(const BaselineConfig& config) {
+    const Index n = config.a.n();
+    if (config.x0 && (config.x0->rows() != n || config.x0->cols() != n))
+        throw ConfigError("run_baseline: x0 dimension mismatch");
+    si_inverter_config c;
+    si_default_config(&c);
+    c.tol = config.tol;
+    c.max_iters = config.max_iters;
+    c.time_budget_seconds = config.time_budget_seconds;
+    c.seed = config.seed;
+    c.residual_every_k = config.track.residual_every_k;
+    c.track_flops = config.track.flops;
+    c.track_wall_time = config.track.wall_time;
+    c.x0_host = config.x0 ? config.x0->data() : nullptr;
+    if (config.on_checkpoint) {
+        c.on_checkpoint = &detail::trampoline;
+        c.user = const_cast<void*>(static_cast<const void*>(&config.on_checkpoint));
+    }
+    std::vector<si_history_point> h(size_t(config.max_iters / std::max<Index>(1, config.track.residual_every_k) + 4));
+    si_run_result r;
+    RunResult out;
+    out.state.x = detail::make<Matrix>(n, n);
+    detail::check(si_run_baseline(detail::context(), config.a.handle(), int(config.method), &c, out.state.x.data(),
+                                  h.data(), int64_t(h.size()), &r));
+    out.state.k = long(r.k);
+    out.state.history = detail::history(h, r.history_count);
+    out.state.flops = r.flops;
+    out.state.seconds = r.seconds;
+    out.termination = Termination(r.termination);
+    out.message = r.message;
+    return out;
+}
+
+/// Matrix newton_schulz_step(x, a) = 2X − XAX, baselines.hpp:15.
+inline Matrix newton_schulz_step(const Matrix& x, const Matrix& a) {
+    const Index n = x.rows();
+    Matrix out = detail::make<Matrix>(n, n);
+    detail::check(si_newton_schulz_step(detail::context(), n, x.data(), a.data(), out.data()));
     return out;
 }
 
@@ -360,6 +434,31 @@ inline Matrix bfgs_step(const Matrix& x, const Matrix& a, const Matrix& s) {
         throw ConfigError("bfgs_step: dimension mismatch");
     Matrix out = detail::make<Matrix>(n, n);
     detail::check(si_bfgs_step(detail::context(), n, q, x.data(), a.data(), s.data(), out.data()));
+    return out;
+}
+
+/// Matrix psb_step / aip_step (x, a, s), qn_updates.hpp.  Throw GramRankDeficientError.
+inline Matrix psb_step(const Matrix& x, const Matrix& a, const Matrix& s) {
+    const Index n = s.rows(), q = s.cols();
+    Matrix out = detail::make<Matrix>(n, n);
+    detail::check(si_psb_step(detail::context(), n, q, x.data(), a.data(), s.data(), out.data()));
+    return out;
+}
+inline Matrix aip_step(const Matrix& x, const Matrix& a, const Matrix& s) {
+    const Index n = s.rows(), q = s.cols();
+    Matrix out = detail::make<Matrix>(n, n);
+    detail::check(si_aip_step(detail::context(), n, q, x.data(), a.data(), s.data(), out.data()));
+    return out;
+}
+struct IteratePair {
+    Matrix primal, inverse;
+};
+/// IteratePair dfp_step(x, x_inv, a, s), qn_updates.hpp.
+inline IteratePair dfp_step(const Matrix& x, const Matrix& x_inv, const Matrix& a, const Matrix& s) {
+    const Index n = s.rows(), q = s.cols();
+    IteratePair out{detail::make<Matrix>(n, n), detail::make<Matrix>(n, n)};
+    detail::check(si_dfp_step(detail::context(), n, q, x.data(), x_inv.data(), a.data(), s.data(), out.primal.data(),
+                              out.inverse.data()));
     return out;
 }
 

@@ -121,7 +121,7 @@ static int grid_for(int64_t work, int threads, int max_blocks = 148 * 16) {
 }
 
 // --------------------------------------------------------------- GEMM ------
-enum TileCfg { T128x128 = 0, T128x64 = 1, T128x32 = 2, T128x128W16 = 3, T64x128 = 4 };
+enum TileCfg { T128x128 = 0, T128x64 = 1, T128x32 = 2, T128x128W16 = 3, T64x128 = 4, T128x128K32 = 5, T128x128W8K32 = 6 };
 
 // development switches: SI_WARPS16=1 selects 16 consumer warps for 128×128
 // tiles; SI_NO_TMA=1 forces the cp.async mainloop.
@@ -227,6 +227,12 @@ static void launch_gemm_tile(Context& c, TileCfg t, const GemmArgs& a, dim3 grid
             case T128x64: launch_tma_cfg<128, 64, 16, 4, 2, 4, AK, BKM, EPI>(c, a, grid, name); break;
             case T128x32: launch_tma_cfg<128, 32, 16, 8, 1, 4, AK, BKM, EPI>(c, a, grid, name); break;
             case T128x128W16: launch_tma_cfg<128, 128, 16, 4, 4, 5, AK, BKM, EPI>(c, a, grid, name); break;
+            case T128x128K32:
+                if constexpr (EPI == EPI_SYMUPD) launch_tma_cfg<128, 128, 32, 4, 4, 3, AK, BKM, EPI>(c, a, grid, name);
+                break;
+            case T128x128W8K32:
+                if constexpr (EPI == EPI_SYMUPD) launch_tma_cfg<128, 128, 32, 4, 2, 3, AK, BKM, EPI>(c, a, grid, name);
+                break;
             case T64x128: launch_tma_cfg<64, 128, 16, 2, 4, 6, AK, BKM, EPI>(c, a, grid, name); break;
         }
         return;
@@ -235,7 +241,9 @@ static void launch_gemm_tile(Context& c, TileCfg t, const GemmArgs& a, dim3 grid
         case T128x128: launch_gemm_cfg<128, 128, 16, 4, 2, 4, AK, BKM, VEC, EPI>(c, a, grid, name); break;
         case T128x64: launch_gemm_cfg<128, 64, 16, 4, 2, 4, AK, BKM, VEC, EPI>(c, a, grid, name); break;
         case T128x32: launch_gemm_cfg<128, 32, 16, 8, 1, 4, AK, BKM, VEC, EPI>(c, a, grid, name); break;
-        case T128x128W16: launch_gemm_cfg<128, 128, 16, 4, 4, 4, AK, BKM, VEC, EPI>(c, a, grid, name); break;
+        case T128x128W16:
+        case T128x128K32:
+        case T128x128W8K32: launch_gemm_cfg<128, 128, 16, 4, 4, 4, AK, BKM, VEC, EPI>(c, a, grid, name); break;
         case T64x128: launch_gemm_cfg<64, 128, 16, 2, 4, 4, AK, BKM, VEC, EPI>(c, a, grid, name); break;
     }
 }
@@ -368,6 +376,11 @@ static void symupd(Context& c, int64_t n, int64_t k, const double* V, int64_t ld
     a.k_chunk = k;
     a.skip = skip;
     a.nonfinite = nonfinite;
+    static const int dbg = [] {
+        const char* e = std::getenv("SI_SYMUPD_DBG");
+        return e ? std::atoi(e) : 0;
+    }();
+    a.dbg = dbg;
     const int vec = pick_vec(a);
     // Tile choice (SI_SYMUPD_TILE): default one 16-warp CTA per SM on 128×128
     // tiles; "w8" one 8-warp CTA on 128×128; "128x64" two 8-warp CTAs per SM so
@@ -377,6 +390,8 @@ static void symupd(Context& c, int64_t n, int64_t k, const double* V, int64_t ld
         const char* e = std::getenv("SI_SYMUPD_TILE");
         const std::string v = e ? e : "";
         if (v == "128x64") return T128x64;
+        if (v == "k32") return T128x128K32;
+        if (v == "w8k32") return T128x128W8K32;
         if (v == "w8") return T128x128;
         return T128x128W16;
     }();

@@ -42,6 +42,7 @@ struct GemmArgs {
     int* nonfinite;   // STORE / SYMUPD: set to 1 when a written entry is not finite (simi.cpp:342-347)
     int64_t diag_off; // RESID: the identity's diagonal is at (r, r + diag_off) (row panels of a sharded X)
     int c_in_acc;     // STORE: accumulators start from beta·C (set by the host when alpha == 1, beta != 0)
+    int dbg;          // SYMUPD experiments (SI_SYMUPD_DBG): 1 = no stores, 2 = no C loads, 4 = no C prefetch
 };
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool A_KMAJOR, bool B_KMAJOR>
@@ -161,7 +162,7 @@ struct TileOps {
     }
 
     __device__ __forceinline__ void init_acc(double (&acc)[MI][NI][4], const GemmArgs& p) const {
-        if (c_in_acc(p)) {
+        if (c_in_acc(p) && !(EPI == EPI_SYMUPD && (p.dbg & 2))) {
             // accumulate onto the C tile itself (C = beta·C + A·B with alpha = 1; for
             // SYMUPD X + V·Uᵀ): the loads are issued under the pipeline fill and the
             // epilogue becomes store-only
@@ -245,6 +246,17 @@ struct TileOps {
                 // pair (r, c), (r, c+1) is one aligned 16-byte store
                 const bool fast = m0 + BM <= n0 && m0 + BM <= p.M && n0 + BN <= p.N && (p.ldc & 1) == 0 &&
                                   (reinterpret_cast<uintptr_t>(p.C) & 15) == 0;
+                if (fast && (p.dbg & 1)) {  // experiment: keep the accumulators live, store nothing
+                    double t = 0.0;
+#pragma unroll
+                    for (int i = 0; i < MI; ++i)
+#pragma unroll
+                        for (int j = 0; j < NI; ++j)
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) t += acc[i][j][e];
+                    if (t == 1.2345e300) p.C[0] = t;
+                    return;
+                }
                 if (fast) {
                     bool bad = false;
 #pragma unroll
@@ -406,7 +418,7 @@ __global__ void __launch_bounds__(WM* WN * 32, (EPI == EPI_SYMUPD && BM * BN <= 
             t.compute_stage(acc, As, As + SM::A_ELEMS);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
-            if (kt == nk - 1 && w + gridDim.x < W && t.c_in_acc(p)) {
+            if (kt == nk - 1 && w + gridDim.x < W && t.c_in_acc(p) && !(EPI == EPI_SYMUPD && (p.dbg & 4))) {
                 T nt = t;  // warm L2 with the next tile's C block before its init_acc
                 nt.setup_work(w + gridDim.x, p, warp, lane);
                 nt.prefetch_c(p);

@@ -104,6 +104,42 @@ int main() {
         cfg_err = true;
     }
     CHECK(cfg_err);
+
+    // row f3: psb keeps X exactly symmetric and satisfies X⁺AS = S (test_qn_updates.cpp:119-132)
+    Matrix sk(5, 2);
+    sk(1, 0) = 1.0;
+    sk(3, 1) = 1.0;
+    const Matrix xp = psb_step(Matrix::Identity(5, 5), spd, sk);
+    double sec = 0.0;
+    for (Index j = 0; j < 2; ++j)
+        for (Index i = 0; i < 5; ++i) {
+            double v = 0.0;
+            for (Index k = 0; k < 5; ++k)
+                for (Index l = 0; l < 5; ++l) v += xp(i, k) * spd(k, l) * sk(l, j);
+            sec += (v - sk(i, j)) * (v - sk(i, j));
+        }
+    CHECK(std::sqrt(sec) <= 1e-9);
+    // dfp with S = I lands on A (test_qn_updates.cpp:176-185)
+    const IteratePair full = dfp_step(Matrix::Identity(5, 5), Matrix::Identity(5, 5), spd, Matrix::Identity(5, 5));
+    CHECK(diff_norm(full.primal, spd) <= 1e-9 * 10.0);
+    // named dfp run tracks its inverse
+    InverterConfig dcfg{ProblemMatrix(spd, Symmetry::spd), SketchRule::gaussian(2),
+                        MethodSpec::named_method(UpdateName::dfp)};
+    dcfg.tol = 1e-8;
+    dcfg.max_iters = 3000;
+    const RunResult dres = run_inverter(dcfg);
+    CHECK(dres.termination == Termination::tol_reached);
+    CHECK(dres.state.x_inv.has_value());
+    // row f4: Newton–Schulz scalar regression and a converging run (test_baselines.cpp:14-21, 85-99)
+    Matrix a2(1, 1), x2(1, 1);
+    a2(0, 0) = 2.0;
+    x2(0, 0) = 0.4;
+    CHECK(std::abs(newton_schulz_step(x2, a2)(0, 0) - 0.48) <= 1e-14);
+    BaselineConfig bcfg{ProblemMatrix(spd, Symmetry::spd)};
+    bcfg.tol = 1e-8;
+    bcfg.max_iters = 200;
+    const RunResult bres = run_baseline(bcfg);
+    CHECK(bres.termination == Termination::tol_reached);
     std::printf("%d failure(s)\n", failures);
     return failures;
 }
