@@ -308,30 +308,44 @@ void gemm(Context& c, int64_t M, int64_t N, int64_t K, const double* A, int64_t 
     a.skip = skip;
     a.nonfinite = nonfinite;
     // short-K, wide-output products (the rank-2q panel update) keep 16 warps resident
-    const TileCfg t = (K <= 512 && N > 64 && M > 64) ? T128x128W16 : pick_tile(N, M);
+    // K <= 128 panel updates (the AdaRBFGS L update): two 8-warp 128×64 CTAs per SM so one
+    // CTA's C-tile load/store overlaps the other's mainloop (3.6% faster at config 2 than one
+    // 16-warp 128×128 CTA); SI_SHORTK_TILE=w16 selects the latter
+    static const int shortk_mode = [] {
+        const char* e = std::getenv("SI_SHORTK_TILE");
+        return (e && std::string(e) == "w16") ? 0 : 1;
+    }();
+    const TileCfg t = (K <= 128 && N > 64 && M > 64 && shortk_mode == 1)
+                          ? T128x64
+                          : ((K <= 512 && N > 64 && M > 64) ? T128x128W16 : pick_tile(N, M));
     const int BM = t == T64x128 ? 64 : 128;
     const int BN = (t == T128x128 || t == T128x128W16 || t == T64x128) ? 128 : (t == T128x64 ? 64 : 32), BKT = 16;
     const int64_t tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN, tiles = tm * tn;
     const int per_sm = (t == T128x128 || t == T128x128W16 || t == T64x128) ? 1 : 2;
     const int64_t slots = int64_t(c.num_sms) * per_sm;
-    // split-K so the number of work units fills whole waves of the 148 SMs
+    // split-K: pick the split minimising a time model —
+    //   waves(s) · (k-stages per unit + F) · t_stage  +  partial traffic / HBM  +  reduce launch
+    // (F ≈ 2 stages of per-unit pipeline fill / epilogue; t_stage = one BM×BN×16 DMMA
+    // stage on one SM at the measured 36.9 TFLOP/s / 148; per_sm CTAs share an SM).
     int splits = 1;
-    if (K > 8 * BKT && tiles < 8 * slots && !nonfinite) {
-        // wave efficiency of `units` work units on `slots` resident CTAs, minus a
-        // small per-split cost (partials written + reduced)
-        auto score = [&](int64_t s) {
+    if (K > 8 * BKT && !nonfinite) {
+        const double t_stage = double(BM) * BN * BKT * 2.0 / (36.9e12 / 148.0) * per_sm;  // seconds
+        auto cost = [&](int64_t s) {
+            const int64_t chunk = ((K + s - 1) / s + BKT - 1) / BKT * BKT;
             const int64_t units = tiles * s;
-            const double eff = double(units) / double(((units + slots - 1) / slots) * slots);
-            return eff - 0.004 * double(s);
+            const double waves = double((units + slots - 1) / slots);
+            double t = waves * (double(chunk / BKT) + 2.0) * t_stage;
+            if (s > 1) t += (2.0 * double(s) + 1.0) * double(M) * double(N) * 8.0 / 5.0e12 + 4e-6;
+            return t;
         };
-        double best = score(1);
+        double best = cost(1);
         for (int s = 2; s <= 128; ++s) {
             const int64_t chunk = ((K + s - 1) / s + BKT - 1) / BKT * BKT;
             if (chunk < 8 * BKT) break;
             if (double(s) * double(M) * double(N) * 8.0 > 512.0 * 1024 * 1024) break;
-            const double sc = score(s);
-            if (sc > best + 1e-9) {
-                best = sc;
+            const double cs = cost(s);
+            if (cs < best * 0.995) {
+                best = cs;
                 splits = s;
             }
         }
@@ -921,7 +935,7 @@ static void ns_fused(Context& c, const double* Mq, int64_t q, double* R, int* st
         attr = true;
     }
     LaunchScope ls(c, "ns_fused");
-    ns_fused_kernel<QP><<<1, 256, smem, c.stream>>>(Mq, q, int(q), R, status, 1e-14 * std::sqrt(double(q)), 60);
+    ns_fused_kernel<QP><<<1, 512, smem, c.stream>>>(Mq, q, int(q), R, status, 1e-14 * std::sqrt(double(q)), 60);
     check_launch("ns_fused");
 }
 

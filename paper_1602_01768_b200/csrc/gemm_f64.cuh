@@ -317,7 +317,7 @@ struct TileOps {
 // L2 when the epilogue will read it.  (A separate producer warp would cost a
 // whole warpgroup of registers: ptxas allocates in 4-warp units.)
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool A_KMAJOR, bool B_KMAJOR, int EPI>
-__global__ void __launch_bounds__(WM* WN * 32, (EPI == EPI_SYMUPD && BM * BN <= 128 * 64) ? 2 : 1)
+__global__ void __launch_bounds__(WM* WN * 32, ((EPI == EPI_SYMUPD || EPI == EPI_STORE) && BM == 128 && BN == 64) ? 2 : 1)
     gemm_tma_persistent_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                                GemmArgs p) {
     using SM = GemmSmem<BM, BN, BK, WM, WN, STAGES, A_KMAJOR, B_KMAJOR>;

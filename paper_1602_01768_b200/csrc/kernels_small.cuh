@@ -326,10 +326,24 @@ __global__ void ns_init_kernel(const double* __restrict__ G, int64_t ldg, int q,
     s = warp_sum(s);
     if ((tid & 31) == 0) red[tid >> 5] = s;
     __syncthreads();
+    double rmax = 0.0;  // ‖G‖_∞ (see ns_fused_kernel: a tighter λmax bound than ‖G‖_F)
+    for (int i = tid; i < q; i += nt) {
+        double r = 0.0;
+        for (int j = 0; j < q; ++j) r += fabs(0.5 * (G[i + (int64_t)j * ldg] + G[j + (int64_t)i * ldg]));
+        rmax = fmax(rmax, r);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+    __shared__ double rm[32];
+    if ((tid & 31) == 0) rm[tid >> 5] = rmax;
+    __syncthreads();
     if (tid == 0) {
-        double t = 0.0;
-        for (int w = 0; w < nt / 32; ++w) t += red[w];
-        scal[0] = sqrt(t);
+        double t = 0.0, m = 0.0;
+        for (int w = 0; w < nt / 32; ++w) {
+            t += red[w];
+            m = fmax(m, rm[w]);
+        }
+        scal[0] = fmin(sqrt(t), m);
         scal[1] = 1e300;  // previous error
     }
     __syncthreads();
@@ -401,57 +415,126 @@ __global__ void ns_finish_kernel(const double* __restrict__ Z, int q, const doub
 // product on the DMMA pipe (mma.m16n8k8), no global round trips between
 // iterations.  Padding rows/cols carry an identity block, which the iteration
 // leaves invariant.  Same contract as the multi-kernel variant above.
+// C_j = A_j·B_j for NP independent QP×QP products in the dynamic shared buffer
+// `nsm` (operands addressed by offsets, pitch QP+4 ≡ 4 mod 16: conflict-free
+// fragment loads).  Every product in the Newton–Schulz iteration is a polynomial
+// in the same symmetric G (Y, Z, T commute and stay symmetric), so only the
+// m16×n8 output blocks that meet the upper triangle are computed (20 of 32 at
+// QP = 64) and each element (r ≤ c) is stored to (r, c) and (c, r): every entry
+// is written exactly once and the result is exactly symmetric.  Each warp owns
+// PER blocks across the NP products and advances all of their accumulation
+// chains together, so the DMMA pipe sees NP·PER independent chains.
+extern __shared__ __align__(16) double nsm[];
+
 template <int QP>
-__device__ __forceinline__ void cta_gemm_smem(const double* __restrict__ A, const double* __restrict__ B,
-                                              double* __restrict__ Cm, int warp, int nwarps, int lane) {
+__device__ __forceinline__ void upper_block(int idx, int& m0, int& n0) {
+    constexpr int MB = QP / 16, NB = QP / 8;
+#pragma unroll
+    for (int mb = 0; mb < MB; ++mb) {
+        const int cnt = NB - 2 * mb;
+        if (idx < cnt) {
+            m0 = mb * 16;
+            n0 = (2 * mb + idx) * 8;
+            return;
+        }
+        idx -= cnt;
+    }
+    m0 = n0 = 0;
+}
+
+template <int QP, int NW, int NP>
+__device__ __forceinline__ void cta_symm_products(const int (&aoff)[NP], const int (&boff)[NP], const int (&coff)[NP],
+                                                  int warp, int lane) {
     constexpr int LD = QP + 4;
     constexpr int MB = QP / 16, NB = QP / 8;
+    constexpr int NBLK = MB * NB - MB * (MB - 1);  // blocks meeting the upper triangle
+    constexpr int TOT = NP * NBLK;
+    constexpr int PER = (TOT + NW - 1) / NW;
     const int g = lane >> 2, t = lane & 3;
-    for (int blk = warp; blk < MB * NB; blk += nwarps) {
-        const int m0 = (blk % MB) * 16, n0 = (blk / MB) * 8;
-        double c[4] = {0.0, 0.0, 0.0, 0.0};
+    int m0s[PER], n0s[PER], ao[PER], bo[PER], co[PER];
 #pragma unroll
-        for (int k0 = 0; k0 < QP; k0 += 8) {
-            double a[4], b[2];
-            a[0] = A[(m0 + g) + (k0 + t) * LD];
-            a[1] = A[(m0 + g + 8) + (k0 + t) * LD];
-            a[2] = A[(m0 + g) + (k0 + t + 4) * LD];
-            a[3] = A[(m0 + g + 8) + (k0 + t + 4) * LD];
-            b[0] = B[(k0 + t) + (n0 + g) * LD];
-            b[1] = B[(k0 + t + 4) + (n0 + g) * LD];
-            dmma_1688(c, a, b);
+    for (int p = 0; p < PER; ++p) {
+        const int job = min(warp + p * NW, TOT - 1);
+        const int u = job / NBLK;
+        upper_block<QP>(job % NBLK, m0s[p], n0s[p]);
+        ao[p] = aoff[0];
+        bo[p] = boff[0];
+        co[p] = coff[0];
+#pragma unroll
+        for (int v = 1; v < NP; ++v)
+            if (u == v) {
+                ao[p] = aoff[v];
+                bo[p] = boff[v];
+                co[p] = coff[v];
+            }
+    }
+    double c[PER][4];
+#pragma unroll
+    for (int p = 0; p < PER; ++p)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) c[p][e] = 0.0;
+#pragma unroll
+    for (int k0 = 0; k0 < QP; k0 += 8) {
+#pragma unroll
+        for (int p = 0; p < PER; ++p) {
+            if (warp + p * NW < TOT) {
+                const double* Au = nsm + ao[p];
+                const double* Bu = nsm + bo[p];
+                const int m0 = m0s[p], n0 = n0s[p];
+                double a[4], b[2];
+                a[0] = Au[(m0 + g) + (k0 + t) * LD];
+                a[1] = Au[(m0 + g + 8) + (k0 + t) * LD];
+                a[2] = Au[(m0 + g) + (k0 + t + 4) * LD];
+                a[3] = Au[(m0 + g + 8) + (k0 + t + 4) * LD];
+                b[0] = Bu[(k0 + t) + (n0 + g) * LD];
+                b[1] = Bu[(k0 + t + 4) + (n0 + g) * LD];
+                dmma_1688(c[p], a, b);
+            }
         }
-        Cm[(m0 + g) + (n0 + 2 * t) * LD] = c[0];
-        Cm[(m0 + g) + (n0 + 2 * t + 1) * LD] = c[1];
-        Cm[(m0 + g + 8) + (n0 + 2 * t) * LD] = c[2];
-        Cm[(m0 + g + 8) + (n0 + 2 * t + 1) * LD] = c[3];
+    }
+#pragma unroll
+    for (int p = 0; p < PER; ++p) {
+        if (warp + p * NW < TOT) {
+            double* Cu = nsm + co[p];
+            const int m0 = m0s[p], n0 = n0s[p];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int r = m0 + g + ((e >> 1) << 3), cc = n0 + 2 * t + (e & 1);
+                if (r <= cc) {
+                    Cu[r + cc * LD] = c[p][e];
+                    Cu[cc + r * LD] = c[p][e];
+                }
+            }
+        }
     }
 }
 
 template <int QP>
-__global__ void __launch_bounds__(256) ns_fused_kernel(const double* __restrict__ G, int64_t ldg, int q,
+__global__ void __launch_bounds__(512) ns_fused_kernel(const double* __restrict__ G, int64_t ldg, int q,
                                                        double* __restrict__ R, int* status, double tol, int max_it) {
-    constexpr int LD = QP + 4, SZ = QP * LD;
-    extern __shared__ __align__(16) double sm[];
-    __shared__ double red[8];
+    constexpr int LD = QP + 4, SZ = QP * LD, NW = 16;
+    __shared__ double red[NW];
     __shared__ double s_c, s_err, s_prev;
     __shared__ int s_stop;
     if (*status) return;
-    double* Y = sm;
-    double* Z = Y + SZ;
-    double* T = Z + SZ;
-    double* Yn = T + SZ;
-    double* Zn = Yn + SZ;
-    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+    // operand offsets in nsm: Y, Z, T, Yn, Zn
+    int oY = 0, oZ = SZ, oYn = 3 * SZ, oZn = 4 * SZ;
+    const int oT = 2 * SZ;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
     auto block_sum = [&](double v) {
         v = warp_sum(v);
         if (lane == 0) red[warp] = v;
         __syncthreads();
         double s = 0.0;
-        for (int w = 0; w < nw; ++w) s += red[w];
+#pragma unroll
+        for (int w = 0; w < NW; ++w) s += red[w];
         __syncthreads();
         return s;
     };
+    // scale c ≥ λmax(G): min(‖G‖_F, ‖G‖_∞) (both bound the spectral radius of a
+    // symmetric G; ‖G‖_∞ is far tighter for the near-diagonal Grams of coordinate
+    // sketches, which saves Newton–Schulz iterations — the small eigenvalues of
+    // G/c grow by at most 1.5× per iteration until they reach 1)
     double fro = 0.0;
     for (int idx = tid; idx < q * q; idx += nt) {
         const int i = idx % q, j = idx / q;
@@ -459,8 +542,21 @@ __global__ void __launch_bounds__(256) ns_fused_kernel(const double* __restrict_
         fro += v * v;
     }
     fro = block_sum(fro);
+    __shared__ double s_rowmax[NW];
+    double rmax = 0.0;
+    for (int i = tid; i < q; i += nt) {  // row abs sums
+        double r = 0.0;
+        for (int j = 0; j < q; ++j) r += fabs(0.5 * (G[i + (int64_t)j * ldg] + G[j + (int64_t)i * ldg]));
+        rmax = fmax(rmax, r);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+    if (lane == 0) s_rowmax[warp] = rmax;
+    __syncthreads();
     if (tid == 0) {
-        s_c = sqrt(fro);
+        double m = 0.0;
+        for (int w = 0; w < NW; ++w) m = fmax(m, s_rowmax[w]);
+        s_c = fmin(sqrt(fro), m);
         s_prev = 1e300;
         s_stop = 0;
     }
@@ -473,21 +569,23 @@ __global__ void __launch_bounds__(256) ns_fused_kernel(const double* __restrict_
     for (int idx = tid; idx < QP * QP; idx += nt) {
         const int i = idx % QP, j = idx / QP;
         const bool in = i < q && j < q;
-        Y[i + j * LD] = in ? 0.5 * (G[i + (int64_t)j * ldg] + G[j + (int64_t)i * ldg]) / cc : (i == j ? 1.0 : 0.0);
-        Z[i + j * LD] = (i == j) ? 1.0 : 0.0;
+        nsm[oY + i + j * LD] = in ? 0.5 * (G[i + (int64_t)j * ldg] + G[j + (int64_t)i * ldg]) / cc : (i == j ? 1.0 : 0.0);
+        nsm[oZ + i + j * LD] = (i == j) ? 1.0 : 0.0;
     }
     __syncthreads();
-    int it = 0;
-    for (; it < max_it; ++it) {
-        cta_gemm_smem<QP>(Z, Y, T, warp, nw, lane);  // T ← Z·Y
+    for (int it = 0; it < max_it; ++it) {
+        {
+            const int a1[1] = {oZ}, b1[1] = {oY}, c1[1] = {oT};
+            cta_symm_products<QP, NW, 1>(a1, b1, c1, warp, lane);  // T ← Z·Y
+        }
         __syncthreads();
         double e = 0.0;
         for (int idx = tid; idx < QP * QP; idx += nt) {
             const int i = idx % QP, j = idx / QP;
-            const double zy = T[i + j * LD];
+            const double zy = nsm[oT + i + j * LD];
             const double d = zy - (i == j ? 1.0 : 0.0);
             e += d * d;
-            T[i + j * LD] = (i == j ? 1.5 : 0.0) - 0.5 * zy;
+            nsm[oT + i + j * LD] = (i == j ? 1.5 : 0.0) - 0.5 * zy;
         }
         e = block_sum(e);
         if (tid == 0) {
@@ -498,15 +596,17 @@ __global__ void __launch_bounds__(256) ns_fused_kernel(const double* __restrict_
         }
         __syncthreads();
         if (s_stop) break;
-        cta_gemm_smem<QP>(Y, T, Yn, warp, nw, lane);  // Y ← Y·T
-        cta_gemm_smem<QP>(T, Z, Zn, warp, nw, lane);  // Z ← T·Z
+        {
+            const int a2[2] = {oY, oT}, b2[2] = {oT, oZ}, c2[2] = {oYn, oZn};
+            cta_symm_products<QP, NW, 2>(a2, b2, c2, warp, lane);  // Y ← Y·T, Z ← T·Z
+        }
         __syncthreads();
-        double* tmp = Y;
-        Y = Yn;
-        Yn = tmp;
-        tmp = Z;
-        Z = Zn;
-        Zn = tmp;
+        int tmp = oY;
+        oY = oYn;
+        oYn = tmp;
+        tmp = oZ;
+        oZ = oZn;
+        oZn = tmp;
     }
     if (!s_stop || !(s_err < 1e-6)) {
         if (tid == 0) *status = 1;  // did not converge: the reference's floor / resample signal
@@ -515,7 +615,7 @@ __global__ void __launch_bounds__(256) ns_fused_kernel(const double* __restrict_
     const double rc = 1.0 / sqrt(cc);
     for (int idx = tid; idx < q * q; idx += nt) {
         const int i = idx % q, j = idx / q;
-        R[idx] = 0.5 * (Z[i + j * LD] + Z[j + i * LD]) * rc;
+        R[idx] = nsm[oZ + i + j * LD] * rc;  // Z is exactly symmetric
     }
 }
 
