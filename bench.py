@@ -248,9 +248,10 @@ def run_reference(args, cfg):
 
 
 def run_sharded(args, cfg):
-    """N > 1: X and A row-sharded over the ranks (paper_1602_01768_b200/dist.py),
-    NCCL all-gathers of Y and W and one packed all-reduce per iteration; the
-    workload (config 3) is fixed, so scaling is strong."""
+    """N > 1: the upper triangle of X in 2P balanced row chunks (SymmetricShardedRBFGS,
+    paper_1602_01768_b200/dist.py), A rows alongside; per iteration one NCCL
+    all-gather of Y, one all-reduce of the W partials and one of the packed
+    [SᵀY | YᵀW] partials.  The workload (config 3) is fixed: strong scaling."""
     import torch
     import torch.distributed as dist
 
@@ -261,22 +262,29 @@ def run_sharded(args, cfg):
     dist.init_process_group("nccl", device_id=torch.device("cuda", local), rank=rank, world_size=world)
     import paper_1602_01768_b200 as si
     from paper_1602_01768_b200 import generators as G
-    from paper_1602_01768_b200.dist import CudaPanelOps, RowShardedRBFGS, row_partition
+    from paper_1602_01768_b200.dist import CudaPanelOps, SymmetricShardedRBFGS
 
     n, q = cfg["n"], cfg["q"]
     stream = torch.cuda.current_stream()
     ctx = si.Context(local, stream=stream.cuda_stream)
     a_full = G.config3_dense_device(n, seed=0) if cfg["gen"] == "config3" else \
         torch.from_numpy(make_dense(cfg)).cuda()
-    starts = row_partition(n, world)
-    r0, r1 = starts[rank], starts[rank + 1]
-    # A symmetric: the row-major tensor is Aᵀ = A, so columns r0..r1 of it are the
-    # column-major m×n row panel A[R_p, :]
-    a_rows = a_full[r0:r1, :].contiguous().reshape(-1)
-    prob = None  # the timed loop needs no residual
+
+    def rows_of_chunk(r0, r1):
+        # column-major (r1−r0)×n panel A[r0:r1, :]: in a row-major (n, n) tensor holding the
+        # symmetric A, columns r0..r1 laid out row-major are exactly that panel
+        return a_full[:, r0:r1].contiguous().reshape(-1)
+
+    sh = SymmetricShardedRBFGS(CudaPanelOps(ctx), n, q, rows_of_chunk, seed=0, prob=None)
+    # host copies of this rank's A rows for the end-to-end pass (pinned, outside any timing)
+    host_rows = {}
+    for c in sh.chunks:
+        r0, r1 = sh.bounds[c], sh.bounds[c + 1]
+        h = torch.empty((r1 - r0) * n, dtype=torch.float64, pin_memory=True)
+        h.copy_(rows_of_chunk(r0, r1))
+        host_rows[(r0, r1)] = h
     del a_full
     torch.cuda.empty_cache()
-    sh = RowShardedRBFGS(CudaPanelOps(ctx), n, q, a_rows, seed=0, prob=prob)
     for _ in range(args.warmup):
         sh.step()
     torch.cuda.synchronize()
@@ -297,9 +305,41 @@ def run_sharded(args, cfg):
     t = torch.tensor([ms], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    m = r1 - r0
-    rank_flops = 2.0 * m * n * q * 2 + 4.0 * m * n * q + 2.0 * m * q * 2 * q + 2.0 * m * 2 * q * 2 * q
+    # this rank's DMMA FLOPs per iteration (its two chunk trapezoids)
+    rank_flops = 0.0
+    for c in sh.chunks:
+        r0 = sh.bounds[c]
+        m = sh.bounds[c + 1] - r0
+        r1 = r0 + m
+        rank_flops += (2.0 * m * n * q                                   # Y rows
+                       + 2.0 * m * q * (n - r0) + 2.0 * m * q * (n - r1)  # W: trapezoid and its transpose
+                       + 2.0 * m * m * q + 4.0 * m * q * (n - r1)         # update: diagonal block (upper) + rest
+                       + 8.0 * m * q * q + 4.0 * m * q * q)                # V rows, P partial
     achieved = rank_flops * args.steps / (ms * 1e-3) / 1e12
+    # ---- e2e: the sharded public API from host buffers (A rows H2D, X gathered to host) ----
+    del sh
+    torch.cuda.empty_cache()
+    k_e2e = args.steps
+    x_host = torch.empty(n * n, dtype=torch.float64, pin_memory=True) if rank == 0 else None
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    sh2 = SymmetricShardedRBFGS(CudaPanelOps(ctx), n, q,
+                                lambda r0, r1: host_rows[(r0, r1)].to("cuda", non_blocking=True), seed=0)
+    for _ in range(k_e2e):
+        sh2.step()
+    xf = sh2.gather_x()
+    if rank == 0:
+        x_host.copy_(xf)
+    torch.cuda.synchronize()
+    dist.barrier()
+    dt = torch.tensor([time.perf_counter() - t0], device="cuda")
+    dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+    e2e = {"value": k_e2e / float(dt.item()), "unit": "iter/s",
+           "h2d_bytes_per_step": int(8 * n * n / k_e2e), "d2h_bytes_per_step": int(8 * n * n / k_e2e),
+           "note": "SymmetricShardedRBFGS from host A rows (each rank uploads its chunks), k iterations, "
+                   "X all-reduced and copied to rank 0's pinned host buffer; slowest rank's wall clock"}
+    del sh2, xf
     if rank == 0:
         alg = 6.0 * n * n * q + 12.0 * n * q * q
         line = {
@@ -308,14 +348,15 @@ def run_sharded(args, cfg):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": cfg["name"], "n": n, "q": q, "sketch": "gaussian, device Philox4x32-10",
-                       "l2": "inputs larger than L2; no flush", "parallelism": f"row-sharded X and A over {world} GPUs",
+                       "l2": "inputs larger than L2; no flush", "parallelism": f"upper triangle of X in 2P balanced row chunks over {world} GPUs "
+                                      "(SymmetricShardedRBFGS), A rows alongside",
                        "algorithmic_gflop_per_step": alg / 1e9},
-            "roofline": {"bound": "tensor", "kernel": "row-panel iteration (all DMMA GEMMs of one rank)",
+            "roofline": {"bound": "tensor", "kernel": "chunk-trapezoid iteration (all DMMA GEMMs of one rank)",
                          "achieved": achieved, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": achieved / FP64_DMMA_PEAK_TFLOPS, "traffic": None,
                          "peak_source": "measured FP64 DMMA peak, profiles/r01_fp64_peak.txt"},
             "cpu_baseline": None,
-            "e2e": None,
+            "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }

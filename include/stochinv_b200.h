@@ -115,7 +115,8 @@ const char* si_version(void);
 void si_default_config(si_inverter_config* cfg); /* reference defaults (simi.hpp:53-71) */
 
 int si_context_create(int device, si_context** out);
-/* Run on a caller-provided cudaStream_t (e.g. torch.cuda.current_stream()). */
+/* Run on a caller-provided cudaStream_t (e.g. torch.cuda.current_stream()).  For the legacy default
+ * stream (NULL) the context uses a private blocking stream, which is ordered with it implicitly. */
 int si_context_create_on_stream(int device, void* cuda_stream, si_context** out);
 int si_context_destroy(si_context* ctx);
 int si_context_synchronize(si_context* ctx);
@@ -243,6 +244,10 @@ int64_t si_solver_redraws(si_solver* s);
  * B is K×N (b_kmajor: B(k,n) = B[k + n*ldb], else B[n + k*ldb]); FP64 DMMA. */
 int si_gemm_device(si_context* ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, int a_kmajor,
                    const double* B, int64_t ldb, int b_kmajor, double* C, int64_t ldc, double alpha, double beta);
+/* X (m×m symmetric, ld ldx) += V·Uᵀ (V, U m×k) on the upper tiles, written mirrored (exactly
+ * symmetric): the K-SYMUPD kernel, used on the diagonal blocks of the symmetric sharded driver. */
+int si_symupd_device(si_context* ctx, int64_t m, int64_t k, const double* V, int64_t ldv, const double* U,
+                     int64_t ldu, double* X, int64_t ldx);
 /* S (n×q, ld lds) ~ N(0,1) from Philox4x32-10(seed, draw): identical bytes on every rank. */
 int si_sketch_gaussian_device(si_context* ctx, double* S, int64_t n, int64_t q, int64_t lds, uint64_t seed,
                               uint64_t draw);
@@ -271,6 +276,11 @@ const double* si_problem_dense_device(si_problem* prob);
 
 /* ---- host RngStream (rng.hpp:13-71), exposed for input generation and tests */
 typedef struct si_rng si_rng;
+/* FactoredState adarbfgs_step(state, a, rule, rng, max_redraws), adarbfgs.hpp:37-38: one factored
+ * update L -> L⁺ drawing from the caller's RngStream (sketch = SI_SKETCH_ADAPTIVE_COLS, _GAUSS or
+ * _COLS_UNIFORM); SI_ERR_NUMERICAL when max_redraws + 1 draws are rejected. */
+int si_adarbfgs_step(si_context* ctx, si_problem* prob, int sketch, int64_t q, si_rng* rng, int max_redraws,
+                     const double* l_host, double* l_out_host);
 int si_rng_create(uint64_t seed, si_rng** out);
 int si_rng_substream(si_rng* r, uint64_t index, si_rng** out); /* rng.hpp:18-20 */
 int si_rng_destroy(si_rng* r);

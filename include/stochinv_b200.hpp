@@ -514,10 +514,29 @@ public:
         return m;
     }
 
+    si_rng* handle() const { return h_.get(); }
+
 private:
     explicit RngStream(si_rng* r) { h_.reset(r, [](si_rng* p) { si_rng_destroy(p); }); }
     std::shared_ptr<si_rng> h_;
 };
+
+/// FactoredState (adarbfgs.hpp:15-22, the step-level subset) and
+/// FactoredState adarbfgs_step(state, a, rule, rng, max_redraws), adarbfgs.hpp:37-38.
+struct FactoredState {
+    Matrix l;
+    long k = 0;
+};
+inline FactoredState adarbfgs_step(const FactoredState& state, const ProblemMatrix& a, const SketchRule& rule,
+                                   RngStream& rng, int max_redraws = 100) {
+    const Index n = a.n();
+    FactoredState next{detail::make<Matrix>(n, n), state.k + 1};
+    const int rc = si_adarbfgs_step(detail::context(), a.handle(), int(rule.kind), rule.q, rng.handle(), max_redraws,
+                                    state.l.data(), next.l.data());
+    if (rc == SI_ERR_CONFIG) throw ConfigError(si_last_error());
+    if (rc != SI_OK) throw NumericalError(si_last_error());
+    return next;
+}
 
 // flops.cpp:43-46, 70-74
 namespace flops {

@@ -16,6 +16,7 @@ from .api import (  # noqa: E402
     BaselineMethod,
     ConfigError,
     Context,
+    FactoredState,
     CudaError,
     GramRankDeficientError,
     HistoryPoint,
@@ -36,6 +37,7 @@ from .api import (  # noqa: E402
     TrackOptions,
     UpdateName,
     adaptive_block_probabilities,
+    adarbfgs_step,
     aip_step,
     dfp_step,
     mr_init,

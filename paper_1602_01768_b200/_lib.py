@@ -94,6 +94,7 @@ _SIGS = {
     "si_solver_residual": (ci, [vp, pd]),
     "si_solver_redraws": (i64, [vp]),
     "si_gemm_device": (ci, [vp, i64, i64, i64, vp, i64, ci, vp, i64, ci, vp, i64, d, d]),
+    "si_symupd_device": (ci, [vp, i64, i64, vp, i64, vp, i64, vp, i64]),
     "si_sketch_gaussian_device": (ci, [vp, vp, i64, i64, i64, u64, u64]),
     "si_rbfgs_core_device": (ci, [vp, vp, i64, i64, vp, vp]),
     "si_gather_columns_device": (ci, [vp, vp, i64, i64, vp, i64, vp]),
@@ -101,6 +102,7 @@ _SIGS = {
     "si_pdiag_update_device": (ci, [vp, vp, i64, i64, vp, vp, vp]),
     "si_residual_rows_device": (ci, [vp, vp, i64, i64, vp, i64, pd]),
     "si_problem_dense_device": (vp, [vp]),
+    "si_adarbfgs_step": (ci, [vp, vp, ci, i64, vp, ci, pd, pd]),
     "si_rng_create": (ci, [u64, C.POINTER(vp)]),
     "si_rng_substream": (ci, [vp, u64, C.POINTER(vp)]),
     "si_rng_destroy": (ci, [vp]),

@@ -750,6 +750,28 @@ class RngStream:
 # --------------------------------------------------------------- solver ----
 
 
+@dataclass
+class FactoredState:  # adarbfgs.hpp:15-22 (the step-level subset)
+    l: np.ndarray
+    k: int = 0
+
+
+def adarbfgs_step(state: FactoredState, a: ProblemMatrix, rule: SketchRule, rng: RngStream,
+                  max_redraws: int = 100) -> FactoredState:
+    """FactoredState adarbfgs_step(state, a, rule, rng, max_redraws) (adarbfgs.cpp:49-75):
+    one factored update on the GPU, drawing from the caller's RngStream."""
+    if not rule.is_adaptive() or rule.kind == SketchKind.adaptive_factor_gauss_device:
+        raise ConfigError("adarbfgs_step: rule must be adaptive-factor-cols or -gauss")
+    n = a.n()
+    l = _f64(state.l)
+    if l.shape != (n, n):
+        raise ConfigError("adarbfgs_step: state dimension mismatch")
+    out = np.empty((n, n), order="F")
+    _check(L.load().si_adarbfgs_step(a.ctx.handle, a.handle, int(rule.kind), int(rule.q), rng._h, int(max_redraws),
+                                     _pd(l), _pd(out)))
+    return FactoredState(out, state.k + 1)
+
+
 class Method(enum.IntEnum):
     rbfgs = 0
     adarbfgs = 1

@@ -226,7 +226,7 @@ int si_context_create(int device, si_context** out) {
 int si_context_create_on_stream(int device, void* stream, si_context** out) {
     return guard([&] {
         auto* h = new si_context();
-        h->c.reset(si::context_create(device, static_cast<cudaStream_t>(stream)));
+        h->c.reset(si::context_create(device, static_cast<cudaStream_t>(stream), true));
         *out = h;
     });
 }
@@ -1336,6 +1336,14 @@ int si_gemm_device(si_context* ctx, int64_t M, int64_t N, int64_t K, const doubl
     });
 }
 
+int si_symupd_device(si_context* ctx, int64_t m, int64_t k, const double* V, int64_t ldv, const double* U,
+                     int64_t ldu, double* X, int64_t ldx) {
+    return guard([&] {
+        require(m >= 0 && k >= 1 && ldv >= m && ldu >= m && ldx >= m, "symupd: bad shape");
+        if (m > 0) si::symupd_device(*ctx->c, m, k, V, ldv, U, ldu, X, ldx);
+    });
+}
+
 int si_sketch_gaussian_device(si_context* ctx, double* S, int64_t n, int64_t q, int64_t lds, uint64_t seed,
                               uint64_t draw) {
     return guard([&] {
@@ -1510,3 +1518,71 @@ int si_rng_uniform_subset(si_rng* r, int64_t n, int64_t q, int64_t* out) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------- adarbfgs_step ---
+// FactoredState adarbfgs_step(state, a, rule, rng, max_redraws), adarbfgs.cpp:49-75:
+// one factored update drawing from the caller's RngStream (probabilities once,
+// then one draw per attempt), NumericalError after max_redraws + 1 rejections.
+int si_adarbfgs_step(si_context* ctx, si_problem* prob, int sketch, int64_t q, si_rng* rng, int max_redraws,
+                     const double* l_host, double* l_out_host) {
+    return guard([&] {
+        auto& c = *ctx->c;
+        si::Problem& a = *prob->p;
+        const int64_t n = a.n;
+        const bool cols = sketch == SI_SKETCH_ADAPTIVE_COLS, uniform = sketch == SI_SKETCH_ADAPTIVE_COLS_UNIFORM,
+                   gauss = sketch == SI_SKETCH_ADAPTIVE_GAUSS;
+        if (!cols && !uniform && !gauss)
+            throw ConfigError("adarbfgs_step: rule must be adaptive-factor-cols or -gauss");
+        require(q >= 1 && q <= n, "SketchRule: q must satisfy 1 <= q <= n");
+        require(max_redraws >= 0, "adarbfgs_step: max_redraws must be >= 0");
+        validate_spd(prob);  // adarbfgs.cpp:53
+        si::AdaWork w;
+        struct Rel {
+            si::AdaWork& w;
+            ~Rel() { w.release(); }
+        } rel{w};
+        w.alloc(n, q, gauss);
+        w.pdiag_refresh = 1;  // a single step: the exact diagonal, as the reference
+        ck(cudaMemcpyAsync(w.L, l_host, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyHostToDevice, c.stream),
+           "h2d l");
+        const auto blocks = cols ? si::contiguous_partition(n, q) : std::vector<std::vector<si::Index>>{};
+        std::vector<double> p;
+        if (cols) {
+            si::ada_enqueue_probabilities(c, a, w);
+            ck(cudaStreamSynchronize(c.stream), "sync");
+            block_probabilities(w.p_pinned, blocks, p);
+        }
+        int st[4];
+        for (int attempt = 0; attempt <= max_redraws; ++attempt) {
+            int mode = 0;
+            w.q = q;
+            if (cols) {
+                const auto& blk = blocks[size_t(rng->r.categorical(p.data(), si::Index(p.size())))];
+                w.q = int64_t(blk.size());
+                for (size_t j = 0; j < blk.size(); ++j) w.idx_pinned[j] = blk[j];
+            } else if (uniform) {
+                const auto idx = si::uniform_subset(rng->r, n, q);
+                for (int64_t j = 0; j < q; ++j) w.idx_pinned[j] = idx[size_t(j)];
+            } else {
+                rng->r.gaussian_fill(w.st_pinned, n, q, n);
+                mode = 1;
+            }
+            if (mode == 0)
+                ck(cudaMemcpyAsync(w.idx_dev, w.idx_pinned, size_t(w.q) * sizeof(int64_t), cudaMemcpyHostToDevice,
+                                   c.stream),
+                   "h2d idx");
+            si::ada_enqueue_update(c, a, w, mode, 0);
+            read_status(c, w.status, st);
+            if (st[0]) {
+                ck(cudaMemsetAsync(w.status, 0, 4 * sizeof(int), c.stream), "reset");
+                continue;
+            }
+            ck(cudaMemcpyAsync(l_out_host, w.L, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyDeviceToHost,
+                               c.stream),
+               "d2h l");
+            ck(cudaStreamSynchronize(c.stream), "sync");
+            return;
+        }
+        throw NumericalError("adarbfgs_step: rejection limit exceeded for " + describe(sketch, q));
+    });
+}

@@ -22,7 +22,7 @@ void cuda_check(cudaError_t e, const char* what) {
 #define CK(x) cuda_check((x), #x)
 
 // ----------------------------------------------------------------- context --
-Context* context_create(int device, cudaStream_t external) {
+Context* context_create(int device, cudaStream_t external, bool on_stream) {
     CK(cudaSetDevice(device));
     auto* c = new Context();
     c->device = device;
@@ -30,6 +30,9 @@ Context* context_create(int device, cudaStream_t external) {
     if (external) {
         c->stream = external;
         c->own_stream = false;
+    } else if (on_stream) {
+        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamDefault));  // blocking: ordered with stream 0
+        c->own_stream = true;
     } else {
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         c->own_stream = true;

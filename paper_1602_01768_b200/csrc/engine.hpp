@@ -131,7 +131,10 @@ struct AdaWork {
 };
 
 // ---- engine entry points (engine.cu) -------------------------------------
-Context* context_create(int device, cudaStream_t external);
+// external == nullptr && !on_stream: a private non-blocking stream.  on_stream: the caller's
+// stream; the legacy default stream (0) is served by a private *blocking* stream, which the
+// legacy stream orders against implicitly in both directions (graphs cannot be captured on 0).
+Context* context_create(int device, cudaStream_t external, bool on_stream = false);
 void problem_upload_dense(Problem& p, const double* host, bool device_src);
 void problem_upload_csr(Problem& p, const int64_t* rowptr, const int32_t* colind, const double* val);
 bool problem_validate_spd(Problem& p);  // Cholesky-based (cuSOLVER potrf on a scratch copy)
@@ -169,6 +172,8 @@ void ada_enqueue_probabilities(Context& c, Problem& a, AdaWork& w);
 void family_alloc(RbfgsWork& w, int update);
 void family_release(RbfgsWork& w);
 void family_enqueue_iteration(Context& c, Problem& a, RbfgsWork& w, bool device_sketch, uint64_t seed);
+void symupd_device(Context& c, int64_t m, int64_t k, const double* V, int64_t ldv, const double* U, int64_t ldu,
+                   double* X, int64_t ldx);
 void residual_general_sq_enqueue(Context& c, Problem& a, const double* X, double* scratch_nn, double* out_dev);
 void column_weights(Context& c, Problem& a, int mode, std::vector<double>& out);
 void lu_inverse_device(Context& c, const double* M, int64_t n, double* out);

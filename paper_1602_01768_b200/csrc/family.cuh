@@ -264,6 +264,13 @@ void family_enqueue_iteration(Context& c, Problem& a, RbfgsWork& w, bool device_
     }
 }
 
+// X (m×m, symmetric, ld ldx) += V·Uᵀ on the upper tiles, mirrored — the K-SYMUPD
+// kernel for callers outside this file (the diagonal blocks of the sharded driver)
+void symupd_device(Context& c, int64_t m, int64_t k, const double* V, int64_t ldv, const double* U, int64_t ldu,
+                   double* X, int64_t ldx) {
+    symupd(c, m, k, V, ldv, U, ldu, X, ldx, 1.0, nullptr, nullptr);
+}
+
 // ‖I − A·X‖² for a general (non-symmetric) X: T = A·X into scratch, then the
 // identity-minus reduction (the dense path uses the residual GEMM directly).
 void residual_general_sq_enqueue(Context& c, Problem& a, const double* X, double* scratch_nn, double* out_dev) {

@@ -85,6 +85,9 @@ class CudaPanelOps:
                                                self._p(T) if T is not None else None,
                                                self._p(idx) if idx is not None else None, self._p(d)))
 
+    def symupd(self, m, k, V, ldv, U, ldu, X, ldx):
+        _check(self.lib.si_symupd_device(self.ctx.handle, m, k, self._p(V), ldv, self._p(U), ldu, self._p(X), ldx))
+
     def residual_rows_sq(self, prob: ProblemMatrix, m, r0, X, ldx) -> float:
         out = C.c_double()
         _check(self.lib.si_residual_rows_device(self.ctx.handle, prob.handle, m, r0, self._p(X), ldx, C.byref(out)))
@@ -388,6 +391,173 @@ class RowShardedAdaRBFGS(_RowPanels):
         self.ops.gemm(m, n, n, self.L, m, False, full, n, False, Xp, m)                       # X_p = L_p·Lᵀ
         part = self.ops.residual_rows_sq(self.prob, m, lay.r0, Xp, m)
         t = torch.tensor([part], dtype=torch.float64, device=self.L.device)
+        if self.world > 1:
+            dist.all_reduce(t)
+        return float(t.item()) ** 0.5
+
+
+def chunk_bounds(n: int, world: int):
+    """2·world contiguous row chunks (sizes differ by at most one)."""
+    return row_partition(n, 2 * world)
+
+
+class SymmetricShardedRBFGS:
+    """RBFGS with the upper triangle of X distributed over the ranks (SURVEY §8e,
+    the symmetric-tile refinement of the row split).
+
+    The rows are cut into 2P chunks; rank p owns chunks p and 2P−1−p, which
+    balances the upper-triangular work (chunk c holds the trapezoid
+    X[R_c, r0_c:n], the diagonal block stored in full).  Per iteration, with
+    every product on the sm_100a engine through the device-pointer C ABI:
+
+        Y_c      = A[R_c, :]·S                          local   2·m·n·q
+        Y        = all-gather(Y_c)                      NCCL    n×q
+        W       += X_c·Y[r0:]  and  X_c[:, m:]ᵀ·Y[R_c]   local   4·area·q
+        W        = all-reduce(W partials)               NCCL    n×q
+        P        = all-reduce(Σ_c Y[R_c]ᵀ·[S W][R_c])    NCCL    2q²
+        M        = core(P)                              replicated
+        V_c      = [S W][R_c]·M                         local
+        X_c     += V_c·[S W][r0:]ᵀ   (diagonal block by K-SYMUPD, exactly symmetric)   2·area·2q
+
+    Per-rank FLOPs ≈ 6n²q/P — the single-GPU count split evenly — against 8n²q/P
+    for the full row panels of RowShardedRBFGS.
+    """
+
+    def __init__(self, ops, n: int, q: int, a_rows_of_chunk, *, seed: int = 0, prob: ProblemMatrix | None = None,
+                 max_redraws: int = 100, device=None):
+        """a_rows_of_chunk(r0, r1) -> A[r0:r1, :] as a flat column-major (r1−r0)×n tensor."""
+        self.ops, self.n, self.q, self.seed, self.prob, self.max_redraws = ops, n, q, seed, prob, max_redraws
+        self.world = dist.get_world_size() if dist.is_initialized() else 1
+        self.rank = dist.get_rank() if dist.is_initialized() else 0
+        self.bounds = chunk_bounds(n, self.world)
+        P = self.world
+        self.chunks = [self.rank, 2 * P - 1 - self.rank]
+        self.draw = 0
+        self.redraws = 0
+        A0 = a_rows_of_chunk(self.bounds[self.chunks[0]], self.bounds[self.chunks[0] + 1])
+        dev = device if device is not None else A0.device
+        f = dict(dtype=torch.float64, device=dev)
+        self.A, self.X = {}, {}
+        for c in self.chunks:
+            r0, r1 = self.bounds[c], self.bounds[c + 1]
+            self.A[c] = A0 if c == self.chunks[0] else a_rows_of_chunk(r0, r1)
+            self.X[c] = torch.zeros((r1 - r0) * (n - r0), **f)
+        self.S = torch.empty(n * q, **f)
+        self.Y = torch.empty(n * q, **f)
+        self.U = torch.empty(n * 2 * q, **f)  # [S W], column-major n×2q
+        self.P = torch.empty(q * 2 * q, **f)
+        self.Pp = torch.empty(q * 2 * q, **f)
+        self.M = torch.empty(4 * q * q, **f)
+        mc = max(self.bounds[c + 1] - self.bounds[c] for c in range(2 * P))
+        self.Yc = torch.empty(mc * q, **f)
+        self.Vc = torch.empty(mc * 2 * q, **f)
+        self.Uc = torch.empty(mc * 2 * q, **f)
+        self.scratch = torch.empty(6 * q * q + 2 * q + 16, **f)
+        self.gather = torch.empty(2 * P * mc * q, **f)
+        self.set_identity()
+
+    def _m(self, c):
+        return self.bounds[c + 1] - self.bounds[c]
+
+    def set_identity(self):
+        for c in self.chunks:
+            m = self._m(c)
+            xv = self.X[c].view(self.n - self.bounds[c], m)  # column-major m×(n−r0) == row-major (n−r0, m)
+            xv.zero_()
+            i = torch.arange(m, device=xv.device)
+            xv[i, i] = 1.0
+
+    def _rows(self, buf, ncols, r0, r1):
+        """rows r0..r1 of a column-major n×ncols buffer, as an (ncols, r1−r0) view."""
+        return buf.view(ncols, self.n)[:, r0:r1]
+
+    def _all_gather_y(self):
+        """Y (n×q) from the ranks' chunk rows; chunk sizes differ by at most one."""
+        n, q, P = self.n, self.q, self.world
+        mc = self.gather.numel() // (2 * P * q)
+        send = torch.zeros(2 * mc * q, dtype=torch.float64, device=self.Y.device)
+        for j, c in enumerate(self.chunks):
+            r0, r1 = self.bounds[c], self.bounds[c + 1]
+            send.view(2, q, mc)[j, :, : r1 - r0].copy_(self._rows(self.Y, q, r0, r1))
+        if P > 1:
+            dist.all_gather_into_tensor(self.gather, send)
+            g = self.gather.view(P, 2, q, mc)
+        else:
+            g = send.view(1, 2, q, mc)
+        for p in range(P):
+            for j, c in enumerate((p, 2 * P - 1 - p)):
+                r0, r1 = self.bounds[c], self.bounds[c + 1]
+                self._rows(self.Y, q, r0, r1).copy_(g[p, j, :, : r1 - r0])
+
+    def step(self):
+        n, q, ops = self.n, self.q, self.ops
+        S, W = self.U[: n * q], self.U[n * q:]
+        for _ in range(self.max_redraws + 1):
+            ops.sketch(S, n, q, n, self.seed, self.draw)
+            self.draw += 1
+            # Y rows of the owned chunks, then the full Y
+            for c in self.chunks:
+                r0, m = self.bounds[c], self._m(c)
+                ops.gemm(m, q, n, self.A[c], m, False, S, n, True, self.Y[r0:], n)
+            self._all_gather_y()
+            # W = X·Y from the upper trapezoids: X_c·Y[r0:] and the strictly-upper part transposed
+            W.zero_()
+            for c in self.chunks:
+                r0, m = self.bounds[c], self._m(c)
+                r1 = r0 + m
+                ops.gemm(m, q, n - r0, self.X[c], m, False, self.Y[r0:], n, True, W[r0:], n, 1.0, 1.0)
+                if r1 < n:
+                    ops.gemm(n - r1, q, m, self.X[c][m * m:], m, True, self.Y[r0:], n, True, W[r1:], n, 1.0, 1.0)
+            if self.world > 1:
+                dist.all_reduce(W)
+            # P = Yᵀ·[S W] over the owned rows, all-reduced
+            self.Pp.zero_()
+            for c in self.chunks:
+                r0, m = self.bounds[c], self._m(c)
+                ops.gemm(q, 2 * q, m, self.Y[r0:], n, True, self.U[r0:], n, True, self.Pp, q, 1.0, 1.0)
+            self.P.copy_(self.Pp)
+            if self.world > 1:
+                dist.all_reduce(self.P)
+            try:
+                ops.core(self.P, q, q, self.M, self.scratch)
+            except GramRankDeficientError:
+                self.redraws += 1
+                continue
+            for c in self.chunks:
+                r0, m = self.bounds[c], self._m(c)
+                r1 = r0 + m
+                # V_c = U[R_c]·M (m×2q); the diagonal block by K-SYMUPD, the rest by one GEMM
+                ops.gemm(m, 2 * q, 2 * q, self.U[r0:], n, False, self.M, 2 * q, True, self.Vc, m)
+                ops.symupd(m, 2 * q, self.Vc, m, self.U[r0:], n, self.X[c], m)
+                if r1 < n:
+                    ops.gemm(m, n - r1, 2 * q, self.Vc, m, False, self.U[r1:], n, False, self.X[c][m * m:], m,
+                             1.0, 1.0)
+            return
+        raise GramRankDeficientError("sketch rejection limit exceeded")
+
+    def gather_x(self) -> torch.Tensor:
+        """Full X (n×n column-major, flat) on every rank (tests / export / residual)."""
+        n = self.n
+        full = torch.zeros(n * n, dtype=torch.float64, device=self.X[self.chunks[0]].device)
+        fv = full.view(n, n)  # fv[j, i] = X(i, j)
+        for c in self.chunks:
+            r0, m = self.bounds[c], self._m(c)
+            xv = self.X[c].view(n - r0, m)  # xv[j', i'] = X(r0 + i', r0 + j')
+            fv[r0:, r0:r0 + m].copy_(xv)          # X(rows, cols ≥ r0)
+            fv[r0:r0 + m, r0:].copy_(xv.t())      # mirror: X(cols, rows)
+        if self.world > 1:  # every entry is written by exactly one rank (its chunk's owner)
+            dist.all_reduce(full)
+        return full
+
+    def residual(self) -> float:
+        """‖I − X·A‖_F (= ‖I − A·X‖_F) over the owned chunks' rows of the gathered X."""
+        n = self.n
+        full = self.gather_x()
+        part = 0.0
+        for c in self.chunks:
+            r0, m = self.bounds[c], self._m(c)
+            part += self.ops.residual_rows_sq(self.prob, m, r0, full[r0:], n)
+        t = torch.tensor([part], dtype=torch.float64, device=full.device)
         if self.world > 1:
             dist.all_reduce(t)
         return float(t.item()) ** 0.5

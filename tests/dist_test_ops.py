@@ -93,3 +93,9 @@ class NumpyPanelOps:
         else:
             t = _view(T, q, n, q)
         d.numpy()[:] += 2.0 * (t * b).sum(axis=0) - (b * b).sum(axis=0)
+
+    def symupd(self, m, k, V, ldv, U, ldu, X, ldx):
+        """X (m×m) += V·Uᵀ on the upper triangle, mirrored (the K-SYMUPD contract)."""
+        x = _view(X, m, m, ldx)
+        full = x + _view(V, m, k, ldv) @ _view(U, m, k, ldu).T
+        x[...] = np.triu(full) + np.triu(full, 1).T

@@ -152,3 +152,65 @@ def test_row_sharded_adarbfgs_matches_oracle(world, n, q, rule, use_l0):
     assert res == pytest.approx(np.linalg.norm(np.eye(n) - a @ lf @ lf.T), rel=1e-9)
     if d is not None:  # the carried Eq. 8.2 diagonal equals the exact diag(LᵀAL)
         assert np.allclose(d, np.einsum("ij,ij->j", lf, a @ lf), rtol=1e-10, atol=0)
+
+
+def _sym_worker(rank, world, port, n, q, iters, seed, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+
+        sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+        from dist_test_ops import NumpyPanelOps
+        from paper_1602_01768_b200.dist import SymmetricShardedRBFGS
+
+        a = _problem(n)
+
+        def rows(r0, r1):
+            return torch.from_numpy(np.asfortranarray(a[r0:r1, :]).reshape(-1, order="F").copy())
+
+        solver = SymmetricShardedRBFGS(NumpyPanelOps(a), n, q, rows, seed=seed)
+        for _ in range(iters):
+            solver.step()
+        x = solver.gather_x().numpy().reshape((n, n), order="F")
+        res = solver.residual()
+        if rank == 0:
+            out_q.put((x, res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n,q", [(1, 24, 4), (2, 37, 3), (3, 50, 5)])
+def test_symmetric_sharded_matches_oracle(world, n, q):
+    iters, seed = 12, 5
+    ctx = mp.get_context("spawn")
+    out_q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sym_worker, args=(r, world, port, n, q, iters, seed, out_q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    x, res = out_q.get(timeout=180)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    a = _problem(n)
+    ref = _oracle_run(a, q, iters, seed)
+    assert np.linalg.norm(x - ref) / np.linalg.norm(ref) <= 1e-9
+    assert np.array_equal(x, x.T)
+    assert res == pytest.approx(np.linalg.norm(np.eye(n) - a @ x), rel=1e-9)
+
+
+def test_chunk_balance():
+    from paper_1602_01768_b200.dist import chunk_bounds
+
+    n, P = 16384, 8
+    b = chunk_bounds(n, P)
+    work = []
+    for p in range(P):
+        w = 0
+        for c in (p, 2 * P - 1 - p):
+            m = b[c + 1] - b[c]
+            w += m * (n - b[c])  # trapezoid area
+        work.append(w)
+    assert max(work) / min(work) < 1.001

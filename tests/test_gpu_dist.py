@@ -105,3 +105,28 @@ def test_row_sharded_ada_world1(env, rule):
     if rule == "cols":
         d = sh.d.cpu().numpy()
         assert np.allclose(d, np.einsum("ij,ij->j", lf, a @ lf), rtol=1e-10, atol=0)
+
+
+def test_symmetric_sharded_world1_matches_solver(env):
+    si, torch, ctx, ops = env
+    from paper_1602_01768_b200 import generators as G
+    from paper_1602_01768_b200.dist import SymmetricShardedRBFGS
+
+    n, q, iters, seed = 600, 24, 12, 3  # odd chunk offsets exercise the unaligned (non-TMA) operands
+    a = G.config1_dense(n, seed=4)
+    prob = si.ProblemMatrix(a, si.Symmetry.spd, context=ctx)
+    at = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+    def rows(r0, r1):
+        return at[:, r0:r1].contiguous().reshape(-1)
+
+    sh = SymmetricShardedRBFGS(ops, n, q, rows, seed=seed, prob=prob)
+    for _ in range(iters):
+        sh.step()
+    x_sh = sh.gather_x().cpu().numpy().reshape((n, n), order="F")
+    sol = si.Solver(prob, si.Method.rbfgs, si.SketchRule.gaussian_device(q), seed=seed)
+    sol.step(iters)
+    x_so = sol.iterate()
+    assert np.linalg.norm(x_sh - x_so) / np.linalg.norm(x_so) <= 1e-9
+    assert np.array_equal(x_sh, x_sh.T)
+    assert sh.residual() == pytest.approx(sol.residual(), rel=1e-9)

@@ -343,3 +343,25 @@ def test_adarbfgs_large_q_run_parity(si):
     res = si.run_adarbfgs(si.AdaConfig(si.ProblemMatrix(a, si.Symmetry.spd), si.SketchRule.adaptive_cols_uniform(q),
                                        tol=0.0, max_iters=12, seed=2, track=si.TrackOptions(residual_every_k=4)))
     assert rel(res.state.l, ref.x) <= ITER_TOL
+
+
+@pytest.mark.parametrize("rule", ["cols", "uniform", "gauss"])
+def test_adarbfgs_step_with_caller_rng_matches_driver(si, rule):
+    """adarbfgs_step (adarbfgs.cpp:49-75) advanced k times from one RngStream(seed)
+    draws the same sketches as run_adarbfgs with that seed (same RNG consumption)."""
+    rng0 = O.RngStream(31)
+    n, q, k = 60, 6, 12
+    a = random_spd(n, rng0)
+    srule = {"cols": si.SketchRule.adaptive_cols(n, q), "uniform": si.SketchRule.adaptive_cols_uniform(q),
+             "gauss": si.SketchRule.adaptive_gauss(q)}[rule]
+    orule = {"cols": O.ADA_COLS, "uniform": O.ADA_COLS_UNIFORM, "gauss": O.ADA_GAUSS}[rule]
+    prob = si.ProblemMatrix(a, si.Symmetry.spd)
+    rng = si.RngStream(7)
+    st = si.FactoredState(np.eye(n))
+    for _ in range(k):
+        st = si.adarbfgs_step(st, prob, srule, rng)
+    assert st.k == k
+    ref = O.run_adarbfgs(a, q, rule=orule, tol=0.0, max_iters=k, every_k=k, seed=7)
+    assert rel(st.l, ref.x) <= ITER_TOL
+    with pytest.raises(si.ConfigError):
+        si.adarbfgs_step(st, prob, si.SketchRule.gaussian(q), rng)
