@@ -124,7 +124,7 @@ static int grid_for(int64_t work, int threads, int max_blocks = 148 * 16) {
 }
 
 // --------------------------------------------------------------- GEMM ------
-enum TileCfg { T128x128 = 0, T128x64 = 1, T128x32 = 2, T128x128W16 = 3, T64x128 = 4, T128x128K32 = 5, T128x128W8K32 = 6 };
+enum TileCfg { T128x128 = 0, T128x64 = 1, T128x32 = 2, T128x128W16 = 3, T64x128 = 4, T128x128K32 = 5, T128x128W8K32 = 6, T128x128W16S6 = 7 };
 
 // development switches: SI_WARPS16=1 selects 16 consumer warps for 128×128
 // tiles; SI_NO_TMA=1 forces the cp.async mainloop.
@@ -236,6 +236,9 @@ static void launch_gemm_tile(Context& c, TileCfg t, const GemmArgs& a, dim3 grid
             case T128x128W8K32:
                 if constexpr (EPI == EPI_SYMUPD) launch_tma_cfg<128, 128, 32, 4, 2, 3, AK, BKM, EPI>(c, a, grid, name);
                 break;
+            case T128x128W16S6:
+                if constexpr (EPI == EPI_SYMUPD) launch_tma_cfg<128, 128, 16, 4, 4, 6, AK, BKM, EPI>(c, a, grid, name);
+                break;
             case T64x128: launch_tma_cfg<64, 128, 16, 2, 4, 6, AK, BKM, EPI>(c, a, grid, name); break;
         }
         return;
@@ -246,7 +249,8 @@ static void launch_gemm_tile(Context& c, TileCfg t, const GemmArgs& a, dim3 grid
         case T128x32: launch_gemm_cfg<128, 32, 16, 8, 1, 4, AK, BKM, VEC, EPI>(c, a, grid, name); break;
         case T128x128W16:
         case T128x128K32:
-        case T128x128W8K32: launch_gemm_cfg<128, 128, 16, 4, 4, 4, AK, BKM, VEC, EPI>(c, a, grid, name); break;
+        case T128x128W8K32:
+        case T128x128W16S6: launch_gemm_cfg<128, 128, 16, 4, 4, 4, AK, BKM, VEC, EPI>(c, a, grid, name); break;
         case T64x128: launch_gemm_cfg<64, 128, 16, 2, 4, 4, AK, BKM, VEC, EPI>(c, a, grid, name); break;
     }
 }
@@ -409,6 +413,7 @@ static void symupd(Context& c, int64_t n, int64_t k, const double* V, int64_t ld
         if (v == "128x64") return T128x64;
         if (v == "k32") return T128x128K32;
         if (v == "w8k32") return T128x128W8K32;
+        if (v == "s6") return T128x128W16S6;
         if (v == "w8") return T128x128;
         return T128x128W16;
     }();

@@ -83,13 +83,17 @@ struct TileOps {
         const int64_t full = tn / R_SYM, rest = tn % R_SYM;  // complete chunks, columns of the last one
         return R_SYM * full * (full + 1) / 2 + rest * (full + 1);
     }
-    __device__ __forceinline__ static void sym_tile(int64_t w, int64_t& tile_m, int64_t& tile_n) {
-        int64_t c = (int64_t)((sqrt(8.0 * (double)w / R_SYM + 1.0) - 1.0) * 0.5);
-        while (c > 0 && R_SYM * c * (c + 1) / 2 > w) --c;
-        while (R_SYM * (c + 1) * (c + 2) / 2 <= w) ++c;
-        const int64_t rem = w - R_SYM * c * (c + 1) / 2;
-        tile_n = c * R_SYM + rem / (c + 1);
-        tile_m = rem % (c + 1);
+    // 32-bit integer arithmetic and an fp32 square-root estimate (exact after the ±1
+    // integer correction): the per-tile decode runs on every work item of a
+    // persistent CTA, where FP64 sqrt and 64-bit divisions were measurable
+    __device__ __forceinline__ static void sym_tile(int64_t w64, int64_t& tile_m, int64_t& tile_n) {
+        const uint32_t w = (uint32_t)w64;
+        uint32_t c = (uint32_t)((sqrtf(8.0f * (float)w / (float)R_SYM + 1.0f) - 1.0f) * 0.5f);
+        while (c > 0 && (uint32_t)R_SYM * c * (c + 1) / 2 > w) --c;
+        while ((uint32_t)R_SYM * (c + 1) * (c + 2) / 2 <= w) ++c;
+        const uint32_t rem = w - (uint32_t)R_SYM * c * (c + 1) / 2;
+        tile_n = (int64_t)(c * R_SYM + rem / (c + 1));
+        tile_m = (int64_t)(rem % (c + 1));
     }
     __device__ __forceinline__ static Work decode(int64_t w, const GemmArgs& p) {
         Work r;
@@ -97,10 +101,11 @@ struct TileOps {
             sym_tile(w, r.tile_m, r.tile_n);
             r.split = 0;
         } else {
-            const int64_t tm = (p.M + BM - 1) / BM, tn = (p.N + BN - 1) / BN;
-            r.tile_m = w % tm;
-            r.tile_n = (w / tm) % tn;
-            r.split = w / (tm * tn);
+            const uint32_t tm = (uint32_t)((p.M + BM - 1) / BM), tn = (uint32_t)((p.N + BN - 1) / BN);
+            const uint32_t w32 = (uint32_t)w, q1 = w32 / tm;
+            r.tile_m = w32 - q1 * tm;
+            r.tile_n = q1 % tn;
+            r.split = q1 / tn;
         }
         return r;
     }
