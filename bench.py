@@ -185,20 +185,25 @@ def dist_env():
     return rank, world, local
 
 
-def cpu_port_steps_per_s(cfg, steps: int):
-    """Oracle (reference algorithm, OpenBLAS on all host threads) bfgs_step rate."""
+def cpu_port_steps_per_s(cfg, steps: int, threads: int = 0):
+    """Oracle (reference algorithm) run_inverter-iteration rate on `threads` host
+    threads (0 = all: OpenBLAS and the elementwise passes)."""
     from oracle import oracle as O
 
     n, q = cfg["n"], cfg["q"]
     a = make_dense(cfg)
-    rng = O.RngStream(0)
-    x = np.asfortranarray(np.eye(n))
-    s = rng.gaussian_matrix(n, q)
-    x = O.bfgs_step(x, a, s)  # warm
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        x = _reference_iteration(O, rng, x, a, n, q)
-    dt = time.perf_counter() - t0
+    O.set_threads(threads)
+    try:
+        rng = O.RngStream(0)
+        x = np.asfortranarray(np.eye(n))
+        s = rng.gaussian_matrix(n, q)
+        x = O.bfgs_step(x, a, s)  # warm
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            x = _reference_iteration(O, rng, x, a, n, q)
+        dt = time.perf_counter() - t0
+    finally:
+        O.set_threads(0)
     return steps / dt, dt
 
 
@@ -594,10 +599,14 @@ def run_ours(args, cfg):
     if rank == 0 and world == 1 and not args.no_cpu:
         steps_cpu = 3 if n >= 8192 else 20
         v, dt = cpu_port_steps_per_s(cfg, steps_cpu)
+        v1, dt1 = cpu_port_steps_per_s(cfg, 1, threads=1)
         cpu = {"value": v, "unit": "iter/s", "cores": os.cpu_count(), "kind": "port",
                "sample": f"{steps_cpu} run_inverter iterations (draw S, bfgs_step, symmetrize; simi.cpp:287-357) "
                          f"of the same workload (n={n}, q={q}) in {dt:.1f} s: oracle restatement with OpenBLAS "
-                         "dgemm and elementwise passes on all host threads"}
+                         "dgemm and elementwise passes on all host threads",
+               "single_thread": {"value": v1, "unit": "iter/s", "cores": 1,
+                                 "sample": f"1 iteration in {dt1:.1f} s with OpenBLAS and the elementwise passes "
+                                           "on one thread (the reference's Eigen is single-threaded)"}}
 
     if rank == 0:
         line = {

@@ -73,6 +73,7 @@ def _load():
     lib.or_run_adarbfgs.argtypes = [
         _i64, _pd, C.c_int, _i64, _d, _i64, _i64, C.c_uint64, C.c_int, _pd, _pd,
         C.POINTER(C.c_int), _pi64, _pi64, _pd, _pd, _pd, _i64, _pi64, _pi64, _i64]
+    lib.or_set_threads.argtypes = [C.c_int]
     lib.or_psb_step.argtypes = [_i64, _i64, _pd, _pd, _pd, _pd]
     lib.or_aip_step.argtypes = [_i64, _i64, _pd, _pd, _pd, _pd]
     lib.or_dfp_step.argtypes = [_i64, _i64, _pd, _pd, _pd, _pd, _pd, _pd]
@@ -243,6 +244,11 @@ def flops_bfgs(n, q) -> float:
 
 def flops_adarbfgs(n, q) -> float:
     return float(lib().or_flops_adarbfgs(n, q))
+
+
+def set_threads(n: int) -> None:
+    """Host threads for OpenBLAS and the elementwise passes (0 = all)."""
+    lib().or_set_threads(int(n))
 
 
 def have_blas() -> bool:

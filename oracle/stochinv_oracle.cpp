@@ -40,11 +40,15 @@
 
 namespace oracle {
 
-// Minimal parallel-for over [0, count) on all host threads (this image has no
+// Host threads for the elementwise passes and OpenBLAS (or_set_threads; 0 = all).
+static int g_threads = 0;
+
+// Minimal parallel-for over [0, count) on the host threads (this image has no
 // OpenMP runtime); used for the O(n²) elementwise passes, GEMMs use OpenBLAS.
 template <class F>
 void parallel_for(long count, F&& f) {
-    const long nt = std::max(1L, std::min<long>(count, long(std::thread::hardware_concurrency())));
+    const long hw = g_threads > 0 ? long(g_threads) : long(std::thread::hardware_concurrency());
+    const long nt = std::max(1L, std::min<long>(count, hw));
     if (nt <= 1) {
         for (long i = 0; i < count; ++i) f(i);
         return;
@@ -118,6 +122,8 @@ Mat operator*(double s, const Mat& a) {
 using cblas_dgemm_t = void (*)(int, int, int, int64_t, int64_t, int64_t, double, const double*, int64_t,
                                const double*, int64_t, double, double*, int64_t);
 static cblas_dgemm_t g_dgemm = nullptr;
+using blas_threads_t = void (*)(int);
+static blas_threads_t g_blas_threads = nullptr;
 static bool g_blas_probed = false;
 
 static void probe_blas() {
@@ -141,6 +147,7 @@ static void probe_blas() {
         auto f = reinterpret_cast<cblas_dgemm_t>(dlsym(h, "scipy_cblas_dgemm64_"));
         if (f) {
             g_dgemm = f;
+            g_blas_threads = reinterpret_cast<blas_threads_t>(dlsym(h, "scipy_openblas_set_num_threads64_"));
             return;
         }
     }
@@ -746,6 +753,12 @@ __attribute__((constructor)) static void oracle_tune_malloc() {
 extern "C" {
 
 const char* or_last_error() { return g_err.c_str(); }
+// host threads for the CPU baseline: n > 0 limits OpenBLAS and the elementwise passes, 0 = all
+void or_set_threads(int n) {
+    probe_blas();
+    g_threads = n;
+    if (g_blas_threads) g_blas_threads(n > 0 ? n : int(std::thread::hardware_concurrency()));
+}
 int or_have_blas() {
     probe_blas();
     return g_dgemm != nullptr;
