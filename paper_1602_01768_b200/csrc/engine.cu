@@ -403,10 +403,11 @@ static void symupd(Context& c, int64_t n, int64_t k, const double* V, int64_t ld
     }();
     a.dbg = dbg;
     const int vec = pick_vec(a);
-    // Tile choice (SI_SYMUPD_TILE): default one 16-warp CTA per SM on 128×128
-    // tiles; "w8" one 8-warp CTA on 128×128; "128x64" two 8-warp CTAs per SM so
-    // one CTA's store epilogue overlaps the other's mainloop (measured 2.5%
-    // slower at config 3: 2.31 vs 2.25 ms).
+    // Tile choice (SI_SYMUPD_TILE): default one 8-warp CTA per SM on 128×128 tiles
+    // (32×64 warp tiles: a clock64 trace of CTA 0 shows ~92% of the DMMA rate per
+    // k-stage against ~88% for "w16", one 16-warp CTA with 32×32 warp tiles);
+    // "128x64" two 8-warp CTAs per SM (2.31 vs 2.25 ms at config 3); "k32",
+    // "w8k32", "s6": BK = 32 / 6 stages (no difference measured).
     static const TileCfg cfg = [] {
         const char* e = std::getenv("SI_SYMUPD_TILE");
         const std::string v = e ? e : "";
@@ -414,8 +415,8 @@ static void symupd(Context& c, int64_t n, int64_t k, const double* V, int64_t ld
         if (v == "k32") return T128x128K32;
         if (v == "w8k32") return T128x128W8K32;
         if (v == "s6") return T128x128W16S6;
-        if (v == "w8") return T128x128;
-        return T128x128W16;
+        if (v == "w16") return T128x128W16;
+        return T128x128;
     }();
     const int64_t bn = cfg == T128x64 ? 64 : 128, r = 128 / bn;
     const int64_t tn = (n + bn - 1) / bn, full = tn / r, rest = tn % r;
