@@ -462,6 +462,26 @@ def run_extra_config(args, cfg):
         "kernel_share_of_step": {k: round(v[1] / ksum, 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])},
         "gpu_launches": int(launches), "clocks": clk.summary(),
     }
+    # HBM-bound stages: algorithmic bytes per launch over the launch's CUDA-event time
+    hbm = {}
+    peak = HBM_PEAK_GBS or 6546.6
+
+    def add_hbm(name, nbytes, what):
+        if name in prof and prof[name][0] > 0:
+            ms_l = prof[name][1] / prof[name][0]
+            gbs = nbytes / (ms_l * 1e-3) / 1e9
+            hbm[name] = {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                         "algorithmic_bytes_per_launch": nbytes, "bytes": what, "ms_per_launch": ms_l}
+
+    if prob.sparse:
+        k = q
+        add_hbm("spmm_csr", 12.0 * prob.nnz + 8.0 * (n + 1) + 2.0 * 8.0 * n * k,
+                "CSR (12·nnz + 8(n+1)) + the row-major n×q panel read once + Y written once")
+        add_hbm("transpose", 2.0 * 8.0 * n * k, "n×q panel read + written (column- to row-major)")
+    add_hbm("sketch_philox", 8.0 * n * q, "n×q Gaussian sketch written")
+    add_hbm("gather_columns", 2.0 * 8.0 * n * q, "n×q columns of L read + written")
+    if hbm:
+        line["roofline_hbm"] = hbm
     print(json.dumps(line), flush=True)
 
 
@@ -548,6 +568,14 @@ def run_ours(args, cfg):
                      "traffic_source": "profiles/r01_traffic.json (ncu --set full, bytes per launch)",
                      "kernel_share_of_step": shares})
     secondary = roof("gemm_symupd") if "gemm_symupd" in prof and dom_name != "gemm_symupd" else None
+    hbm_lines = {}
+    if "sketch_philox" in prof and prof["sketch_philox"][0] > 0:
+        ms_l = prof["sketch_philox"][1] / prof["sketch_philox"][0]
+        gbs = 8.0 * n * q / (ms_l * 1e-3) / 1e9
+        pk = HBM_PEAK_GBS or 6546.6
+        hbm_lines["sketch_philox"] = {"bound": "hbm", "achieved": gbs, "peak": pk, "unit": "GB/s", "frac": gbs / pk,
+                                      "algorithmic_bytes_per_launch": 8.0 * n * q,
+                                      "bytes": "n×q Gaussian sketch written (Philox4x32-10 + Box-Muller, FP64)"}
 
     # ---- e2e through the public driver with host buffers ----
     e2e = None
@@ -621,6 +649,7 @@ def run_ours(args, cfg):
                        "achieved_tflops_per_step": alg_flops / (per_step_ms * 1e-3) / 1e12},
             "roofline": roofline,
             "roofline_secondary": secondary,
+            "roofline_hbm": hbm_lines or None,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
