@@ -244,6 +244,11 @@ int64_t si_solver_redraws(si_solver* s);
  * B is K×N (b_kmajor: B(k,n) = B[k + n*ldb], else B[n + k*ldb]); FP64 DMMA. */
 int si_gemm_device(si_context* ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, int a_kmajor,
                    const double* B, int64_t ldb, int b_kmajor, double* C, int64_t ldc, double alpha, double beta);
+/* Y (m×k, ld ldy) = A_rows·P for a CSR row panel on the device (m rows, int64 rowptr relative to
+ * the panel, int32 global column indices < n) and a dense n×k operand P (ld ldp): the sharded
+ * drivers' A·S for sparse A (configs 4/5). */
+int si_spmm_csr_device(si_context* ctx, int64_t m, int64_t n, const int64_t* rowptr, const int32_t* colind,
+                       const double* val, const double* P, int64_t ldp, int64_t k, double* Y, int64_t ldy);
 /* X (m×m symmetric, ld ldx) += V·Uᵀ (V, U m×k) on the upper tiles, written mirrored (exactly
  * symmetric): the K-SYMUPD kernel, used on the diagonal blocks of the symmetric sharded driver. */
 int si_symupd_device(si_context* ctx, int64_t m, int64_t k, const double* V, int64_t ldv, const double* U,

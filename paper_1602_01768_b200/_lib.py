@@ -94,6 +94,7 @@ _SIGS = {
     "si_solver_residual": (ci, [vp, pd]),
     "si_solver_redraws": (i64, [vp]),
     "si_gemm_device": (ci, [vp, i64, i64, i64, vp, i64, ci, vp, i64, ci, vp, i64, d, d]),
+    "si_spmm_csr_device": (ci, [vp, i64, i64, vp, vp, vp, vp, i64, i64, vp, i64]),
     "si_symupd_device": (ci, [vp, i64, i64, vp, i64, vp, i64, vp, i64]),
     "si_sketch_gaussian_device": (ci, [vp, vp, i64, i64, i64, u64, u64]),
     "si_rbfgs_core_device": (ci, [vp, vp, i64, i64, vp, vp]),

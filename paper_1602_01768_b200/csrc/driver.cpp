@@ -1336,6 +1336,14 @@ int si_gemm_device(si_context* ctx, int64_t M, int64_t N, int64_t K, const doubl
     });
 }
 
+int si_spmm_csr_device(si_context* ctx, int64_t m, int64_t n, const int64_t* rowptr, const int32_t* colind,
+                       const double* val, const double* P, int64_t ldp, int64_t k, double* Y, int64_t ldy) {
+    return guard([&] {
+        require(m >= 0 && n >= 1 && k >= 0 && ldp >= n && ldy >= m, "spmm_csr: bad shape");
+        if (m > 0 && k > 0) si::spmm_csr_rows(*ctx->c, m, n, rowptr, colind, val, P, ldp, k, Y, ldy);
+    });
+}
+
 int si_symupd_device(si_context* ctx, int64_t m, int64_t k, const double* V, int64_t ldv, const double* U,
                      int64_t ldu, double* X, int64_t ldx) {
     return guard([&] {

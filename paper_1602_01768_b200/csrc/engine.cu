@@ -555,6 +555,23 @@ void apply_a(Context& c, Problem& a, const double* P, int64_t ldp, int64_t k, do
     check_launch("spmm_csr");
 }
 
+// Y (m×k, ld ldy) = A_rows·P for a CSR row panel (m rows, global column indices < n)
+// and a dense n×k operand P: the row-major copy + warp-per-row kernel of apply_a.
+void spmm_csr_rows(Context& c, int64_t m, int64_t n, const int64_t* rowptr, const int32_t* colind, const double* val,
+                   const double* P, int64_t ldp, int64_t k, double* Y, int64_t ldy) {
+    double* Pr = c.ensure_ws(size_t(n) * size_t(k));
+    {
+        LaunchScope ls(c, "transpose");
+        dim3 grid(unsigned((n + 31) / 32), unsigned((k + 31) / 32));
+        transpose_kernel<<<grid, dim3(32, 8), 0, c.stream>>>(P, n, k, ldp, Pr, nullptr);
+        check_launch("transpose");
+    }
+    LaunchScope ls(c, "spmm_csr");
+    spmm_csr_rowmajor_kernel<<<grid_for(m * 32, 256, c.num_sms * 32), 256, 0, c.stream>>>(m, rowptr, colind, val, Pr,
+                                                                                         k, Y, ldy, nullptr);
+    check_launch("spmm_csr");
+}
+
 void set_identity(Context& c, double* X, int64_t n) {
     LaunchScope ls(c, "set_identity");
     set_identity_kernel<<<grid_for(n * n, 256), 256, 0, c.stream>>>(X, n, n);

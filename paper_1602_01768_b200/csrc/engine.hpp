@@ -148,6 +148,8 @@ void gemm(Context& c, int64_t M, int64_t N, int64_t K, const double* A, int64_t 
 void apply_a(Context& c, Problem& a, const double* P, int64_t ldp, int64_t k, double* Y, int64_t ldy,
              const int* skip = nullptr);
 
+void spmm_csr_rows(Context& c, int64_t m, int64_t n, const int64_t* rowptr, const int32_t* colind, const double* val,
+                   const double* P, int64_t ldp, int64_t k, double* Y, int64_t ldy);
 void rbfgs_enqueue_iteration(Context& c, Problem& a, RbfgsWork& w, bool device_sketch, uint64_t seed);
 // the q×q stage: Gram inverse (PD check into status[0]) and the 2q×2q core M
 void rbfgs_core_enqueue(Context& c, const double* P, int64_t ldp, int64_t q, double* Ginv, double* T, double* M,

@@ -85,6 +85,10 @@ class CudaPanelOps:
                                                self._p(T) if T is not None else None,
                                                self._p(idx) if idx is not None else None, self._p(d)))
 
+    def spmm(self, m, n, rowptr, colind, val, P, ldp, k, Y, ldy):
+        _check(self.lib.si_spmm_csr_device(self.ctx.handle, m, n, self._p(rowptr), self._p(colind), self._p(val),
+                                           self._p(P), ldp, k, self._p(Y), ldy))
+
     def symupd(self, m, k, V, ldv, U, ldu, X, ldx):
         _check(self.lib.si_symupd_device(self.ctx.handle, m, k, self._p(V), ldv, self._p(U), ldu, self._p(X), ldx))
 
@@ -92,6 +96,44 @@ class CudaPanelOps:
         out = C.c_double()
         _check(self.lib.si_residual_rows_device(self.ctx.handle, prob.handle, m, r0, self._p(X), ldx, C.byref(out)))
         return out.value
+
+
+@dataclass
+class CsrRows:
+    """Rows [r0, r1) of a sparse A as a device CSR panel: rowptr relative to the
+    panel (int64, m+1), global column indices (int32), values (float64)."""
+    rowptr: torch.Tensor
+    colind: torch.Tensor
+    val: torch.Tensor
+    r0: int
+    m: int
+
+    @staticmethod
+    def from_host(rowptr, colind, val, r0: int, r1: int, device) -> "CsrRows":
+        b, e = int(rowptr[r0]), int(rowptr[r1])
+        rp = torch.from_numpy(np.asarray(rowptr[r0:r1 + 1], dtype=np.int64) - b).to(device)
+        ci = torch.from_numpy(np.ascontiguousarray(colind[b:e], dtype=np.int32)).to(device)
+        va = torch.from_numpy(np.ascontiguousarray(val[b:e], dtype=np.float64)).to(device)
+        return CsrRows(rp, ci, va, r0, r1 - r0)
+
+    def diagonal(self) -> torch.Tensor:
+        """A[r0 + i, r0 + i] for the panel's rows (length m)."""
+        counts = (self.rowptr[1:] - self.rowptr[:-1]).to(torch.int64)
+        rows = torch.repeat_interleave(torch.arange(self.m, device=self.val.device), counts)
+        d = torch.zeros(self.m, dtype=torch.float64, device=self.val.device)
+        hit = self.colind.to(torch.int64) == rows + self.r0
+        d.index_add_(0, rows[hit], self.val[hit])
+        return d
+
+
+def apply_rows(ops, A, n: int, P, ldp: int, k: int, out, ldo: int):
+    """out (m×k, ld ldo) = A_rows·P for a dense column-major m×n panel (flat tensor, ld m)
+    or a CsrRows panel; P is n×k (ld ldp)."""
+    if isinstance(A, CsrRows):
+        ops.spmm(A.m, n, A.rowptr, A.colind, A.val, P, ldp, k, out, ldo)
+    else:
+        m = A.numel() // n
+        ops.gemm(m, k, n, A, m, False, P, ldp, True, out, ldo)
 
 
 @dataclass
@@ -167,7 +209,7 @@ class RowShardedRBFGS(_RowPanels):
         self.prob = prob
         self.max_redraws = max_redraws
         self.redraws = 0
-        dev = device if device is not None else a_rows.device
+        dev = device if device is not None else (a_rows.val.device if isinstance(a_rows, CsrRows) else a_rows.device)
         m, mm = self.lay.m, self.lay.m_max
         f = dict(dtype=torch.float64, device=dev)
         self.A = a_rows
@@ -206,7 +248,7 @@ class RowShardedRBFGS(_RowPanels):
             draw = self.draw
             self.draw += 1
             ops.sketch(self.S, n, q, n, self.seed, draw)
-            ops.gemm(m, q, n, self.A, m, False, self.S, n, True, self.Yp, m)           # Y_p = A_p·S
+            apply_rows(ops, self.A, n, self.S, n, q, self.Yp, m)                         # Y_p = A_p·S
             self._all_gather_rows(self.Yp, self.Y, q)                                   # Y
             Sv = self.S.view(q, n)
             Upv = self.Up.view(2 * q, m)
@@ -280,7 +322,7 @@ class RowShardedAdaRBFGS(_RowPanels):
         self.draw = 0
         self.redraws = 0
         self.k = 0
-        dev = a_rows.device
+        dev = a_rows.val.device if isinstance(a_rows, CsrRows) else a_rows.device
         m = self.lay.m
         f = dict(dtype=torch.float64, device=dev)
         self.A = a_rows
@@ -307,7 +349,10 @@ class RowShardedAdaRBFGS(_RowPanels):
             Lv[self.lay.r0 + i, i] = 1.0
             if self.d is not None:  # diag(LᵀAL) at L = I is diag(A): the diagonal entries of the local rows
                 self.d.zero_()
-                self.d[self.lay.r0 + i] = self.A.view(n, m)[self.lay.r0 + i, i]
+                if isinstance(self.A, CsrRows):
+                    self.d[self.lay.r0 + i] = self.A.diagonal()
+                else:
+                    self.d[self.lay.r0 + i] = self.A.view(n, m)[self.lay.r0 + i, i]
                 if self.world > 1:
                     dist.all_reduce(self.d)
         else:
@@ -328,7 +373,7 @@ class RowShardedAdaRBFGS(_RowPanels):
         n, m = lay.n, lay.m
         full = self.gather_l()
         AL = torch.empty(m * n, dtype=torch.float64, device=self.L.device)
-        self.ops.gemm(m, n, n, self.A, m, False, full, n, True, AL, m)  # (A·L)[R_p, :] = A_p·L
+        apply_rows(self.ops, self.A, n, full, n, n, AL, m)  # (A·L)[R_p, :] = A_p·L
         part = (AL.view(n, m) * self.L.view(n, m)).sum(dim=1)
         if self.world > 1:
             dist.all_reduce(part)
@@ -362,7 +407,7 @@ class RowShardedAdaRBFGS(_RowPanels):
                 self.idx[:q].copy_(torch.tensor(cols, dtype=torch.int64))
                 ops.gather_columns(self.L, m, m, self.idx, q, self.Sp)                        # S_p = L_p[:, C]
             self._all_gather_rows(self.Sp[: m * q], self.S[: n * q], q)                       # S
-            ops.gemm(m, q, n, self.A, m, False, self.S, n, True, self.ASp, m)                 # (AS)_p = A_p·S
+            apply_rows(ops, self.A, n, self.S, n, q, self.ASp, m)                                # (AS)_p = A_p·S
             G, Z = self.GZ[: q * q], self.GZ[q * q: q * q + q * n]
             ops.gemm(q, q, m, self.Sp, m, True, self.ASp, m, True, G, q)                       # S_pᵀ(AS)_p
             ops.gemm(q, n, m, self.ASp, m, True, self.L, m, True, Z, q)                        # (AS)_pᵀ L_p
@@ -425,7 +470,8 @@ class SymmetricShardedRBFGS:
 
     def __init__(self, ops, n: int, q: int, a_rows_of_chunk, *, seed: int = 0, prob: ProblemMatrix | None = None,
                  max_redraws: int = 100, device=None):
-        """a_rows_of_chunk(r0, r1) -> A[r0:r1, :] as a flat column-major (r1−r0)×n tensor."""
+        """a_rows_of_chunk(r0, r1) -> A[r0:r1, :] as a flat column-major (r1−r0)×n tensor or a
+        CsrRows panel (sparse A, configs 4/5)."""
         self.ops, self.n, self.q, self.seed, self.prob, self.max_redraws = ops, n, q, seed, prob, max_redraws
         self.world = dist.get_world_size() if dist.is_initialized() else 1
         self.rank = dist.get_rank() if dist.is_initialized() else 0
@@ -435,7 +481,7 @@ class SymmetricShardedRBFGS:
         self.draw = 0
         self.redraws = 0
         A0 = a_rows_of_chunk(self.bounds[self.chunks[0]], self.bounds[self.chunks[0] + 1])
-        dev = device if device is not None else A0.device
+        dev = device if device is not None else (A0.val.device if isinstance(A0, CsrRows) else A0.device)
         f = dict(dtype=torch.float64, device=dev)
         self.A, self.X = {}, {}
         for c in self.chunks:
@@ -497,8 +543,8 @@ class SymmetricShardedRBFGS:
             self.draw += 1
             # Y rows of the owned chunks, then the full Y
             for c in self.chunks:
-                r0, m = self.bounds[c], self._m(c)
-                ops.gemm(m, q, n, self.A[c], m, False, S, n, True, self.Y[r0:], n)
+                r0 = self.bounds[c]
+                apply_rows(ops, self.A[c], n, S, n, q, self.Y[r0:], n)
             self._all_gather_y()
             # W = X·Y from the upper trapezoids: X_c·Y[r0:] and the strictly-upper part transposed
             W.zero_()

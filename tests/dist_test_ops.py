@@ -99,3 +99,9 @@ class NumpyPanelOps:
         x = _view(X, m, m, ldx)
         full = x + _view(V, m, k, ldv) @ _view(U, m, k, ldu).T
         x[...] = np.triu(full) + np.triu(full, 1).T
+
+    def spmm(self, m, n, rowptr, colind, val, P, ldp, k, Y, ldy):
+        import scipy.sparse as sp
+
+        a = sp.csr_matrix((val.numpy(), colind.numpy().astype(np.int64), rowptr.numpy()), shape=(m, n))
+        _view(Y, m, k, ldy)[...] = a @ _view(P, n, k, ldp)

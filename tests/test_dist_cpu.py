@@ -87,7 +87,30 @@ def test_row_partition():
     assert row_partition(8, 8) == list(range(9))
 
 
-def _ada_worker(rank, world, port, n, q, iters, seed, rule, use_l0, out_q):
+def _rows(a, r0, r1, sparse):
+    if not sparse:
+        return torch.from_numpy(np.asfortranarray(a[r0:r1, :]).reshape(-1, order="F").copy())
+    import scipy.sparse as sp
+
+    from paper_1602_01768_b200.dist import CsrRows
+
+    c = sp.csr_matrix(a)
+    return CsrRows.from_host(c.indptr.astype(np.int64), c.indices.astype(np.int32), c.data, r0, r1, "cpu")
+
+
+def _sparse_problem(n):
+    """A sparse SPD stand-in (banded, like config 5) as a dense array for the oracle."""
+    rng = O.RngStream(11)
+    a = np.zeros((n, n))
+    for i in range(n):
+        for j in range(max(0, i - 3), i):
+            v = 2 * rng.uniform() - 1
+            a[i, j] = a[j, i] = v
+    a[np.arange(n), np.arange(n)] = 1.0 + np.abs(a).sum(axis=1)
+    return a
+
+
+def _ada_worker(rank, world, port, n, q, iters, seed, rule, use_l0, out_q, sparse=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -98,10 +121,10 @@ def _ada_worker(rank, world, port, n, q, iters, seed, rule, use_l0, out_q):
         from dist_test_ops import NumpyPanelOps
         from paper_1602_01768_b200.dist import RowShardedAdaRBFGS, row_partition
 
-        a = _problem(n)
+        a = _sparse_problem(n) if sparse else _problem(n)
         starts = row_partition(n, world)
         r0, r1 = starts[rank], starts[rank + 1]
-        a_rows = torch.from_numpy(np.asfortranarray(a[r0:r1, :]).reshape(-1, order="F").copy())
+        a_rows = _rows(a, r0, r1, sparse)
         l0_rows = None
         if use_l0:
             l0 = _l0(n)
@@ -122,16 +145,17 @@ def _l0(n):
     return np.eye(n) + 0.01 * O.RngStream(77).gaussian_matrix(n, n)
 
 
-@pytest.mark.parametrize("world,n,q,rule,use_l0", [
-    (1, 24, 4, "cols", False), (2, 37, 4, "cols", False), (2, 40, 6, "uniform", False),
-    (2, 33, 3, "gauss", False), (2, 30, 5, "cols", True),
+@pytest.mark.parametrize("world,n,q,rule,use_l0,sparse", [
+    (1, 24, 4, "cols", False, False), (2, 37, 4, "cols", False, False), (2, 40, 6, "uniform", False, False),
+    (2, 33, 3, "gauss", False, False), (2, 30, 5, "cols", True, False), (2, 41, 4, "cols", False, True),
+    (2, 36, 4, "uniform", False, True),
 ])
-def test_row_sharded_adarbfgs_matches_oracle(world, n, q, rule, use_l0):
+def test_row_sharded_adarbfgs_matches_oracle(world, n, q, rule, use_l0, sparse):
     iters, seed = 15, 4
     ctx = mp.get_context("spawn")
     out_q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_ada_worker, args=(r, world, port, n, q, iters, seed, rule, use_l0, out_q))
+    procs = [ctx.Process(target=_ada_worker, args=(r, world, port, n, q, iters, seed, rule, use_l0, out_q, sparse))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -139,7 +163,7 @@ def test_row_sharded_adarbfgs_matches_oracle(world, n, q, rule, use_l0):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    a = _problem(n)
+    a = _sparse_problem(n) if sparse else _problem(n)
     l0 = _l0(n) if use_l0 else None
     if rule == "gauss":  # same Philox-stand-in sketch sequence as the test double
         ref = np.asfortranarray(l0 if l0 is not None else np.eye(n))
@@ -154,7 +178,7 @@ def test_row_sharded_adarbfgs_matches_oracle(world, n, q, rule, use_l0):
         assert np.allclose(d, np.einsum("ij,ij->j", lf, a @ lf), rtol=1e-10, atol=0)
 
 
-def _sym_worker(rank, world, port, n, q, iters, seed, out_q):
+def _sym_worker(rank, world, port, n, q, iters, seed, out_q, sparse=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -165,10 +189,10 @@ def _sym_worker(rank, world, port, n, q, iters, seed, out_q):
         from dist_test_ops import NumpyPanelOps
         from paper_1602_01768_b200.dist import SymmetricShardedRBFGS
 
-        a = _problem(n)
+        a = _sparse_problem(n) if sparse else _problem(n)
 
         def rows(r0, r1):
-            return torch.from_numpy(np.asfortranarray(a[r0:r1, :]).reshape(-1, order="F").copy())
+            return _rows(a, r0, r1, sparse)
 
         solver = SymmetricShardedRBFGS(NumpyPanelOps(a), n, q, rows, seed=seed)
         for _ in range(iters):
@@ -181,20 +205,22 @@ def _sym_worker(rank, world, port, n, q, iters, seed, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n,q", [(1, 24, 4), (2, 37, 3), (3, 50, 5)])
-def test_symmetric_sharded_matches_oracle(world, n, q):
+@pytest.mark.parametrize("world,n,q,sparse", [(1, 24, 4, False), (2, 37, 3, False), (3, 50, 5, False),
+                                             (2, 45, 4, True)])
+def test_symmetric_sharded_matches_oracle(world, n, q, sparse):
     iters, seed = 12, 5
     ctx = mp.get_context("spawn")
     out_q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_sym_worker, args=(r, world, port, n, q, iters, seed, out_q)) for r in range(world)]
+    procs = [ctx.Process(target=_sym_worker, args=(r, world, port, n, q, iters, seed, out_q, sparse))
+             for r in range(world)]
     for p in procs:
         p.start()
     x, res = out_q.get(timeout=180)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    a = _problem(n)
+    a = _sparse_problem(n) if sparse else _problem(n)
     ref = _oracle_run(a, q, iters, seed)
     assert np.linalg.norm(x - ref) / np.linalg.norm(ref) <= 1e-9
     assert np.array_equal(x, x.T)

@@ -130,3 +130,35 @@ def test_symmetric_sharded_world1_matches_solver(env):
     assert np.linalg.norm(x_sh - x_so) / np.linalg.norm(x_so) <= 1e-9
     assert np.array_equal(x_sh, x_sh.T)
     assert sh.residual() == pytest.approx(sol.residual(), rel=1e-9)
+
+
+def test_sharded_drivers_with_csr_panels_world1(env):
+    """Sparse A through the sharded drivers' CSR row panels (si_spmm_csr_device):
+    the symmetric-chunk RBFGS driver against the single-GPU solver on the same CSR
+    problem, and the row-sharded AdaRBFGS driver against the oracle."""
+    si, torch, ctx, ops = env
+    from oracle import oracle as O
+    from paper_1602_01768_b200 import generators as G
+    from paper_1602_01768_b200.dist import CsrRows, RowShardedAdaRBFGS, SymmetricShardedRBFGS
+
+    n, q, iters = 1024, 32, 10
+    rowptr, colind, val = G.config5_csr(n, half_bandwidth=16, seed=1)
+    prob = si.ProblemMatrix(csr=(rowptr, colind, val), n=n, symmetry=si.Symmetry.spd, context=ctx)
+    sh = SymmetricShardedRBFGS(ops, n, q, lambda r0, r1: CsrRows.from_host(rowptr, colind, val, r0, r1, "cuda"),
+                               seed=4)
+    for _ in range(iters):
+        sh.step()
+    x_sh = sh.gather_x().cpu().numpy().reshape((n, n), order="F")
+    sol = si.Solver(prob, si.Method.rbfgs, si.SketchRule.gaussian_device(q), seed=4)
+    sol.step(iters)
+    x_so = sol.iterate()
+    assert np.linalg.norm(x_sh - x_so) / np.linalg.norm(x_so) <= 1e-9
+    assert np.array_equal(x_sh, x_sh.T)
+
+    a = prob.data()
+    ada = RowShardedAdaRBFGS(ops, n, 16, CsrRows.from_host(rowptr, colind, val, 0, n, "cuda"), rule="cols", seed=2)
+    for _ in range(12):
+        ada.step()
+    lf = ada.gather_l().cpu().numpy().reshape((n, n), order="F")
+    ref = O.run_adarbfgs(a, 16, rule=O.ADA_COLS, tol=0.0, max_iters=12, every_k=12, seed=2).x
+    assert np.linalg.norm(lf - ref) / np.linalg.norm(ref) <= 1e-9
