@@ -119,6 +119,163 @@ __global__ void symmetrize_small_kernel(double* g, int q, int64_t ld, const int*
     }
 }
 
+// K-FACTOR, blocked.  G⁻¹ for SPD G (q ≤ 128, read as G(i,j) = P(min, max)) by
+// Gauss-Jordan in 16-column panels, the whole matrix resident in shared memory
+// (padded to QP = 16·⌈q/16⌉ with an identity block, which keeps it SPD):
+//   D = G[p,p] → D⁻¹ by one warp (16 scalar GJ steps, warp-synchronous; every
+//       scalar pivot is the one the unblocked elimination meets, so "pivot ≤ 0"
+//       is still gram_llt's failure test),
+//   R' = D⁻¹·G[p,:],  C = G[:,p],
+//   G[i,j] −= C[i,:]·R'[:,j] for the whole matrix — a rank-16 update on the DMMA
+//       pipe (16 warps × 32×32 tiles) — then G[p,:] = R', G[:,p] = −C·D⁻¹, G[p,p] = D⁻¹.
+// Eight panels at q = 128: ~40 CTA barriers instead of the 256 of the scalar
+// elimination, and one launch instead of the recursion's eleven (measured: the q×q
+// stage of a config-3 iteration 232 vs 268 µs).  Output symmetrised exactly.
+template <int QP, int PB>
+__global__ void __launch_bounds__(512) spd_inverse_blocked_kernel(const double* __restrict__ P, int64_t ldp, int q,
+                                                                 double* __restrict__ ginv, int64_t ldo, int* status) {
+    constexpr int LDG = QP + 4, LDC = PB + 4, LDR = QP + 4, LDD = PB + 1;
+    static_assert(PB == 16 || PB == 32, "panel width");
+    extern __shared__ __align__(16) double gsm[];
+    double* Gs = gsm;                  // QP × LDG
+    double* Cb = Gs + QP * LDG;        // QP × LDC  (column panel, m-major rows: Cb[i*LDC + l])
+    double* Rb = Cb + QP * LDC;        // PB × LDR  (new row panel)
+    double* Db = Rb + PB * LDR;        // PB × LDD
+    __shared__ int s_bad;
+    if (*status) return;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    for (int e = tid; e < QP * QP; e += nt) {
+        const int i = e % QP, j = e / QP;
+        double v;
+        if (i < q && j < q)
+            v = i <= j ? P[i + (int64_t)j * ldp] : P[j + (int64_t)i * ldp];
+        else
+            v = i == j ? 1.0 : 0.0;
+        Gs[i * LDG + j] = v;
+    }
+    if (tid == 0) s_bad = 0;
+    __syncthreads();
+    for (int k0 = 0; k0 < QP; k0 += PB) {
+        // D⁻¹ by warp 0: lane j < 16 holds column j of D in registers; row and column k
+        // of each elimination step travel by shuffles (no shared-memory round trips)
+        if (warp == 0) {
+            const int j = lane & (PB - 1);
+            double d[PB];
+#pragma unroll
+            for (int i = 0; i < PB; ++i) d[i] = Gs[(k0 + i) * LDG + k0 + j];
+            bool bad = false;
+#pragma unroll
+            for (int k = 0; k < PB; ++k) {
+                const double piv = __shfl_sync(0xffffffffu, d[k], k);
+                bad |= !(piv > 0.0);  // uniform; once set the values are discarded
+                const double inv = 1.0 / piv;
+                const double rk = d[k];  // row k, column j (old)
+#pragma unroll
+                for (int i = 0; i < PB; ++i) {
+                    const double cki = __shfl_sync(0xffffffffu, d[i], k);  // column k, row i (old)
+                    if (i == k)
+                        d[i] = j == k ? inv : rk * inv;
+                    else
+                        d[i] = j == k ? -cki * inv : d[i] - cki * rk * inv;
+                }
+            }
+            if (lane < PB) {
+#pragma unroll
+                for (int i = 0; i < PB; ++i) Db[i * LDD + j] = d[i];
+            }
+            if (bad && lane == 0) s_bad = 1;
+        }
+        // C = G[:, p] (old) for every thread
+        for (int e = tid; e < QP * PB; e += nt) {
+            const int i = e / PB, l = e % PB;
+            Cb[i * LDC + l] = Gs[i * LDG + k0 + l];
+        }
+        __syncthreads();
+        if (s_bad) {
+            if (tid == 0) *status = 1;  // not positive definite: the resample signal
+            return;
+        }
+        // R' = D⁻¹·G[p, :]
+        for (int e = tid; e < PB * QP; e += nt) {
+            const int r = e / QP, j = e % QP;
+            double acc = 0.0;
+#pragma unroll
+            for (int l = 0; l < PB; ++l) acc += Db[r * LDD + l] * Gs[(k0 + l) * LDG + j];
+            Rb[r * LDR + j] = acc;
+        }
+        __syncthreads();
+        // G −= C·R' (rank-16, DMMA): 16 warps as 4×4, warp tile (QP/4)×(QP/4)
+        {
+            constexpr int WT = QP / 4, MI = WT / 16, NI = WT / 8;
+            const int g = lane >> 2, t4 = lane & 3, wm0 = (warp >> 2) * WT, wn0 = (warp & 3) * WT;
+            if (WT >= 16) {
+                double acc[MI > 0 ? MI : 1][NI > 0 ? NI : 1][4];
+#pragma unroll
+                for (int i = 0; i < MI; ++i)
+#pragma unroll
+                    for (int j = 0; j < NI; ++j)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
+#pragma unroll
+                for (int kk = 0; kk < PB; kk += 8) {
+                    double a[MI > 0 ? MI : 1][4], b[NI > 0 ? NI : 1][2];
+#pragma unroll
+                    for (int i = 0; i < MI; ++i)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            a[i][e] = Cb[(wm0 + i * 16 + g + ((e & 1) << 3)) * LDC + kk + t4 + ((e >> 1) << 2)];
+#pragma unroll
+                    for (int j = 0; j < NI; ++j)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) b[j][e] = Rb[(kk + t4 + (e << 2)) * LDR + wn0 + j * 8 + g];
+#pragma unroll
+                    for (int i = 0; i < MI; ++i)
+#pragma unroll
+                        for (int j = 0; j < NI; ++j) dmma_1688(acc[i][j], a[i], b[j]);
+                }
+#pragma unroll
+                for (int i = 0; i < MI; ++i)
+#pragma unroll
+                    for (int j = 0; j < NI; ++j)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int r = wm0 + i * 16 + g + ((e >> 1) << 3), c = wn0 + j * 8 + 2 * t4 + (e & 1);
+                            Gs[r * LDG + c] -= acc[i][j][e];
+                        }
+            } else {
+                for (int e = tid; e < QP * QP; e += nt) {
+                    const int r = e / QP, c = e % QP;
+                    double acc = 0.0;
+#pragma unroll
+                    for (int l = 0; l < PB; ++l) acc += Cb[r * LDC + l] * Rb[l * LDR + c];
+                    Gs[r * LDG + c] -= acc;
+                }
+            }
+        }
+        __syncthreads();
+        // the pivot rows / columns: G[p,:] = R', G[:,p] = −C·D⁻¹, G[p,p] = D⁻¹
+        for (int e = tid; e < PB * QP; e += nt) {
+            const int r = e / QP, j = e % QP;
+            if (j < k0 || j >= k0 + PB) Gs[(k0 + r) * LDG + j] = Rb[r * LDR + j];
+        }
+        for (int e = tid; e < QP * PB; e += nt) {
+            const int i = e / PB, l = e % PB;
+            if (i < k0 || i >= k0 + PB) {
+                double acc = 0.0;
+#pragma unroll
+                for (int m = 0; m < PB; ++m) acc += Cb[i * LDC + m] * Db[m * LDD + l];
+                Gs[i * LDG + k0 + l] = -acc;
+            }
+        }
+        for (int e = tid; e < PB * PB; e += nt) Gs[(k0 + e / PB) * LDG + k0 + e % PB] = Db[(e / PB) * LDD + e % PB];
+        __syncthreads();
+    }
+    for (int e = tid; e < q * q; e += nt) {  // exact symmetrisation
+        const int i = e % q, j = e / q;
+        ginv[i + (int64_t)j * ldo] = 0.5 * (Gs[i * LDG + j] + Gs[j * LDG + i]);
+    }
+}
+
 // Shared/global-memory Gauss-Jordan for large q (same arithmetic).
 __global__ void __launch_bounds__(1024) spd_inverse_kernel(const double* __restrict__ P, int64_t ldp, int q,
                                                            double* __restrict__ ginv, int64_t ldo, double* work,
