@@ -668,6 +668,7 @@ def run_ours(args, cfg):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         prob2 = si.ProblemMatrix(a_np, si.Symmetry.spd, context=ctx)  # H2D of A
+        t_prob = time.perf_counter()
         res = si.run_inverter(si.InverterConfig(prob2, si.SketchRule.gaussian_device(q), tol=0.0, max_iters=k_e2e,
                                                 seed=0, track=si.TrackOptions(residual_every_k=k_e2e)),
                               out=x_out)
@@ -677,9 +678,10 @@ def run_ours(args, cfg):
         e2e = {"value": e2e_v, "unit": "iter/s", "h2d_bytes_per_step": int(8 * n * n / k_e2e),
                "d2h_bytes_per_step": int(16 + 8 * n * n / k_e2e + 8 * 2 / k_e2e),
                "run_iterations": k_e2e,
+               "phases_ms": {"problem_upload_validate": 1e3 * (t_prob - t0), "run_inverter": 1e3 * (t1 - t_prob)},
                "note": "one run_inverter call (si_run_inverter) of the BASELINE run length from a host A: H2D of A, "
                        "SPD validation, device sketches, status word read back each iteration, the reference's "
-                       "forced residual checkpoints at k=1 and k=max (2n^3 each), X returned to host, all inside "
+                       "forced residual checkpoints at k=1 (X1 = I + V·Uᵀ: 4n²·2q from the rank-2q form) and k=max (2n^3), X returned to host, all inside "
                        "the timer; byte counts per step with the A/X transfers amortised over the run"}
         del prob2
 

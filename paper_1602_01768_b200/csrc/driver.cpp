@@ -519,10 +519,12 @@ static void run_inverter_impl(si_context* ctx, si_problem* prob, const si_invert
     struct Rel {
         si::RbfgsWork& w;
         double* scratch = nullptr;
+        double* lowrank = nullptr;  // n×2q: A·V for the first checkpoint
         ~Rel() {
             si::family_release(w);
             w.release();
             if (scratch) cudaFree(scratch);
+            if (lowrank) cudaFree(lowrank);
         }
     } rel{w};
     w.alloc(n, q, true);
@@ -549,6 +551,16 @@ static void run_inverter_impl(si_context* ctx, si_problem* prob, const si_invert
             return std::sqrt(c.scalar_host[0]);
         }
         return residual_norm(c, a, tracked);
+    };
+    // k = 1 from the default X0 = I: X1 = I + V·Uᵀ (the BFGS rank-2q form still in the
+    // workspace), so the checkpoint needs 4n²·2q flops instead of the 2n³ product
+    const bool lowrank_first = !cfg->x0_host && upd == SI_UPDATE_BFGS && a.dense;
+    auto first_residual = [&]() -> double {
+        if (!rel.lowrank) ck(cudaMalloc(&rel.lowrank, size_t(n) * size_t(2 * q) * sizeof(double)), "malloc");
+        si::lowrank_residual_sq_enqueue(c, a, 2 * w.q, w.V, n, w.U, n, rel.lowrank, c.scalar_dev);
+        ck(cudaMemcpyAsync(c.scalar_host, c.scalar_dev, sizeof(double), cudaMemcpyDeviceToHost, c.stream), "d2h");
+        ck(cudaStreamSynchronize(c.stream), "sync");
+        return std::sqrt(c.scalar_host[0]);
     };
 
     HistoryWriter hist{history, history_cap, 0, cfg};
@@ -658,7 +670,7 @@ static void run_inverter_impl(si_context* ctx, si_problem* prob, const si_invert
             return;
         }
         if (k == 1 || k == cfg->max_iters || k % cfg->residual_every_k == 0) {  // simi.cpp:361-375
-            const double rel_res = residual() / base;
+            const double rel_res = (k == 1 && lowrank_first ? first_residual() : residual()) / base;
             hist.record(k, rel_res, flops, seconds);
             if (rel_res <= cfg->tol) {
                 finish(SI_TOL_REACHED, "");

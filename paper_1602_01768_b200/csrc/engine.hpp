@@ -164,6 +164,9 @@ void rbfgs_enqueue_sketch_upload(Context& c, RbfgsWork& w);  // s_pinned -> S
 void residual_sq_enqueue(Context& c, Problem& a, const double* X, double* out_dev, double* scratch_nxn);
 // ‖I − A‖²_F: the base residual when X0 = I (default), O(n²) instead of 2n³
 void identity_residual_sq_enqueue(Context& c, Problem& a, double* out_dev);
+// ‖I − A·(I + V·Uᵀ)‖²_F with V, U n×k (dense A): the k = 1 checkpoint from X0 = I, 4n²k flops
+void lowrank_residual_sq_enqueue(Context& c, Problem& a, int64_t k, const double* V, int64_t ldv, const double* U,
+                                 int64_t ldu, double* P, double* out_dev);
 void factored_residual_sq_enqueue(Context& c, Problem& a, const double* L, double* AL, double* out_dev);
 void set_identity(Context& c, double* X, int64_t n);
 

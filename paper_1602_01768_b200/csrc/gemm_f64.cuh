@@ -41,7 +41,8 @@ struct GemmArgs {
     const int* skip;  // if set and nonzero, the launch is a no-op (failed Gram upstream)
     int* nonfinite;   // STORE / SYMUPD: set to 1 when a written entry is not finite (simi.cpp:342-347)
     int64_t diag_off; // RESID: the identity's diagonal is at (r, r + diag_off) (row panels of a sharded X)
-    int c_in_acc;     // STORE: accumulators start from beta·C (set by the host when alpha == 1, beta != 0)
+    int c_in_acc;     // STORE: accumulators start from beta·C (set by the host when alpha == 1, beta != 0);
+                      // RESID: from beta·C (the A + P·Uᵀ form of the first checkpoint)
     int dbg;          // SYMUPD experiments (SI_SYMUPD_DBG): 1 = no stores, 2 = no C loads, 4 = no C prefetch
 };
 
@@ -162,7 +163,7 @@ struct TileOps {
     // STORE with alpha = 1 and beta ≠ 0 also starts from C (p.c_in_acc)
     __device__ __forceinline__ bool c_in_acc(const GemmArgs& p) const {
         if constexpr (EPI == EPI_SYMUPD) return true;
-        if constexpr (EPI == EPI_STORE) return p.c_in_acc != 0;
+        if constexpr (EPI == EPI_STORE || EPI == EPI_RESID) return p.c_in_acc != 0;
         return false;
     }
 
