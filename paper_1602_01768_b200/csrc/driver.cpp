@@ -552,12 +552,14 @@ static void run_inverter_impl(si_context* ctx, si_problem* prob, const si_invert
         }
         return residual_norm(c, a, tracked);
     };
-    // k = 1 from the default X0 = I: X1 = I + V·Uᵀ (the BFGS rank-2q form still in the
-    // workspace), so the checkpoint needs 4n²·2q flops instead of the 2n³ product
+    // k = 1 from the default X0 = I: X1 = I + [Z R]·[W' Z]ᵀ (the BFGS rank-2q form still in
+    // the workspace), so the checkpoint needs 4n²·2q flops instead of the 2n³ product
     const bool lowrank_first = !cfg->x0_host && upd == SI_UPDATE_BFGS && a.dense;
     auto first_residual = [&]() -> double {
         if (!rel.lowrank) ck(cudaMalloc(&rel.lowrank, size_t(n) * size_t(2 * q) * sizeof(double)), "malloc");
-        si::lowrank_residual_sq_enqueue(c, a, 2 * w.q, w.V, n, w.U, n, rel.lowrank, c.scalar_dev);
+        // X1 = I + [Z R]·[W' Z]ᵀ (rbfgs_enqueue_iteration's buffers: U = [S | W' | Z | R])
+        const int64_t nq = n * w.q;
+        si::lowrank_residual_sq_enqueue(c, a, 2 * w.q, w.U + 2 * nq, n, w.U + nq, n, 1.0, rel.lowrank, c.scalar_dev);
         ck(cudaMemcpyAsync(c.scalar_host, c.scalar_dev, sizeof(double), cudaMemcpyDeviceToHost, c.stream), "d2h");
         ck(cudaStreamSynchronize(c.stream), "sync");
         return std::sqrt(c.scalar_host[0]);

@@ -298,7 +298,7 @@ static TileCfg pick_tile(int64_t N, int64_t M = 1 << 30) {
 
 void gemm(Context& c, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, bool a_kmajor, const double* B,
           int64_t ldb, bool b_kmajor, double* C, int64_t ldc, double alpha, double beta, const int* skip,
-          int* nonfinite) {
+          int* nonfinite, const double* Csrc) {
     if (M <= 0 || N <= 0) return;
     GemmArgs a{};
     a.M = M;
@@ -314,6 +314,7 @@ void gemm(Context& c, int64_t M, int64_t N, int64_t K, const double* A, int64_t 
     a.beta = beta;
     a.skip = skip;
     a.nonfinite = nonfinite;
+    a.Csrc = Csrc;
     // short-K, wide-output products (the rank-2q panel update) keep 16 warps resident
     // K <= 128 panel updates (the AdaRBFGS L update): two 8-warp 128×64 CTAs per SM so one
     // CTA's C-tile load/store overlaps the other's mainloop (3.6% faster at config 2 than one
@@ -375,7 +376,8 @@ void gemm(Context& c, int64_t M, int64_t N, int64_t K, const double* A, int64_t 
     launch_gemm_layout<EPI_PARTIAL>(c, t, a_kmajor, b_kmajor, vec, a, dim3(unsigned(tm), unsigned(tn), unsigned(splits)),
                                     "gemm_splitk");
     LaunchScope ls(c, "splitk_reduce");
-    splitk_reduce_kernel<<<grid_for(M * N, 256), 256, 0, c.stream>>>(a.ws, splits, M, N, C, ldc, alpha, beta, skip);
+    splitk_reduce_kernel<<<grid_for(M * N, 256), 256, 0, c.stream>>>(a.ws, splits, M, N, C, ldc, alpha, beta, skip,
+                                                                       Csrc);
     check_launch("splitk_reduce");
 }
 
@@ -590,7 +592,7 @@ void RbfgsWork::alloc(int64_t n_, int64_t q_, bool own) {
     own_x = own;
     if (own) dmalloc(&X, size_t(n) * size_t(n));
     dmalloc(&Y, size_t(n) * size_t(q));
-    dmalloc(&U, size_t(n) * size_t(2 * q));
+    dmalloc(&U, size_t(n) * size_t(4 * q));  // [S | W | Z | R] (BFGS); [S | W] for the other updates
     dmalloc(&V, size_t(n) * size_t(2 * q));
     dmalloc(&P, size_t(q) * size_t(2 * q));
     dmalloc(&Ginv, size_t(q) * size_t(q));
@@ -741,6 +743,16 @@ void rbfgs_core_enqueue(Context& c, const double* P, int64_t ldp, int64_t q, dou
     gemm(c, q, q, q, Ginv, q, false, T, q, true, M, 2 * q, 1.0, 1.0, status);          // M11 = Ginv + Ginv·T
 }
 
+// K-FACTOR for the single-GPU RBFGS iteration: G⁻¹ (with the gram_llt PD test) and
+// Ĝ = G − H' from P = [G | H'] (H' = YᵀW' = −H).
+void rbfgs_gram_enqueue(Context& c, const double* P, int64_t ldp, int64_t q, double* Ginv, double* Ghat,
+                        double* scratch, int* status) {
+    spd_inverse(c, P, ldp, q, Ginv, scratch, status);
+    LaunchScope ls(c, "ghat");
+    ghat_kernel<<<grid_for(q * q, 256), 256, 0, c.stream>>>(P, ldp, int(q), Ghat, status);
+    check_launch("ghat");
+}
+
 void philox_sketch(Context& c, double* S, int64_t n, int64_t q, int64_t lds, uint64_t seed,
                    const unsigned long long* counter_dev, uint64_t draw, const int* skip) {
     LaunchScope ls(c, "sketch_philox");
@@ -749,12 +761,22 @@ void philox_sketch(Context& c, double* S, int64_t n, int64_t q, int64_t lds, uin
     check_launch("philox");
 }
 
-// One RBFGS iteration:  X⁺ = X + [S W]·M·[S W]ᵀ.  Every launch
-// is skipped on the device once K-FACTOR flags a non-PD Gram (status[0]).
+// One RBFGS iteration.  With Y = A·S, W = X·Y, G = SᵀAS = YᵀS, H = YᵀW and
+// Z = S·G⁻¹, the reference's expanded update (qn_updates.cpp:176-186:
+// S·t2 + X − S·k − (S·k)ᵀ + S(k·t1ᵀ)Sᵀ with k = G⁻¹Wᵀ, S·t2 = Z·G·Zᵀ) is
+//     X⁺ = X + Z(G + H)Zᵀ − Z·Wᵀ − W·Zᵀ = X + [Z R]·[W' Z]ᵀ,
+//     W' = −W,  R = Z·Ĝ + W',  Ĝ = G + H = G − YᵀW',
+// so the q×q stage needs only G⁻¹ (K-FACTOR, with the PD test) and Ĝ, the
+// n-row stage is two n×q×q products (4nq² flops instead of the 8nq² of
+// V = [S W]·M plus two q×q×q core products), and [S | W' | Z | R] sit side by
+// side in one n×4q buffer so [S W'], [W' Z] and [Z R] are contiguous windows.
+// Every launch is skipped on the device once K-FACTOR flags a non-PD Gram (status[0]).
 void rbfgs_enqueue_iteration(Context& c, Problem& a, RbfgsWork& w, bool device_sketch, uint64_t seed) {
     const int64_t n = w.n, q = w.q;
     double* S = w.U;
-    double* W = w.U + n * q;
+    double* Wn = S + n * q;  // W' = −X·Y
+    double* Z = Wn + n * q;
+    double* R = Z + n * q;
     const int* skip = w.status;
     if (device_sketch) {
         LaunchScope ls(c, "sketch_philox");
@@ -762,12 +784,13 @@ void rbfgs_enqueue_iteration(Context& c, Problem& a, RbfgsWork& w, bool device_s
                                                                                    skip);
         check_launch("philox");
     }
-    apply_a(c, a, S, n, q, w.Y, n, skip);                                    // Y = A·S
-    gemm(c, n, q, n, w.X, n, false, w.Y, n, true, W, n, 1.0, 0.0, skip);     // W = X·Y
-    gemm(c, q, 2 * q, n, w.Y, n, true, w.U, n, true, w.P, q, 1.0, 0.0, skip);  // P = Yᵀ·[S W] = [G | H]
-    rbfgs_core_enqueue(c, w.P, q, q, w.Ginv, w.T, w.M, w.factor_scratch, w.status);  // Ginv, PD check, M
-    gemm(c, n, 2 * q, 2 * q, w.U, n, false, w.M, 2 * q, true, w.V, n, 1.0, 0.0, skip);  // V = U·M
-    symupd(c, n, 2 * q, w.V, n, w.U, n, w.X, n, 1.0, skip, w.status + 1);            // X += V·Uᵀ
+    apply_a(c, a, S, n, q, w.Y, n, skip);                                       // Y = A·S
+    gemm(c, n, q, n, w.X, n, false, w.Y, n, true, Wn, n, -1.0, 0.0, skip);      // W' = −X·Y
+    gemm(c, q, 2 * q, n, w.Y, n, true, S, n, true, w.P, q, 1.0, 0.0, skip);     // P = Yᵀ·[S W'] = [G | −H]
+    rbfgs_gram_enqueue(c, w.P, q, q, w.Ginv, w.T, w.factor_scratch, w.status);  // G⁻¹ + PD test, Ĝ = G + H
+    gemm(c, n, q, q, S, n, false, w.Ginv, q, true, Z, n, 1.0, 0.0, skip);       // Z = S·G⁻¹
+    gemm(c, n, q, q, Z, n, false, w.T, q, true, R, n, 1.0, 1.0, skip, nullptr, Wn);  // R = Z·Ĝ + W'
+    symupd(c, n, 2 * q, Z, n, Wn, n, w.X, n, 1.0, skip, w.status + 1);         // X += [Z R]·[W' Z]ᵀ
     if (device_sketch) {
         LaunchScope ls(c, "advance_counter");
         advance_counter_kernel<<<1, 1, 0, c.stream>>>(w.counter, w.status);
@@ -922,12 +945,12 @@ void residual_sq_enqueue(Context& c, Problem& a, const double* X, double* out_de
     check_launch("sum_reduce");
 }
 
-// First checkpoint from X0 = I (simi.cpp:361-375 at k = 1): X1 = I + V·Uᵀ, so
-// ‖I − A·X1‖² = ‖I − A − (A·V)·Uᵀ‖² — P = A·V (2n²·k) then one residual GEMM with
+// First checkpoint from X0 = I (simi.cpp:361-375 at k = 1): X1 = I + sign·V·Uᵀ, so
+// ‖I − A·X1‖² = ‖I − A − sign·(A·V)·Uᵀ‖² — P = A·V (2n²·k) then one residual GEMM with
 // K = k whose accumulators start from the A tile, 4n²k in all instead of 2n³
 // (config 3: 0.27 TFLOP instead of 8.8).  Dense A only.
 void lowrank_residual_sq_enqueue(Context& c, Problem& a, int64_t k, const double* V, int64_t ldv, const double* U,
-                                 int64_t ldu, double* P, double* out_dev) {
+                                 int64_t ldu, double sign, double* P, double* out_dev) {
     const int64_t n = a.n;
     if (!a.dense) throw std::invalid_argument("lowrank residual: dense A only");
     apply_a(c, a, V, ldv, k, P, n, nullptr);  // P = A·V
@@ -941,8 +964,8 @@ void lowrank_residual_sq_enqueue(Context& c, Problem& a, int64_t k, const double
     g.ldb = ldu;
     g.C = a.a;
     g.ldc = n;
-    g.alpha = 1.0;
-    g.beta = 1.0;
+    g.alpha = sign;  // acc = sign·A + P·Uᵀ = sign·(A·X1); the epilogue takes δ − sign·acc
+    g.beta = sign;
     g.c_in_acc = 1;
     g.k_chunk = k;
     const int64_t TM = (n + 127) / 128, TN = (n + 127) / 128;

@@ -143,7 +143,7 @@ void problem_download_dense(Problem& p, double* host);
 // generic dense product C = alpha·op(A)·op(B) + beta·C with leading dimensions
 void gemm(Context& c, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, bool a_kmajor, const double* B,
           int64_t ldb, bool b_kmajor, double* C, int64_t ldc, double alpha, double beta, const int* skip = nullptr,
-          int* nonfinite = nullptr);
+          int* nonfinite = nullptr, const double* Csrc = nullptr);  // Csrc: beta·Csrc (ld ldc) instead of beta·C
 // Y = A·P for the problem matrix (dense GEMM or CSR SpMM), P n×k
 void apply_a(Context& c, Problem& a, const double* P, int64_t ldp, int64_t k, double* Y, int64_t ldy,
              const int* skip = nullptr);
@@ -153,6 +153,9 @@ void spmm_csr_rows(Context& c, int64_t m, int64_t n, const int64_t* rowptr, cons
 void rbfgs_enqueue_iteration(Context& c, Problem& a, RbfgsWork& w, bool device_sketch, uint64_t seed);
 // the q×q stage: Gram inverse (PD check into status[0]) and the 2q×2q core M
 void rbfgs_core_enqueue(Context& c, const double* P, int64_t ldp, int64_t q, double* Ginv, double* T, double* M,
+                        double* scratch, int* status);
+// the q×q stage of the single-GPU iteration: G⁻¹ (PD check into status[0]) and Ĝ = G + H
+void rbfgs_gram_enqueue(Context& c, const double* P, int64_t ldp, int64_t q, double* Ginv, double* Ghat,
                         double* scratch, int* status);
 // Gaussian sketch from Philox(seed, draw): draw read from counter_dev if non-null
 void philox_sketch(Context& c, double* S, int64_t n, int64_t q, int64_t lds, uint64_t seed,
@@ -164,9 +167,9 @@ void rbfgs_enqueue_sketch_upload(Context& c, RbfgsWork& w);  // s_pinned -> S
 void residual_sq_enqueue(Context& c, Problem& a, const double* X, double* out_dev, double* scratch_nxn);
 // ‖I − A‖²_F: the base residual when X0 = I (default), O(n²) instead of 2n³
 void identity_residual_sq_enqueue(Context& c, Problem& a, double* out_dev);
-// ‖I − A·(I + V·Uᵀ)‖²_F with V, U n×k (dense A): the k = 1 checkpoint from X0 = I, 4n²k flops
+// ‖I − A·(I + sign·V·Uᵀ)‖²_F with V, U n×k (dense A): the k = 1 checkpoint from X0 = I, 4n²k flops
 void lowrank_residual_sq_enqueue(Context& c, Problem& a, int64_t k, const double* V, int64_t ldv, const double* U,
-                                 int64_t ldu, double* P, double* out_dev);
+                                 int64_t ldu, double sign, double* P, double* out_dev);
 void factored_residual_sq_enqueue(Context& c, Problem& a, const double* L, double* AL, double* out_dev);
 void set_identity(Context& c, double* X, int64_t n);
 

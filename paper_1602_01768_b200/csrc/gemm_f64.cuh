@@ -43,6 +43,7 @@ struct GemmArgs {
     int64_t diag_off; // RESID: the identity's diagonal is at (r, r + diag_off) (row panels of a sharded X)
     int c_in_acc;     // STORE: accumulators start from beta·C (set by the host when alpha == 1, beta != 0);
                       // RESID: from beta·C (the A + P·Uᵀ form of the first checkpoint)
+    const double* Csrc;  // STORE: beta·Csrc(m,n) (ld ldc) instead of beta·C — out-of-place C = alpha·A·B + beta·Csrc
     int dbg;          // SYMUPD experiments (SI_SYMUPD_DBG): 1 = no stores, 2 = no C loads, 4 = no C prefetch
 };
 
@@ -146,14 +147,15 @@ struct TileOps {
 
     // L2 prefetch of this thread's part of a C tile (the next work item's X block)
     __device__ __forceinline__ void prefetch_c(const GemmArgs& p) const {
+        const double* src = (EPI == EPI_STORE && p.Csrc) ? p.Csrc : p.C;
 #pragma unroll
         for (int i = 0; i < MI; ++i)
 #pragma unroll
             for (int j = 0; j < NI; ++j) {
                 const int64_t r = row(i, 0), c = col(j, 0);
-                if (r < p.M && c < p.N) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p.C + r + c * p.ldc));
+                if (r < p.M && c < p.N) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(src + r + c * p.ldc));
                 if (r < p.M && c + 1 < p.N)
-                    asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p.C + r + (c + 1) * p.ldc));
+                    asm volatile("prefetch.global.L2 [%0];\n" ::"l"(src + r + (c + 1) * p.ldc));
             }
     }
     // fragment element e of block (i, j) sits at (wm0 + 16i + g + 8(e>>1), wn0 + 8j + 2t + (e&1))
@@ -173,6 +175,7 @@ struct TileOps {
             // SYMUPD X + V·Uᵀ): the loads are issued under the pipeline fill and the
             // epilogue becomes store-only
             const double b = EPI == EPI_SYMUPD ? 1.0 : p.beta;
+            const double* src = (EPI == EPI_STORE && p.Csrc) ? p.Csrc : p.C;
 #pragma unroll
             for (int i = 0; i < MI; ++i)
 #pragma unroll
@@ -180,7 +183,7 @@ struct TileOps {
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const int64_t r = row(i, e), c = col(j, e);
-                        acc[i][j][e] = (r < p.M && c < p.N) ? b * p.C[r + c * p.ldc] : 0.0;
+                        acc[i][j][e] = (r < p.M && c < p.N) ? b * src[r + c * p.ldc] : 0.0;
                     }
         } else {
 #pragma unroll
@@ -231,7 +234,7 @@ struct TileOps {
                     for (int e = 0; e < 4; ++e) {
                         const int64_t r = row(i, e), c = col(j, e);
                         if (r < p.M && c < p.N) {
-                            const double d = (r + p.diag_off == c ? 1.0 : 0.0) - acc[i][j][e];
+                            const double d = (r + p.diag_off == c ? 1.0 : 0.0) - p.alpha * acc[i][j][e];
                             local += d * d;
                         }
                     }
@@ -293,7 +296,8 @@ struct TileOps {
                         const double v = acc[i][j][e];
                         if constexpr (EPI == EPI_STORE) {
                             double* cp = p.C + r + c * p.ldc;
-                            const double nv = p.c_in_acc ? v : (p.beta != 0.0 ? p.alpha * v + p.beta * *cp : p.alpha * v);
+                            const double* cs = p.Csrc ? p.Csrc + r + c * p.ldc : cp;
+                            const double nv = p.c_in_acc ? v : (p.beta != 0.0 ? p.alpha * v + p.beta * *cs : p.alpha * v);
                             *cp = nv;
                             if (p.nonfinite && !isfinite(nv)) atomicOr(p.nonfinite, 1);
                         } else if constexpr (EPI == EPI_PARTIAL) {

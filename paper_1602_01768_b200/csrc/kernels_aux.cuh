@@ -13,7 +13,8 @@ namespace si {
 
 // C(m,n) = alpha * sum_z ws[z][m,n] + beta * C(m,n)
 __global__ void splitk_reduce_kernel(const double* __restrict__ ws, int splits, int64_t M, int64_t N, double* C,
-                                     int64_t ldc, double alpha, double beta, const int* skip) {
+                                     int64_t ldc, double alpha, double beta, const int* skip,
+                                     const double* Csrc = nullptr) {
     if (skip && *skip) return;
     const int64_t total = M * N;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
@@ -22,7 +23,8 @@ __global__ void splitk_reduce_kernel(const double* __restrict__ ws, int splits, 
         for (int z = 0; z < splits; ++z) s += ws[z * total + idx];
         const int64_t m = idx % M, n = idx / M;
         double* c = C + m + n * ldc;
-        *c = beta != 0.0 ? alpha * s + beta * *c : alpha * s;
+        const double* cs = Csrc ? Csrc + m + n * ldc : c;
+        *c = beta != 0.0 ? alpha * s + beta * *cs : alpha * s;
     }
 }
 
@@ -103,6 +105,18 @@ __global__ void __launch_bounds__(MAXT) spd_inverse_reg_kernel(const double* __r
             const int i = r0 + r;
             if (i < q) ginv[i + (int64_t)j * ldo] = a[r];
         }
+    }
+}
+
+// Ĝ = G − H' for the RBFGS update X⁺ = X + [Z R]·[W' Z]ᵀ (engine.cu): G read from
+// the upper triangle of P[:, 0:q] (as K-FACTOR reads it), H' = P[:, q:2q] = −YᵀXY symmetrised
+__global__ void ghat_kernel(const double* __restrict__ P, int64_t ldp, int q, double* __restrict__ gh, const int* skip) {
+    if (skip && *skip) return;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < q * q; idx += gridDim.x * blockDim.x) {
+        const int i = idx % q, j = idx / q;
+        const double g = i <= j ? P[i + (int64_t)j * ldp] : P[j + (int64_t)i * ldp];
+        const double h = 0.5 * (P[i + (int64_t)(q + j) * ldp] + P[j + (int64_t)(q + i) * ldp]);
+        gh[idx] = g - h;
     }
 }
 
