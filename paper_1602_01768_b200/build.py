@@ -31,7 +31,7 @@ CXX_FLAGS = ["-std=gnu++20", "-O3", "-march=x86-64-v3", "-fPIC", "-Wall", "-Wext
 
 SOURCES_CU = ["engine.cu"]
 SOURCES_CXX = ["driver.cpp", "io.cpp"]
-HEADERS = ["common.cuh", "gemm_f64.cuh", "kernels_aux.cuh", "kernels_small.cuh", "family.cuh", "engine.hpp", "host_rng.hpp"]
+HEADERS = ["common.cuh", "gemm_f64.cuh", "kernels_aux.cuh", "kernels_small.cuh", "kernels_core.cuh", "family.cuh", "engine.hpp", "host_rng.hpp"]
 
 
 def _newer(target: str, deps: list[str]) -> bool:

@@ -13,6 +13,7 @@
 #include "gemm_f64.cuh"
 #include "kernels_aux.cuh"
 #include "kernels_small.cuh"
+#include "kernels_core.cuh"
 
 namespace si {
 
@@ -745,8 +746,35 @@ void rbfgs_core_enqueue(Context& c, const double* P, int64_t ldp, int64_t q, dou
 
 // K-FACTOR for the single-GPU RBFGS iteration: G⁻¹ (with the gram_llt PD test) and
 // Ĝ = G − H' from P = [G | H'] (H' = YᵀW' = −H).
+template <int QP>
+static void launch_gram_fused(Context& c, const double* P, int64_t ldp, int64_t q, double* Ginv, double* Ghat,
+                              int* status) {
+    constexpr int LF = 16, NT = 512;
+    using SM = core::GramSmem<QP, LF>;
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(rbfgs_gram_kernel<QP, LF, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(SM::BYTES)));
+        attr = true;
+    }
+    LaunchScope ls(c, "gram_inverse");
+    rbfgs_gram_kernel<QP, LF, NT><<<1, NT, SM::BYTES, c.stream>>>(P, ldp, int(q), Ginv, Ghat, status);
+    check_launch("gram_inverse");
+}
+
 void rbfgs_gram_enqueue(Context& c, const double* P, int64_t ldp, int64_t q, double* Ginv, double* Ghat,
                         double* scratch, int* status) {
+    // q ≤ 128: one single-CTA launch (kernels_core.cuh); SI_GRAM_UNFUSED=1 keeps K-FACTOR + ghat
+    static const bool unfused = std::getenv("SI_GRAM_UNFUSED") != nullptr;
+    if (!unfused && q <= 128) {
+        if (q <= 32)
+            launch_gram_fused<32>(c, P, ldp, q, Ginv, Ghat, status);
+        else if (q <= 64)
+            launch_gram_fused<64>(c, P, ldp, q, Ginv, Ghat, status);
+        else
+            launch_gram_fused<128>(c, P, ldp, q, Ginv, Ghat, status);
+        return;
+    }
     spd_inverse(c, P, ldp, q, Ginv, scratch, status);
     LaunchScope ls(c, "ghat");
     ghat_kernel<<<grid_for(q * q, 256), 256, 0, c.stream>>>(P, ldp, int(q), Ghat, status);

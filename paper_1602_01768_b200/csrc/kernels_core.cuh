@@ -1,15 +1,14 @@
-// K-CORE (fused): the whole q×q stage of one RBFGS iteration in ONE single-CTA
-// launch for q ≤ 128.  From P = [G | H] (q×2q, G = YᵀS read from its upper
-// triangle as gram_llt reads the lower one of SᵀAS, H = YᵀW):
+// K-FACTOR (fused, q ≤ 128): the whole q×q stage of one RBFGS iteration in ONE
+// single-CTA launch.  From P = [G | H'] (q×2q, G = YᵀS read from its upper
+// triangle as gram_llt reads the lower one of SᵀAS, H' = YᵀW' = −YᵀXY):
 //
-//   G⁻¹ + PD test          recursive 2×2 block (Schur) inverse in shared memory,
-//                          leaves of LF×LF inverted by one warp in registers
-//   T   = H·G⁻¹            (global scratch for q = 128, shared memory otherwise)
-//   M   = [[G⁻¹ + G⁻¹·T, −G⁻¹], [−G⁻¹, 0]]   (2q×2q, ld 2q), G⁻¹ (q×q, ld q)
+//   G⁻¹ + PD test   recursive 2×2 block (Schur-complement) inverse in shared
+//                   memory; LF×LF leaves by symmetric sweeps in one warp
+//                   (registers + broadcast rows, warp barriers only);
+//                   the block products on the DMMA pipe (m16n8k8 .f64)
+//   Ĝ = G − H'      (symmetrised), written straight from the load
 //
-// This replaces K-FACTOR + core_layout + two q×q×q GEMM launches (five to
-// seven launches, each a separate dependency step of the graph) of the
-// RBFGS iteration (qn_updates.cpp:176-186 via SURVEY App. C1).
+// It replaces spd_inverse + symmetrize_small + ghat (two or three launches).
 //
 // PD test: block elimination meets the same Schur-complement pivots, in the
 // same order, as the unblocked elimination / Cholesky; a leaf pivot that is not
@@ -20,28 +19,34 @@
 // Block inverse of G = [[A, B], [Bᵀ, D]] (h = N/2), in place:
 //   A ← A⁻¹;  T1 = A⁻¹·B;  D ← S = D − Bᵀ·T1;  D ← S⁻¹;
 //   B ← −T1·S⁻¹;  A ← A⁻¹ − B·T1ᵀ (= A⁻¹ + T2·T1ᵀ);  lower-left ← Bᵀ.
-// Products run on the DMMA pipe (m16n8k8 .f64) with all 16 warps.
 #pragma once
 #include "common.cuh"
 
 namespace si {
 namespace core {
 
-constexpr int kThreads = 512;
-constexpr int kWarps = kThreads / 32;
 
-// C(M×N) = A(M×K)·B(K×N) by warp tiles of (16·MI)×(8·NI) fragments; operands
-// come from the accessors a(i, k), b(k, j) (shared or global memory, any
-// layout) and every result element is handed to epi(i, j, v).
-template <int M, int N, int K, class FA, class FB, class FE>
-__device__ __forceinline__ void block_mma(int warp, int lane, FA a_at, FB b_at, FE epi) {
-    constexpr int MI = (M >= 32 && N >= 32 && (M / 32) * (N / 32) >= kWarps) ? 2 : 1;
-    constexpr int NI = (M >= 32 && N >= 32 && (M / 32) * (N / 32) >= kWarps) ? 4 : ((M / 16) * (N / 16) >= kWarps ? 2 : 1);
+// Code size matters more than anything else here: the kernel runs once per
+// iteration right after the big GEMMs have flushed the instruction caches, so
+// every phase is one out-of-line copy shared by all its call sites (a fully
+// inlined recursion measured 139 µs in place against 72 µs with a warm cache).
+
+// C(M×M) ∘= A(M×M)·B(M×M) on the DMMA pipe by warp tiles of (16·MI)×(8·NI)
+// fragments; element (i, k) of A is A[i·asi + k·ask], B(k, j) = B[k·bsk + j·bsj],
+// C(i, j) = C[i·ldc + j].  mode: 0 C = AB, 1 C −= AB, 2 C = −AB,
+// 3 C −= AB and Mr(j, i) = Xs(i, j) (pitch ldm: the lower-left mirror of B).
+template <int M, int NWARP>
+__device__ __noinline__ void mma_phase(const double* A, int asi, int ask, const double* B, int bsk, int bsj, double* C,
+                                       int ldc, int mode, double* Mr, const double* Xs, int ldm) {
+    constexpr bool BIG = M >= 32 && (M / 32) * (M / 32) >= NWARP;
+    constexpr int MI = BIG ? 2 : 1;
+    constexpr int NI = BIG ? 4 : ((M / 16) * (M / 16) >= NWARP ? 2 : 1);
     constexpr int TM = 16 * MI, TN = 8 * NI;
-    static_assert(M % TM == 0 && N % TN == 0 && K % 8 == 0, "block_mma tiling");
-    constexpr int TILES = (M / TM) * (N / TN);
+    static_assert(M % TM == 0 && M % TN == 0 && M % 8 == 0, "mma_phase tiling");
+    constexpr int TILES = (M / TM) * (M / TN);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, t4 = lane & 3;
-    for (int tile = warp; tile < TILES; tile += kWarps) {
+    for (int tile = warp; tile < TILES; tile += NWARP) {
         const int m0 = (tile % (M / TM)) * TM, n0 = (tile / (M / TM)) * TN;
         double acc[MI][NI][4];
 #pragma unroll
@@ -50,17 +55,18 @@ __device__ __forceinline__ void block_mma(int warp, int lane, FA a_at, FB b_at, 
             for (int j = 0; j < NI; ++j)
 #pragma unroll
                 for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
-#pragma unroll 4
-        for (int kk = 0; kk < K; kk += 8) {
+#pragma unroll 1
+        for (int kk = 0; kk < M; kk += 8) {
             double a[MI][4], b[NI][2];
 #pragma unroll
             for (int i = 0; i < MI; ++i)
 #pragma unroll
-                for (int e = 0; e < 4; ++e) a[i][e] = a_at(m0 + i * 16 + g + ((e & 1) << 3), kk + t4 + ((e >> 1) << 2));
+                for (int e = 0; e < 4; ++e)
+                    a[i][e] = A[(m0 + i * 16 + g + ((e & 1) << 3)) * asi + (kk + t4 + ((e >> 1) << 2)) * ask];
 #pragma unroll
             for (int j = 0; j < NI; ++j)
 #pragma unroll
-                for (int e = 0; e < 2; ++e) b[j][e] = b_at(kk + t4 + (e << 2), n0 + j * 8 + g);
+                for (int e = 0; e < 2; ++e) b[j][e] = B[(kk + t4 + (e << 2)) * bsk + (n0 + j * 8 + g) * bsj];
 #pragma unroll
             for (int i = 0; i < MI; ++i)
 #pragma unroll
@@ -71,40 +77,77 @@ __device__ __forceinline__ void block_mma(int warp, int lane, FA a_at, FB b_at, 
 #pragma unroll
             for (int j = 0; j < NI; ++j)
 #pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    epi(m0 + i * 16 + g + ((e >> 1) << 3), n0 + j * 8 + 2 * t4 + (e & 1), acc[i][j][e]);
+                for (int e = 0; e < 4; ++e) {
+                    const int r = m0 + i * 16 + g + ((e >> 1) << 3), c = n0 + j * 8 + 2 * t4 + (e & 1);
+                    const double v = acc[i][j][e];
+                    double* cp = C + r * ldc + c;
+                    if (mode == 0)
+                        *cp = v;
+                    else if (mode == 2)
+                        *cp = -v;
+                    else
+                        *cp -= v;
+                    if (mode == 3) Mr[c * ldm + r] = Xs[r * ldm + c];
+                }
     }
+    __syncthreads();
 }
 
-// LF×LF leaf at (o, o) of Gs (row-major, pitch LDG) inverted in place by warp 0:
-// lane j holds column j, row and column k of each Gauss-Jordan step travel by
-// shuffles.  Pivots are the Schur-complement pivots of the whole matrix.
-template <int LF, int LDG>
-__device__ __forceinline__ void leaf_inverse(double* Gs, int o, int warp, int lane, int* s_bad) {
+// LF×LF leaf (row-major, pitch ld) inverted in place by one warp with the
+// symmetric sweep operator (ã_kk = −1/p, ã_ik = a_ik/p, ã_ij = a_ij − a_ik·a_kj/p;
+// sweeping every pivot gives −A⁻¹, and the working matrix stays symmetric): lane j
+// keeps column j in registers, and since column k = row k, step k only needs every
+// lane's d[k] — one shared-memory store per lane, a warp barrier and broadcast
+// loads.  Row k+1 is updated and published first, so the next pivot's reciprocal
+// overlaps the rest of the step.  The pivots p are the Schur-complement pivots of
+// the whole matrix.
+template <int LF>
+__device__ __noinline__ void leaf_inverse(double* Gb, int ld, double* pp, int* s_bad) {
+    static_assert(LF == 16 || LF == 32, "leaf size");
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (warp == 0) {
         const int j = lane & (LF - 1);
         double d[LF];
 #pragma unroll
-        for (int i = 0; i < LF; ++i) d[i] = Gs[(o + i) * LDG + o + j];
+        for (int i = 0; i < LF; ++i) d[i] = Gb[i * ld + j];
         bool bad = false;
+        if (lane < LF) pp[lane] = d[0];
+        __syncwarp();
+        double inv_next = 1.0 / pp[0];
+        bad |= !(pp[0] > 0.0);
 #pragma unroll
         for (int k = 0; k < LF; ++k) {
-            const double piv = __shfl_sync(0xffffffffu, d[k], k);
-            bad |= !(piv > 0.0);
-            const double inv = 1.0 / piv;
-            const double rk = d[k];
-#pragma unroll
-            for (int i = 0; i < LF; ++i) {
-                const double cki = __shfl_sync(0xffffffffu, d[i], k);
-                if (i == k)
-                    d[i] = j == k ? inv : rk * inv;
-                else
-                    d[i] = j == k ? -cki * inv : d[i] - cki * rk * inv;
+            const double* buf = pp + (k & 1) * LF;
+            double* nbuf = pp + ((k + 1) & 1) * LF;
+            const double inv = inv_next;
+            const double akj = d[k] * inv;
+            if (k + 1 < LF) {
+                const double r1 = buf[k + 1];
+                d[k + 1] = j == k ? r1 * inv : d[k + 1] - r1 * akj;
+                if (lane < LF) nbuf[lane] = d[k + 1];
+                __syncwarp();
+                const double piv = nbuf[k + 1];
+                bad |= !(piv > 0.0);
+                inv_next = 1.0 / piv;
             }
+#pragma unroll
+            for (int i = 0; i < LF; i += 2) {
+                const double2 r = *reinterpret_cast<const double2*>(buf + i);
+                const double ri[2] = {r.x, r.y};
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int ii = i + u;
+                    if (ii == k)
+                        d[ii] = j == k ? -inv : akj;
+                    else if (ii != k + 1)
+                        d[ii] = j == k ? ri[u] * inv : d[ii] - ri[u] * akj;
+                }
+            }
+            __syncwarp();  // every lane has read buf before step k+1 overwrites it (as nbuf)
         }
         if (lane < LF) {
 #pragma unroll
-            for (int i = 0; i < LF; ++i) Gs[(o + i) * LDG + o + j] = d[i];
+            for (int i = 0; i < LF; ++i) Gb[i * ld + j] = -d[i];
         }
         if (bad && lane == 0) *s_bad = 1;
     }
@@ -112,144 +155,79 @@ __device__ __forceinline__ void leaf_inverse(double* Gs, int o, int warp, int la
 }
 
 // In-place inverse of the N×N block at (o, o); scr holds the T1 panels of this
-// level and the ones below ((N/2)×(N/2+4), then (N/4)×(N/4+4), ...).
-template <int N, int LF, int LDG>
-__device__ void block_inverse(double* Gs, int o, double* scr, int warp, int lane, int* s_bad) {
+// level and the ones below ((N/2)×(N/2+4), then (N/4)×(N/4+4), ...) and the
+// leaf ping-pong rows.
+template <int N, int LF, int LDG, int NW>
+__device__ __forceinline__ void block_inverse(double* Gs, int o, double* scr, int* s_bad) {
     if constexpr (N <= LF) {
-        leaf_inverse<N, LDG>(Gs, o, warp, lane, s_bad);
+        leaf_inverse<N>(Gs + o * LDG + o, LDG, scr, s_bad);
     } else {
         constexpr int h = N / 2, LDT = h + 4;
-        double* T1 = scr;
+        double* T1 = scr;                // h×h, pitch LDT
         double* sub = scr + h * LDT;
-        block_inverse<h, LF, LDG>(Gs, o, sub, warp, lane, s_bad);  // A ← A⁻¹
-        block_mma<h, h, h>(  // T1 = A⁻¹·B
-            warp, lane, [&](int i, int k) { return Gs[(o + i) * LDG + o + k]; },
-            [&](int k, int j) { return Gs[(o + k) * LDG + o + h + j]; },
-            [&](int i, int j, double v) { T1[i * LDT + j] = v; });
-        __syncthreads();
-        block_mma<h, h, h>(  // D ← D − Bᵀ·T1
-            warp, lane, [&](int i, int k) { return Gs[(o + k) * LDG + o + h + i]; },
-            [&](int k, int j) { return T1[k * LDT + j]; },
-            [&](int i, int j, double v) { Gs[(o + h + i) * LDG + o + h + j] -= v; });
-        __syncthreads();
-        block_inverse<h, LF, LDG>(Gs, o + h, sub, warp, lane, s_bad);  // D ← S⁻¹
-        block_mma<h, h, h>(  // B ← −T1·S⁻¹
-            warp, lane, [&](int i, int k) { return T1[i * LDT + k]; },
-            [&](int k, int j) { return Gs[(o + h + k) * LDG + o + h + j]; },
-            [&](int i, int j, double v) { Gs[(o + i) * LDG + o + h + j] = -v; });
-        __syncthreads();
-        block_mma<h, h, h>(  // A ← A⁻¹ − B·T1ᵀ, lower-left ← Bᵀ
-            warp, lane, [&](int i, int k) { return Gs[(o + i) * LDG + o + h + k]; },
-            [&](int k, int j) { return T1[j * LDT + k]; },
-            [&](int i, int j, double v) {
-                Gs[(o + i) * LDG + o + j] -= v;
-                Gs[(o + h + j) * LDG + o + i] = Gs[(o + i) * LDG + o + h + j];
-            });
-        __syncthreads();
+        double* A = Gs + o * LDG + o;   // A block; B = A + h, D = A + h·LDG + h, lower-left = A + h·LDG
+        block_inverse<h, LF, LDG, NW>(Gs, o, sub, s_bad);                                     // A ← A⁻¹
+        mma_phase<h, NW>(A, LDG, 1, A + h, LDG, 1, T1, LDT, 0, nullptr, nullptr, 0);           // T1 = A⁻¹·B
+        mma_phase<h, NW>(A + h, 1, LDG, T1, LDT, 1, A + h * LDG + h, LDG, 1, nullptr, nullptr, 0);  // D −= Bᵀ·T1
+        block_inverse<h, LF, LDG, NW>(Gs, o + h, sub, s_bad);                                 // D ← S⁻¹
+        mma_phase<h, NW>(T1, LDT, 1, A + h * LDG + h, LDG, 1, A + h, LDG, 2, nullptr, nullptr, 0);  // B ← −T1·S⁻¹
+        // A −= B·T1ᵀ and lower-left ← Bᵀ (mirror of the B block into A + h·LDG)
+        mma_phase<h, NW>(A + h, LDG, 1, T1, 1, LDT, A, LDG, 3, A + h * LDG, A + h, LDG);
     }
 }
 
-template <int N, int LF>
+template <int N, int LF, int LDG>
 constexpr int scratch_doubles() {
     if constexpr (N <= LF)
-        return 0;
+        return 2 * N;  // leaf ping-pong rows
     else
-        return (N / 2) * (N / 2 + 4) + scratch_doubles<N / 2, LF>();
+        return (N / 2) * (N / 2 + 4) + scratch_doubles<N / 2, LF, LDG>();
 }
 
-template <int QP>
-struct CoreSmem {
+template <int QP, int LF>
+struct GramSmem {
     static constexpr int LDG = QP + 4;
-    static constexpr bool H_SMEM = QP <= 64;  // H and T in shared memory; global (L2) at QP = 128
-    static constexpr int G_ELEMS = QP * LDG;
-    static constexpr int HT_ELEMS = H_SMEM ? 2 * QP * LDG : 0;
-    template <int LF>
-    static constexpr size_t bytes() {
-        return sizeof(double) * size_t(G_ELEMS + HT_ELEMS + scratch_doubles<QP, LF>());
-    }
+    static constexpr size_t BYTES = sizeof(double) * size_t(QP * LDG + scratch_doubles<QP, LF, LDG>());
 };
 
 }  // namespace core
 
-// One CTA of core::kThreads threads.  tg: q×q global scratch for T (used when QP = 128).
-template <int QP, int LF>
-__global__ void __launch_bounds__(core::kThreads, 1)
-    rbfgs_core_fused_kernel(const double* __restrict__ P, int64_t ldp, int q, double* __restrict__ ginv,
-                            double* __restrict__ tg, double* __restrict__ M, int* status) {
-    using SM = core::CoreSmem<QP>;
+// One CTA of NT threads: ginv (q×q, ld q) = G⁻¹ symmetrised,
+// ghat (q×q, ld q) = G − (H' + H'ᵀ)/2; status[0] = 1 when G is not PD.
+template <int QP, int LF, int NT>
+__global__ void __launch_bounds__(NT, 1)
+    rbfgs_gram_kernel(const double* __restrict__ P, int64_t ldp, int q, double* __restrict__ ginv,
+                      double* __restrict__ ghat, int* status) {
+    using SM = core::GramSmem<QP, LF>;
     constexpr int LDG = SM::LDG;
-    extern __shared__ __align__(16) double csm[];
+    extern __shared__ __align__(16) double gsm_[];
     __shared__ int s_bad;
     if (*status) return;
-    double* Gs = csm;
-    double* Hs = Gs + SM::G_ELEMS;                             // H_SMEM only
-    double* Ts = Hs + (SM::H_SMEM ? QP * LDG : 0);             // H_SMEM only
-    double* scr = Gs + SM::G_ELEMS + SM::HT_ELEMS;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const double* H = P + (int64_t)q * ldp;
+    double* Gs = gsm_;
+    double* scr = Gs + QP * LDG;
+    const int tid = threadIdx.x;
     if (tid == 0) s_bad = 0;
-    for (int e = tid; e < QP * QP; e += core::kThreads) {
+    for (int e = tid; e < QP * QP; e += NT) {
         const int i = e % QP, j = e / QP;  // column-major walk: coalesced reads of P
         double v;
-        if (i < q && j < q)
+        if (i < q && j < q) {
             v = i <= j ? P[i + (int64_t)j * ldp] : P[j + (int64_t)i * ldp];
-        else
+            if (ghat) ghat[i + (int64_t)j * q] = v - 0.5 * (P[i + (int64_t)(q + j) * ldp] + P[j + (int64_t)(q + i) * ldp]);
+        } else {
             v = i == j ? 1.0 : 0.0;  // identity padding keeps the block SPD
+        }
         Gs[i * LDG + j] = v;
-        if constexpr (SM::H_SMEM) Hs[i * LDG + j] = (i < q && j < q) ? H[i + (int64_t)j * ldp] : 0.0;
     }
     __syncthreads();
-    core::block_inverse<QP, LF, LDG>(Gs, 0, scr, warp, lane, &s_bad);
-    if (s_bad) {  // uniform (read after the leaf's barrier)
+    core::block_inverse<QP, LF, LDG, NT / 32>(Gs, 0, scr, &s_bad);
+    __syncthreads();
+    if (s_bad) {  // uniform
         if (tid == 0) *status = 1;
         return;
     }
-    // exact symmetrisation of G⁻¹ (the implied projector is symmetric); write G⁻¹
-    for (int e = tid; e < QP * QP; e += core::kThreads) {
-        const int i = e % QP, j = e / QP;
-        if (i < j) {
-            const double v = 0.5 * (Gs[i * LDG + j] + Gs[j * LDG + i]);
-            Gs[i * LDG + j] = v;
-            Gs[j * LDG + i] = v;
-        }
-    }
-    __syncthreads();
-    for (int e = tid; e < q * q; e += core::kThreads) {
+    for (int e = tid; e < q * q; e += NT) {  // exact symmetrisation
         const int i = e % q, j = e / q;
-        const double v = Gs[i * LDG + j];
-        ginv[e] = v;
-        M[i + (int64_t)(q + j) * (2 * q)] = -v;  // M12
-        M[q + i + (int64_t)j * (2 * q)] = -v;    // M21
-        M[q + i + (int64_t)(q + j) * (2 * q)] = 0.0;
-    }
-    // T = H·G⁻¹
-    if constexpr (SM::H_SMEM) {
-        core::block_mma<QP, QP, QP>(
-            warp, lane, [&](int i, int k) { return Hs[i * LDG + k]; }, [&](int k, int j) { return Gs[k * LDG + j]; },
-            [&](int i, int j, double v) { Ts[i * LDG + j] = v; });
-    } else {
-        core::block_mma<QP, QP, QP>(
-            warp, lane, [&](int i, int k) { return (i < q && k < q) ? H[i + (int64_t)k * ldp] : 0.0; },
-            [&](int k, int j) { return Gs[k * LDG + j]; },
-            [&](int i, int j, double v) {
-                if (i < q && j < q) tg[i + (int64_t)j * q] = v;
-            });
-    }
-    __syncthreads();  // T visible to the block (shared or global)
-    // M11 = G⁻¹ + G⁻¹·T
-    if constexpr (SM::H_SMEM) {
-        core::block_mma<QP, QP, QP>(
-            warp, lane, [&](int i, int k) { return Gs[i * LDG + k]; }, [&](int k, int j) { return Ts[k * LDG + j]; },
-            [&](int i, int j, double v) {
-                if (i < q && j < q) M[i + (int64_t)j * (2 * q)] = Gs[i * LDG + j] + v;
-            });
-    } else {
-        core::block_mma<QP, QP, QP>(
-            warp, lane, [&](int i, int k) { return Gs[i * LDG + k]; },
-            [&](int k, int j) { return (k < q && j < q) ? tg[k + (int64_t)j * q] : 0.0; },
-            [&](int i, int j, double v) {
-                if (i < q && j < q) M[i + (int64_t)j * (2 * q)] = Gs[i * LDG + j] + v;
-            });
+        ginv[e] = 0.5 * (Gs[i * LDG + j] + Gs[j * LDG + i]);
     }
 }
 
