@@ -84,6 +84,13 @@ __device__ __forceinline__ void named_bar_sync(int id, int threads) {
     asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(threads));
 }
 
+// Programmatic dependent launch: a kernel launched with the PDL attribute may start
+// while its predecessor drains; griddep_wait() blocks until the predecessor has
+// completed and its writes are visible (a no-op without the attribute), and
+// griddep_launch() lets the successor's CTAs start their own prologue early.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -158,6 +158,28 @@ static void launch_gemm_cfg(Context& c, const GemmArgs& a, dim3 grid, const char
     check_launch(name);
 }
 
+// ---- programmatic dependent launch: the iteration's kernels call griddep_wait()
+// before touching their inputs, so each may be launched while its predecessor
+// drains (SI_NO_PDL=1 turns the attribute off)
+static bool pdl_enabled() {
+    static const bool on = std::getenv("SI_NO_PDL") == nullptr;
+    return on;
+}
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    CK(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+
 // ---- TMA descriptors (cuTensorMapEncodeTiled through the runtime's driver entry point)
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -215,10 +237,10 @@ static void launch_tma_cfg(Context& c, const GemmArgs& a, dim3 grid, const char*
         make_tmap(&tb, a.B, a.N, a.K, a.ldb, BN + 4, BK);
     LaunchScope ls(c, name);
     if (persist)
-        kern_p<<<unsigned(std::min<int64_t>(work, int64_t(c.num_sms) * per_sm)), WM * WN * 32, SM::TMA_BYTES,
-                 c.stream>>>(ta, tb, a);
+        launch_pdl(kern_p, dim3(unsigned(std::min<int64_t>(work, int64_t(c.num_sms) * per_sm))), dim3(WM * WN * 32),
+                   SM::TMA_BYTES, c.stream, ta, tb, a);
     else
-        kern_g<<<grid, WM * WN * 32, SM::TMA_BYTES, c.stream>>>(ta, tb, a);
+        launch_pdl(kern_g, grid, dim3(WM * WN * 32), SM::TMA_BYTES, c.stream, ta, tb, a);
     check_launch(name);
 }
 
@@ -377,8 +399,8 @@ void gemm(Context& c, int64_t M, int64_t N, int64_t K, const double* A, int64_t 
     launch_gemm_layout<EPI_PARTIAL>(c, t, a_kmajor, b_kmajor, vec, a, dim3(unsigned(tm), unsigned(tn), unsigned(splits)),
                                     "gemm_splitk");
     LaunchScope ls(c, "splitk_reduce");
-    splitk_reduce_kernel<<<grid_for(M * N, 256), 256, 0, c.stream>>>(a.ws, splits, M, N, C, ldc, alpha, beta, skip,
-                                                                       Csrc);
+    launch_pdl(splitk_reduce_kernel, dim3(grid_for(M * N, 256)), dim3(256), 0, c.stream, (const double*)a.ws, splits, M,
+               N, C, ldc, alpha, beta, skip, Csrc);
     check_launch("splitk_reduce");
 }
 
@@ -758,7 +780,8 @@ static void launch_gram_fused(Context& c, const double* P, int64_t ldp, int64_t 
         attr = true;
     }
     LaunchScope ls(c, "gram_inverse");
-    rbfgs_gram_kernel<QP, LF, NT><<<1, NT, SM::BYTES, c.stream>>>(P, ldp, int(q), Ginv, Ghat, status);
+    launch_pdl(rbfgs_gram_kernel<QP, LF, NT>, dim3(1), dim3(NT), SM::BYTES, c.stream, P, ldp, int(q), Ginv, Ghat,
+               status);
     check_launch("gram_inverse");
 }
 
@@ -808,8 +831,8 @@ void rbfgs_enqueue_iteration(Context& c, Problem& a, RbfgsWork& w, bool device_s
     const int* skip = w.status;
     if (device_sketch) {
         LaunchScope ls(c, "sketch_philox");
-        philox_gaussian_kernel<<<grid_for((n * q + 1) / 2, 256), 256, 0, c.stream>>>(S, n, q, n, seed, w.counter,
-                                                                                   skip);
+        launch_pdl(philox_gaussian_kernel, dim3(grid_for((n * q + 1) / 2, 256)), dim3(256), 0, c.stream, S, n, q, n,
+                   seed, (const unsigned long long*)w.counter, skip, 0ull);
         check_launch("philox");
     }
     apply_a(c, a, S, n, q, w.Y, n, skip);                                       // Y = A·S
@@ -821,7 +844,7 @@ void rbfgs_enqueue_iteration(Context& c, Problem& a, RbfgsWork& w, bool device_s
     symupd(c, n, 2 * q, Z, n, Wn, n, w.X, n, 1.0, skip, w.status + 1);         // X += [Z R]·[W' Z]ᵀ
     if (device_sketch) {
         LaunchScope ls(c, "advance_counter");
-        advance_counter_kernel<<<1, 1, 0, c.stream>>>(w.counter, w.status);
+        launch_pdl(advance_counter_kernel, dim3(1), dim3(1), 0, c.stream, w.counter, w.status);
         check_launch("advance");
     }
 }

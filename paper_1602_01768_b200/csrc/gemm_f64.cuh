@@ -335,13 +335,24 @@ __global__ void __launch_bounds__(WM* WN * 32, ((EPI == EPI_SYMUPD || EPI == EPI
     constexpr int NW = WM * WN;
     constexpr uint32_t STAGE_BYTES = SM::STAGE_ELEMS * sizeof(double);
 
-    if (p.skip && *p.skip) return;
     extern __shared__ __align__(128) double smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(smem) + SM::BAR_OFFSET);
     uint64_t* empty = full + STAGES;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool producer = tid == 0;
+    if (producer) {  // prologue before the dependency wait (overlaps the predecessor's tail under PDL)
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NW);
+        }
+        mbar_fence_init();
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+    }
+    griddep_wait();
+    griddep_launch();
+    if (p.skip && *p.skip) return;
     const int64_t W = T::work_count(p);
     auto chunk_kt = [&](int64_t split) {
         const int64_t kb = split * p.k_chunk;
@@ -393,15 +404,6 @@ __global__ void __launch_bounds__(WM* WN * 32, ((EPI == EPI_SYMUPD || EPI == EPI
         while (pw < W && pissued < cg + STAGES - 1) issue_next();
     };
 
-    if (producer) {
-        for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], NW);
-        }
-        mbar_fence_init();
-        tma_prefetch_desc(&tmA);
-        tma_prefetch_desc(&tmB);
-    }
     __syncthreads();
     if (producer) pump(0);
 
@@ -448,12 +450,23 @@ __global__ void __launch_bounds__(WM* WN * 32, 1)
     constexpr int NW = WM * WN;
     constexpr uint32_t STAGE_BYTES = SM::STAGE_ELEMS * sizeof(double);
 
-    if (p.skip && *p.skip) return;
     extern __shared__ __align__(128) double smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(smem) + SM::BAR_OFFSET);
     uint64_t* empty = full + STAGES;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {  // prologue before the dependency wait (overlaps the predecessor's tail under PDL)
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NW);
+        }
+        mbar_fence_init();
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+    }
+    griddep_wait();
+    griddep_launch();
+    if (p.skip && *p.skip) return;
     T t;
     t.setup(warp, lane);
     const int64_t k_begin = (int64_t)blockIdx.z * p.k_chunk;
@@ -478,15 +491,6 @@ __global__ void __launch_bounds__(WM* WN * 32, 1)
             tma_load_2d(Bs, &tmB, (int32_t)t.n0, kc, &full[s]);
     };
 
-    if (producer) {
-        for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], NW);
-        }
-        mbar_fence_init();
-        tma_prefetch_desc(&tmA);
-        tma_prefetch_desc(&tmB);
-    }
     __syncthreads();
     if (producer)
         for (int kt = 0; kt < STAGES - 1 && kt < num_kt; ++kt) issue(kt);

@@ -15,6 +15,8 @@ namespace si {
 __global__ void splitk_reduce_kernel(const double* __restrict__ ws, int splits, int64_t M, int64_t N, double* C,
                                      int64_t ldc, double alpha, double beta, const int* skip,
                                      const double* Csrc = nullptr) {
+    griddep_wait();
+    griddep_launch();
     if (skip && *skip) return;
     const int64_t total = M * N;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
@@ -386,6 +388,8 @@ struct Philox {
 __global__ void philox_gaussian_kernel(double* __restrict__ S, int64_t n, int64_t q, int64_t lds, uint64_t seed,
                                        const unsigned long long* draw_counter, const int* skip,
                                        unsigned long long draw_value = 0) {
+    griddep_wait();
+    griddep_launch();
     if (skip && *skip) return;
     const uint64_t draw = draw_counter ? *draw_counter : draw_value;
     const int64_t total = n * q;
@@ -410,6 +414,8 @@ __global__ void philox_gaussian_kernel(double* __restrict__ S, int64_t n, int64_
 // iteration's Gram was rejected, count it (status[2]) and clear the skip flag so
 // the next enqueued iteration runs -- a rejected draw becomes a redraw.
 __global__ void advance_counter_kernel(unsigned long long* counter, int* status) {
+    griddep_wait();
+    griddep_launch();
     *counter += 1ull;
     if (status[0]) {
         status[2] += 1;

@@ -202,6 +202,8 @@ __global__ void __launch_bounds__(NT, 1)
     constexpr int LDG = SM::LDG;
     extern __shared__ __align__(16) double gsm_[];
     __shared__ int s_bad;
+    griddep_wait();
+    griddep_launch();
     if (*status) return;
     double* Gs = gsm_;
     double* scr = Gs + QP * LDG;
