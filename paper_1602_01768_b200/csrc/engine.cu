@@ -1185,7 +1185,9 @@ void ada_core_enqueue(Context& c, const double* G, int64_t q, const double* Z, i
 
 void gather_columns(Context& c, const double* L, int64_t rows, int64_t ld, const int64_t* idx, int64_t q, double* out) {
     LaunchScope ls(c, "gather_columns");
-    gather_columns_kernel<<<grid_for(rows * q, 256), 256, 0, c.stream>>>(L, rows, ld, idx, q, out);
+    const int64_t bx = std::max<int64_t>(1, std::min<int64_t>((rows + 255) / 256, int64_t(c.num_sms) * 16 / std::max<int64_t>(q, 1) + 1));
+    const int64_t by = std::min<int64_t>(q, 65535);
+    gather_columns_kernel<<<dim3(unsigned(bx), unsigned(by)), 256, 0, c.stream>>>(L, rows, ld, idx, q, out);
     check_launch("gather");
 }
 

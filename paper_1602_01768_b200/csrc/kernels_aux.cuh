@@ -23,7 +23,15 @@ __global__ void splitk_reduce_kernel(const double* __restrict__ ws, int splits, 
          idx += (int64_t)gridDim.x * blockDim.x) {
         double s = 0.0;
         for (int z = 0; z < splits; ++z) s += ws[z * total + idx];
-        const int64_t m = idx % M, n = idx / M;
+        int64_t m, n;
+        if (total < (int64_t(1) << 31)) {  // 32-bit index arithmetic
+            const uint32_t i32 = (uint32_t)idx, m32 = (uint32_t)M, q32 = i32 / m32;
+            n = q32;
+            m = i32 - q32 * m32;
+        } else {
+            n = idx / M;
+            m = idx - n * M;
+        }
         double* c = C + m + n * ldc;
         const double* cs = Csrc ? Csrc + m + n * ldc : c;
         *c = beta != 0.0 ? alpha * s + beta * *cs : alpha * s;
@@ -405,8 +413,21 @@ __global__ void philox_gaussian_kernel(double* __restrict__ S, int64_t n, int64_
         double sn, cs;
         sincospi(2.0 * u2, &sn, &cs);
         const int64_t l0 = 2 * e, l1 = 2 * e + 1;
-        S[(l0 % n) + (l0 / n) * lds] = r * cs;
-        if (l1 < total) S[(l1 % n) + (l1 / n) * lds] = r * sn;
+        int64_t i0, j0, i1, j1;
+        if (total < (int64_t(1) << 31)) {  // 32-bit index arithmetic (a 64-bit division is a long software sequence)
+            const uint32_t n32 = (uint32_t)n, a = (uint32_t)l0, b = (uint32_t)l1;
+            j0 = a / n32;
+            i0 = a - (uint32_t)j0 * n32;
+            j1 = b / n32;
+            i1 = b - (uint32_t)j1 * n32;
+        } else {
+            j0 = l0 / n;
+            i0 = l0 - j0 * n;
+            j1 = l1 / n;
+            i1 = l1 - j1 * n;
+        }
+        S[i0 + j0 * lds] = r * cs;
+        if (l1 < total) S[i1 + j1 * lds] = r * sn;
     }
 }
 
@@ -461,9 +482,12 @@ __global__ void set_identity_kernel(double* X, int64_t n, int64_t ldx) {
 // coordinate S̃ (adarbfgs.cpp:13 without the dense GEMM).
 __global__ void gather_columns_kernel(const double* __restrict__ L, int64_t n, int64_t ldl,
                                       const int64_t* __restrict__ idx, int64_t q, double* __restrict__ S) {
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * q; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = e % n, j = e / n;
-        S[e] = L[i + idx[j] * ldl];
+    // grid.y walks the q gathered columns, grid.x the rows: coalesced, no index division
+    for (int64_t j = blockIdx.y; j < q; j += gridDim.y) {
+        const double* __restrict__ src = L + idx[j] * ldl;
+        double* __restrict__ dst = S + j * n;
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+            dst[i] = src[i];
     }
 }
 
