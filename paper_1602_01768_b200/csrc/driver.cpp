@@ -340,7 +340,7 @@ static void bfgs_step_impl(si_context* ctx, si::Problem& a, int64_t q, const dou
     } rel{w};
     w.alloc(n, q, true);
     ck(cudaMemcpyAsync(w.X, x_host, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyHostToDevice, c.stream), "h2d");
-    std::memcpy(w.s_pinned, s_host, size_t(n) * size_t(q) * sizeof(double));
+    std::memcpy(w.pinned(), s_host, size_t(n) * size_t(q) * sizeof(double));
     si::rbfgs_enqueue_sketch_upload(c, w);
     si::rbfgs_enqueue_iteration(c, a, w, false, 0);
     int st[4];
@@ -485,10 +485,29 @@ static void validate_update(int u, si_problem* prob) {
 
 // ---------------------------------------------------------- run_inverter ---
 // simi.cpp:217-381 for MethodSpec::named_method(bfgs | psb | aip | dfp).
+// SI_TRACE=1: wall time of the driver's phases on stderr (stream synchronised at each mark)
+struct PhaseTrace {
+    bool on = std::getenv("SI_TRACE") != nullptr;
+    cudaStream_t s;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), last = t0;
+    explicit PhaseTrace(cudaStream_t st) : s(st) {}
+    void mark(const char* what) {
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[si trace] %-28s %9.3f ms (total %9.3f ms)\n", what,
+                     std::chrono::duration<double, std::milli>(now - last).count(),
+                     std::chrono::duration<double, std::milli>(now - t0).count());
+        last = now;
+    }
+    ~PhaseTrace() { mark("release"); }
+};
+
 static void run_inverter_impl(si_context* ctx, si_problem* prob, const si_inverter_config* cfg, double* x_out,
                               double* x_inv_out, si_history_point* history, int64_t history_cap,
                               si_run_result* result) {
     auto& c = *ctx->c;
+    PhaseTrace trace(c.stream);
     si::Problem& a = *prob->p;
     const int64_t n = a.n, q = cfg->q;
     const int upd = cfg->update;
@@ -515,20 +534,37 @@ static void run_inverter_impl(si_context* ctx, si_problem* prob, const si_invert
         if (asym > 1e-10 * std::max(1.0, nrm)) throw ConfigError("run_inverter: this method requires a symmetric x0");
     }
 
-    si::RbfgsWork w;
+    // the bfgs workspace stays in the context between calls when X is at most a quarter of
+    // device memory: re-running a problem of the same shape allocates and frees nothing
+    // (cudaFree / cudaFreeHost of gigabyte buffers measured 3-400 ms)
+    size_t mem_free = 0, mem_total = 0;
+    ck(cudaMemGetInfo(&mem_free, &mem_total), "meminfo");
+    const bool cacheable = upd == SI_UPDATE_BFGS && double(n) * double(n) * 8.0 <= 0.25 * double(mem_total);
+    si::RbfgsWork* wp = cacheable ? c.take_rbfgs(n, q) : nullptr;
+    if (!wp) {
+        wp = new si::RbfgsWork;
+        wp->alloc(n, q, true);
+        si::family_alloc(*wp, upd);
+    }
+    si::RbfgsWork& w = *wp;
+    w.q = q;
     struct Rel {
-        si::RbfgsWork& w;
+        si::Context& c;
+        si::RbfgsWork* w;
+        bool cacheable;
         double* scratch = nullptr;
-        double* lowrank = nullptr;  // n×2q: A·V for the first checkpoint
         ~Rel() {
-            si::family_release(w);
-            w.release();
             if (scratch) cudaFree(scratch);
-            if (lowrank) cudaFree(lowrank);
+            if (cacheable) {
+                c.keep_rbfgs(w);
+                return;
+            }
+            si::family_release(*w);
+            w->release();
+            delete w;
         }
-    } rel{w};
-    w.alloc(n, q, true);
-    si::family_alloc(w, upd);
+    } rel{c, wp, cacheable};
+    trace.mark("alloc");
     if (cfg->x0_host)
         ck(cudaMemcpyAsync(w.X, cfg->x0_host, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyHostToDevice,
                            c.stream),
@@ -556,10 +592,10 @@ static void run_inverter_impl(si_context* ctx, si_problem* prob, const si_invert
     // the workspace), so the checkpoint needs 4n²·2q flops instead of the 2n³ product
     const bool lowrank_first = !cfg->x0_host && upd == SI_UPDATE_BFGS && a.dense;
     auto first_residual = [&]() -> double {
-        if (!rel.lowrank) ck(cudaMalloc(&rel.lowrank, size_t(n) * size_t(2 * q) * sizeof(double)), "malloc");
+        if (!w.lowrank) ck(cudaMalloc(&w.lowrank, size_t(n) * size_t(2 * q) * sizeof(double)), "malloc");
         // X1 = I + [Z R]·[W' Z]ᵀ (rbfgs_enqueue_iteration's buffers: U = [S | W' | Z | R])
         const int64_t nq = n * w.q;
-        si::lowrank_residual_sq_enqueue(c, a, 2 * w.q, w.U + 2 * nq, n, w.U + nq, n, 1.0, rel.lowrank, c.scalar_dev);
+        si::lowrank_residual_sq_enqueue(c, a, 2 * w.q, w.U + 2 * nq, n, w.U + nq, n, 1.0, w.lowrank, c.scalar_dev);
         ck(cudaMemcpyAsync(c.scalar_host, c.scalar_dev, sizeof(double), cudaMemcpyDeviceToHost, c.stream), "d2h");
         ck(cudaStreamSynchronize(c.stream), "sync");
         return std::sqrt(c.scalar_host[0]);
@@ -584,6 +620,7 @@ static void run_inverter_impl(si_context* ctx, si_problem* prob, const si_invert
                                c.stream),
                "d2h x_inv");
         ck(cudaStreamSynchronize(c.stream), "sync");
+        trace.mark("finish (x download)");
     };
 
     // simi.cpp:242-246; for the default X0 = I (and H0 = I), ‖I − A·I‖ = ‖I − A‖ needs no GEMM
@@ -596,6 +633,7 @@ static void run_inverter_impl(si_context* ctx, si_problem* prob, const si_invert
         ck(cudaStreamSynchronize(c.stream), "sync");
         base = std::sqrt(c.scalar_host[0]);
     }
+    trace.mark("x0 + base residual");
     if (base == 0.0) {
         hist.record(0, 0.0, 0.0, 0.0);
         finish(SI_TOL_REACHED, "");
@@ -633,7 +671,98 @@ static void run_inverter_impl(si_context* ctx, si_problem* prob, const si_invert
     si::RngStream rng(cfg->seed);  // simi.cpp:275
     const bool device_sketch = sk == SI_SKETCH_GAUSSIAN_DEVICE;
     DeviceTimer tm;
-    int st[4];
+    int st[8];
+    // simi.cpp:361-375: the residual checkpoint after iteration k
+    auto checkpoint = [&]() -> bool {
+        trace.mark("iterations");
+        const double rel_res = (k == 1 && lowrank_first ? first_residual() : residual()) / base;
+        trace.mark(k == 1 && lowrank_first ? "checkpoint (rank-2q)" : "checkpoint");
+        hist.record(k, rel_res, flops, seconds);
+        if (rel_res <= cfg->tol) {
+            finish(SI_TOL_REACHED, "");
+            return true;
+        }
+        if (cfg->time_budget_seconds > 0.0 && seconds > cfg->time_budget_seconds) {
+            finish(SI_MAX_ITERS, "time budget exhausted");
+            return true;
+        }
+        return false;
+    };
+    // Device sketches (bfgs): the iterations between two checkpoints are enqueued back to
+    // back — one captured CUDA graph per iteration, no host round trip — and the device
+    // keeps the accounting (advance_batch_kernel): a rejected draw or a non-finite iterate
+    // stops the batch at the exact iteration, so k, the redraw count and limit, the draws
+    // and the iterates are those of the eager loop below.  SI_RUN_EAGER=1 forces the latter.
+    if (device_sketch && upd == SI_UPDATE_BFGS && std::getenv("SI_RUN_EAGER") == nullptr) {
+        w.batch = true;
+        struct Graph {
+            cudaGraphExec_t exec = nullptr;
+            PhaseTrace* tr = nullptr;
+            ~Graph() {
+                if (exec) cudaGraphExecDestroy(exec);
+                if (tr) tr->mark("graph destroy");
+            }
+        } g;
+        g.tr = &trace;
+        const bool graphs = !c.profiling && std::getenv("SI_NO_GRAPH") == nullptr;
+        bool warmed = false;
+        int64_t graph_launches = 0;
+        int consecutive = 0;  // failed attempts of iteration k + 1
+        const int64_t every = cfg->residual_every_k, kmax = cfg->max_iters;
+        k = 0;
+        while (k < kmax) {
+            const int64_t kc = k == 0 ? 1 : std::min(((k + every) / every) * every, kmax);  // next checkpoint
+            ck(cudaMemsetAsync(w.status, 0, 8 * sizeof(int), c.stream), "reset");
+            ck(cudaEventRecord(tm.a, c.stream), "event");
+            for (int64_t b = k; b < kc; ++b) {
+                if (!graphs || !warmed) {  // the first iteration runs eagerly: sizes workspaces, sets attributes
+                    si::family_enqueue_iteration(c, a, w, true, cfg->seed);
+                    warmed = true;
+                    continue;
+                }
+                if (!g.exec) {
+                    const int64_t l0 = c.launches;
+                    cudaGraph_t gr = nullptr;
+                    ck(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal), "capture");
+                    si::family_enqueue_iteration(c, a, w, true, cfg->seed);
+                    ck(cudaStreamEndCapture(c.stream, &gr), "end capture");
+                    ck(cudaGraphInstantiate(&g.exec, gr, 0), "instantiate");
+                    cudaGraphDestroy(gr);
+                    graph_launches = c.launches - l0;
+                    c.launches = l0;
+                }
+                ck(cudaGraphLaunch(g.exec, c.stream), "graph launch");
+                c.launches += graph_launches;
+            }
+            ck(cudaEventRecord(tm.b, c.stream), "event");
+            ck(cudaMemcpyAsync(st, w.status, 8 * sizeof(int), cudaMemcpyDeviceToHost, c.stream), "status d2h");
+            ck(cudaStreamSynchronize(c.stream), "sync");
+            const int64_t accepted = st[3];
+            k += accepted;
+            result->redraws += st[2];
+            if (cfg->track_wall_time) seconds += tm.seconds();
+            if (cfg->track_flops) flops += double(accepted) * flops_named(upd, double(n), double(w.q));
+            if (st[1]) {  // simi.cpp:342-347
+                finish(SI_TERMINATION_ERROR, "diverged: non-finite entries at iteration " + std::to_string(k));
+                return;
+            }
+            if (st[4]) {  // a rejected draw of iteration k + 1 stopped the batch (simi.cpp:331-333)
+                consecutive = (accepted > 0 ? 0 : consecutive) + 1;
+                if (consecutive > cfg->max_redraws) {
+                    k += 1;
+                    finish(SI_TERMINATION_ERROR, "sketch rejection limit exceeded for " + describe(sk, q) +
+                                                     " at iteration " + std::to_string(k));
+                    return;
+                }
+                continue;
+            }
+            consecutive = 0;
+            if (checkpoint()) return;
+        }
+        k = kmax;
+        finish(SI_MAX_ITERS, "");
+        return;
+    }
     for (k = 1; k <= cfg->max_iters; ++k) {
         bool stepped = false;
         for (int failures = 0; !stepped; ++failures) {
@@ -643,14 +772,15 @@ static void run_inverter_impl(si_context* ctx, si_problem* prob, const si_invert
                 return;
             }
             if (sk == SI_SKETCH_GAUSSIAN) {
-                rng.gaussian_fill(w.s_pinned, n, q, n);  // rng.hpp:42-49
+                rng.gaussian_fill(w.pinned(), n, q, n);  // rng.hpp:42-49
             } else if (sk == SI_SKETCH_COORDINATE_BLOCK) {
                 const si::Index i = rng.categorical(p.data(), si::Index(p.size()));
                 const auto& blk = blocks[size_t(i)];
                 // the last block of contiguous_partition may be narrower: this draw has q' = |C_i| columns
                 w.q = int64_t(blk.size());
-                std::fill(w.s_pinned, w.s_pinned + n * w.q, 0.0);
-                for (size_t j = 0; j < blk.size(); ++j) w.s_pinned[blk[j] + int64_t(j) * n] = 1.0;
+                double* sp = w.pinned();
+                std::fill(sp, sp + n * w.q, 0.0);
+                for (size_t j = 0; j < blk.size(); ++j) sp[blk[j] + int64_t(j) * n] = 1.0;
             }
             if (!device_sketch) si::rbfgs_enqueue_sketch_upload(c, w);
             ck(cudaEventRecord(tm.a, c.stream), "event");  // timer starts after the draw (simi.cpp:298)
@@ -672,16 +802,7 @@ static void run_inverter_impl(si_context* ctx, si_problem* prob, const si_invert
             return;
         }
         if (k == 1 || k == cfg->max_iters || k % cfg->residual_every_k == 0) {  // simi.cpp:361-375
-            const double rel_res = (k == 1 && lowrank_first ? first_residual() : residual()) / base;
-            hist.record(k, rel_res, flops, seconds);
-            if (rel_res <= cfg->tol) {
-                finish(SI_TOL_REACHED, "");
-                return;
-            }
-            if (cfg->time_budget_seconds > 0.0 && seconds > cfg->time_budget_seconds) {
-                finish(SI_MAX_ITERS, "time budget exhausted");
-                return;
-            }
+            if (checkpoint()) return;
         }
     }
     k = cfg->max_iters;
@@ -886,7 +1007,7 @@ static void named_step_impl(si_context* ctx, int update, int64_t n, int64_t q, c
     const size_t nn = size_t(n) * size_t(n) * sizeof(double);
     ck(cudaMemcpyAsync(w.X, x_host, nn, cudaMemcpyHostToDevice, c.stream), "h2d");
     if (update == SI_UPDATE_DFP) ck(cudaMemcpyAsync(w.H, x_inv_host, nn, cudaMemcpyHostToDevice, c.stream), "h2d");
-    std::memcpy(w.s_pinned, s_host, size_t(n) * size_t(q) * sizeof(double));
+    std::memcpy(w.pinned(), s_host, size_t(n) * size_t(q) * sizeof(double));
     si::rbfgs_enqueue_sketch_upload(c, w);
     si::family_enqueue_iteration(c, a, w, false, 0);
     int st[4];
@@ -1217,9 +1338,9 @@ static void solver_one(si_solver* s, const double* s_host, const int64_t* idx_ho
         const bool dev = s_host == nullptr && s->sketch == SI_SKETCH_GAUSSIAN_DEVICE;
         if (!dev) {
             if (s_host)
-                std::memcpy(s->rw.s_pinned, s_host, size_t(n) * size_t(q) * sizeof(double));
+                std::memcpy(s->rw.pinned(), s_host, size_t(n) * size_t(q) * sizeof(double));
             else
-                s->rng->gaussian_fill(s->rw.s_pinned, n, q, n);
+                s->rng->gaussian_fill(s->rw.pinned(), n, q, n);
             si::rbfgs_enqueue_sketch_upload(c, s->rw);
         }
         si::rbfgs_enqueue_iteration(c, a, s->rw, dev, s->seed);

@@ -52,11 +52,33 @@ Context::~Context() {
     }
     for (auto e : event_pool) cudaEventDestroy(e);
     if (ws) cudaFree(ws);
+    if (cached_rw) {
+        cached_rw->release();
+        delete cached_rw;
+    }
     if (aux_status) cudaFree(aux_status);
     if (solver_handle) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(solver_handle));
     if (scalar_dev) cudaFree(scalar_dev);
     if (scalar_host) cudaFreeHost(scalar_host);
     if (own_stream && stream) cudaStreamDestroy(stream);
+}
+
+RbfgsWork* Context::take_rbfgs(int64_t n, int64_t q) {
+    if (!cached_rw || cached_rw->n != n || cached_rw->q != q) return nullptr;
+    RbfgsWork* w = cached_rw;
+    cached_rw = nullptr;
+    CK(cudaMemsetAsync(w->status, 0, 8 * sizeof(int), stream));
+    CK(cudaMemsetAsync(w->counter, 0, sizeof(unsigned long long), stream));
+    w->batch = false;
+    return w;
+}
+
+void Context::keep_rbfgs(RbfgsWork* w) {
+    if (cached_rw) {
+        cached_rw->release();
+        delete cached_rw;
+    }
+    cached_rw = w;
 }
 
 double* Context::ensure_ws(size_t doubles) {
@@ -622,11 +644,17 @@ void RbfgsWork::alloc(int64_t n_, int64_t q_, bool own) {
     dmalloc(&T, size_t(q) * size_t(q));
     dmalloc(&M, size_t(2 * q) * size_t(2 * q));
     dmalloc(&factor_scratch, 4 * size_t(q) * size_t(q) + size_t(2 * q) + 16);
-    dmalloc(&status, 4);
+    dmalloc(&status, 8);
     dmalloc(&counter, 1);
-    CK(cudaMemset(status, 0, 4 * sizeof(int)));
+    CK(cudaMemset(status, 0, 8 * sizeof(int)));
     CK(cudaMemset(counter, 0, sizeof(unsigned long long)));
-    CK(cudaMallocHost(&s_pinned, size_t(n) * size_t(q) * sizeof(double)));
+}
+
+// pinned staging for host-drawn sketches, allocated on first use: page-locking
+// n·q doubles costs 7-19 ms, which device-sketch runs never need
+double* RbfgsWork::pinned() {
+    if (!s_pinned) CK(cudaMallocHost(&s_pinned, size_t(n) * size_t(q) * sizeof(double)));
+    return s_pinned;
 }
 
 void RbfgsWork::release() {
@@ -636,6 +664,8 @@ void RbfgsWork::release() {
     if (status) cudaFree(status);
     if (counter) cudaFree(counter);
     if (s_pinned) cudaFreeHost(s_pinned);
+    if (lowrank) cudaFree(lowrank);
+    lowrank = nullptr;
     X = Y = U = V = P = Ginv = T = M = factor_scratch = nullptr;
     status = nullptr;
     counter = nullptr;
@@ -844,7 +874,8 @@ void rbfgs_enqueue_iteration(Context& c, Problem& a, RbfgsWork& w, bool device_s
     symupd(c, n, 2 * q, Z, n, Wn, n, w.X, n, 1.0, skip, w.status + 1);         // X += [Z R]·[W' Z]ᵀ
     if (device_sketch) {
         LaunchScope ls(c, "advance_counter");
-        launch_pdl(advance_counter_kernel, dim3(1), dim3(1), 0, c.stream, w.counter, w.status);
+        launch_pdl(w.batch ? advance_batch_kernel : advance_counter_kernel, dim3(1), dim3(1), 0, c.stream, w.counter,
+                   w.status);
         check_launch("advance");
     }
 }

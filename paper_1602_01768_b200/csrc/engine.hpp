@@ -53,6 +53,10 @@ struct Context {
     void* solver_handle = nullptr;  // cusolverDn handle for validate_spd (lazy, reused)
     int* aux_status = nullptr;      // status words of device-pointer entry points
 
+    // run_inverter's bfgs workspace kept between calls (take / keep, driver.cpp)
+    struct RbfgsWork* cached_rw = nullptr;
+    struct RbfgsWork* take_rbfgs(int64_t n, int64_t q);
+    void keep_rbfgs(struct RbfgsWork* w);
     double* ensure_ws(size_t doubles);
     int class_id(const char* name);
     void resolve_profile();
@@ -98,12 +102,18 @@ struct RbfgsWork {
     double *Bs = nullptr, *Bs2 = nullptr, *V2 = nullptr, *M2 = nullptr, *H = nullptr, *Ginv2 = nullptr;
     double *Y = nullptr, *U = nullptr, *P = nullptr, *Ginv = nullptr, *T = nullptr, *M = nullptr, *V = nullptr;
     double* factor_scratch = nullptr;
-    int* status = nullptr;  // [0] Gram not PD (skip), [1] non-finite iterate
+    int* status = nullptr;  // [0] Gram not PD (skip), [1] non-finite iterate, [2] rejected draws,
+                            // [3] accepted steps, [4] batch stopped (8 ints)
     unsigned long long* counter = nullptr;
-    double* s_pinned = nullptr;  // host staging for host-drawn sketches
+    double* s_pinned = nullptr;  // host staging for host-drawn sketches (lazy: pinned())
+    double* lowrank = nullptr;   // n×2q scratch of the rank-2q first checkpoint (lazy)
+    double* pinned();
     void alloc(int64_t n, int64_t q, bool own_x);
     void release();
     bool own_x = true;
+    // run_inverter's batched device-sketch mode: iterations are enqueued back to back
+    // between checkpoints and advance_batch_kernel keeps the accounting (status[3..4])
+    bool batch = false;
 };
 
 // Workspace of one AdaRBFGS factor update (adarbfgs.cpp:12-21):

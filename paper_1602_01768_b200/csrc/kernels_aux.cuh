@@ -444,6 +444,31 @@ __global__ void advance_counter_kernel(unsigned long long* counter, int* status)
     }
 }
 
+// End of an iteration in run_inverter's batched mode (iterations enqueued back to
+// back between two checkpoints, no host round trip): every executed attempt
+// advances the draw counter once, exactly as the eager loop does; an accepted step
+// is counted in status[3]; a rejected Gram (status[0]) or a non-finite iterate
+// (status[1]) stops the batch (status[4], with status[0] left set so every later
+// launch of the batch is a no-op) and the host resumes from the exact iteration —
+// so a batched run draws the same sketches and produces the same iterates as the
+// eager loop.
+__global__ void advance_batch_kernel(unsigned long long* counter, int* status) {
+    griddep_wait();
+    griddep_launch();
+    if (status[4]) return;
+    *counter += 1ull;
+    if (status[0]) {
+        status[2] += 1;
+        status[4] = 1;
+        return;
+    }
+    status[3] += 1;
+    if (status[1]) {
+        status[4] = 1;
+        status[0] = 1;
+    }
+}
+
 // A <- (A + Aᵀ)/2 in place (ProblemMatrix construction, problem_matrix.cpp:9-18).
 // Block (bx, by) with bx <= by owns tile pair (I=bx, J=by) and its mirror.
 __global__ void symmetrize_kernel(double* A, int64_t n) {

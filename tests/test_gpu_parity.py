@@ -293,6 +293,66 @@ def test_device_sketch_statistics_and_convergence(si):
     assert np.array_equal(res.state.x, res.state.x.T)
 
 
+@pytest.mark.parametrize("every,iters", [(1, 12), (7, 30), (10, 10), (4, 9)])
+def test_batched_device_run_matches_eager_loop(si, every, iters, monkeypatch):
+    """run_inverter with device sketches enqueues the iterations between checkpoints
+    back to back (advance_batch_kernel keeps the accounting on the device); the eager
+    per-iteration loop (SI_RUN_EAGER=1) must give the same k, history and iterate."""
+    from paper_1602_01768_b200 import generators as G
+
+    a = G.config1_dense(200, seed=3)
+    prob = si.ProblemMatrix(a, si.Symmetry.spd)
+
+    def run():
+        return si.run_inverter(si.InverterConfig(prob, si.SketchRule.gaussian_device(12), tol=0.0, max_iters=iters,
+                                                 seed=4, track=si.TrackOptions(residual_every_k=every)))
+
+    batched = run()
+    monkeypatch.setenv("SI_RUN_EAGER", "1")
+    eager = run()
+    assert batched.state.k == eager.state.k == iters
+    assert [h.k for h in batched.state.history] == [h.k for h in eager.state.history]
+    assert [h.residual for h in batched.state.history] == [h.residual for h in eager.state.history]
+    assert [h.flops for h in batched.state.history] == [h.flops for h in eager.state.history]
+    assert np.array_equal(batched.state.x, eager.state.x)
+
+
+def test_batched_device_run_tolerance_and_rejections(si, monkeypatch):
+    """Tolerance stop at a checkpoint, and the redraw contract on a numerically
+    rank-one problem — batched and eager agree on
+    the termination, k, the redraw count and the message."""
+    from paper_1602_01768_b200 import generators as G
+
+    a = G.config1_dense(128, seed=5)
+    prob = si.ProblemMatrix(a, si.Symmetry.spd)
+    outs = []
+    for eager in (False, True):
+        if eager:
+            monkeypatch.setenv("SI_RUN_EAGER", "1")
+        outs.append(si.run_inverter(si.InverterConfig(prob, si.SketchRule.gaussian_device(16), tol=0.3,
+                                                      max_iters=5000, seed=6,
+                                                      track=si.TrackOptions(residual_every_k=5))))
+    assert outs[0].termination == outs[1].termination == si.Termination.tol_reached
+    assert outs[0].state.k == outs[1].state.k and outs[0].state.k % 5 == 0
+    assert np.array_equal(outs[0].state.x, outs[1].state.x)
+    monkeypatch.delenv("SI_RUN_EAGER")
+    # numerically rank-one Gram matrices: most sketched Grams fail the PD test (the
+    # Schur pivots after the first are rounding noise), so draws are rejected and
+    # redrawn; both loops must meet the same pivots and reach the same outcome
+    lp = si.ProblemMatrix(np.diag(np.r_[1.0, np.full(39, 1e-300)]), si.Symmetry.spd)
+    res = []
+    for eager in (False, True):
+        if eager:
+            monkeypatch.setenv("SI_RUN_EAGER", "1")
+        res.append(si.run_inverter(si.InverterConfig(lp, si.SketchRule.gaussian_device(4), tol=0.0, max_iters=10,
+                                                     seed=1, max_redraws=3)))
+    assert res[0].termination == res[1].termination
+    assert res[0].state.k == res[1].state.k
+    assert res[0].message == res[1].message
+    assert res[0].state.redraws == res[1].state.redraws > 0
+    assert [h.residual for h in res[0].state.history] == [h.residual for h in res[1].state.history]
+
+
 def test_solver_step_matches_driver(si):
     from paper_1602_01768_b200 import generators as G
 
