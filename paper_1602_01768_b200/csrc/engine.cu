@@ -897,10 +897,14 @@ static void resid_gemm_rect(Context& c, int64_t M, int64_t N, int64_t K, const d
     g.alpha = 1.0;
     g.k_chunk = K;
     g.diag_off = diag_off;
-    const int64_t TM = (M + 127) / 128, TN = (N + 127) / 128;
+    // fewer 128×128 tiles than SMs (small n, e.g. config 1's checkpoints): 64×128 tiles
+    // double the CTAs (the sum of squares cannot be split over K)
+    const bool small = ((M + 127) / 128) * ((N + 127) / 128) < int64_t(c.num_sms);
+    const int64_t BMr = small ? 64 : 128;
+    const int64_t TM = (M + BMr - 1) / BMr, TN = (N + 127) / 128;
     g.ws = c.ensure_ws(size_t(TM * TN));
     const int vec = pick_vec(g);
-    launch_gemm_layout<EPI_RESID>(c, use_w16() ? T128x128W16 : T128x128, false, BKM, vec, g,
+    launch_gemm_layout<EPI_RESID>(c, small ? T64x128 : (use_w16() ? T128x128W16 : T128x128), false, BKM, vec, g,
                                   dim3(unsigned(TM), unsigned(TN), 1), "gemm_resid");
     LaunchScope ls(c, "sum_reduce");
     sum_reduce_kernel<<<1, 1024, 0, c.stream>>>(g.ws, TM * TN, out_dev);
