@@ -1065,8 +1065,18 @@ void lowrank_residual_sq_enqueue(Context& c, Problem& a, int64_t k, const double
 
 // ‖I − (A·L)·Lᵀ‖² (adarbfgs.cpp:112-115): AL = A·L into scratch, then a
 // residual GEMM against Lᵀ (B operand N-major) with no n×n write.
+// X = L·Lᵀ first (K-SYMUPD on a zeroed scratch: upper tiles, mirrored — n³ flops), then
+// the ordinary ‖I − A·X‖ (2n³ dense, 2·nnz·n CSR): 3n³ instead of the 4n³ of
+// (A·L)·Lᵀ; SI_FACTORED_RESID_AL=1 keeps the latter.
 void factored_residual_sq_enqueue(Context& c, Problem& a, const double* L, double* AL, double* out_dev) {
     const int64_t n = a.n;
+    static const bool via_al = env_flag("SI_FACTORED_RESID_AL");
+    if (!via_al) {
+        CK(cudaMemsetAsync(AL, 0, size_t(n) * size_t(n) * sizeof(double), c.stream));
+        symupd(c, n, n, L, n, L, n, AL, n, 1.0, nullptr, nullptr);
+        residual_sq_enqueue(c, a, AL, out_dev, nullptr);
+        return;
+    }
     apply_a(c, a, L, n, n, AL, n, nullptr);
     resid_gemm<false>(c, n, AL, n, L, n, out_dev);
 }
