@@ -52,6 +52,10 @@ Context::~Context() {
     }
     for (auto e : event_pool) cudaEventDestroy(e);
     if (ws) cudaFree(ws);
+    if (ws_side) cudaFree(ws_side);
+    if (side) cudaStreamDestroy(side);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
     if (cached_rw) {
         cached_rw->release();
         delete cached_rw;
@@ -62,6 +66,41 @@ Context::~Context() {
     if (scalar_host) cudaFreeHost(scalar_host);
     if (own_stream && stream) cudaStreamDestroy(stream);
 }
+
+void Context::fork() {
+    if (!side) {
+        CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    }
+    CK(cudaEventRecord(ev_fork, stream));
+    CK(cudaStreamWaitEvent(side, ev_fork, 0));
+}
+
+void Context::join() {
+    CK(cudaEventRecord(ev_join, side));
+    CK(cudaStreamWaitEvent(stream, ev_join, 0));
+}
+
+// Enqueue on the side stream with its own split-K workspace (RAII swap of stream / ws).
+struct SideScope {
+    Context& c;
+    cudaStream_t s0;
+    double* w0;
+    size_t n0;
+    explicit SideScope(Context& ctx) : c(ctx), s0(ctx.stream), w0(ctx.ws), n0(ctx.ws_doubles) {
+        c.stream = c.side;
+        c.ws = c.ws_side;
+        c.ws_doubles = c.ws_side_doubles;
+    }
+    ~SideScope() {
+        c.ws_side = c.ws;
+        c.ws_side_doubles = c.ws_doubles;
+        c.stream = s0;
+        c.ws = w0;
+        c.ws_doubles = n0;
+    }
+};
 
 RbfgsWork* Context::take_rbfgs(int64_t n, int64_t q) {
     if (!cached_rw || cached_rw->n != n || cached_rw->q != q) return nullptr;
@@ -1210,6 +1249,30 @@ static void inv_sqrt(Context& c, const double* Mq, int64_t q, double* R, double*
 // The q×n stage of adarbfgs_update_factor (adarbfgs.cpp:13-19): R = G^{-1/2} and
 // B = T − R·Z with T = S̃ᵀ (coordinate: idx, St null) or T = (S̃ᵀS̃)^{-1/2}·S̃ᵀ
 // (Gaussian S̃ = St, n×q; T written to Tq, q×n).  Floor hits set status[0].
+// the parts of ada_core_enqueue before / after Z is needed (the overlapped schedule)
+static void ada_core_root(Context& c, const double* G, int64_t q, int64_t n, const double* St, double* G2, double* R2,
+                          double* Tq, double* R, double* scratch, int* st) {
+    inv_sqrt(c, G, q, R, scratch, st);  // R = G^{-1/2}
+    if (St) {
+        gemm(c, q, q, n, St, n, true, St, n, true, G2, q, 1.0, 0.0, st);  // S̃ᵀS̃
+        inv_sqrt(c, G2, q, R2, scratch, st);
+        gemm(c, q, n, q, R2, q, false, St, n, false, Tq, q, 1.0, 0.0, st);  // T = R2·S̃ᵀ
+    }
+}
+
+static void ada_core_b(Context& c, int64_t q, const double* Z, int64_t n, const int64_t* idx, const double* St,
+                       const double* Tq, const double* R, double* B, int* st) {
+    if (!St) {
+        gemm(c, q, n, q, R, q, false, Z, q, true, B, q, -1.0, 0.0, st);  // B = −R·Z
+        LaunchScope ls(c, "add_selector");
+        add_selector_kernel<<<grid_for(q, 128), 128, 0, c.stream>>>(B, q, idx, st);  // + T = S̃ᵀ
+        check_launch("add_selector");
+    } else {
+        CK(cudaMemcpyAsync(B, Tq, size_t(q) * size_t(n) * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+        gemm(c, q, n, q, R, q, false, Z, q, true, B, q, -1.0, 1.0, st);  // B = T − R·Z
+    }
+}
+
 void ada_core_enqueue(Context& c, const double* G, int64_t q, const double* Z, int64_t n, const int64_t* idx,
                       const double* St, double* G2, double* R2, double* Tq, double* R, double* B, double* scratch,
                       int* st) {
@@ -1265,10 +1328,25 @@ void ada_enqueue_update(Context& c, Problem& a, AdaWork& w, int mode, uint64_t s
     }
     apply_a(c, a, w.S, n, q, w.AS, n, st);                                 // AS = A·S
     gemm(c, q, q, n, w.S, n, true, w.AS, n, true, w.G, q, 1.0, 0.0, st);   // G = Sᵀ·AS
-    gemm(c, q, n, n, w.AS, n, true, w.L, n, true, w.Z, q, 1.0, 0.0, st);   // Z = (AS)ᵀ·L
-    ada_core_enqueue(c, w.G, q, w.Z, n, w.idx_dev, mode == 0 ? nullptr : w.St, w.G2, w.R2, w.Tm, w.R, w.B,
-                     w.eig_scratch, st);
-    gemm(c, n, q, q, w.S, n, false, w.R, q, true, w.SR, n, 1.0, 0.0, st);  // SR = S·R
+    // Z = (AS)ᵀ·L does not depend on R: it runs on the side stream (every SM but the
+    // one holding the inverse square root) while the q×q stage and SR = S·R run here
+    static const bool overlap = std::getenv("SI_ADA_SERIAL") == nullptr;
+    if (overlap) {
+        c.fork();
+        {
+            SideScope side(c);
+            gemm(c, q, n, n, w.AS, n, true, w.L, n, true, w.Z, q, 1.0, 0.0, st);  // Z = (AS)ᵀ·L
+        }
+        ada_core_root(c, w.G, q, n, mode == 0 ? nullptr : w.St, w.G2, w.R2, w.Tm, w.R, w.eig_scratch, st);
+        gemm(c, n, q, q, w.S, n, false, w.R, q, true, w.SR, n, 1.0, 0.0, st);  // SR = S·R
+        c.join();
+        ada_core_b(c, q, w.Z, n, w.idx_dev, mode == 0 ? nullptr : w.St, w.Tm, w.R, w.B, st);
+    } else {
+        gemm(c, q, n, n, w.AS, n, true, w.L, n, true, w.Z, q, 1.0, 0.0, st);  // Z = (AS)ᵀ·L
+        ada_core_enqueue(c, w.G, q, w.Z, n, w.idx_dev, mode == 0 ? nullptr : w.St, w.G2, w.R2, w.Tm, w.R, w.B,
+                         w.eig_scratch, st);
+        gemm(c, n, q, q, w.S, n, false, w.R, q, true, w.SR, n, 1.0, 0.0, st);  // SR = S·R
+    }
     gemm(c, n, n, q, w.SR, n, false, w.B, q, true, w.L, n, 1.0, 1.0, st, st + 1);  // L += SR·B (+ finite check)
     if (w.pdiag_valid) {  // carry diag(LᵀAL) across the accepted update (App. C3)
         pdiag_update(c, w.B, q, n, mode == 0 ? nullptr : w.Tm, w.idx_dev, st, w.pdiag);

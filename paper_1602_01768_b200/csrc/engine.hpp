@@ -53,6 +53,14 @@ struct Context {
     void* solver_handle = nullptr;  // cusolverDn handle for validate_spd (lazy, reused)
     int* aux_status = nullptr;      // status words of device-pointer entry points
 
+    // second stream + split-K workspace for work that overlaps a single-CTA stage
+    // (AdaRBFGS: Z = (AS)ᵀ·L under the inverse square root); fork / join by events
+    cudaStream_t side = nullptr;
+    double* ws_side = nullptr;
+    size_t ws_side_doubles = 0;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    void fork();  // side stream waits for everything enqueued on `stream` so far
+    void join();  // `stream` waits for everything enqueued on `side` so far
     // run_inverter's bfgs workspace kept between calls (take / keep, driver.cpp)
     struct RbfgsWork* cached_rw = nullptr;
     struct RbfgsWork* take_rbfgs(int64_t n, int64_t q);
