@@ -698,6 +698,11 @@ def run_ours(args, cfg):
         a_np = a_host  # pinned host buffer (config 3) / numpy (config 1)
         x_pinned = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
         x_out = x_pinned.numpy().T  # Fortran-ordered view of a pinned buffer
+        # untimed warm-up call of the same shapes (module loading, graph capture, workspace)
+        warm = si.ProblemMatrix(a_np, si.Symmetry.spd, context=ctx)
+        si.run_inverter(si.InverterConfig(warm, si.SketchRule.gaussian_device(q), tol=0.0, max_iters=2, seed=1,
+                                          track=si.TrackOptions(residual_every_k=2)), out=x_out)
+        del warm
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         prob2 = si.ProblemMatrix(a_np, si.Symmetry.spd, context=ctx)  # H2D of A
@@ -712,10 +717,12 @@ def run_ours(args, cfg):
                "d2h_bytes_per_step": int(16 + 8 * n * n / k_e2e + 8 * 2 / k_e2e),
                "run_iterations": k_e2e,
                "phases_ms": {"problem_upload_validate": 1e3 * (t_prob - t0), "run_inverter": 1e3 * (t1 - t_prob)},
-               "note": "one run_inverter call (si_run_inverter) of the BASELINE run length from a host A: H2D of A, "
-                       "SPD validation, device sketches, status word read back each iteration, the reference's "
-                       "forced residual checkpoints at k=1 (X1 = I + V·Uᵀ: 4n²·2q from the rank-2q form) and k=max (2n^3), X returned to host, all inside "
-                       "the timer; byte counts per step with the A/X transfers amortised over the run"}
+               "note": "one run_inverter call (si_run_inverter) of the BASELINE run length from a host A, after one "
+                       "untimed 2-iteration warm-up call of the same shapes: H2D of A, SPD validation, device "
+                       "sketches with the iterations between checkpoints enqueued back to back, the reference's "
+                       "forced residual checkpoints at k=1 (X1 = I + [Z R]·[W' Z]ᵀ: 4n²·2q from the rank-2q form) "
+                       "and k=max (2n^3), X returned to host, all inside the timer; byte counts per step with the "
+                       "A/X transfers amortised over the run"}
         del prob2
 
     # ---- time to ε: config 1 only, both normalisations ----
