@@ -1192,7 +1192,92 @@ int si_run_adarbfgs(si_context* ctx, si_problem* prob, const si_inverter_config*
         const auto blocks = cols ? si::contiguous_partition(n, q) : std::vector<std::vector<si::Index>>{};
         si::RngStream rng(cfg->seed);
         std::vector<double> p;
-        int st[4];
+        int st[8];
+        // adarbfgs.cpp:179-194: the factored residual checkpoint after iteration k
+        auto checkpoint = [&]() -> bool {
+            const double rel = factored_residual_norm(c, a, w) / base;
+            hist.record(k, rel, flops, seconds);
+            if (rel <= cfg->tol) {
+                finish(SI_TOL_REACHED, "");
+                return true;
+            }
+            if (cfg->time_budget_seconds > 0.0 && seconds > cfg->time_budget_seconds) {
+                finish(SI_MAX_ITERS, "time budget exhausted");
+                return true;
+            }
+            return false;
+        };
+        // Samplers whose draws do not depend on the iterate (q uniform coordinates; device
+        // Gaussian S̃): up to 64 attempts between two checkpoints are drawn on the host, their
+        // index sets uploaded once, and enqueued back to back; ada_advance_batch_kernel stops
+        // the batch at a rejected square root or a non-finite factor, and the host rewinds the
+        // RngStream to just after the rejected draw — the same attempts, draws, k and
+        // iterates as the per-iteration loop (SI_RUN_EAGER=1), without a round trip per
+        // iteration.  The reference's Eq. 8.2 sampler needs the device probabilities before
+        // every draw and stays per-iteration.
+        if ((sk == SI_SKETCH_ADAPTIVE_COLS_UNIFORM || sk == SI_SKETCH_ADAPTIVE_GAUSS_DEVICE) &&
+            std::getenv("SI_RUN_EAGER") == nullptr) {
+            const int mode = sk == SI_SKETCH_ADAPTIVE_COLS_UNIFORM ? 0 : 2;
+            constexpr int64_t CAP = 64;
+            w.batch = true;
+            if (mode == 0) w.ensure_ring(int(CAP));
+            int64_t* const idx0 = w.idx_dev;
+            std::vector<si::RngStream> snaps;
+            int consecutive = 0;
+            const int64_t every = cfg->residual_every_k, kmax = cfg->max_iters;
+            k = 0;
+            while (k < kmax) {
+                const int64_t kc = k == 0 ? 1 : std::min(((k + every) / every) * every, kmax);  // next checkpoint
+                const int64_t nb = std::min(kc - k, CAP);
+                const auto t0 = std::chrono::steady_clock::now();
+                if (mode == 0) {
+                    snaps.clear();
+                    for (int64_t b = 0; b < nb; ++b) {
+                        snaps.push_back(rng);  // the stream before draw b
+                        const auto idx = si::uniform_subset(rng, n, q);
+                        for (int64_t j = 0; j < q; ++j) w.idx_ring_pinned[b * q + j] = idx[size_t(j)];
+                    }
+                    snaps.push_back(rng);
+                    ck(cudaMemcpyAsync(w.idx_ring, w.idx_ring_pinned, size_t(nb) * size_t(q) * sizeof(int64_t),
+                                       cudaMemcpyHostToDevice, c.stream),
+                       "h2d idx");
+                }
+                ck(cudaMemsetAsync(w.status, 0, 8 * sizeof(int), c.stream), "reset");
+                for (int64_t b = 0; b < nb; ++b) {
+                    if (mode == 0) w.idx_dev = w.idx_ring + b * q;
+                    si::ada_enqueue_update(c, a, w, mode, cfg->seed);
+                }
+                w.idx_dev = idx0;
+                ck(cudaMemcpyAsync(st, w.status, 8 * sizeof(int), cudaMemcpyDeviceToHost, c.stream), "status d2h");
+                ck(cudaStreamSynchronize(c.stream), "sync");
+                const auto t1 = std::chrono::steady_clock::now();
+                const int64_t accepted = st[5];
+                k += accepted;
+                result->redraws += st[2];
+                if (cfg->track_wall_time) seconds += std::chrono::duration<double>(t1 - t0).count();
+                if (cfg->track_flops) flops += double(accepted) * flops_adarbfgs(double(n), double(q));
+                if (st[1]) {
+                    finish(SI_TERMINATION_ERROR, "diverged: non-finite factor at iteration " + std::to_string(k));
+                    return;
+                }
+                if (st[4]) {  // attempt `accepted` of this batch was rejected: redraw from just after it
+                    if (mode == 0) rng = snaps[size_t(accepted) + 1];
+                    consecutive = (accepted > 0 ? 0 : consecutive) + 1;
+                    if (consecutive > cfg->max_redraws) {
+                        k += 1;
+                        finish(SI_TERMINATION_ERROR, "sketch rejection limit exceeded for " + describe(sk, q) +
+                                                         " at iteration " + std::to_string(k));
+                        return;
+                    }
+                    continue;
+                }
+                consecutive = 0;
+                if (k == kc && checkpoint()) return;
+            }
+            k = kmax;
+            finish(SI_MAX_ITERS, "");
+            return;
+        }
         for (k = 1; k <= cfg->max_iters; ++k) {
             bool stepped = false;
             const auto t0 = std::chrono::steady_clock::now();  // timer includes probabilities + draws (:143)
@@ -1247,16 +1332,7 @@ int si_run_adarbfgs(si_context* ctx, si_problem* prob, const si_inverter_config*
                 return;
             }
             if (k == 1 || k == cfg->max_iters || k % cfg->residual_every_k == 0) {
-                const double rel = factored_residual_norm(c, a, w) / base;
-                hist.record(k, rel, flops, seconds);
-                if (rel <= cfg->tol) {
-                    finish(SI_TOL_REACHED, "");
-                    return;
-                }
-                if (cfg->time_budget_seconds > 0.0 && seconds > cfg->time_budget_seconds) {
-                    finish(SI_MAX_ITERS, "time budget exhausted");
-                    return;
-                }
+                if (checkpoint()) return;
             }
         }
         k = cfg->max_iters;

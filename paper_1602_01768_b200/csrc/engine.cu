@@ -1135,9 +1135,9 @@ void AdaWork::alloc(int64_t n_, int64_t q_, bool gaussian) {
     dmalloc(&eig_scratch, 6 * size_t(q) * size_t(q) + 8 * size_t(q) + 32);
     dmalloc(&idx_dev, size_t(q));
     dmalloc(&pdiag, size_t(n));
-    dmalloc(&status, 4);
+    dmalloc(&status, 8);
     dmalloc(&counter, 1);
-    CK(cudaMemset(status, 0, 4 * sizeof(int)));
+    CK(cudaMemset(status, 0, 8 * sizeof(int)));
     CK(cudaMemset(counter, 0, sizeof(unsigned long long)));
     CK(cudaMallocHost(&idx_pinned, size_t(q) * sizeof(int64_t)));
     CK(cudaMallocHost(&p_pinned, size_t(n) * sizeof(double)));
@@ -1151,6 +1151,11 @@ void AdaWork::alloc(int64_t n_, int64_t q_, bool gaussian) {
 }
 
 void AdaWork::release() {
+    if (idx_ring) cudaFree(idx_ring);
+    if (idx_ring_pinned) cudaFreeHost(idx_ring_pinned);
+    idx_ring = nullptr;
+    idx_ring_pinned = nullptr;
+    ring_cap = 0;
     for (double* p : {L, S, AS, SR, G, R, Z, B, eig_scratch, pdiag, St, G2, R2, Tm, AL})
         if (p) cudaFree(p);
     if (idx_dev) cudaFree(idx_dev);
@@ -1352,11 +1357,25 @@ void ada_enqueue_update(Context& c, Problem& a, AdaWork& w, int mode, uint64_t s
         pdiag_update(c, w.B, q, n, mode == 0 ? nullptr : w.Tm, w.idx_dev, st, w.pdiag);
         ++w.pdiag_age;
     }
-    if (mode == 2) {
+    if (w.batch) {
+        LaunchScope ls(c, "advance_counter");
+        ada_advance_batch_kernel<<<1, 1, 0, c.stream>>>(mode == 2 ? w.counter : nullptr, w.status);
+        check_launch("advance");
+    } else if (mode == 2) {
         LaunchScope ls(c, "advance_counter");
         advance_counter_kernel<<<1, 1, 0, c.stream>>>(w.counter, w.status);
         check_launch("advance");
     }
+}
+
+// device ring of index sets for run_adarbfgs's batched loop (cap attempts of q indices)
+void AdaWork::ensure_ring(int cap) {
+    if (cap <= ring_cap) return;
+    if (idx_ring) cudaFree(idx_ring);
+    if (idx_ring_pinned) cudaFreeHost(idx_ring_pinned);
+    ring_cap = cap;
+    dmalloc(&idx_ring, size_t(cap) * size_t(q));
+    CK(cudaMallocHost(&idx_ring_pinned, size_t(cap) * size_t(q) * sizeof(int64_t)));
 }
 
 // pdiag_j = l_jᵀ A l_j (diag(LᵀAL), Eq 8.2 numerators), copied to p_pinned.

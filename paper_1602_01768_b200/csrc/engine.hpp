@@ -138,6 +138,13 @@ struct AdaWork {
     double* st_pinned = nullptr;
     double* AL = nullptr;  // n×n scratch for residual / probabilities (lazy)
     double* pdiag = nullptr;  // n: diag(LᵀAL), exact or carried by App. C3
+    // run_adarbfgs's batched loop: index sets of up to ring_cap attempts (device + pinned),
+    // ada_advance_batch_kernel accounting in status[4] (stopped) / status[5] (accepted)
+    bool batch = false;
+    int64_t* idx_ring = nullptr;
+    int64_t* idx_ring_pinned = nullptr;
+    int ring_cap = 0;
+    void ensure_ring(int cap);
     bool pdiag_valid = false;
     int pdiag_age = 0;       // incremental updates since the last exact refresh
     int pdiag_refresh = 64;  // exact A·L refresh period (SI_PDIAG_REFRESH; 1 = every iteration)

@@ -469,6 +469,26 @@ __global__ void advance_batch_kernel(unsigned long long* counter, int* status) {
     }
 }
 
+// run_adarbfgs's batched loop (AdaRBFGS analogue of advance_batch_kernel; status[3] is
+// the Newton–Schulz stop flag there, so the accepted count lives in status[5]): a
+// rejected square root (status[0]) or a non-finite factor (status[1]) stops the batch
+// at that attempt; every executed attempt advances the Philox counter (device-Gaussian
+// S̃) exactly once.
+__global__ void ada_advance_batch_kernel(unsigned long long* counter, int* status) {
+    if (status[4]) return;
+    if (counter) *counter += 1ull;
+    if (status[0]) {
+        status[2] += 1;
+        status[4] = 1;
+        return;
+    }
+    status[5] += 1;
+    if (status[1]) {
+        status[4] = 1;
+        status[0] = 1;
+    }
+}
+
 // A <- (A + Aᵀ)/2 in place (ProblemMatrix construction, problem_matrix.cpp:9-18).
 // Block (bx, by) with bx <= by owns tile pair (I=bx, J=by) and its mirror.
 __global__ void symmetrize_kernel(double* A, int64_t n) {

@@ -353,6 +353,50 @@ def test_batched_device_run_tolerance_and_rejections(si, monkeypatch):
     assert [h.residual for h in res[0].state.history] == [h.residual for h in res[1].state.history]
 
 
+@pytest.mark.parametrize("rule,every,iters", [("uniform", 10, 35), ("uniform", 1, 6), ("gauss_device", 7, 20)])
+def test_batched_adarbfgs_matches_eager_loop(si, rule, every, iters, monkeypatch):
+    """run_adarbfgs enqueues up to 64 attempts between checkpoints (host-drawn uniform
+    index sets uploaded once; device Philox S̃) — same k, history and factor as the
+    per-iteration loop (SI_RUN_EAGER=1)."""
+    rng = O.RngStream(41)
+    n, q = 72, 6
+    a = random_spd(n, rng)
+    prob = si.ProblemMatrix(a, si.Symmetry.spd)
+    srule = si.SketchRule.adaptive_cols_uniform(q) if rule == "uniform" else si.SketchRule.adaptive_gauss_device(q)
+
+    def run():
+        return si.run_adarbfgs(si.AdaConfig(prob, srule, tol=0.0, max_iters=iters, seed=3,
+                                            track=si.TrackOptions(residual_every_k=every)))
+
+    batched = run()
+    monkeypatch.setenv("SI_RUN_EAGER", "1")
+    eager = run()
+    assert batched.state.k == eager.state.k == iters
+    assert [h.k for h in batched.state.history] == [h.k for h in eager.state.history]
+    assert [h.residual for h in batched.state.history] == [h.residual for h in eager.state.history]
+    assert np.array_equal(batched.state.l, eager.state.l)
+
+
+def test_batched_adarbfgs_rejections_match_eager(si, monkeypatch):
+    """A = diag(1, …, 1, 1e-300): every coordinate Gram containing the last index is
+    numerically singular and its inverse square root is rejected (the resample signal),
+    the others are accepted — batched and eager loops meet the same draws, redraws and
+    iterates."""
+    n, q = 40, 4
+    prob = si.ProblemMatrix(np.diag(np.r_[np.ones(n - 1), 1e-300]), si.Symmetry.spd)
+    outs = []
+    for eager in (False, True):
+        if eager:
+            monkeypatch.setenv("SI_RUN_EAGER", "1")
+        outs.append(si.run_adarbfgs(si.AdaConfig(prob, si.SketchRule.adaptive_cols_uniform(q), tol=0.0, max_iters=30,
+                                                 seed=8, max_redraws=100, track=si.TrackOptions(residual_every_k=10))))
+    assert outs[0].termination == outs[1].termination
+    assert outs[0].state.k == outs[1].state.k
+    assert outs[0].state.redraws == outs[1].state.redraws > 0
+    assert [h.residual for h in outs[0].state.history] == [h.residual for h in outs[1].state.history]
+    assert np.array_equal(outs[0].state.l, outs[1].state.l, equal_nan=True)
+
+
 def test_solver_step_matches_driver(si):
     from paper_1602_01768_b200 import generators as G
 
