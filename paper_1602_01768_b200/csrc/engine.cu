@@ -494,7 +494,7 @@ static void symupd(Context& c, int64_t n, int64_t k, const double* V, int64_t ld
     // k-stage against ~88% for "w16", one 16-warp CTA with 32×32 warp tiles);
     // "128x64" two 8-warp CTAs per SM (2.31 vs 2.25 ms at config 3); "k32",
     // "w8k32", "s6": BK = 32 / 6 stages (no difference measured).
-    static const TileCfg cfg = [] {
+    static const TileCfg forced = [] {
         const char* e = std::getenv("SI_SYMUPD_TILE");
         const std::string v = e ? e : "";
         if (v == "128x64") return T128x64;
@@ -502,8 +502,13 @@ static void symupd(Context& c, int64_t n, int64_t k, const double* V, int64_t ld
         if (v == "w8k32") return T128x128W8K32;
         if (v == "s6") return T128x128W16S6;
         if (v == "w16") return T128x128W16;
-        return T128x128;
+        if (v == "128x128") return T128x128;
+        return TileCfg(-1);
     }();
+    // small n (fewer upper 128×128 tiles than SMs, e.g. config 1): 128×64 tiles, two CTAs
+    // per SM, twice the work items
+    const int64_t t128 = (n + 127) / 128;
+    const TileCfg cfg = int(forced) >= 0 ? forced : (t128 * (t128 + 1) / 2 < int64_t(c.num_sms) ? T128x64 : T128x128);
     const int64_t bn = cfg == T128x64 ? 64 : 128, r = 128 / bn;
     const int64_t tn = (n + bn - 1) / bn, full = tn / r, rest = tn % r;
     const int64_t work = r * full * (full + 1) / 2 + rest * (full + 1);  // TileOps::sym_work_count
