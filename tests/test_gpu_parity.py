@@ -293,18 +293,20 @@ def test_device_sketch_statistics_and_convergence(si):
     assert np.array_equal(res.state.x, res.state.x.T)
 
 
-@pytest.mark.parametrize("every,iters", [(1, 12), (7, 30), (10, 10), (4, 9)])
-def test_batched_device_run_matches_eager_loop(si, every, iters, monkeypatch):
+@pytest.mark.parametrize("n,q,every,iters", [(200, 12, 1, 12), (200, 12, 7, 30), (200, 12, 10, 10), (200, 12, 4, 9),
+                                             (301, 100, 3, 7), (333, 130, 5, 11)])
+def test_batched_device_run_matches_eager_loop(si, n, q, every, iters, monkeypatch):
     """run_inverter with device sketches enqueues the iterations between checkpoints
     back to back (advance_batch_kernel keeps the accounting on the device); the eager
-    per-iteration loop (SI_RUN_EAGER=1) must give the same k, history and iterate."""
+    per-iteration loop (SI_RUN_EAGER=1) must give the same k, history and iterate
+    (odd n, a padded K-FACTOR block at q = 100, the GEMM-recursion inverse at q = 130)."""
     from paper_1602_01768_b200 import generators as G
 
-    a = G.config1_dense(200, seed=3)
+    a = G.config1_dense(n, seed=3)
     prob = si.ProblemMatrix(a, si.Symmetry.spd)
 
     def run():
-        return si.run_inverter(si.InverterConfig(prob, si.SketchRule.gaussian_device(12), tol=0.0, max_iters=iters,
+        return si.run_inverter(si.InverterConfig(prob, si.SketchRule.gaussian_device(q), tol=0.0, max_iters=iters,
                                                  seed=4, track=si.TrackOptions(residual_every_k=every)))
 
     batched = run()
