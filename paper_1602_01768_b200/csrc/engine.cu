@@ -407,7 +407,13 @@ void gemm(Context& c, int64_t M, int64_t N, int64_t K, const double* A, int64_t 
         const char* e = std::getenv("SI_SHORTK_TILE");
         return (e && std::string(e) == "w16") ? 0 : 1;
     }();
-    const TileCfg t = (K <= 128 && N > 64 && M > 64 && shortk_mode == 1)
+    // the largest K that takes the two-CTA 128×64 tiles: 256 measured 2.5% faster than the
+    // 16-warp 128×128 tiles on config 4's L update (137.0 vs 140.6 ms); SI_SHORTK_MAX overrides
+    static const int64_t shortk_max = [] {
+        const char* e = std::getenv("SI_SHORTK_MAX");
+        return e ? std::atoll(e) : 256;
+    }();
+    const TileCfg t = (K <= shortk_max && N > 64 && M > 64 && shortk_mode == 1)
                           ? T128x64
                           : ((K <= 512 && N > 64 && M > 64) ? T128x128W16 : pick_tile(N, M));
     const int BM = t == T64x128 ? 64 : 128;
