@@ -1193,7 +1193,9 @@ static void ns_fused(Context& c, const double* Mq, int64_t q, double* R, int* st
         attr = true;
     }
     LaunchScope ls(c, "ns_fused");
-    ns_fused_kernel<QP><<<1, 512, smem, c.stream>>>(Mq, q, int(q), R, status, 1e-14 * std::sqrt(double(q)), 60);
+    static const int accelerate = env_flag("SI_NS_NEWTON_ONLY") ? 0 : 1;
+    ns_fused_kernel<QP><<<1, 512, smem, c.stream>>>(Mq, q, int(q), R, status, 1e-14 * std::sqrt(double(q)), 60,
+                                                     accelerate);
     check_launch("ns_fused");
 }
 
