@@ -124,10 +124,11 @@ void require(bool cond, const char* msg) {
 }
 
 // ProblemMatrix::validate_spd semantics (problem_matrix.cpp:28-41)
-void validate_spd(si_problem* prob) {
+void validate_spd(si_problem* prob, double* scratch_nn = nullptr) {
     if (prob->p->symmetry != SI_SPD)
         throw std::invalid_argument("ProblemMatrix: operation requires an spd-flagged matrix");
-    if (!si::problem_validate_spd(*prob->p)) throw std::runtime_error("ProblemMatrix: spd flag set but Cholesky failed");
+    if (!si::problem_validate_spd(*prob->p, scratch_nn))
+        throw std::runtime_error("ProblemMatrix: spd flag set but Cholesky failed");
 }
 
 double host_frobenius_asym(const double* x, int64_t n, double* norm_out) {
@@ -475,12 +476,12 @@ static double flops_named(int u, double n, double q) {  // flops.cpp:22-46
 }
 
 // validate_update (qn_updates.cpp:79-92): psb needs a symmetric A, bfgs / aip / dfp an SPD one
-static void validate_update(int u, si_problem* prob) {
+static void validate_update(int u, si_problem* prob, double* scratch_nn = nullptr) {
     if (u == SI_UPDATE_PSB) {
         if (prob->p->symmetry == SI_GENERAL) throw ConfigError("psb requires a symmetric matrix");
         return;
     }
-    validate_spd(prob);
+    validate_spd(prob, scratch_nn);
 }
 
 // ---------------------------------------------------------- run_inverter ---
@@ -525,14 +526,9 @@ static void run_inverter_impl(si_context* ctx, si_problem* prob, const si_invert
     require(cfg->max_iters >= 1, "run_inverter: max_iters must be >= 1");
     require(cfg->max_redraws >= 0, "run_inverter: max_redraws must be >= 0");
     require(cfg->residual_every_k >= 1, "run_inverter: residual_every_k must be >= 1");
-    validate_update(upd, prob);
+    if (upd == SI_UPDATE_PSB) validate_update(upd, prob);  // (spd checks below, on the workspace)
     const bool symmetric_iterates = upd != SI_UPDATE_AIP;  // simi.cpp:77-81
     const bool tracks_inverse = upd == SI_UPDATE_DFP;
-    if (cfg->x0_host && symmetric_iterates) {
-        double nrm = 0.0;
-        const double asym = host_frobenius_asym(cfg->x0_host, n, &nrm);
-        if (asym > 1e-10 * std::max(1.0, nrm)) throw ConfigError("run_inverter: this method requires a symmetric x0");
-    }
 
     // the bfgs workspace stays in the context between calls when X is at most a quarter of
     // device memory: re-running a problem of the same shape allocates and frees nothing
@@ -565,6 +561,15 @@ static void run_inverter_impl(si_context* ctx, si_problem* prob, const si_invert
         }
     } rel{c, wp, cacheable};
     trace.mark("alloc");
+    // validate_config (simi.cpp:185-213): the Cholesky of A runs in the iterate's buffer,
+    // which is initialised right after
+    validate_update(upd, prob, w.X);
+    if (cfg->x0_host && symmetric_iterates) {
+        double nrm = 0.0;
+        const double asym = host_frobenius_asym(cfg->x0_host, n, &nrm);
+        if (asym > 1e-10 * std::max(1.0, nrm)) throw ConfigError("run_inverter: this method requires a symmetric x0");
+    }
+    trace.mark("validate (Cholesky)");
     if (cfg->x0_host)
         ck(cudaMemcpyAsync(w.X, cfg->x0_host, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyHostToDevice,
                            c.stream),
@@ -604,6 +609,7 @@ static void run_inverter_impl(si_context* ctx, si_problem* prob, const si_invert
     HistoryWriter hist{history, history_cap, 0, cfg};
     double flops = 0.0, seconds = 0.0;
     int64_t k = 0;
+    bool x_early = false;  // X download issued before the last checkpoint (overlaps its 2n³ residual)
     auto finish = [&](int term, const std::string& msg) {
         result->termination = term;
         result->k = k;
@@ -612,9 +618,12 @@ static void run_inverter_impl(si_context* ctx, si_problem* prob, const si_invert
         result->history_count = hist.count;
         result->max_symmetry_drift = 0.0;  // symmetric updates write X (and H) exactly symmetric (mirrored tiles)
         set_message(result, msg);
-        if (x_out)
+        if (x_early) {  // the final X is already on its way on the side stream
+            c.join();
+        } else if (x_out) {
             ck(cudaMemcpyAsync(x_out, w.X, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, c.stream),
                "d2h x");
+        }
         if (x_inv_out && tracks_inverse)
             ck(cudaMemcpyAsync(x_inv_out, w.H, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyDeviceToHost,
                                c.stream),
@@ -757,6 +766,13 @@ static void run_inverter_impl(si_context* ctx, si_problem* prob, const si_invert
                 continue;
             }
             consecutive = 0;
+            if (k == kmax && x_out) {  // X is final: download it on the side stream under the last residual
+                c.fork();
+                ck(cudaMemcpyAsync(x_out, w.X, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyDeviceToHost,
+                                   c.side),
+                   "d2h x");
+                x_early = true;
+            }
             if (checkpoint()) return;
         }
         k = kmax;

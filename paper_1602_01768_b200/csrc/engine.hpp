@@ -162,7 +162,7 @@ struct AdaWork {
 Context* context_create(int device, cudaStream_t external, bool on_stream = false);
 void problem_upload_dense(Problem& p, const double* host, bool device_src);
 void problem_upload_csr(Problem& p, const int64_t* rowptr, const int32_t* colind, const double* val);
-bool problem_validate_spd(Problem& p);  // Cholesky-based (cuSOLVER potrf on a scratch copy)
+bool problem_validate_spd(Problem& p, double* scratch_nn = nullptr);  // Cholesky-based (cuSOLVER potrf on a scratch copy)
 void problem_download_dense(Problem& p, double* host);
 
 // generic dense product C = alpha·op(A)·op(B) + beta·C with leading dimensions
