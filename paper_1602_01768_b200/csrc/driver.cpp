@@ -1143,7 +1143,8 @@ int si_run_adarbfgs(si_context* ctx, si_problem* prob, const si_inverter_config*
             throw ConfigError("run_adarbfgs: rule must be adaptive");
         require(cfg->tol >= 0.0, "run_adarbfgs: tol must be >= 0");
         require(cfg->max_iters >= 1, "run_adarbfgs: max_iters must be >= 1");
-        validate_spd(prob);
+        if (prob->p->symmetry != SI_SPD)
+            throw std::invalid_argument("ProblemMatrix: operation requires an spd-flagged matrix");
         const bool cols = sk == SI_SKETCH_ADAPTIVE_COLS;
         const bool gauss = sk == SI_SKETCH_ADAPTIVE_GAUSS || sk == SI_SKETCH_ADAPTIVE_GAUSS_DEVICE;
 
@@ -1153,6 +1154,7 @@ int si_run_adarbfgs(si_context* ctx, si_problem* prob, const si_inverter_config*
             ~Rel() { w.release(); }
         } rel{w};
         w.alloc(n, q, gauss);
+        validate_spd(prob, w.L);  // adarbfgs.cpp:97; the Cholesky runs in L's buffer, initialised next
         if (cfg->x0_host)
             ck(cudaMemcpyAsync(w.L, cfg->x0_host, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyHostToDevice,
                                c.stream),
