@@ -4,6 +4,7 @@
 #include <cusolverDn.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -205,15 +206,22 @@ static bool tma_disabled() {
     return v == 1;
 }
 
+// Kernel attributes (dynamic shared memory limit) are per device: set once per device
+// the first time a context on that device launches the kernel.
+struct DeviceOnce {
+    std::atomic<uint64_t> mask{0};
+    bool first(int device) {
+        const uint64_t bit = 1ull << (device & 63);
+        return !(mask.fetch_or(bit) & bit);
+    }
+};
+
 template <int BM, int BN, int BK, int WM, int WN, int ST, bool AK, bool BKM, int VEC, int EPI>
 static void launch_gemm_cfg(Context& c, const GemmArgs& a, dim3 grid, const char* name) {
     using SM = GemmSmem<BM, BN, BK, WM, WN, ST, AK, BKM>;
     auto kern = gemm_f64_kernel<BM, BN, BK, WM, WN, ST, AK, BKM, VEC, EPI>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SM::BYTES)));
-        attr_set = true;
-    }
+    static DeviceOnce once;
+    if (once.first(c.device)) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SM::BYTES)));
     LaunchScope ls(c, name);
     kern<<<grid, WM * WN * 32, SM::BYTES, c.stream>>>(a);
     check_launch(name);
@@ -277,14 +285,14 @@ static void launch_tma_cfg(Context& c, const GemmArgs& a, dim3 grid, const char*
     const bool persist = EPI == EPI_SYMUPD || a.K <= 1024;
     auto kern_p = gemm_tma_persistent_kernel<BM, BN, BK, WM, WN, ST, AK, BKM, EPI>;
     auto kern_g = gemm_tma_kernel<BM, BN, BK, WM, WN, ST, AK, BKM, EPI>;
-    static bool attr_set = false;
-    static int per_sm = 1;
-    if (!attr_set) {
+    static DeviceOnce once;
+    static int per_sm = 1;  // same for every B200
+    if (once.first(c.device)) {
         CK(cudaFuncSetAttribute(kern_p, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SM::TMA_BYTES)));
         CK(cudaFuncSetAttribute(kern_g, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SM::TMA_BYTES)));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern_p, WM * WN * 32, SM::TMA_BYTES));
-        per_sm = std::max(per_sm, 1);
-        attr_set = true;
+        int v = 1;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern_p, WM * WN * 32, SM::TMA_BYTES));
+        per_sm = std::max(v, 1);
     }
     const int64_t work = int64_t(grid.x) * grid.y * grid.z;
     CUtensorMap ta, tb;
@@ -751,11 +759,10 @@ static void spd_inverse_blocked(Context& c, const double* P, int64_t ldp, int64_
                                 int* status) {
     constexpr size_t smem =
         sizeof(double) * (size_t(QP) * (QP + 4) + size_t(QP) * (PB + 4) + size_t(PB) * (QP + 4) + PB * (PB + 1));
-    static bool attr = false;
-    if (!attr) {
+    static DeviceOnce once;
+    if (once.first(c.device)) {
         CK(cudaFuncSetAttribute(spd_inverse_blocked_kernel<QP, PB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(smem)));
-        attr = true;
     }
     LaunchScope ls(c, "spd_inverse");
     spd_inverse_blocked_kernel<QP, PB><<<1, 512, smem, c.stream>>>(P, ldp, int(q), ginv, ldo, status);
@@ -856,11 +863,10 @@ static void launch_gram_fused(Context& c, const double* P, int64_t ldp, int64_t 
                               int* status) {
     constexpr int LF = 16, NT = 512;
     using SM = core::GramSmem<QP, LF>;
-    static bool attr = false;
-    if (!attr) {
+    static DeviceOnce once;
+    if (once.first(c.device)) {
         CK(cudaFuncSetAttribute(rbfgs_gram_kernel<QP, LF, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(SM::BYTES)));
-        attr = true;
     }
     LaunchScope ls(c, "gram_inverse");
     launch_pdl(rbfgs_gram_kernel<QP, LF, NT>, dim3(1), dim3(NT), SM::BYTES, c.stream, P, ldp, int(q), Ginv, Ghat,
@@ -1190,10 +1196,9 @@ void AdaWork::release() {
 template <int QP>
 static void ns_fused(Context& c, const double* Mq, int64_t q, double* R, int* status) {
     const size_t smem = size_t(5) * QP * (QP + 4) * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
+    static DeviceOnce once;
+    if (once.first(c.device)) {
         CK(cudaFuncSetAttribute(ns_fused_kernel<QP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        attr = true;
     }
     LaunchScope ls(c, "ns_fused");
     static const int accelerate = env_flag("SI_NS_NEWTON_ONLY") ? 0 : 1;
@@ -1254,10 +1259,9 @@ static void inv_sqrt(Context& c, const double* Mq, int64_t q, double* R, double*
     double* Qm = scratch + q * q;
     double* work = scratch + 2 * q * q;
     const size_t smem = (2 * size_t(q) * size_t(q) + 4 * size_t(q)) * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
+    static DeviceOnce once;
+    if (once.first(c.device)) {
         CK(cudaFuncSetAttribute(jacobi_isqrt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr = true;
     }
     {
         LaunchScope ls(c, "jacobi_isqrt");
