@@ -187,7 +187,7 @@ static int grid_for(int64_t work, int threads, int max_blocks = 148 * 16) {
 }
 
 // --------------------------------------------------------------- GEMM ------
-enum TileCfg { T128x128 = 0, T128x64 = 1, T128x32 = 2, T128x128W16 = 3, T64x128 = 4, T128x128K32 = 5, T128x128W8K32 = 6, T128x128W16S6 = 7 };
+enum TileCfg { T128x128 = 0, T128x64 = 1, T128x32 = 2, T128x128W16 = 3, T64x128 = 4, T128x128K32 = 5, T128x128W8K32 = 6, T128x128W16S6 = 7, T64x64 = 8 };
 
 // development switches: SI_WARPS16=1 selects 16 consumer warps for 128×128
 // tiles; SI_NO_TMA=1 forces the cp.async mainloop.
@@ -332,6 +332,10 @@ static void launch_gemm_tile(Context& c, TileCfg t, const GemmArgs& a, dim3 grid
                 if constexpr (EPI == EPI_SYMUPD) launch_tma_cfg<128, 128, 16, 4, 4, 6, AK, BKM, EPI>(c, a, grid, name);
                 break;
             case T64x128: launch_tma_cfg<64, 128, 16, 2, 4, 6, AK, BKM, EPI>(c, a, grid, name); break;
+            case T64x64:
+                if constexpr (EPI == EPI_STORE || EPI == EPI_PARTIAL)
+                    launch_tma_cfg<64, 64, 16, 2, 2, 6, AK, BKM, EPI>(c, a, grid, name);
+                break;
         }
         return;
     }
@@ -344,6 +348,10 @@ static void launch_gemm_tile(Context& c, TileCfg t, const GemmArgs& a, dim3 grid
         case T128x128W8K32:
         case T128x128W16S6: launch_gemm_cfg<128, 128, 16, 4, 4, 4, AK, BKM, VEC, EPI>(c, a, grid, name); break;
         case T64x128: launch_gemm_cfg<64, 128, 16, 2, 4, 4, AK, BKM, VEC, EPI>(c, a, grid, name); break;
+        case T64x64:
+            if constexpr (EPI == EPI_STORE || EPI == EPI_PARTIAL)
+                launch_gemm_cfg<64, 64, 16, 2, 2, 4, AK, BKM, VEC, EPI>(c, a, grid, name);
+            break;
     }
 }
 
@@ -382,6 +390,7 @@ static int pick_vec(const GemmArgs& a) {
 }
 
 static TileCfg pick_tile(int64_t N, int64_t M = 1 << 30) {
+    if (M <= 64 && N <= 64) return T64x64;  // small Grams (q ≤ 64: G = SᵀAS, [G | H']): no 3/4-empty tiles
     if (M <= 64 && N > 64) return T64x128;  // q×n products (Z = (AS)ᵀL, Grams): no half-empty tiles
     if (N <= 32) return T128x32;
     if (N <= 64) return T128x64;
@@ -424,8 +433,9 @@ void gemm(Context& c, int64_t M, int64_t N, int64_t K, const double* A, int64_t 
     const TileCfg t = (K <= shortk_max && N > 64 && M > 64 && shortk_mode == 1)
                           ? T128x64
                           : ((K <= 512 && N > 64 && M > 64) ? T128x128W16 : pick_tile(N, M));
-    const int BM = t == T64x128 ? 64 : 128;
-    const int BN = (t == T128x128 || t == T128x128W16 || t == T64x128) ? 128 : (t == T128x64 ? 64 : 32), BKT = 16;
+    const int BM = (t == T64x128 || t == T64x64) ? 64 : 128;
+    const int BN = (t == T128x128 || t == T128x128W16 || t == T64x128) ? 128 : ((t == T128x64 || t == T64x64) ? 64 : 32),
+              BKT = 16;
     const int64_t tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN, tiles = tm * tn;
     const int per_sm = (t == T128x128 || t == T128x128W16 || t == T64x128) ? 1 : 2;
     const int64_t slots = int64_t(c.num_sms) * per_sm;
