@@ -1148,12 +1148,31 @@ int si_run_adarbfgs(si_context* ctx, si_problem* prob, const si_inverter_config*
         const bool cols = sk == SI_SKETCH_ADAPTIVE_COLS;
         const bool gauss = sk == SI_SKETCH_ADAPTIVE_GAUSS || sk == SI_SKETCH_ADAPTIVE_GAUSS_DEVICE;
 
-        si::AdaWork w;
+        // the workspace stays in the context between calls when L is at most a quarter of
+        // device memory (as run_inverter's)
+        size_t mem_free = 0, mem_total = 0;
+        ck(cudaMemGetInfo(&mem_free, &mem_total), "meminfo");
+        const bool cacheable = double(n) * double(n) * 8.0 <= 0.25 * double(mem_total);
+        si::AdaWork* wp = cacheable ? c.take_ada(n, q, gauss) : nullptr;
+        if (!wp) {
+            wp = new si::AdaWork;
+            wp->alloc(n, q, gauss);
+        }
+        si::AdaWork& w = *wp;
+        w.q = q;
         struct Rel {
-            si::AdaWork& w;
-            ~Rel() { w.release(); }
-        } rel{w};
-        w.alloc(n, q, gauss);
+            si::Context& c;
+            si::AdaWork* w;
+            bool cacheable, gauss;
+            ~Rel() {
+                if (cacheable) {
+                    c.keep_ada(w, gauss);
+                    return;
+                }
+                w->release();
+                delete w;
+            }
+        } rel{c, wp, cacheable, gauss};
         validate_spd(prob, w.L);  // adarbfgs.cpp:97; the Cholesky runs in L's buffer, initialised next
         if (cfg->x0_host)
             ck(cudaMemcpyAsync(w.L, cfg->x0_host, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyHostToDevice,

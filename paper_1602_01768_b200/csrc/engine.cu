@@ -61,6 +61,10 @@ Context::~Context() {
         cached_rw->release();
         delete cached_rw;
     }
+    if (cached_aw) {
+        cached_aw->release();
+        delete cached_aw;
+    }
     if (aux_status) cudaFree(aux_status);
     if (solver_handle) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(solver_handle));
     if (scalar_dev) cudaFree(scalar_dev);
@@ -119,6 +123,28 @@ void Context::keep_rbfgs(RbfgsWork* w) {
         delete cached_rw;
     }
     cached_rw = w;
+}
+
+AdaWork* Context::take_ada(int64_t n, int64_t q, bool gaussian) {
+    if (!cached_aw || cached_aw->n != n || cached_aw->q != q || cached_aw_gauss != gaussian) return nullptr;
+    AdaWork* w = cached_aw;
+    cached_aw = nullptr;
+    CK(cudaMemsetAsync(w->status, 0, 8 * sizeof(int), stream));
+    CK(cudaMemsetAsync(w->counter, 0, sizeof(unsigned long long), stream));
+    w->batch = false;
+    w->pdiag_valid = false;
+    w->pdiag_age = 0;
+    w->pdiag_refresh = 64;
+    return w;
+}
+
+void Context::keep_ada(AdaWork* w, bool gaussian) {
+    if (cached_aw) {
+        cached_aw->release();
+        delete cached_aw;
+    }
+    cached_aw = w;
+    cached_aw_gauss = gaussian;
 }
 
 double* Context::ensure_ws(size_t doubles) {

@@ -65,6 +65,11 @@ struct Context {
     struct RbfgsWork* cached_rw = nullptr;
     struct RbfgsWork* take_rbfgs(int64_t n, int64_t q);
     void keep_rbfgs(struct RbfgsWork* w);
+    // run_adarbfgs's workspace, same policy
+    struct AdaWork* cached_aw = nullptr;
+    bool cached_aw_gauss = false;
+    struct AdaWork* take_ada(int64_t n, int64_t q, bool gaussian);
+    void keep_ada(struct AdaWork* w, bool gaussian);
     double* ensure_ws(size_t doubles);
     int class_id(const char* name);
     void resolve_profile();
