@@ -440,6 +440,159 @@ __global__ void __launch_bounds__(WM* WN * 32, ((EPI == EPI_SYMUPD || EPI == EPI
     }
 }
 
+// ------------------------------------------------------ C-panel TMA path --
+// Short-K panel updates C ← beta·C + A·B (the AdaRBFGS factor update L += SR·B, K = q):
+// with only a few k-stages per tile the C-tile loads dominate (ncu: long-scoreboard
+// stalls, DMMA half idle), so the producer also fetches every work item's C tile by TMA
+// into one of two shared-memory buffers, one work item ahead, and the accumulators are
+// seeded from shared memory.  Persistent, one CTA per SM; EPI_STORE with beta·C seeding.
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool A_KMAJOR, bool B_KMAJOR>
+struct CPanelSmem {
+    using SM = GemmSmem<BM, BN, BK, WM, WN, STAGES, A_KMAJOR, B_KMAJOR>;
+    static constexpr int LDCS = BM + 4;                       // C buffer pitch (column-major tile)
+    static constexpr size_t RING = size_t(STAGES) * SM::STAGE_ELEMS * sizeof(double);
+    static constexpr size_t CBUF = size_t(BN) * LDCS * sizeof(double);
+    static constexpr size_t BAR_OFFSET = (RING + 2 * CBUF + 127) / 128 * 128;
+    static constexpr size_t BYTES = BAR_OFFSET + (2 * STAGES + 4) * sizeof(uint64_t);
+};
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool A_KMAJOR, bool B_KMAJOR>
+__global__ void __launch_bounds__(WM* WN * 32, 1)
+    gemm_tma_cpanel_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                           const __grid_constant__ CUtensorMap tmC, GemmArgs p) {
+    using SM = GemmSmem<BM, BN, BK, WM, WN, STAGES, A_KMAJOR, B_KMAJOR>;
+    using CP = CPanelSmem<BM, BN, BK, WM, WN, STAGES, A_KMAJOR, B_KMAJOR>;
+    using T = TileOps<BM, BN, BK, WM, WN, A_KMAJOR, B_KMAJOR, EPI_STORE>;
+    constexpr int NW = WM * WN;
+    constexpr uint32_t STAGE_BYTES = SM::STAGE_ELEMS * sizeof(double);
+    constexpr uint32_t C_BYTES = uint32_t(BN) * CP::LDCS * sizeof(double);
+
+    extern __shared__ __align__(128) double smem[];
+    double* cbuf = reinterpret_cast<double*>(reinterpret_cast<char*>(smem) + CP::RING);
+    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(smem) + CP::BAR_OFFSET);
+    uint64_t* empty = full + STAGES;
+    uint64_t* cfull = empty + STAGES;  // [2]
+    uint64_t* cempty = cfull + 2;      // [2]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool producer = tid == 0;
+    if (producer) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NW);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&cfull[s], 1);
+            mbar_init(&cempty[s], NW);
+        }
+        mbar_fence_init();
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+        tma_prefetch_desc(&tmC);
+    }
+    griddep_wait();
+    griddep_launch();
+    if (p.skip && *p.skip) return;
+    const int64_t W = T::work_count(p);
+    const int nk = (int)((p.K + BK - 1) / BK);  // unsplit
+
+    // C tile of this CTA's i-th work item into buffer i & 1
+    int64_t cw = blockIdx.x;
+    int ci = 0;
+    auto issue_c = [&]() {
+        const int b = ci & 1;
+        if (ci >= 2) mbar_wait(&cempty[b], (uint32_t)(((ci >> 1) - 1) & 1));
+        const typename T::Work wk = T::decode(cw, p);
+        mbar_arrive_expect_tx(&cfull[b], C_BYTES);
+        tma_load_2d(cbuf + size_t(b) * BN * CP::LDCS, &tmC, (int32_t)(wk.tile_m * BM), (int32_t)(wk.tile_n * BN),
+                    &cfull[b]);
+        ++ci;
+        cw += gridDim.x;
+    };
+    int64_t pw = blockIdx.x;
+    int pk = 0, ps = 0, pround = 0, pissued = 0;
+    typename T::Work pwork{};
+    if (producer && pw < W) pwork = T::decode(pw, p);
+    auto issue_next = [&]() {
+        if (pk == 0) {  // entering work item pw: its successor's C tile goes out now (one item ahead)
+            if (cw < W && cw <= pw + gridDim.x) issue_c();
+        }
+        const int s = ps;
+        if (pround > 0) mbar_wait(&empty[s], (uint32_t)((pround - 1) & 1));
+        double* As = smem + s * SM::STAGE_ELEMS;
+        double* Bs = As + SM::A_ELEMS;
+        const int32_t kc = (int32_t)((int64_t)pk * BK);
+        const int32_t mc = (int32_t)(pwork.tile_m * BM), nc = (int32_t)(pwork.tile_n * BN);
+        mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+        if constexpr (A_KMAJOR)
+            tma_load_2d(As, &tmA, kc, mc, &full[s]);
+        else
+            tma_load_2d(As, &tmA, mc, kc, &full[s]);
+        if constexpr (B_KMAJOR)
+            tma_load_2d(Bs, &tmB, kc, nc, &full[s]);
+        else
+            tma_load_2d(Bs, &tmB, nc, kc, &full[s]);
+        ++pissued;
+        if (++ps == STAGES) {
+            ps = 0;
+            ++pround;
+        }
+        if (++pk == nk) {
+            pk = 0;
+            pw += gridDim.x;
+            if (pw < W) pwork = T::decode(pw, p);
+        }
+    };
+    auto pump = [&](int cg) {
+        while (pw < W && pissued < cg + STAGES - 1) issue_next();
+    };
+    __syncthreads();
+    if (producer) {
+        if (cw < W) issue_c();  // the first item's C tile, then the stages (which send the second's)
+        pump(0);
+    }
+
+    T t;
+    int cg = 0, cs = 0, item = 0;
+    uint32_t cphase = 0;
+    for (int64_t w = blockIdx.x; w < W; w += gridDim.x, ++item) {
+        t.setup_work(w, p, warp, lane);
+        double acc[T::MI][T::NI][4];
+        {  // seed from the C tile in shared memory (beta·C)
+            const int b = item & 1;
+            mbar_wait(&cfull[b], (uint32_t)((item >> 1) & 1));
+            const double* Cs = cbuf + size_t(b) * BN * CP::LDCS;
+#pragma unroll
+            for (int i = 0; i < T::MI; ++i)
+#pragma unroll
+                for (int j = 0; j < T::NI; ++j)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int lr = t.wm0 + i * 16 + t.g + ((e >> 1) << 3), lc = t.wn0 + j * 8 + 2 * t.t4 + (e & 1);
+                        acc[i][j][e] = p.beta * Cs[lc * CP::LDCS + lr];
+                    }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&cempty[b]);
+        }
+        for (int kt = 0; kt < nk; ++kt, ++cg) {
+            if (warp == 0) {
+                if (producer) pump(cg);
+                __syncwarp();
+            }
+            const int s = cs;
+            mbar_wait(&full[s], cphase);
+            if (++cs == STAGES) {
+                cs = 0;
+                cphase ^= 1u;
+            }
+            const double* As = smem + s * SM::STAGE_ELEMS;
+            t.compute_stage(acc, As, As + SM::A_ELEMS);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+        t.epilogue(acc, p, tid, NW * 32, [] {});  // c_in_acc: store-only
+    }
+}
+
 // One CTA per work item (grid = tiles × splits): the long-K products (Y = A·S,
 // W = X·Y), whose pipeline fill is amortised over ≥ 100 k-stages.
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool A_KMAJOR, bool B_KMAJOR, int EPI>
