@@ -357,7 +357,7 @@ static void launch_cpanel_cfg(Context& c, const GemmArgs& a, int64_t work) {
         make_tmap(&tb, a.B, a.K, a.N, a.ldb, BK + 4, BN);
     else
         make_tmap(&tb, a.B, a.N, a.K, a.ldb, BN + 4, BK);
-    make_tmap(&tc, a.C, a.M, a.N, a.ldc, BM + 4, BN);
+    make_tmap(&tc, a.Csrc ? a.Csrc : a.C, a.M, a.N, a.ldc, BM + 4, BN);  // the seed (beta·Csrc or beta·C)
     LaunchScope ls(c, "gemm_cpanel");
     launch_pdl(kern, dim3(unsigned(std::min<int64_t>(work, int64_t(c.num_sms)))), dim3(WM * WN * 32), CP::BYTES, c.stream,
                ta, tb, tc, a);
@@ -534,8 +534,8 @@ void gemm(Context& c, int64_t M, int64_t N, int64_t K, const double* A, int64_t 
             const char* e = std::getenv("SI_CPANEL_KMAX");
             return e ? std::atoll(e) : 256;
         }();
-        if (cpanel && t == T128x64 && a.c_in_acc && !Csrc && K <= cpanel_kmax && tma_ok(a) && a.ldc % 2 == 0 &&
-            aligned_ptr(C, 16)) {
+        if (cpanel && t == T128x64 && a.c_in_acc && K <= cpanel_kmax && tma_ok(a) && a.ldc % 2 == 0 &&
+            aligned_ptr(C, 16) && aligned_ptr(Csrc ? Csrc : C, 16)) {
             if (!a_kmajor && b_kmajor)
                 launch_cpanel_cfg<false, true>(c, a, tm * tn);
             else if (!a_kmajor && !b_kmajor)
