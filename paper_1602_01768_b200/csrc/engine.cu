@@ -969,6 +969,7 @@ void rbfgs_gram_enqueue(Context& c, const double* P, int64_t ldp, int64_t q, dou
         return;
     }
     spd_inverse(c, P, ldp, q, Ginv, scratch, status);
+    if (!Ghat) return;
     LaunchScope ls(c, "ghat");
     ghat_kernel<<<grid_for(q * q, 256), 256, 0, c.stream>>>(P, ldp, int(q), Ghat, status);
     check_launch("ghat");
@@ -1006,9 +1007,30 @@ void rbfgs_enqueue_iteration(Context& c, Problem& a, RbfgsWork& w, bool device_s
         check_launch("philox");
     }
     apply_a(c, a, S, n, q, w.Y, n, skip);                                       // Y = A·S
-    gemm(c, n, q, n, w.X, n, false, w.Y, n, true, Wn, n, -1.0, 0.0, skip);      // W' = −X·Y
-    gemm(c, q, 2 * q, n, w.Y, n, true, S, n, true, w.P, q, 1.0, 0.0, skip);     // P = Yᵀ·[S W'] = [G | −H]
-    rbfgs_gram_enqueue(c, w.P, q, q, w.Ginv, w.T, w.factor_scratch, w.status);  // G⁻¹ + PD test, Ĝ = G + H
+    // G = SᵀAS needs only Y: its one-CTA inverse (K-FACTOR) runs on the side stream while
+    // W' = −X·Y occupies the other SMs; H' = YᵀW' and Ĝ follow the join (config 3: 6.267 ->
+    // 6.233 ms).  Small n keeps the serial order — one [G | H'] product, then K-FACTOR with Ĝ —
+    // because the split product and the extra launches cost more than K-FACTOR there
+    // (config 1: 0.064 vs 0.068 ms); SI_RBFGS_SERIAL=1 forces it.
+    static const bool serial = std::getenv("SI_RBFGS_SERIAL") != nullptr;
+    if (!serial && n >= 8192) {
+        gemm(c, q, q, n, w.Y, n, true, S, n, true, w.P, q, 1.0, 0.0, skip);               // G = Yᵀ·S
+        c.fork();
+        {
+            SideScope side(c);
+            rbfgs_gram_enqueue(c, w.P, q, q, w.Ginv, nullptr, w.factor_scratch, w.status);  // G⁻¹ + PD test
+        }
+        gemm(c, n, q, n, w.X, n, false, w.Y, n, true, Wn, n, -1.0, 0.0, skip);            // W' = −X·Y
+        gemm(c, q, q, n, w.Y, n, true, Wn, n, true, w.P + q * q, q, 1.0, 0.0, skip);      // H' = Yᵀ·W'
+        c.join();
+        LaunchScope ls(c, "ghat");
+        ghat_kernel<<<grid_for(q * q, 256), 256, 0, c.stream>>>(w.P, q, int(q), w.T, w.status);  // Ĝ = G − H'
+        check_launch("ghat");
+    } else {
+        gemm(c, n, q, n, w.X, n, false, w.Y, n, true, Wn, n, -1.0, 0.0, skip);      // W' = −X·Y
+        gemm(c, q, 2 * q, n, w.Y, n, true, S, n, true, w.P, q, 1.0, 0.0, skip);     // P = Yᵀ·[S W'] = [G | −H]
+        rbfgs_gram_enqueue(c, w.P, q, q, w.Ginv, w.T, w.factor_scratch, w.status);  // G⁻¹ + PD test, Ĝ = G + H
+    }
     gemm(c, n, q, q, S, n, false, w.Ginv, q, true, Z, n, 1.0, 0.0, skip);       // Z = S·G⁻¹
     gemm(c, n, q, q, Z, n, false, w.T, q, true, R, n, 1.0, 1.0, skip, nullptr, Wn);  // R = Z·Ĝ + W'
     symupd(c, n, 2 * q, Z, n, Wn, n, w.X, n, 1.0, skip, w.status + 1);         // X += [Z R]·[W' Z]ᵀ
