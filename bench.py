@@ -684,7 +684,8 @@ def run_ours(args, cfg):
     roofline.update({"peak_source": "measured FP64 DMMA peak, profiles/r01_fp64_peak.txt (MEASURED_PEAKS.json has "
                                     "no FP64 entry; tcgen05 has no f64 kind)",
                      "traffic_source": "profiles/r01_traffic.json (ncu --set full, bytes per launch)",
-                     "kernel_share_of_step": shares})
+                     "kernel_share_of_step": shares,
+                     "kernel_share_note": "per-launch CUDA events in an eager profiling pass (shares of the summed kernel times); K-FACTOR (gram_inverse) runs on a second stream under W' = -X·Y, so its time overlaps gemm_splitk"})
     secondary = roof("gemm_symupd") if "gemm_symupd" in prof and dom_name != "gemm_symupd" else None
     hbm_lines = {}
     if "sketch_philox" in prof and prof["sketch_philox"][0] > 0:

@@ -55,6 +55,7 @@ Context::~Context() {
     if (ws) cudaFree(ws);
     if (ws_side) cudaFree(ws_side);
     if (side) cudaStreamDestroy(side);
+    if (side_hi) cudaStreamDestroy(side_hi);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (cached_rw) {
@@ -72,18 +73,21 @@ Context::~Context() {
     if (own_stream && stream) cudaStreamDestroy(stream);
 }
 
-void Context::fork() {
+void Context::fork(bool high) {
     if (!side) {
         CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+        int lo = 0, hi = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CK(cudaStreamCreateWithPriority(&side_hi, cudaStreamNonBlocking, hi));
         CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
     }
     CK(cudaEventRecord(ev_fork, stream));
-    CK(cudaStreamWaitEvent(side, ev_fork, 0));
+    CK(cudaStreamWaitEvent(high ? side_hi : side, ev_fork, 0));
 }
 
-void Context::join() {
-    CK(cudaEventRecord(ev_join, side));
+void Context::join(bool high) {
+    CK(cudaEventRecord(ev_join, high ? side_hi : side));
     CK(cudaStreamWaitEvent(stream, ev_join, 0));
 }
 
@@ -93,8 +97,8 @@ struct SideScope {
     cudaStream_t s0;
     double* w0;
     size_t n0;
-    explicit SideScope(Context& ctx) : c(ctx), s0(ctx.stream), w0(ctx.ws), n0(ctx.ws_doubles) {
-        c.stream = c.side;
+    explicit SideScope(Context& ctx, bool high = false) : c(ctx), s0(ctx.stream), w0(ctx.ws), n0(ctx.ws_doubles) {
+        c.stream = high ? c.side_hi : c.side;
         c.ws = c.ws_side;
         c.ws_doubles = c.ws_side_doubles;
     }
@@ -1015,14 +1019,14 @@ void rbfgs_enqueue_iteration(Context& c, Problem& a, RbfgsWork& w, bool device_s
     static const bool serial = std::getenv("SI_RBFGS_SERIAL") != nullptr;
     if (!serial && n >= 8192) {
         gemm(c, q, q, n, w.Y, n, true, S, n, true, w.P, q, 1.0, 0.0, skip);               // G = Yᵀ·S
-        c.fork();
+        c.fork(true);  // high priority: K-FACTOR takes the first free SM instead of queueing behind W'
         {
-            SideScope side(c);
+            SideScope side(c, true);
             rbfgs_gram_enqueue(c, w.P, q, q, w.Ginv, nullptr, w.factor_scratch, w.status);  // G⁻¹ + PD test
         }
         gemm(c, n, q, n, w.X, n, false, w.Y, n, true, Wn, n, -1.0, 0.0, skip);            // W' = −X·Y
         gemm(c, q, q, n, w.Y, n, true, Wn, n, true, w.P + q * q, q, 1.0, 0.0, skip);      // H' = Yᵀ·W'
-        c.join();
+        c.join(true);
         LaunchScope ls(c, "ghat");
         ghat_kernel<<<grid_for(q * q, 256), 256, 0, c.stream>>>(w.P, q, int(q), w.T, w.status);  // Ĝ = G − H'
         check_launch("ghat");

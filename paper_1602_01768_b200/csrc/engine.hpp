@@ -55,12 +55,12 @@ struct Context {
 
     // second stream + split-K workspace for work that overlaps a single-CTA stage
     // (AdaRBFGS: Z = (AS)ᵀ·L under the inverse square root); fork / join by events
-    cudaStream_t side = nullptr;
+    cudaStream_t side = nullptr, side_hi = nullptr;  // side_hi: highest stream priority
     double* ws_side = nullptr;
     size_t ws_side_doubles = 0;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    void fork();  // side stream waits for everything enqueued on `stream` so far
-    void join();  // `stream` waits for everything enqueued on `side` so far
+    void fork(bool high = false);  // side (or side_hi) waits for everything enqueued on `stream` so far
+    void join(bool high = false);  // `stream` waits for everything enqueued on side (side_hi) so far
     // run_inverter's bfgs workspace kept between calls (take / keep, driver.cpp)
     struct RbfgsWork* cached_rw = nullptr;
     struct RbfgsWork* take_rbfgs(int64_t n, int64_t q);
