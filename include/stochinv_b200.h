@@ -120,6 +120,10 @@ int si_context_create(int device, si_context** out);
 int si_context_create_on_stream(int device, void* cuda_stream, si_context** out);
 int si_context_destroy(si_context* ctx);
 int si_context_synchronize(si_context* ctx);
+/* si_run_inverter / si_run_adarbfgs keep their last workspace (the n×n iterate and panels,
+ * when it is at most a quarter of device memory) in the context so a rerun of the same
+ * shape allocates nothing; this frees it now (it is also freed by si_context_destroy). */
+int si_context_release_workspaces(si_context* ctx);
 /* Kernel launches issued by this context so far (the bench's gpu_launches). */
 int64_t si_context_launch_count(si_context* ctx);
 /* Per-kernel-class device timing (CUDA events around each launch). */

@@ -45,6 +45,7 @@ _SIGS = {
     "si_context_create_on_stream": (ci, [ci, vp, C.POINTER(vp)]),
     "si_context_destroy": (ci, [vp]),
     "si_context_synchronize": (ci, [vp]),
+    "si_context_release_workspaces": (ci, [vp]),
     "si_context_launch_count": (i64, [vp]),
     "si_context_set_profiling": (ci, [vp, ci]),
     "si_context_profile": (ci, [vp, vp, pi64, pd, ci]),

@@ -88,6 +88,10 @@ class Context:
     def launch_count(self) -> int:
         return int(L.load().si_context_launch_count(self._h))
 
+    def release_workspaces(self):
+        """Free the run_inverter / run_adarbfgs workspace the context keeps between calls."""
+        _check(L.load().si_context_release_workspaces(self._h))
+
     def set_profiling(self, on: bool):
         _check(L.load().si_context_set_profiling(self._h, 1 if on else 0))
 

@@ -240,6 +240,14 @@ int si_context_synchronize(si_context* ctx) {
     return guard([&] { ck(cudaStreamSynchronize(ctx->c->stream), "sync"); });
 }
 
+int si_context_release_workspaces(si_context* ctx) {
+    return guard([&] {
+        ck(cudaStreamSynchronize(ctx->c->stream), "sync");
+        ctx->c->keep_rbfgs(nullptr);
+        ctx->c->keep_ada(nullptr, false);
+    });
+}
+
 int64_t si_context_launch_count(si_context* ctx) { return ctx->c->launches; }
 
 int si_context_set_profiling(si_context* ctx, int enabled) {

@@ -399,6 +399,30 @@ def test_batched_adarbfgs_rejections_match_eager(si, monkeypatch):
     assert np.array_equal(outs[0].state.l, outs[1].state.l, equal_nan=True)
 
 
+def test_workspace_reuse_and_release(si):
+    """run_inverter / run_adarbfgs keep their workspace in the context: a rerun of the same
+    shape gives the same result, and releasing the cache changes nothing but memory."""
+    from paper_1602_01768_b200 import generators as G
+
+    a = G.config1_dense(160, seed=4)
+    ctx = si.Context(0)
+    prob = si.ProblemMatrix(a, si.Symmetry.spd, context=ctx)
+    cfg = si.InverterConfig(prob, si.SketchRule.gaussian_device(8), tol=0.0, max_iters=9, seed=2,
+                            track=si.TrackOptions(residual_every_k=4))
+    r1 = si.run_inverter(cfg)
+    r2 = si.run_inverter(cfg)
+    ctx.release_workspaces()
+    r3 = si.run_inverter(cfg)
+    assert np.array_equal(r1.state.x, r2.state.x) and np.array_equal(r1.state.x, r3.state.x)
+    acfg = si.AdaConfig(prob, si.SketchRule.adaptive_cols_uniform(8), tol=0.0, max_iters=7, seed=3,
+                        track=si.TrackOptions(residual_every_k=3))
+    l1 = si.run_adarbfgs(acfg).state.l
+    l2 = si.run_adarbfgs(acfg).state.l
+    ctx.release_workspaces()
+    l3 = si.run_adarbfgs(acfg).state.l
+    assert np.array_equal(l1, l2) and np.array_equal(l1, l3)
+
+
 def test_solver_step_matches_driver(si):
     from paper_1602_01768_b200 import generators as G
 
