@@ -292,6 +292,7 @@ def run_sharded(args, cfg):
     torch.cuda.empty_cache()
     for _ in range(args.warmup):
         sh.step()
+    sh.finalize()
     torch.cuda.synchronize()
     dist.barrier()
     launches0 = ctx.launch_count()
@@ -302,6 +303,7 @@ def run_sharded(args, cfg):
         e0.record(stream)
         for _ in range(args.steps):
             sh.step()
+        sh.finalize()  # the last PD status (deferred check): a redraw would be inside the timer
         e1.record(stream)
         torch.cuda.synchronize()
         dist.barrier()
@@ -423,6 +425,8 @@ def run_extra_sharded(args, cfg):
         e0.record(stream)
         for _ in range(args.steps):
             drv.step()
+        if hasattr(drv, "finalize"):
+            drv.finalize()
         e1.record(stream)
         torch.cuda.synchronize()
         dist.barrier()

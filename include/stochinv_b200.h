@@ -263,6 +263,12 @@ int si_sketch_gaussian_device(si_context* ctx, double* S, int64_t n, int64_t q, 
 /* From P = [SᵀY | YᵀW] (q×2q, ld ldp) build M = [[G⁻¹ + G⁻¹HG⁻¹, −G⁻¹], [−G⁻¹, 0]] (2q×2q, ld 2q).
  * scratch: 6q² + 2q + 16 doubles.  Returns SI_ERR_RESAMPLE when G = SᵀAS is not positive definite. */
 int si_rbfgs_core_device(si_context* ctx, const double* P, int64_t ldp, int64_t q, double* M, double* scratch);
+/* The same core, fully asynchronous: the PD status goes to status_dev (one device int, 0 = G
+ * positive definite) and M is written as 0 on rejection, so an update enqueued behind it leaves
+ * X unchanged.  The caller reads status_dev later (deferred check: the driver enqueues the
+ * update and the next iteration before it knows whether this draw is accepted). */
+int si_rbfgs_core_device_async(si_context* ctx, const double* P, int64_t ldp, int64_t q, double* M,
+                               double* scratch, int* status_dev);
 /* Σ_{i<m, j<n} (δ(r0+i, j) − (X_rows·A)(i, j))², X_rows = rows [r0, r0+m) of X (ld ldx), dense A. */
 int si_residual_rows_device(si_context* ctx, si_problem* prob, int64_t m, int64_t r0, const double* x_rows,
                             int64_t ldx, double* out_host);

@@ -99,6 +99,7 @@ _SIGS = {
     "si_symupd_device": (ci, [vp, i64, i64, vp, i64, vp, i64, vp, i64]),
     "si_sketch_gaussian_device": (ci, [vp, vp, i64, i64, i64, u64, u64]),
     "si_rbfgs_core_device": (ci, [vp, vp, i64, i64, vp, vp]),
+    "si_rbfgs_core_device_async": (ci, [vp, vp, i64, i64, vp, vp, vp]),
     "si_gather_columns_device": (ci, [vp, vp, i64, i64, vp, i64, vp]),
     "si_ada_core_device": (ci, [vp, vp, i64, vp, i64, vp, vp, vp, vp, vp, vp]),
     "si_pdiag_update_device": (ci, [vp, vp, i64, i64, vp, vp, vp]),

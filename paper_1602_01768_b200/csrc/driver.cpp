@@ -1632,6 +1632,20 @@ int si_rbfgs_core_device(si_context* ctx, const double* P, int64_t ldp, int64_t 
     });
 }
 
+int si_rbfgs_core_device_async(si_context* ctx, const double* P, int64_t ldp, int64_t q, double* M,
+                               double* scratch, int* status_dev) {
+    return guard([&] {
+        auto& c = *ctx->c;
+        require(q >= 1 && ldp >= q && status_dev != nullptr, "rbfgs_core_async: bad shape");
+        ck(cudaMemsetAsync(status_dev, 0, sizeof(int), c.stream), "memset");
+        double* ginv = scratch;
+        double* t = scratch + q * q;
+        double* fs = scratch + 2 * q * q;
+        si::rbfgs_core_enqueue(c, P, ldp, q, ginv, t, M, fs, status_dev);
+        si::zero_on_status(c, M, 4 * q * q, status_dev);
+    });
+}
+
 int si_gather_columns_device(si_context* ctx, const double* L, int64_t rows, int64_t ldl, const int64_t* idx_dev,
                              int64_t q, double* out) {
     return guard([&] {

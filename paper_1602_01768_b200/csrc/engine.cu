@@ -941,6 +941,12 @@ void rbfgs_core_enqueue(Context& c, const double* P, int64_t ldp, int64_t q, dou
     gemm(c, q, q, q, Ginv, q, false, T, q, true, M, 2 * q, 1.0, 1.0, status);          // M11 = Ginv + Ginv·T
 }
 
+void zero_on_status(Context& c, double* M, int64_t count, const int* status) {
+    LaunchScope ls(c, "zero_on_status");
+    zero_on_status_kernel<<<grid_for(count, 256), 256, 0, c.stream>>>(M, count, status);
+    check_launch("zero_on_status");
+}
+
 // K-FACTOR for the single-GPU RBFGS iteration: G⁻¹ (with the gram_llt PD test) and
 // Ĝ = G − H' from P = [G | H'] (H' = YᵀW' = −H).
 template <int QP>

@@ -367,6 +367,15 @@ __global__ void core_layout_kernel(const double* __restrict__ ginv, int q, doubl
     }
 }
 
+// A rejected core (status[0] != 0) leaves M = 0, so the update that follows it,
+// X += V·Uᵀ with V = U·M, adds exact zeros: the sharded driver enqueues the update
+// before it reads the PD status (deferred check, dist.py SymmetricShardedRBFGS).
+__global__ void zero_on_status_kernel(double* __restrict__ M, int64_t count, const int* status) {
+    if (!*status) return;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x)
+        M[i] = 0.0;
+}
+
 // ---------------------------------------------------------------- K-RNG --
 struct Philox {
     __device__ static void round(uint32_t& c0, uint32_t& c1, uint32_t& c2, uint32_t& c3, uint32_t k0, uint32_t k1) {

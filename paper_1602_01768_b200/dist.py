@@ -25,6 +25,7 @@ the per-rank FLOPs are 8n²q/P against 6n²q on one GPU (documented in DESIGN.md
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import torch
@@ -68,6 +69,11 @@ class CudaPanelOps:
 
     def core(self, P, ldp, q, M, scratch):
         _check(self.lib.si_rbfgs_core_device(self.ctx.handle, self._p(P), ldp, q, self._p(M), self._p(scratch)))
+
+    def core_async(self, P, ldp, q, M, scratch, status):
+        """core() without the host read: status (device int32) = 0 when G is PD, M = 0 otherwise."""
+        _check(self.lib.si_rbfgs_core_device_async(self.ctx.handle, self._p(P), ldp, q, self._p(M),
+                                                   self._p(scratch), self._p(status)))
 
     def gather_columns(self, Lp, rows, ldl, idx, q, out):
         _check(self.lib.si_gather_columns_device(self.ctx.handle, self._p(Lp), rows, ldl, self._p(idx), q,
@@ -469,10 +475,22 @@ class SymmetricShardedRBFGS:
     """
 
     def __init__(self, ops, n: int, q: int, a_rows_of_chunk, *, seed: int = 0, prob: ProblemMatrix | None = None,
-                 max_redraws: int = 100, device=None):
+                 max_redraws: int = 100, device=None, deferred: bool | None = None):
         """a_rows_of_chunk(r0, r1) -> A[r0:r1, :] as a flat column-major (r1−r0)×n tensor or a
-        CsrRows panel (sparse A, configs 4/5)."""
+        CsrRows panel (sparse A, configs 4/5).
+
+        deferred (default: when ops has core_async and SI_SHARD_SYNC_PD is unset): the PD test
+        of SᵀAS is read one attempt late.  A rejected core leaves M = 0, so its update adds
+        exact zeros and the attempt behind it is the redraw the synchronous loop would make;
+        the draws, the accepted updates and the redraw accounting are those of the synchronous
+        loop once finalize() has run (gather_x / residual call it)."""
         self.ops, self.n, self.q, self.seed, self.prob, self.max_redraws = ops, n, q, seed, prob, max_redraws
+        if deferred is None:
+            deferred = hasattr(ops, "core_async") and not os.environ.get("SI_SHARD_SYNC_PD") and max_redraws >= 1
+        self.deferred = deferred
+        self._pending = []        # (slot, event) of attempts whose PD status is not read yet
+        self._consecutive = 0     # rejections since the last accepted attempt
+        self._attempts = 0
         self.world = dist.get_world_size() if dist.is_initialized() else 1
         self.rank = dist.get_rank() if dist.is_initialized() else 0
         self.bounds = chunk_bounds(n, self.world)
@@ -500,6 +518,10 @@ class SymmetricShardedRBFGS:
         self.Uc = torch.empty(mc * 2 * q, **f)
         self.scratch = torch.empty(6 * q * q + 2 * q + 16, **f)
         self.gather = torch.empty(2 * P * mc * q, **f)
+        self._ring = 64
+        self._status = torch.zeros(self._ring, dtype=torch.int32, device=dev)
+        self._status_host = torch.zeros(self._ring, dtype=torch.int32,
+                                        pin_memory=self._status.is_cuda)
         self.set_identity()
 
     def _m(self, c):
@@ -536,53 +558,104 @@ class SymmetricShardedRBFGS:
                 self._rows(self.Y, q, r0, r1).copy_(g[p, j, :, : r1 - r0])
 
     def step(self):
-        n, q, ops = self.n, self.q, self.ops
-        S, W = self.U[: n * q], self.U[n * q:]
+        if not self.deferred:
+            return self._step_sync()
+        if self._consecutive:  # inside a rejection run: no speculation past the redraw limit
+            self._settle(keep=0)
+        self._attempt()
+        self._settle(keep=1)
+
+    def finalize(self):
+        """Read every outstanding PD status (redrawing for the rejected ones)."""
+        if self.deferred:
+            self._settle(keep=0)
+
+    def _attempt(self):
+        slot = self._attempts % self._ring
+        self._attempts += 1
+        st = self._status[slot:slot + 1]
+        self._one_attempt(lambda P, M: self.ops.core_async(P, self.q, self.q, M, self.scratch, st))
+        self._status_host[slot:slot + 1].copy_(st, non_blocking=True)
+        ev = None
+        if st.is_cuda:
+            ev = torch.cuda.Event()
+            ev.record()
+        self._pending.append((slot, ev))
+
+    def _settle(self, keep: int):
+        """Read the oldest statuses until at most `keep` attempts are outstanding.  A rejected
+        attempt was a no-op (M = 0) and the attempt behind it is its redraw, so each rejection
+        owes one more attempt; inside a rejection run the attempts are read one at a time."""
+        owed = 0
+        while self._pending and (len(self._pending) > keep or owed or self._consecutive):
+            slot, ev = self._pending.pop(0)
+            if ev is not None:
+                ev.synchronize()
+            if int(self._status_host[slot]) == 0:
+                self._consecutive = 0
+            else:
+                self.redraws += 1
+                self._consecutive += 1
+                if self._consecutive > self.max_redraws:
+                    self._consecutive = 0
+                    raise GramRankDeficientError("sketch rejection limit exceeded")
+                owed += 1
+            if not self._pending and owed:
+                owed -= 1
+                self._attempt()
+
+    def _step_sync(self):
         for _ in range(self.max_redraws + 1):
-            ops.sketch(S, n, q, n, self.seed, self.draw)
-            self.draw += 1
-            # Y rows of the owned chunks, then the full Y
-            for c in self.chunks:
-                r0 = self.bounds[c]
-                apply_rows(ops, self.A[c], n, S, n, q, self.Y[r0:], n)
-            self._all_gather_y()
-            # W = X·Y from the upper trapezoids: X_c·Y[r0:] and the strictly-upper part transposed
-            W.zero_()
-            for c in self.chunks:
-                r0, m = self.bounds[c], self._m(c)
-                r1 = r0 + m
-                ops.gemm(m, q, n - r0, self.X[c], m, False, self.Y[r0:], n, True, W[r0:], n, 1.0, 1.0)
-                if r1 < n:
-                    ops.gemm(n - r1, q, m, self.X[c][m * m:], m, True, self.Y[r0:], n, True, W[r1:], n, 1.0, 1.0)
-            if self.world > 1:
-                dist.all_reduce(W)
-            # P = Yᵀ·[S W] over the owned rows, all-reduced
-            self.Pp.zero_()
-            for c in self.chunks:
-                r0, m = self.bounds[c], self._m(c)
-                ops.gemm(q, 2 * q, m, self.Y[r0:], n, True, self.U[r0:], n, True, self.Pp, q, 1.0, 1.0)
-            self.P.copy_(self.Pp)
-            if self.world > 1:
-                dist.all_reduce(self.P)
             try:
-                ops.core(self.P, q, q, self.M, self.scratch)
+                self._one_attempt(lambda P, M: self.ops.core(P, self.q, self.q, M, self.scratch))
             except GramRankDeficientError:
                 self.redraws += 1
                 continue
-            for c in self.chunks:
-                r0, m = self.bounds[c], self._m(c)
-                r1 = r0 + m
-                # V_c = U[R_c]·M (m×2q); the diagonal block by K-SYMUPD, the rest by one GEMM
-                ops.gemm(m, 2 * q, 2 * q, self.U[r0:], n, False, self.M, 2 * q, True, self.Vc, m)
-                ops.symupd(m, 2 * q, self.Vc, m, self.U[r0:], n, self.X[c], m)
-                if r1 < n:
-                    ops.gemm(m, n - r1, 2 * q, self.Vc, m, False, self.U[r1:], n, False, self.X[c][m * m:], m,
-                             1.0, 1.0)
             return
         raise GramRankDeficientError("sketch rejection limit exceeded")
 
+    def _one_attempt(self, core):
+        n, q, ops = self.n, self.q, self.ops
+        S, W = self.U[: n * q], self.U[n * q:]
+        ops.sketch(S, n, q, n, self.seed, self.draw)
+        self.draw += 1
+        # Y rows of the owned chunks, then the full Y
+        for c in self.chunks:
+            r0 = self.bounds[c]
+            apply_rows(ops, self.A[c], n, S, n, q, self.Y[r0:], n)
+        self._all_gather_y()
+        # W = X·Y from the upper trapezoids: X_c·Y[r0:] and the strictly-upper part transposed
+        W.zero_()
+        for c in self.chunks:
+            r0, m = self.bounds[c], self._m(c)
+            r1 = r0 + m
+            ops.gemm(m, q, n - r0, self.X[c], m, False, self.Y[r0:], n, True, W[r0:], n, 1.0, 1.0)
+            if r1 < n:
+                ops.gemm(n - r1, q, m, self.X[c][m * m:], m, True, self.Y[r0:], n, True, W[r1:], n, 1.0, 1.0)
+        if self.world > 1:
+            dist.all_reduce(W)
+        # P = Yᵀ·[S W] over the owned rows, all-reduced
+        self.Pp.zero_()
+        for c in self.chunks:
+            r0, m = self.bounds[c], self._m(c)
+            ops.gemm(q, 2 * q, m, self.Y[r0:], n, True, self.U[r0:], n, True, self.Pp, q, 1.0, 1.0)
+        self.P.copy_(self.Pp)
+        if self.world > 1:
+            dist.all_reduce(self.P)
+        core(self.P, self.M)
+        for c in self.chunks:
+            r0, m = self.bounds[c], self._m(c)
+            r1 = r0 + m
+            # V_c = U[R_c]·M (m×2q); the diagonal block by K-SYMUPD, the rest by one GEMM
+            ops.gemm(m, 2 * q, 2 * q, self.U[r0:], n, False, self.M, 2 * q, True, self.Vc, m)
+            ops.symupd(m, 2 * q, self.Vc, m, self.U[r0:], n, self.X[c], m)
+            if r1 < n:
+                ops.gemm(m, n - r1, 2 * q, self.Vc, m, False, self.U[r1:], n, False, self.X[c][m * m:], m,
+                         1.0, 1.0)
+
     def gather_x(self) -> torch.Tensor:
         """Full X (n×n column-major, flat) on every rank (tests / export / residual)."""
+        self.finalize()
         n = self.n
         full = torch.zeros(n * n, dtype=torch.float64, device=self.X[self.chunks[0]].device)
         fv = full.view(n, n)  # fv[j, i] = X(i, j)

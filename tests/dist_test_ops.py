@@ -54,6 +54,16 @@ class NumpyPanelOps:
         m[q:, :q] = -gi
         _view(M, 2 * q, 2 * q, 2 * q)[...] = m
 
+    def core_async(self, P, ldp, q, M, scratch, status):
+        from paper_1602_01768_b200.api import GramRankDeficientError
+
+        try:
+            self.core(P, ldp, q, M, scratch)
+            status[0] = 0
+        except GramRankDeficientError:
+            _view(M, 2 * q, 2 * q, 2 * q)[...] = 0.0
+            status[0] = 1
+
     def residual_rows_sq(self, prob, m, r0, X, ldx):
         x = _view(X, m, self.a.shape[0], ldx)
         r = x @ self.a

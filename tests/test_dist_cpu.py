@@ -240,3 +240,54 @@ def test_chunk_balance():
             w += m * (n - b[c])  # trapezoid area
         work.append(w)
     assert max(work) / min(work) < 1.001
+
+
+def _rejecting_ops(a, reject_calls):
+    """NumpyPanelOps whose core rejects on the given call indices (forced non-PD Grams)."""
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from dist_test_ops import NumpyPanelOps
+    from paper_1602_01768_b200.api import GramRankDeficientError
+
+    class Ops(NumpyPanelOps):
+        calls = 0
+
+        def core(self, P, ldp, q, M, scratch):
+            i = Ops.calls
+            Ops.calls += 1
+            if i in reject_calls:
+                raise GramRankDeficientError("forced")
+            super().core(P, ldp, q, M, scratch)
+
+    Ops.calls = 0
+    return Ops(a)
+
+
+@pytest.mark.parametrize("reject,steps,max_redraws", [((), 7, 3), ((1,), 7, 3), ((0, 3, 4, 5, 9), 7, 3),
+                                                      ((2, 3, 4), 6, 2), ((6,), 7, 1)])
+def test_symmetric_deferred_pd_check_matches_sync(reject, steps, max_redraws):
+    """The deferred PD read (update enqueued before the status is known, M = 0 on rejection)
+    gives the synchronous loop's X, draw count and redraw count, also at the redraw limit."""
+    from paper_1602_01768_b200.api import GramRankDeficientError
+    from paper_1602_01768_b200.dist import SymmetricShardedRBFGS
+
+    n, q, seed = 21, 3, 7
+    a = _problem(n)
+
+    def run(deferred):
+        s = SymmetricShardedRBFGS(_rejecting_ops(a, set(reject)), n, q, lambda r0, r1: _rows(a, r0, r1, False),
+                                  seed=seed, max_redraws=max_redraws, deferred=deferred)
+        err = None
+        try:
+            for _ in range(steps):
+                s.step()
+            s.finalize()
+        except GramRankDeficientError as e:
+            err = e
+        return s.gather_x().numpy().copy(), s.draw, s.redraws, err is not None
+
+    xs, ds, rs, es = run(False)
+    xd, dd, rd, ed = run(True)
+    assert (dd, rd, ed) == (ds, rs, es)
+    assert np.array_equal(xd, xs)

@@ -162,3 +162,42 @@ def test_sharded_drivers_with_csr_panels_world1(env):
     lf = ada.gather_l().cpu().numpy().reshape((n, n), order="F")
     ref = O.run_adarbfgs(a, 16, rule=O.ADA_COLS, tol=0.0, max_iters=12, every_k=12, seed=2).x
     assert np.linalg.norm(lf - ref) / np.linalg.norm(ref) <= 1e-9
+
+
+@pytest.mark.parametrize("max_redraws", [100, 1])
+def test_symmetric_deferred_pd_check_gpu(env, max_redraws):
+    """si_rbfgs_core_device_async + the deferred status read against the synchronous loop
+    on an indefinite A (44 of 96 eigenvalues negative), so that many Gaussian draws give a non-PD
+    SᵀAS: identical X, draw count and redraw count (and the same error at a tight limit)."""
+    si, torch, ctx, ops = env
+    from paper_1602_01768_b200.api import GramRankDeficientError
+    from paper_1602_01768_b200.dist import SymmetricShardedRBFGS
+
+    n, q, iters, seed = 96, 2, 16, 11
+    rng = np.random.default_rng(0)
+    qm, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    lam = np.concatenate([np.linspace(0.5, 1.5, 52), -np.linspace(0.5, 1.5, n - 52)])
+    a = (qm * lam) @ qm.T
+    a = 0.5 * (a + a.T)
+    at = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+    def rows(r0, r1):
+        return at[:, r0:r1].contiguous().reshape(-1)
+
+    def run(deferred):
+        sh = SymmetricShardedRBFGS(ops, n, q, rows, seed=seed, max_redraws=max_redraws, deferred=deferred)
+        err = False
+        try:
+            for _ in range(iters):
+                sh.step()
+            sh.finalize()
+        except GramRankDeficientError:
+            err = True
+        return sh.gather_x().cpu().numpy(), sh.draw, sh.redraws, err
+
+    xs, ds, rs, es = run(False)
+    xd, dd, rd, ed = run(True)
+    if max_redraws == 100:
+        assert rs > 0 and not es  # the problem does exercise rejections
+    assert (dd, rd, ed) == (ds, rs, es)
+    assert np.array_equal(xd, xs)
