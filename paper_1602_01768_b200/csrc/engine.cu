@@ -932,6 +932,11 @@ static void spd_inverse(Context& c, const double* P, int64_t ldp, int64_t q, dou
 void rbfgs_core_enqueue(Context& c, const double* P, int64_t ldp, int64_t q, double* Ginv, double* T, double* M,
                         double* scratch, int* status) {
     spd_inverse(c, P, ldp, q, Ginv, scratch, status);
+    rbfgs_core_tail(c, P, ldp, q, Ginv, T, M, status);
+}
+
+void rbfgs_core_tail(Context& c, const double* P, int64_t ldp, int64_t q, const double* Ginv, double* T, double* M,
+                     int* status) {
     {
         LaunchScope ls(c, "core_layout");
         core_layout_kernel<<<grid_for(4 * q * q, 256), 256, 0, c.stream>>>(Ginv, int(q), M, status);

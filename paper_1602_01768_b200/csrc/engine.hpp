@@ -184,6 +184,9 @@ void rbfgs_enqueue_iteration(Context& c, Problem& a, RbfgsWork& w, bool device_s
 // the q×q stage: Gram inverse (PD check into status[0]) and the 2q×2q core M
 void rbfgs_core_enqueue(Context& c, const double* P, int64_t ldp, int64_t q, double* Ginv, double* T, double* M,
                         double* scratch, int* status);
+// M from a given G⁻¹ (the part of rbfgs_core_enqueue after the inverse)
+void rbfgs_core_tail(Context& c, const double* P, int64_t ldp, int64_t q, const double* Ginv, double* T, double* M,
+                     int* status);
 // M[0:count) = 0 when status[0] != 0 (the deferred PD check of the sharded driver)
 void zero_on_status(Context& c, double* M, int64_t count, const int* status);
 // the q×q stage of the single-GPU iteration: G⁻¹ (PD check into status[0]) and Ĝ = G + H
