@@ -518,6 +518,19 @@ class SymmetricShardedRBFGS:
         self.Uc = torch.empty(mc * 2 * q, **f)
         self.scratch = torch.empty(6 * q * q + 2 * q + 16, **f)
         self.gather = torch.empty(2 * P * mc * q, **f)
+        # Y gather: each rank writes its two chunks' Y rows straight into send (2 × q × mc,
+        # padding rows never read); the gathered (P, 2, q, mc) block goes to Y's rows in one
+        # index_copy (src: valid gathered columns, dst: their global rows)
+        self._mc = mc
+        self.send = torch.zeros(2 * mc * q, **f)
+        src, dst = [], []
+        for p in range(P):
+            for j, c in enumerate((p, 2 * P - 1 - p)):
+                r0, r1 = self.bounds[c], self.bounds[c + 1]
+                src.extend((p * 2 + j) * mc + i for i in range(r1 - r0))
+                dst.extend(range(r0, r1))
+        self._y_src = torch.tensor(src, dtype=torch.int64, device=dev)
+        self._y_dst = torch.tensor(dst, dtype=torch.int64, device=dev)
         self._ring = 64
         self._status = torch.zeros(self._ring, dtype=torch.int32, device=dev)
         self._status_host = torch.zeros(self._ring, dtype=torch.int32,
@@ -540,22 +553,15 @@ class SymmetricShardedRBFGS:
         return buf.view(ncols, self.n)[:, r0:r1]
 
     def _all_gather_y(self):
-        """Y (n×q) from the ranks' chunk rows; chunk sizes differ by at most one."""
-        n, q, P = self.n, self.q, self.world
-        mc = self.gather.numel() // (2 * P * q)
-        send = torch.zeros(2 * mc * q, dtype=torch.float64, device=self.Y.device)
-        for j, c in enumerate(self.chunks):
-            r0, r1 = self.bounds[c], self.bounds[c + 1]
-            send.view(2, q, mc)[j, :, : r1 - r0].copy_(self._rows(self.Y, q, r0, r1))
+        """Y (n×q) from the ranks' chunk rows (already in self.send); chunk sizes differ by at most one."""
+        n, q, P, mc = self.n, self.q, self.world, self._mc
         if P > 1:
-            dist.all_gather_into_tensor(self.gather, send)
-            g = self.gather.view(P, 2, q, mc)
+            dist.all_gather_into_tensor(self.gather, self.send)
+            g = self.gather
         else:
-            g = send.view(1, 2, q, mc)
-        for p in range(P):
-            for j, c in enumerate((p, 2 * P - 1 - p)):
-                r0, r1 = self.bounds[c], self.bounds[c + 1]
-                self._rows(self.Y, q, r0, r1).copy_(g[p, j, :, : r1 - r0])
+            g = self.send
+        cols = g.view(P * 2, q, mc).permute(1, 0, 2).reshape(q, P * 2 * mc)  # one copy
+        self.Y.view(q, n).index_copy_(1, self._y_dst, cols.index_select(1, self._y_src))
 
     def step(self):
         if not self.deferred:
@@ -620,9 +626,8 @@ class SymmetricShardedRBFGS:
         ops.sketch(S, n, q, n, self.seed, self.draw)
         self.draw += 1
         # Y rows of the owned chunks, then the full Y
-        for c in self.chunks:
-            r0 = self.bounds[c]
-            apply_rows(ops, self.A[c], n, S, n, q, self.Y[r0:], n)
+        for j, c in enumerate(self.chunks):
+            apply_rows(ops, self.A[c], n, S, n, q, self.send[j * q * self._mc:], self._mc)
         self._all_gather_y()
         # W = X·Y from the upper trapezoids: X_c·Y[r0:] and the strictly-upper part transposed
         W.zero_()
