@@ -510,7 +510,6 @@ class SymmetricShardedRBFGS:
         self.Y = torch.empty(n * q, **f)
         self.U = torch.empty(n * 2 * q, **f)  # [S W], column-major n×2q
         self.P = torch.empty(q * 2 * q, **f)
-        self.Pp = torch.empty(q * 2 * q, **f)
         self.M = torch.empty(4 * q * q, **f)
         mc = max(self.bounds[c + 1] - self.bounds[c] for c in range(2 * P))
         self.Yc = torch.empty(mc * q, **f)
@@ -640,11 +639,9 @@ class SymmetricShardedRBFGS:
         if self.world > 1:
             dist.all_reduce(W)
         # P = Yᵀ·[S W] over the owned rows, all-reduced
-        self.Pp.zero_()
-        for c in self.chunks:
+        for j, c in enumerate(self.chunks):  # the first chunk overwrites P (beta = 0)
             r0, m = self.bounds[c], self._m(c)
-            ops.gemm(q, 2 * q, m, self.Y[r0:], n, True, self.U[r0:], n, True, self.Pp, q, 1.0, 1.0)
-        self.P.copy_(self.Pp)
+            ops.gemm(q, 2 * q, m, self.Y[r0:], n, True, self.U[r0:], n, True, self.P, q, 1.0, float(j > 0))
         if self.world > 1:
             dist.all_reduce(self.P)
         core(self.P, self.M)
