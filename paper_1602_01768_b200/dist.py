@@ -342,6 +342,11 @@ class RowShardedAdaRBFGS(_RowPanels):
         self.B = torch.empty(q * n, **f)
         self.scratch = torch.empty(8 * q * q + 8 * q + 32, **f)
         self.idx = torch.zeros(q, dtype=torch.int64, device=dev)
+        # pinned staging for the host-drawn indices (a pageable H2D copy would synchronize the
+        # stream at the start of every step); 4 slots, each reused only after the ada_core
+        # status reads of the attempts in between
+        self._idx_host = torch.zeros((4, q), dtype=torch.int64, pin_memory=self.idx.is_cuda)
+        self._idx_slot = 0
         self.St = torch.empty(n * q, **f) if rule == "gauss" else None
         self.T = torch.empty(q * n, **f) if rule == "gauss" else None
         self.gather_buf = torch.empty(self.world * self.lay.m_max * q, **f)
@@ -410,7 +415,10 @@ class RowShardedAdaRBFGS(_RowPanels):
                 else:
                     cols = [int(v) for v in self.rng.uniform_subset(n, lay.q)]
                 q = len(cols)
-                self.idx[:q].copy_(torch.tensor(cols, dtype=torch.int64))
+                h = self._idx_host[self._idx_slot, :q]
+                self._idx_slot = (self._idx_slot + 1) % 4
+                h.numpy()[:] = cols
+                self.idx[:q].copy_(h, non_blocking=True)
                 ops.gather_columns(self.L, m, m, self.idx, q, self.Sp)                        # S_p = L_p[:, C]
             self._all_gather_rows(self.Sp[: m * q], self.S[: n * q], q)                       # S
             apply_rows(ops, self.A, n, self.S, n, q, self.ASp, m)                                # (AS)_p = A_p·S
