@@ -165,18 +165,24 @@ class _RowPanels:
         """panel: this rank's m×ncols column-major panel; out: n×ncols column-major."""
         lay = self.lay
         mm = lay.m_max
+        if self.world == 1:
+            out[: lay.n * ncols].copy_(panel[: lay.n * ncols])
+            return
         send = self.send_buf[: mm * ncols].view(ncols, mm)
         send[:, : lay.m].copy_(panel.view(ncols, lay.m))
-        if self.world == 1:
-            out.view(ncols, lay.n).copy_(send[:, : lay.n])
-            return
         gbuf = self.gather_buf[: self.world * mm * ncols]
         dist.all_gather_into_tensor(gbuf, send.reshape(-1))
-        g = gbuf.view(self.world, ncols, mm)
+        # (P, ncols, mm) -> out's rows: one transposing copy when the panels are equal, else
+        # the valid columns picked by one index_select (instead of P strided copies)
+        cols = gbuf.view(self.world, ncols, mm).permute(1, 0, 2).reshape(ncols, self.world * mm)
         ov = out.view(ncols, lay.n)
-        for p in range(self.world):
-            a, b = lay.starts[p], lay.starts[p + 1]
-            ov[:, a:b].copy_(g[p, :, : b - a])
+        if self.world * mm == lay.n:
+            ov.copy_(cols)
+            return
+        if getattr(self, "_row_src", None) is None or self._row_src.device != out.device:
+            src = [p * mm + i for p in range(self.world) for i in range(lay.starts[p + 1] - lay.starts[p])]
+            self._row_src = torch.tensor(src, dtype=torch.int64, device=out.device)
+        ov.copy_(cols.index_select(1, self._row_src))
 
     def _gather_panel(self, panel, out):
         """All-gather an m×n row panel (column-major, flat) into the full n×n matrix."""
