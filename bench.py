@@ -4,25 +4,36 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 3]
 
 Workload (config.workload): BASELINE config 3 — dense SPD A = Q·diag(λ)·Qᵀ,
-n = 16384, RBFGS with a Gaussian sketch q = 128 (the first RBFGS config that is
-GPU-sized and the one the ≥60% DMMA target names).  A "step" is one RBFGS
-iteration: sketch → Y = A·S → W = X·Y → [G|H] = Yᵀ[S W] → Gram inverse + core
-→ V = U·M → X ← X + V·Uᵀ (symmetric).  Inputs (A, X: 2.1 GB each) exceed the
-126 MB L2, so no flush is needed between steps.
+n = 16384, RBFGS with a Gaussian sketch q = 128 (the largest dense RBFGS config
+and the one the ≥60% DMMA target names).  A "step" is one RBFGS iteration:
+sketch → Y = A·S → W' = −X·Y → [G | H'] = Yᵀ[S W'] → K-FACTOR (G⁻¹, PD test) →
+Z = S·G⁻¹, R = Z·Ĝ + W' → X ← X + [Z R]·[W' Z]ᵀ (K-SYMUPD, upper tiles mirrored).
+A and X (2.1 GB each) exceed the 126 MB L2, so no flush is needed between steps.
+A is synthesised on the host by generators.py (numpy / BLAS over the reference
+RngStream) in both arms, so both time the same A bytes.
 
 value  : iterations/s, device-timed with CUDA events on the launch stream
-         (inputs resident in HBM; device counter-based sketches).
+         (inputs resident in HBM; device counter-based sketches, Philox4x32-10),
+         iterations between checkpoints replayed as one captured CUDA graph each.
 e2e    : the same metric through the public driver si_run_inverter (the call a
-         user makes) with host buffers: A uploaded from pinned host memory and
-         X read back inside the timed region, a status word read back every
-         iteration, residual checkpoint at the last iteration.
-roofline: the dominant kernel (fused symmetric rank-2q update) — algorithmic
-         FLOPs per launch (2n²·2q/2 = 2n²q, upper triangle) ÷ its CUDA-event
-         time, against the measured FP64 DMMA peak (profiles/r01_fp64_peak.txt).
+         user makes) with host buffers: A uploaded from host memory and
+         validated (SPD), 100 iterations with the reference's forced residual
+         checkpoints at k = 1 and k = 100, X copied back to host, all inside the
+         timer.
+roofline: the dominant kernel class (split-K long-K GEMMs Y = A·S and
+         W' = −X·Y): algorithmic FLOPs per launch (2n²q) ÷ its CUDA-event time,
+         against the measured FP64 DMMA peak (profiles/r01_fp64_peak.txt);
+         roofline_secondary is K-SYMUPD (2n²q on the upper tiles).
+time_to_eps: config 1 (n = 1024, q = 32) to ‖I−AX‖_F/√n ≤ 1e-2 and to the
+         reference normalisation ‖I−AX_k‖_F/‖I−AX_0‖_F ≤ 1e-2; config 3 with an
+         iteration cap (labelled, with the residual reached).
 cpu_baseline: the oracle (C++ restatement of the reference, OpenBLAS) running
-         the same bfgs_step on the host cores, a bounded sample of steps.
---impl reference: the reference algorithm on the host cores (oracle port; the
-         reference itself cannot be built here), same metric.
+         run_inverter iterations on the host cores, a bounded sample of steps.
+--impl reference: the reference algorithm on all host cores (the oracle port —
+         the reference itself needs Eigen, absent here), same config,
+         metric and steps; it imports neither this package nor torch.
+--gpus N without WORLD_SIZE in the environment relaunches itself under
+torch.distributed.run with N ranks (127.0.0.1) and rank 0 prints the line.
 """
 from __future__ import annotations
 
@@ -74,30 +85,54 @@ CONFIGS = {
 _DENSE_CACHE = {}
 
 
-def make_dense(cfg):
-    """Host (column-major) copy of the config's A; config 3 is synthesised on the GPU."""
+def load_generators(rng_cls=None):
+    """generators.py loaded by path (not through the package, whose import loads the
+    CUDA library) with the given RngStream class: the oracle's for the reference arm,
+    the library's (byte-identical) for ours."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location(
+        "si_generators", os.path.join(ROOT, "paper_1602_01768_b200", "generators.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    if rng_cls is not None:
+        mod.use_rng(rng_cls)
+    return mod
+
+
+def make_dense(cfg, rng_cls=None):
+    """Host column-major A of the config (numpy / BLAS, identical bytes in both arms)."""
     key = cfg["name"]
     if key in _DENSE_CACHE:
         return _DENSE_CACHE[key]
-    from paper_1602_01768_b200 import generators as G
-
+    G = load_generators(rng_cls)
     if cfg["gen"] == "config1":
         a = G.config1_dense(cfg["n"], seed=0)
+    elif cfg["gen"] == "config2":
+        a = G.config2_dense(cfg["n"], seed=0)
     else:
-        import torch
-
-        if torch.cuda.is_available():
-            t = G.config3_dense_device(cfg["n"], seed=0)
-            host = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
-            host.copy_(t)
-            del t
-            torch.cuda.empty_cache()
-            a = host.numpy().T  # symmetric: row-major buffer == column-major A
-            a = np.asfortranarray(a) if not a.flags.f_contiguous else a
-        else:
-            a = G.config3_dense(cfg["n"], seed=0)
+        a = G.config3_dense(cfg["n"], seed=0)
     _DENSE_CACHE[key] = a
     return a
+
+
+def config_of(cfg):
+    """The `config` object of the JSON line — identical in both arms."""
+    return {"workload": cfg["name"], "n": cfg["n"], "q": cfg["q"],
+            "sketch": f"gaussian(q={cfg['q']}): n×q i.i.d. N(0,1), drawn fresh each iteration",
+            "l2": "inputs larger than L2 (A, X 2.1 GB each); no flush" if cfg["n"] * cfg["n"] * 8 > 126e6 else
+                  "inputs fit in L2; no flush (latency-bound extra line)"}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -217,6 +252,9 @@ def _reference_iteration(O, rng, x, a, n, q):
 
 
 def run_reference(args, cfg):
+    """The reference's CPU RBFGS (the oracle port of simi.cpp:287-357 with OpenBLAS on
+    all host threads) on the same config: rank 0 only, no GPU, no import of this
+    package or torch; A from generators.py over the oracle's RngStream."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
@@ -224,30 +262,31 @@ def run_reference(args, cfg):
 
     cores = os.cpu_count()
     n, q = cfg["n"], cfg["q"]
-    a = make_dense(cfg)
+    t_gen = time.perf_counter()
+    a = make_dense(cfg, O.RngStream)
+    t_gen = time.perf_counter() - t_gen
     rng = O.RngStream(0)
     x = np.asfortranarray(np.eye(n))
-    # warm-up and timed steps are bounded samples of the same workload: the CPU
-    # needs seconds per iteration at n = 16384 (see cpu_baseline.sample)
-    for _ in range(min(args.warmup, 1)):
+    for _ in range(args.warmup):
         x = _reference_iteration(O, rng, x, a, n, q)
-    steps = max(1, min(args.steps, 5)) if n >= 8192 else args.steps
     t0 = time.perf_counter()
-    for _ in range(steps):
+    for _ in range(args.steps):
         x = _reference_iteration(O, rng, x, a, n, q)
     dt = time.perf_counter() - t0
-    v = steps / dt
+    v = args.steps / dt
     line = {
         "impl": "reference", "metric": "rbfgs_iterations_per_s", "value": v, "unit": "iter/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / steps,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg["name"], "n": n, "q": q, "sketch": "gaussian (reference RngStream)"},
-        "cpu_baseline": {"value": v, "unit": "iter/s", "cores": cores, "kind": "port",
-                         "sample": f"{steps} run_inverter iterations (draw S, bfgs_step, symmetrize; "
-                                   f"simi.cpp:287-357) at n={n}, q={q}: oracle restatement with OpenBLAS dgemm "
-                                   "and the elementwise passes on all host threads; the reference itself "
-                                   "(Eigen) cannot be built in this image"},
+        "config": config_of(cfg),
+        "sketch_rng": "host RngStream (mt19937_64 + std::normal_distribution, rng.hpp:42-49)",
+        "cpu_baseline": {"value": v, "unit": "iter/s", "cores": cores, "kind": "port", "cpu_model": cpu_model(),
+                         "sample": f"{args.steps} run_inverter iterations after {args.warmup} warm-up ones (draw S, "
+                                   f"bfgs_step, symmetrize; simi.cpp:287-357) at n={n}, q={q}: oracle restatement "
+                                   "with OpenBLAS dgemm and the elementwise passes on all host threads; the reference "
+                                   "itself (Eigen) cannot be built in this image"},
         "e2e": {"value": v, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "input_generation_s": t_gen,
     }
     print(json.dumps(line), flush=True)
 
@@ -266,14 +305,12 @@ def run_sharded(args, cfg):
     os.environ.setdefault("MASTER_PORT", "29531")
     dist.init_process_group("nccl", device_id=torch.device("cuda", local), rank=rank, world_size=world)
     import paper_1602_01768_b200 as si
-    from paper_1602_01768_b200 import generators as G
     from paper_1602_01768_b200.dist import CudaPanelOps, SymmetricShardedRBFGS
 
     n, q = cfg["n"], cfg["q"]
     stream = torch.cuda.current_stream()
     ctx = si.Context(local, stream=stream.cuda_stream)
-    a_full = G.config3_dense_device(n, seed=0) if cfg["gen"] == "config3" else \
-        torch.from_numpy(make_dense(cfg)).cuda()
+    a_full = torch.from_numpy(make_dense(cfg).T).cuda()  # row-major view of the symmetric A
 
     def rows_of_chunk(r0, r1):
         # column-major (r1−r0)×n panel A[r0:r1, :]: in a row-major (n, n) tensor holding the
@@ -605,6 +642,51 @@ def config2_time_to_eps(si, prob, n, q):
     return out
 
 
+def time_to_eps(args, si, ctx, cfg, prob, a_host):
+    """Time to ε through run_inverter (wall clock of the whole driver call,
+    checkpoints included, after an untimed warm-up call of the same shapes):
+      config 1 (n = 1024, q = 32) to ‖I−AX‖_F/√n ≤ 1e-2 and to the reference
+        normalisation ‖I−AX_k‖_F/‖I−AX_0‖_F ≤ 1e-2, checkpoints every 10 iterations;
+      the bench workload (config 3) to ‖I−AX‖_F/√n ≤ 1e-2 with an iteration cap
+        (--tte-cap, checkpoints every 100: 2n³ each), labelled with the residual reached."""
+    import torch
+
+    out = {}
+    jobs = []
+    c1 = CONFIGS[1]
+    a1 = make_dense(c1)
+    p1 = si.ProblemMatrix(a1, si.Symmetry.spd, context=ctx)
+    base1 = float(np.linalg.norm(np.eye(c1["n"]) - a1))
+    for label, tol in (("sqrt_n_1e-2", 1e-2 * math.sqrt(c1["n"]) / base1), ("reference_rel_1e-2", 1e-2)):
+        jobs.append((f"{c1['name']}/{label}", p1, c1, tol, 20000, 10, base1,
+                     "||I-AX||_F/sqrt(n) <= 1e-2" if label.startswith("sqrt") else "||I-AX_k||_F/||I-AX_0||_F <= 1e-2"))
+    if cfg["name"] != c1["name"]:
+        n = cfg["n"]
+        # ‖I − A‖²_F = ‖A‖²_F − 2·tr(A) + n (no n×n temporary)
+        base = math.sqrt(max(float(np.linalg.norm(a_host)) ** 2 - 2.0 * float(np.trace(a_host)) + n, 0.0))
+        jobs.append((f"{cfg['name']}/sqrt_n_1e-2_capped", prob, cfg, 1e-2 * math.sqrt(n) / base, args.tte_cap, 100,
+                     base, "||I-AX||_F/sqrt(n) <= 1e-2 (iteration cap %d)" % args.tte_cap))
+    warmed = set()
+    for name, pr, c, tol, cap, every, base, target in jobs:
+        if id(pr) not in warmed:  # untimed warm-up of the same shapes (graph capture, workspace)
+            si.run_inverter(si.InverterConfig(pr, si.SketchRule.gaussian_device(c["q"]), tol=0.0, max_iters=every + 1,
+                                              seed=1, track=si.TrackOptions(residual_every_k=every), return_x=False))
+            warmed.add(id(pr))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = si.run_inverter(si.InverterConfig(pr, si.SketchRule.gaussian_device(c["q"]), tol=tol, max_iters=cap,
+                                              seed=0, track=si.TrackOptions(residual_every_k=every), return_x=False))
+        t1 = time.perf_counter()
+        rel = r.state.history[-1].residual
+        out[name] = {"seconds": t1 - t0, "iterations": r.state.k, "reached": r.termination.name == "tol_reached",
+                     "termination": r.termination.name, "target": target,
+                     "relative_residual": rel, "residual_sqrt_n": rel * base / math.sqrt(c["n"]),
+                     "step_seconds": r.state.seconds,
+                     "checkpoints": f"every {every} iterations (2n^3 residual each, included in seconds)"}
+    del p1
+    return out
+
+
 def run_ours(args, cfg):
     import torch
 
@@ -734,27 +816,10 @@ def run_ours(args, cfg):
                        "A/X transfers amortised over the run"}
         del prob2
 
-    # ---- time to ε: config 1 only, both normalisations ----
+    # ---- time to ε: config 1 (both normalisations) + config 3 (capped) ----
     tte = None
-    if rank == 0 and cfg["gen"] == "config1":
-        import numpy as np
-
-        base = float(np.linalg.norm(np.eye(n) - a_host))
-        tte = {}
-        si.run_inverter(si.InverterConfig(prob, si.SketchRule.gaussian_device(q), tol=0.0, max_iters=11, seed=1,
-                                          track=si.TrackOptions(residual_every_k=10), return_x=False))  # warm-up
-        for label, tol in (("sqrt_n_1e-2", 1e-2 * math.sqrt(n) / base), ("reference_rel_1e-2", 1e-2)):
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            r = si.run_inverter(si.InverterConfig(prob, si.SketchRule.gaussian_device(q), tol=tol, max_iters=20000,
-                                                  seed=0, track=si.TrackOptions(residual_every_k=10),
-                                                  return_x=False))
-            t1 = time.perf_counter()
-            tte[label] = {"seconds": t1 - t0, "iterations": r.state.k, "reached": r.termination.name,
-                          "relative_residual": r.state.history[-1].residual,
-                          "target": "||I-AX||_F/sqrt(n) <= 1e-2" if label.startswith("sqrt") else
-                                    "||I-AX_k||_F/||I-AX_0||_F <= 1e-2",
-                          "checkpoints": "every 10 iterations (2n^3 residual each, included)"}
+    if rank == 0 and not args.no_tte:
+        tte = time_to_eps(args, si, ctx, cfg, prob, a_host)
 
     # ---- CPU baseline (oracle on host cores, bounded sample) ----
     cpu = None
@@ -762,7 +827,7 @@ def run_ours(args, cfg):
         steps_cpu = 3 if n >= 8192 else 20
         v, dt = cpu_port_steps_per_s(cfg, steps_cpu)
         v1, dt1 = cpu_port_steps_per_s(cfg, 1, threads=1)
-        cpu = {"value": v, "unit": "iter/s", "cores": os.cpu_count(), "kind": "port",
+        cpu = {"value": v, "unit": "iter/s", "cores": os.cpu_count(), "kind": "port", "cpu_model": cpu_model(),
                "sample": f"{steps_cpu} run_inverter iterations (draw S, bfgs_step, symmetrize; simi.cpp:287-357) "
                          f"of the same workload (n={n}, q={q}) in {dt:.1f} s: oracle restatement with OpenBLAS "
                          "dgemm and elementwise passes on all host threads",
@@ -775,12 +840,11 @@ def run_ours(args, cfg):
             "metric": "rbfgs_iterations_per_s", "value": value, "unit": "iter/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step_ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg["name"], "n": n, "q": q, "sketch": "gaussian, device Philox4x32-10",
-                       "l2": ("inputs larger than L2 (A, X 2.1 GB each); no flush" if n * n * 8 > 126e6 else
-                              "inputs fit in L2 (A, X %.0f MB); no flush — latency-bound extra line" % (n * n * 8e-6)),
-                       "parallelism": "replicas" if world > 1 else "single-gpu",
-                       "algorithmic_gflop_per_step": alg_flops / 1e9,
-                       "achieved_tflops_per_step": alg_flops / (per_step_ms * 1e-3) / 1e12},
+            "config": config_of(cfg),
+            "sketch_rng": "device Philox4x32-10 + Box-Muller (counter in device memory)",
+            "parallelism": "replicas" if world > 1 else "single-gpu",
+            "algorithmic_gflop_per_step": alg_flops / 1e9,
+            "achieved_tflops_per_step": alg_flops / (per_step_ms * 1e-3) / 1e12,
             "roofline": roofline,
             "roofline_secondary": secondary,
             "roofline_hbm": hbm_lines or None,
@@ -796,6 +860,19 @@ def run_ours(args, cfg):
         torch.distributed.destroy_process_group()
 
 
+def self_launch(nproc: int) -> int:
+    """`bench.py --gpus N` outside torchrun: relaunch under torch.distributed.run with N
+    ranks on 127.0.0.1 (one process per GPU); rank 0 prints the JSON line."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     load_peaks()
     p = argparse.ArgumentParser()
@@ -805,11 +882,15 @@ def main():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", type=int, default=3, choices=sorted(CONFIGS))
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-tte", action="store_true", help="skip the time_to_eps block")
+    p.add_argument("--tte-cap", type=int, default=1000, help="iteration cap of the config-3 time-to-eps run")
     p.add_argument("--sharded", action="store_true", help="use the row-sharded driver even at N=1")
     p.add_argument("--sampler", default="uniform", choices=["uniform", "eq82"],
                    help="AdaRBFGS configs 2/4: paper uniform sampler or the reference's Eq. 8.2 blocks")
     args = p.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args.gpus))
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)

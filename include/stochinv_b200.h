@@ -126,6 +126,13 @@ int si_context_synchronize(si_context* ctx);
 int si_context_release_workspaces(si_context* ctx);
 /* Kernel launches issued by this context so far (the bench's gpu_launches). */
 int64_t si_context_launch_count(si_context* ctx);
+/* Draw log (an addition for parity checks): from now on the drivers append every executed
+ * sampling attempt's outcome to buf (up to cap entries) — the block index for coordinate_block /
+ * adaptive_cols (rng.hpp:28-36 categorical), the q coordinates for adaptive_cols_uniform —
+ * in draw order, rejected attempts included.  NULL turns it off.  si_context_draw_count returns
+ * the entries produced (may exceed cap). */
+int si_context_set_draw_log(si_context* ctx, int64_t* buf, int64_t cap);
+int64_t si_context_draw_count(si_context* ctx);
 /* Per-kernel-class device timing (CUDA events around each launch). */
 int si_context_set_profiling(si_context* ctx, int enabled);
 /* Returns the number of classes; fills up to cap entries (name, launches, total ms). */

@@ -47,6 +47,8 @@ _SIGS = {
     "si_context_synchronize": (ci, [vp]),
     "si_context_release_workspaces": (ci, [vp]),
     "si_context_launch_count": (i64, [vp]),
+    "si_context_set_draw_log": (ci, [vp, pi64, i64]),
+    "si_context_draw_count": (i64, [vp]),
     "si_context_set_profiling": (ci, [vp, ci]),
     "si_context_profile": (ci, [vp, vp, pi64, pd, ci]),
     "si_context_reset_profile": (ci, [vp]),

@@ -88,6 +88,23 @@ class Context:
     def launch_count(self) -> int:
         return int(L.load().si_context_launch_count(self._h))
 
+    def set_draw_log(self, cap: int) -> None:
+        """Record the drivers' sampling outcomes (block indices / uniform coordinates, every
+        executed attempt in draw order) from now on; read them with draw_log()."""
+        self._draw_buf = np.zeros(max(int(cap), 1), dtype=np.int64) if cap else None
+        buf = self._draw_buf
+        _check(L.load().si_context_set_draw_log(self._h, buf.ctypes.data_as(L.pi64) if buf is not None else None,
+                                                 int(cap)))
+
+    def draw_log(self) -> np.ndarray:
+        cnt = int(L.load().si_context_draw_count(self._h))
+        buf = getattr(self, "_draw_buf", None)
+        if buf is None:
+            return np.zeros(0, dtype=np.int64)
+        if cnt > buf.size:
+            raise RuntimeError(f"draw log overflow: {cnt} entries, capacity {buf.size}")
+        return buf[:cnt].copy()
+
     def release_workspaces(self):
         """Free the run_inverter / run_adarbfgs workspace the context keeps between calls."""
         _check(L.load().si_context_release_workspaces(self._h))

@@ -31,7 +31,12 @@ CXX_FLAGS = ["-std=gnu++20", "-O3", "-march=x86-64-v3", "-fPIC", "-Wall", "-Wext
 
 SOURCES_CU = ["engine.cu"]
 SOURCES_CXX = ["driver.cpp", "io.cpp"]
-HEADERS = ["common.cuh", "gemm_f64.cuh", "kernels_aux.cuh", "kernels_small.cuh", "kernels_core.cuh", "family.cuh", "engine.hpp", "host_rng.hpp"]
+# per-source header dependencies (the public C header does not reach engine.cu)
+_KERNEL_HDRS = ["common.cuh", "gemm_f64.cuh", "kernels_aux.cuh", "kernels_small.cuh", "kernels_core.cuh",
+                "family.cuh", "engine.hpp"]
+_HOST_HDRS = ["engine.hpp", "host_rng.hpp", "../../include/stochinv_b200.h"]
+DEPS = {"engine.cu": _KERNEL_HDRS, "driver.cpp": _HOST_HDRS, "io.cpp": _HOST_HDRS}
+HEADERS = sorted(set(_KERNEL_HDRS + _HOST_HDRS))
 
 
 def _newer(target: str, deps: list[str]) -> bool:
@@ -57,20 +62,23 @@ def build(force: bool = False) -> str:
         raise RuntimeError(f"nvcc not found at {NVCC}")
     os.makedirs(BUILD, exist_ok=True)
     os.makedirs(LIB_DIR, exist_ok=True)
-    hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "stochinv_b200.h")]
-    objs = []
-    for src in SOURCES_CU:
+    objs, jobs = [], []
+    for src in SOURCES_CU + SOURCES_CXX:
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, src + ".o")
-        if force or _newer(o, [s] + hdrs):
-            _run([NVCC] + NVCC_FLAGS + ["-c", s, "-o", o], log=os.path.join(BUILD, src + ".ptxas.log"))
+        deps = [s] + [os.path.normpath(os.path.join(CSRC, h)) for h in DEPS[src]]
+        if force or _newer(o, deps):
+            if src.endswith(".cu"):
+                jobs.append(([NVCC] + NVCC_FLAGS + ["-c", s, "-o", o], os.path.join(BUILD, src + ".ptxas.log")))
+            else:
+                jobs.append((["g++"] + CXX_FLAGS + ["-c", s, "-o", o], None))
         objs.append(o)
-    for src in SOURCES_CXX:
-        s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src + ".o")
-        if force or _newer(o, [s] + hdrs):
-            _run(["g++"] + CXX_FLAGS + ["-c", s, "-o", o])
-        objs.append(o)
+    if jobs:  # the translation units compile in parallel
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(max_workers=len(jobs)) as ex:
+            for f in [ex.submit(_run, cmd, log) for cmd, log in jobs]:
+                f.result()
     if force or _newer(LIB, objs):
         _run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcusolver", "-lcublas",
                                                           f"-Xlinker=-rpath={CUDA}/lib64"])

@@ -87,6 +87,16 @@ struct DeviceTimer {
 
 struct si_context {
     std::unique_ptr<si::Context> c;
+    // optional draw log (si_context_set_draw_log): every executed sampling attempt of the
+    // drivers appends its outcome — the block index (coordinate_block, adaptive_cols) or the q
+    // coordinates (adaptive_cols_uniform) — in the order the reference draws them
+    int64_t* draw_log = nullptr;
+    int64_t draw_cap = 0;
+    int64_t draw_count = 0;
+    void log_draw(int64_t v) {
+        if (draw_log && draw_count < draw_cap) draw_log[draw_count] = v;
+        ++draw_count;
+    }
 };
 
 struct si_problem {
@@ -249,6 +259,15 @@ int si_context_release_workspaces(si_context* ctx) {
 }
 
 int64_t si_context_launch_count(si_context* ctx) { return ctx->c->launches; }
+
+int si_context_set_draw_log(si_context* ctx, int64_t* buf, int64_t cap) {
+    ctx->draw_log = buf;
+    ctx->draw_cap = buf ? cap : 0;
+    ctx->draw_count = 0;
+    return SI_OK;
+}
+
+int64_t si_context_draw_count(si_context* ctx) { return ctx->draw_count; }
 
 int si_context_set_profiling(si_context* ctx, int enabled) {
     return guard([&] {
@@ -799,6 +818,7 @@ static void run_inverter_impl(si_context* ctx, si_problem* prob, const si_invert
                 rng.gaussian_fill(w.pinned(), n, q, n);  // rng.hpp:42-49
             } else if (sk == SI_SKETCH_COORDINATE_BLOCK) {
                 const si::Index i = rng.categorical(p.data(), si::Index(p.size()));
+                ctx->log_draw(i);
                 const auto& blk = blocks[size_t(i)];
                 // the last block of contiguous_partition may be narrower: this draw has q' = |C_i| columns
                 w.q = int64_t(blk.size());
@@ -1297,6 +1317,10 @@ int si_run_adarbfgs(si_context* ctx, si_problem* prob, const si_inverter_config*
                 ck(cudaStreamSynchronize(c.stream), "sync");
                 const auto t1 = std::chrono::steady_clock::now();
                 const int64_t accepted = st[5];
+                if (mode == 0) {  // the attempts that executed: all, or up to the rejected one
+                    const int64_t ran = st[4] ? accepted + 1 : nb;
+                    for (int64_t b = 0; b < ran * q; ++b) ctx->log_draw(w.idx_ring_pinned[b]);
+                }
                 k += accepted;
                 result->redraws += st[2];
                 if (cfg->track_wall_time) seconds += std::chrono::duration<double>(t1 - t0).count();
@@ -1335,12 +1359,16 @@ int si_run_adarbfgs(si_context* ctx, si_problem* prob, const si_inverter_config*
                 int mode = 0;
                 if (cols) {
                     const si::Index i = rng.categorical(p.data(), si::Index(p.size()));
+                    ctx->log_draw(i);
                     const auto& blk = blocks[size_t(i)];
                     w.q = int64_t(blk.size());  // a narrower last block draws q' = |C_i| columns
                     for (size_t j = 0; j < blk.size(); ++j) w.idx_pinned[j] = blk[j];
                 } else if (sk == SI_SKETCH_ADAPTIVE_COLS_UNIFORM) {
                     const auto idx = si::uniform_subset(rng, n, q);
-                    for (int64_t j = 0; j < q; ++j) w.idx_pinned[j] = idx[size_t(j)];
+                    for (int64_t j = 0; j < q; ++j) {
+                        w.idx_pinned[j] = idx[size_t(j)];
+                        ctx->log_draw(idx[size_t(j)]);
+                    }
                 } else if (sk == SI_SKETCH_ADAPTIVE_GAUSS) {
                     rng.gaussian_fill(w.st_pinned, n, q, n);
                     mode = 1;

@@ -9,6 +9,12 @@ datasets (LIBSVM / UF), with their shapes, sizes and value distributions.
 
 Dense configs return column-major float64 arrays; sparse configs return CSR
 (rowptr int64, colind int32, val float64).
+
+The module is importable on its own (bench.py's reference arm loads it by path,
+without the package and its CUDA library): the RngStream class is injected
+through `use_rng` (the oracle's and the library's streams are byte-identical,
+tests/test_boundary_cpu.py) and defaults to the library's.  Input synthesis
+is host-side numpy / BLAS only, so both bench arms build the same A bytes.
 """
 from __future__ import annotations
 
@@ -16,7 +22,23 @@ import math
 
 import numpy as np
 
-from .api import RngStream
+_RNG = None
+
+
+def use_rng(cls) -> None:
+    """Select the RngStream implementation (a class with substream /
+    gaussian_matrix / uniform_matrix, rng.hpp:13-71)."""
+    global _RNG
+    _RNG = cls
+
+
+def RngStream(seed: int = 0):
+    global _RNG
+    if _RNG is None:
+        from paper_1602_01768_b200.api import RngStream as _R
+
+        _RNG = _R
+    return _RNG(seed)
 
 
 def config1_dense(n: int = 1024, seed: int = 0, m: int | None = None) -> np.ndarray:
@@ -41,20 +63,38 @@ def config2_dense(n: int = 4096, seed: int = 0, m: int | None = None, density: f
 
 def config3_dense(n: int = 16384, seed: int = 0, reflectors: int = 8) -> np.ndarray:
     """A = Q·diag(λ)·Qᵀ, Q = H_8···H_1 Householder reflectors with N(0,1) vectors,
-    λ_j = 10^(−3 + 3u_j) log-uniform in [1e-3, 1] (BASELINE config 3)."""
+    λ_j = 10^(−3 + 3u_j) log-uniform in [1e-3, 1] (BASELINE config 3).
+
+    Each reflector is applied two-sided in place on the upper triangle
+    (A ← H A H = A − v uᵀ − u vᵀ, u = βAv − ½β²(vᵀAv)v: BLAS dsymv + dsyr2),
+    then the upper triangle is mirrored, so A is exactly symmetric and no n×n
+    temporary is made (≈5 s at n = 16384)."""
+    from scipy.linalg import blas
+
     r = RngStream(seed).substream(3)
     v = r.gaussian_matrix(n, reflectors)
     lam = 10.0 ** (-3.0 + 3.0 * r.uniform_matrix(n, 1)[:, 0])
     a = np.zeros((n, n), order="F")
     a[np.diag_indices(n)] = lam
-    for i in range(reflectors):  # A <- H_i A H_i, H = I − β v vᵀ
-        vi = v[:, i]
+    for i in range(reflectors):
+        vi = np.ascontiguousarray(v[:, i])
         beta = 2.0 / float(vi @ vi)
-        p = a @ vi
+        p = blas.dsymv(1.0, a, vi, lower=0)
         u = beta * p - 0.5 * beta * beta * float(vi @ p) * vi
-        a -= np.outer(vi, u)
-        a -= np.outer(u, vi)
-    return np.asfortranarray(0.5 * (a + a.T))
+        a = blas.dsyr2(-1.0, vi, u, a=a, lower=0, overwrite_a=1)
+    _mirror_upper(a)
+    return a
+
+
+def _mirror_upper(a: np.ndarray, blk: int = 2048) -> None:
+    n = a.shape[0]
+    for j0 in range(0, n, blk):
+        j1 = min(j0 + blk, n)
+        for i0 in range(j1, n, blk):
+            i1 = min(i0 + blk, n)
+            a[i0:i1, j0:j1] = a[j0:j1, i0:i1].T
+        d = a[j0:j1, j0:j1]
+        a[j0:j1, j0:j1] = np.triu(d) + np.triu(d, 1).T
 
 
 def config3_dense_device(n: int = 16384, seed: int = 0, reflectors: int = 8, device: str = "cuda"):
