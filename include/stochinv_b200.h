@@ -119,6 +119,29 @@ int si_context_create(int device, si_context** out);
  * stream (NULL) the context uses a private blocking stream, which is ordered with it implicitly. */
 int si_context_create_on_stream(int device, void* cuda_stream, si_context** out);
 int si_context_destroy(si_context* ctx);
+
+/* ---- multi-GPU contexts -----------------------
+ * A multi-GPU context drives P ranks over NCCL (NVLink / NVSwitch); si_run_inverter (bfgs),
+ * si_run_adarbfgs and the si_solver_* calls on it run the iteration sharded — X's upper
+ * triangle in 2P row chunks (RBFGS), L in P row panels (AdaRBFGS), A replicated — with the
+ * reference's run semantics (run_inverter simi.hpp:105, run_adarbfgs adarbfgs.hpp:59).
+ * Problems created on it are replicated to every local rank.  NCCL is loaded on demand.
+ *   _multi:    one process driving `ndev` distinct devices (ncclCommInitAll);
+ *   _rank:     one process per GPU (torchrun / MPI): every rank passes the id rank 0 got
+ *              from si_nccl_unique_id (the caller broadcasts the bytes); cuda_stream may be
+ *              NULL (private stream) or the caller's stream; x_out / l_out of the drivers are
+ *              filled on rank 0 only;
+ *   _loopback: `nranks` virtual ranks on ONE device sharing one stream, the collectives
+ *              replayed as device copies — a single-GPU harness for the P > 1 logic (tests),
+ *              not a performance configuration. */
+#define SI_NCCL_ID_BYTES 128
+int si_nccl_unique_id(void* id_out);
+int si_context_create_multi(const int* devices, int ndev, si_context** out);
+int si_context_create_rank(int device, void* cuda_stream, int nranks, int rank, const void* nccl_id, si_context** out);
+int si_context_create_loopback(int device, int nranks, si_context** out);
+/* global rank count, the global rank of this process's first local rank, local rank count
+ * (1, 0, 1 for a single-GPU context) */
+int si_context_ranks(si_context* ctx, int* nranks, int* first_rank, int* local_ranks);
 int si_context_synchronize(si_context* ctx);
 /* si_run_inverter / si_run_adarbfgs keep their last workspace (the n×n iterate and panels,
  * when it is at most a quarter of device memory) in the context so a rerun of the same
@@ -183,6 +206,10 @@ int si_bfgs_step_problem(si_context* ctx, si_problem* prob, int64_t q, const dou
  * Returns SI_ERR_RESAMPLE when an inverse square root hits its floor. */
 int si_adarbfgs_update_factor(si_context* ctx, int64_t n, int64_t q, const double* l_host, const double* a_host,
                               const double* stilde_host, double* l_out_host);
+/* Matrix sym_inv_sqrt(const Matrix& m, double floor_rel = 1e-14), linalg.hpp (linalg.cpp:144-155):
+ * r_out (q×q) = M^{-1/2} for symmetric M; SI_ERR_NUMERICAL ("matrix is not positive definite") iff
+ * an eigenvalue λ ≤ 1e-14·λmax or λ ≤ 0 — the rule the AdaRBFGS update applies to SᵀAS. */
+int si_sym_inv_sqrt(si_context* ctx, int64_t q, const double* m_host, double* r_out_host);
 /* Vector adaptive_block_probabilities(l, a, blocks), adarbfgs.hpp:32-33; blocks given in CSR
  * form (block_offsets[nblocks+1], block_indices[n]). */
 int si_adaptive_block_probabilities(si_context* ctx, int64_t n, const double* l_host, const double* a_host,

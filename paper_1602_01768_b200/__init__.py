@@ -48,6 +48,8 @@ from .api import (  # noqa: E402
     run_baseline,
     spectral_norm_estimate,
     adarbfgs_update_factor,
+    sym_inv_sqrt,
+    nccl_unique_id,
     bfgs_step,
     build_ridge_hessian,
     contiguous_partition,

@@ -48,6 +48,12 @@ _SIGS = {
     "si_context_release_workspaces": (ci, [vp]),
     "si_context_launch_count": (i64, [vp]),
     "si_context_set_draw_log": (ci, [vp, pi64, i64]),
+    "si_nccl_unique_id": (ci, [vp]),
+    "si_context_create_multi": (ci, [C.POINTER(ci), ci, C.POINTER(vp)]),
+    "si_context_create_rank": (ci, [ci, vp, ci, ci, vp, C.POINTER(vp)]),
+    "si_context_create_loopback": (ci, [ci, ci, C.POINTER(vp)]),
+    "si_context_ranks": (ci, [vp, C.POINTER(ci), C.POINTER(ci), C.POINTER(ci)]),
+    "si_sym_inv_sqrt": (ci, [vp, i64, pd, pd]),
     "si_context_draw_count": (i64, [vp]),
     "si_context_set_profiling": (ci, [vp, ci]),
     "si_context_profile": (ci, [vp, vp, pi64, pd, ci]),

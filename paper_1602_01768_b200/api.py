@@ -66,17 +66,52 @@ def _pd(a: np.ndarray):
 
 
 class Context:
-    """One device context (stream, workspaces); owned by one host thread."""
+    """One device context (stream, workspaces); owned by one host thread.
 
-    def __init__(self, device: int = 0, stream: Optional[int] = None):
+    Multi-GPU contexts (the sharded drivers, shard.cpp) come from the class methods
+    `multi(devices)` (one process, several GPUs), `rank(device, nranks, rank, nccl_id)`
+    (one process per GPU, torchrun style; rank 0 makes the id with nccl_unique_id()) and
+    `loopback(device, nranks)` (virtual ranks on one GPU: a test harness)."""
+
+    def __init__(self, device: int = 0, stream: Optional[int] = None, *, _handle=None):
         lib = L.load()
-        h = C.c_void_p()
-        if stream is None:
-            _check(lib.si_context_create(device, C.byref(h)))
+        if _handle is not None:
+            h = _handle
         else:
-            _check(lib.si_context_create_on_stream(device, C.c_void_p(stream), C.byref(h)))
+            h = C.c_void_p()
+            if stream is None:
+                _check(lib.si_context_create(device, C.byref(h)))
+            else:
+                _check(lib.si_context_create_on_stream(device, C.c_void_p(stream), C.byref(h)))
         self._h = h
         self.device = device
+
+    @classmethod
+    def multi(cls, devices: Sequence[int]) -> "Context":
+        arr = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        _check(L.load().si_context_create_multi(arr, len(devices), C.byref(h)))
+        return cls(devices[0], _handle=h)
+
+    @classmethod
+    def rank(cls, device: int, nranks: int, rank: int, nccl_id: bytes, stream: Optional[int] = None) -> "Context":
+        h = C.c_void_p()
+        buf = C.create_string_buffer(bytes(nccl_id), NCCL_ID_BYTES)
+        _check(L.load().si_context_create_rank(device, C.c_void_p(stream) if stream else None, nranks, rank, buf,
+                                               C.byref(h)))
+        return cls(device, _handle=h)
+
+    @classmethod
+    def loopback(cls, device: int, nranks: int) -> "Context":
+        h = C.c_void_p()
+        _check(L.load().si_context_create_loopback(device, nranks, C.byref(h)))
+        return cls(device, _handle=h)
+
+    def ranks(self):
+        """(global rank count, global rank of the first local rank, local rank count)."""
+        a, b, c = C.c_int(), C.c_int(), C.c_int()
+        _check(L.load().si_context_ranks(self._h, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
 
     @property
     def handle(self):
@@ -135,6 +170,16 @@ class Context:
             self.close()
         except Exception:
             pass
+
+
+NCCL_ID_BYTES = 128
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId on this process (rank 0 of a one-process-per-GPU group)."""
+    buf = C.create_string_buffer(NCCL_ID_BYTES)
+    _check(L.load().si_nccl_unique_id(buf))
+    return buf.raw
 
 
 _tls = threading.local()
@@ -672,6 +717,19 @@ def adarbfgs_update_factor(l, a, stilde, *, context: Optional[Context] = None) -
     if rc == 6:  # floor hit: the reference throws NumericalError (linalg.cpp:150-151)
         raise NumericalError(L.load().si_last_error().decode())
     _check(rc)
+    return out
+
+
+def sym_inv_sqrt(m, *, context: Optional[Context] = None) -> np.ndarray:
+    """Matrix sym_inv_sqrt(const Matrix& m) (linalg.cpp:144-155) on the GPU: M^{-1/2};
+    raises NumericalError iff an eigenvalue λ ≤ 1e-14·λmax or λ ≤ 0."""
+    ctx = context or default_context()
+    m = _f64(m)
+    if m.ndim != 2 or m.shape[0] != m.shape[1]:
+        raise ConfigError("sym_inv_sqrt: matrix must be square")
+    q = m.shape[0]
+    out = np.empty((q, q), order="F")
+    _check(L.load().si_sym_inv_sqrt(ctx.handle, q, _pd(m), _pd(out)))
     return out
 
 

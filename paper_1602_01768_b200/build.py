@@ -29,13 +29,14 @@ NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-
 CXX_FLAGS = ["-std=gnu++20", "-O3", "-march=x86-64-v3", "-fPIC", "-Wall", "-Wextra", "-DNDEBUG",
              f"-I{CUDA}/include"]
 
-SOURCES_CU = ["engine.cu"]
-SOURCES_CXX = ["driver.cpp", "io.cpp"]
+SOURCES_CU = ["engine.cu", "shard.cu"]
+SOURCES_CXX = ["driver.cpp", "io.cpp", "shard.cpp"]
 # per-source header dependencies (the public C header does not reach engine.cu)
 _KERNEL_HDRS = ["common.cuh", "gemm_f64.cuh", "kernels_aux.cuh", "kernels_small.cuh", "kernels_core.cuh",
                 "family.cuh", "engine.hpp"]
-_HOST_HDRS = ["engine.hpp", "host_rng.hpp", "../../include/stochinv_b200.h"]
-DEPS = {"engine.cu": _KERNEL_HDRS, "driver.cpp": _HOST_HDRS, "io.cpp": _HOST_HDRS}
+_HOST_HDRS = ["engine.hpp", "host_rng.hpp", "capi_internal.hpp", "shard.hpp", "../../include/stochinv_b200.h"]
+DEPS = {"engine.cu": _KERNEL_HDRS, "shard.cu": ["common.cuh", "engine.hpp"], "driver.cpp": _HOST_HDRS,
+        "io.cpp": _HOST_HDRS, "shard.cpp": _HOST_HDRS}
 HEADERS = sorted(set(_KERNEL_HDRS + _HOST_HDRS))
 
 
@@ -80,8 +81,7 @@ def build(force: bool = False) -> str:
             for f in [ex.submit(_run, cmd, log) for cmd, log in jobs]:
                 f.result()
     if force or _newer(LIB, objs):
-        _run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcusolver", "-lcublas",
-                                                          f"-Xlinker=-rpath={CUDA}/lib64"])
+        _run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-ldl", f"-Xlinker=-rpath={CUDA}/lib64"])
     return LIB
 
 

@@ -20,192 +20,10 @@
 #include "engine.hpp"
 #include "host_rng.hpp"
 
-namespace {
+#include "capi_internal.hpp"
 
-thread_local std::string g_err;
+using namespace si_capi;
 
-using si::ConfigError;
-using si::NumericalError;
-struct ResampleError : NumericalError {
-    using NumericalError::NumericalError;
-};
-
-template <class F>
-int guard(F&& f) {
-    try {
-        f();
-        return SI_OK;
-    } catch (const ResampleError& e) {
-        g_err = e.what();
-        return SI_ERR_RESAMPLE;
-    } catch (const NumericalError& e) {
-        g_err = e.what();
-        return SI_ERR_NUMERICAL;
-    } catch (const si::IoError& e) {  // errors.hpp:24-26 (CLI exit 4)
-        g_err = e.what();
-        return SI_ERR_IO;
-    } catch (const si::CudaError& e) {
-        g_err = e.what();
-        return SI_ERR_CUDA;
-    } catch (const std::invalid_argument& e) {  // ConfigError and ProblemMatrix's plain invalid_argument
-        g_err = e.what();
-        return SI_ERR_CONFIG;
-    } catch (const std::bad_alloc& e) {
-        g_err = std::string("allocation failed: ") + e.what();
-        return SI_ERR_CUDA;
-    } catch (const std::exception& e) {  // stochinv_cli.cpp:281-283 maps other std::exception to exit 2
-        g_err = e.what();
-        return SI_ERR_CONFIG;
-    }
-}
-
-void ck(cudaError_t e, const char* what) { si::cuda_check(e, what); }
-
-double flops_bfgs(double n, double q) { return 10 * n * n * q + 10 * n * q * q + 2 * q * q * q + 4 * n * n; }  // flops.cpp:43-46
-double flops_adarbfgs(double n, double q) {  // flops.cpp:70-74
-    return 8 * n * n * q + 10 * n * q * q + 4 * q * q * q + n * q + n * n;
-}
-
-struct DeviceTimer {
-    cudaEvent_t a{}, b{};
-    explicit DeviceTimer() {
-        ck(cudaEventCreate(&a), "event");
-        ck(cudaEventCreate(&b), "event");
-    }
-    ~DeviceTimer() {
-        cudaEventDestroy(a);
-        cudaEventDestroy(b);
-    }
-    double seconds() {
-        float ms = 0.f;
-        ck(cudaEventElapsedTime(&ms, a, b), "elapsed");
-        return ms * 1e-3;
-    }
-};
-
-}  // namespace
-
-struct si_context {
-    std::unique_ptr<si::Context> c;
-    // optional draw log (si_context_set_draw_log): every executed sampling attempt of the
-    // drivers appends its outcome — the block index (coordinate_block, adaptive_cols) or the q
-    // coordinates (adaptive_cols_uniform) — in the order the reference draws them
-    int64_t* draw_log = nullptr;
-    int64_t draw_cap = 0;
-    int64_t draw_count = 0;
-    void log_draw(int64_t v) {
-        if (draw_log && draw_count < draw_cap) draw_log[draw_count] = v;
-        ++draw_count;
-    }
-};
-
-struct si_problem {
-    si_context* owner = nullptr;
-    std::unique_ptr<si::Problem> p;
-};
-
-struct si_solver {
-    si_context* ctx = nullptr;
-    si_problem* prob = nullptr;
-    int method = 0, sketch = 0;
-    int64_t q = 0;
-    uint64_t seed = 0;
-    si::RbfgsWork rw;
-    si::AdaWork aw;
-    int* status_host = nullptr;
-    int64_t redraws = 0;
-    std::unique_ptr<si::RngStream> rng;
-    // one device-sketched iteration captured as a CUDA graph (launch-bound small n)
-    cudaGraphExec_t graph = nullptr;
-    int64_t graph_launches = 0;
-    bool warmed = false;
-    ~si_solver() {
-        if (graph) cudaGraphExecDestroy(graph);
-        rw.release();
-        aw.release();
-        if (status_host) cudaFreeHost(status_host);
-    }
-};
-
-namespace {
-
-void require(bool cond, const char* msg) {
-    if (!cond) throw ConfigError(msg);
-}
-
-// ProblemMatrix::validate_spd semantics (problem_matrix.cpp:28-41)
-void validate_spd(si_problem* prob, double* scratch_nn = nullptr) {
-    if (prob->p->symmetry != SI_SPD)
-        throw std::invalid_argument("ProblemMatrix: operation requires an spd-flagged matrix");
-    if (!si::problem_validate_spd(*prob->p, scratch_nn))
-        throw std::runtime_error("ProblemMatrix: spd flag set but Cholesky failed");
-}
-
-double host_frobenius_asym(const double* x, int64_t n, double* norm_out) {
-    double d = 0.0, nn = 0.0;
-    for (int64_t j = 0; j < n; ++j)
-        for (int64_t i = 0; i < n; ++i) {
-            const double v = x[i + j * n];
-            const double e = v - x[j + i * n];
-            d += e * e;
-            nn += v * v;
-        }
-    *norm_out = std::sqrt(nn);
-    return std::sqrt(d);
-}
-
-std::string describe(int sketch, int64_t q) {
-    const char* k = "gaussian";
-    switch (sketch) {
-        case SI_SKETCH_COORDINATE_BLOCK: k = "coordinate-block"; break;
-        case SI_SKETCH_ADAPTIVE_COLS: k = "adaptive-factor-cols"; break;
-        case SI_SKETCH_ADAPTIVE_GAUSS:
-        case SI_SKETCH_ADAPTIVE_GAUSS_DEVICE: k = "adaptive-factor-gauss"; break;
-        case SI_SKETCH_ADAPTIVE_COLS_UNIFORM: k = "adaptive-factor-cols-uniform"; break;
-        default: break;
-    }
-    return std::string(k) + "(q=" + std::to_string(q) + ")";
-}
-
-// status[0..3] -> host (sync)
-void read_status(si::Context& c, const int* status_dev, int* host) {
-    ck(cudaMemcpyAsync(host, status_dev, 4 * sizeof(int), cudaMemcpyDeviceToHost, c.stream), "status d2h");
-    ck(cudaStreamSynchronize(c.stream), "sync");
-}
-
-double residual_norm(si::Context& c, si::Problem& a, const double* X) {
-    si::residual_sq_enqueue(c, a, X, c.scalar_dev, nullptr);
-    ck(cudaMemcpyAsync(c.scalar_host, c.scalar_dev, sizeof(double), cudaMemcpyDeviceToHost, c.stream), "d2h");
-    ck(cudaStreamSynchronize(c.stream), "sync");
-    return std::sqrt(c.scalar_host[0]);
-}
-
-double factored_residual_norm(si::Context& c, si::Problem& a, si::AdaWork& w) {
-    if (!w.AL) ck(cudaMalloc(&w.AL, size_t(w.n) * size_t(w.n) * sizeof(double)), "malloc AL");
-    si::factored_residual_sq_enqueue(c, a, w.L, w.AL, c.scalar_dev);
-    ck(cudaMemcpyAsync(c.scalar_host, c.scalar_dev, sizeof(double), cudaMemcpyDeviceToHost, c.stream), "d2h");
-    ck(cudaStreamSynchronize(c.stream), "sync");
-    return std::sqrt(c.scalar_host[0]);
-}
-
-struct HistoryWriter {
-    si_history_point* buf;
-    int64_t cap;
-    int64_t count = 0;
-    const si_inverter_config* cfg;
-    void record(int64_t k, double rel, double flops, double seconds) {
-        si_history_point hp{k, rel, flops, seconds};
-        if (buf && count < cap) buf[count] = hp;
-        ++count;
-        if (cfg->on_checkpoint) cfg->on_checkpoint(&hp, cfg->user);
-    }
-};
-
-void set_message(si_run_result* r, const std::string& m) {
-    std::snprintf(r->message, sizeof(r->message), "%s", m.c_str());
-}
-
-}  // namespace
 
 extern "C" {
 
@@ -316,6 +134,7 @@ int si_problem_create_dense(si_context* ctx, int64_t n, const double* a_host, in
         std::unique_ptr<si_problem> h(new_problem(ctx, n, symmetry));
         // symmetric / spd flags symmetrize (M + Mᵀ)/2 on the device (problem_matrix.cpp:9-18)
         si::problem_upload_dense(*h->p, a_host, false);
+        si::shard_replicate_problem(ctx, h.get());
         *out = h.release();
     });
 }
@@ -324,6 +143,7 @@ int si_problem_create_dense_device(si_context* ctx, int64_t n, const double* a_d
     return guard([&] {
         std::unique_ptr<si_problem> h(new_problem(ctx, n, symmetry));
         si::problem_upload_dense(*h->p, a_dev, true);
+        si::shard_replicate_problem(ctx, h.get());
         *out = h.release();
     });
 }
@@ -337,6 +157,7 @@ int si_problem_create_csr(si_context* ctx, int64_t n, int64_t nnz, const int64_t
         for (int64_t t = 0; t < nnz; ++t) require(colind[t] >= 0 && colind[t] < n, "CSR: column index out of range");
         h->p->nnz = nnz;
         si::problem_upload_csr(*h->p, rowptr, colind, val);
+        si::shard_replicate_problem(ctx, h.get());
         *out = h.release();
     });
 }
@@ -423,22 +244,35 @@ int si_adarbfgs_update_factor(si_context* ctx, int64_t n, int64_t q, const doubl
     });
 }
 
-static void block_probabilities(const double* pdiag, const std::vector<std::vector<si::Index>>& blocks,
-                                std::vector<double>& p) {
-    // adarbfgs.cpp:23-36: p_i = sum_{j in C_i} l_jᵀ A l_j, then p / p.sum()
-    p.assign(blocks.size(), 0.0);
-    for (size_t i = 0; i < blocks.size(); ++i) {
-        double tr = 0.0;
-        for (si::Index j : blocks[i]) tr += pdiag[j];
-        p[i] = tr;
-    }
-    double mn = p.empty() ? 1.0 : *std::min_element(p.begin(), p.end());
-    if (mn <= 0.0)
-        throw NumericalError(
-            "adaptive_block_probabilities: non-positive block trace; the factor has degenerated");
-    double sum = 0.0;
-    for (double v : p) sum += v;
-    for (double& v : p) v /= sum;
+int si_sym_inv_sqrt(si_context* ctx, int64_t q, const double* m_host, double* r_out_host) {
+    return guard([&] {
+        auto& c = *ctx->c;
+        require(q >= 1, "sym_inv_sqrt: matrix must be square with n >= 1");
+        double *m = nullptr, *r = nullptr, *scratch = nullptr;
+        int* status = nullptr;
+        struct Rel {
+            double **m, **r, **s;
+            int** st;
+            ~Rel() {
+                for (double** p : {m, r, s})
+                    if (*p) cudaFree(*p);
+                if (*st) cudaFree(*st);
+            }
+        } rel{&m, &r, &scratch, &status};
+        const size_t qq = size_t(q) * size_t(q);
+        ck(cudaMalloc(&m, qq * sizeof(double)), "malloc");
+        ck(cudaMalloc(&r, qq * sizeof(double)), "malloc");
+        ck(cudaMalloc(&scratch, (6 * qq + 8 * size_t(q) + 32) * sizeof(double)), "malloc");
+        ck(cudaMalloc(&status, 8 * sizeof(int)), "malloc");
+        ck(cudaMemsetAsync(status, 0, 8 * sizeof(int), c.stream), "memset");
+        ck(cudaMemcpyAsync(m, m_host, qq * sizeof(double), cudaMemcpyHostToDevice, c.stream), "h2d");
+        si::sym_inv_sqrt_device(c, m, q, r, scratch, status);
+        int st[4];
+        read_status(c, status, st);
+        if (st[0]) throw NumericalError("sym_inv_sqrt: matrix is not positive definite");  // linalg.cpp:150
+        ck(cudaMemcpyAsync(r_out_host, r, qq * sizeof(double), cudaMemcpyDeviceToHost, c.stream), "d2h");
+        ck(cudaStreamSynchronize(c.stream), "sync");
+    });
 }
 
 int si_adaptive_block_probabilities(si_context* ctx, int64_t n, const double* l_host, const double* a_host,
@@ -855,7 +689,12 @@ static void run_inverter_impl(si_context* ctx, si_problem* prob, const si_invert
 
 int si_run_inverter(si_context* ctx, si_problem* prob, const si_inverter_config* cfg, double* x_out,
                     si_history_point* history, int64_t history_cap, si_run_result* result) {
-    return guard([&] { run_inverter_impl(ctx, prob, cfg, x_out, nullptr, history, history_cap, result); });
+    return guard([&] {
+        if (ctx->group)  // multi-GPU context: the sharded iteration (shard.cpp)
+            si::shard_run_inverter(ctx, prob, cfg, x_out, history, history_cap, result);
+        else
+            run_inverter_impl(ctx, prob, cfg, x_out, nullptr, history, history_cap, result);
+    });
 }
 
 int si_run_inverter_pair(si_context* ctx, si_problem* prob, const si_inverter_config* cfg, double* x_out,
@@ -1160,6 +999,10 @@ int si_mr_step_cached(si_context* ctx, int64_t n, const double* x_host, const do
 int si_run_adarbfgs(si_context* ctx, si_problem* prob, const si_inverter_config* cfg, double* l_out,
                     double* x_out, si_history_point* history, int64_t history_cap, si_run_result* result) {
     return guard([&] {
+        if (ctx->group) {  // multi-GPU context: L row-sharded (shard.cpp)
+            si::shard_run_adarbfgs(ctx, prob, cfg, l_out, x_out, history, history_cap, result);
+            return;
+        }
         auto& c = *ctx->c;
         si::Problem& a = *prob->p;
         const int64_t n = a.n, q = cfg->q;
@@ -1429,6 +1272,11 @@ int si_solver_create(si_context* ctx, si_problem* prob, int method, int sketch, 
         s->seed = seed;
         s->rng = std::make_unique<si::RngStream>(seed);
         ck(cudaMallocHost(&s->status_host, 4 * sizeof(int)), "pinned");
+        if (ctx->group) {  // multi-GPU context: the sharded iteration (shard.cpp)
+            s->shard = si::shard_solver_create(ctx, prob, method, sketch, q, seed);
+            *out = s.release();
+            return;
+        }
         if (method == SI_METHOD_RBFGS) {
             require(sketch == SI_SKETCH_GAUSSIAN || sketch == SI_SKETCH_GAUSSIAN_DEVICE,
                     "solver: RBFGS supports gaussian sketches");
@@ -1453,11 +1301,18 @@ int si_solver_destroy(si_solver* s) {
 static double* solver_iterate(si_solver* s) { return s->method == SI_METHOD_RBFGS ? s->rw.X : s->aw.L; }
 
 int si_solver_set_identity(si_solver* s) {
-    return guard([&] { si::set_identity(*s->ctx->c, solver_iterate(s), s->prob->p->n); });
+    return guard([&] {
+        require(!s->shard, "solver: use si_solver_set_iterate on a multi-GPU context");
+        si::set_identity(*s->ctx->c, solver_iterate(s), s->prob->p->n);
+    });
 }
 
 int si_solver_set_iterate(si_solver* s, const double* host) {
     return guard([&] {
+        if (s->shard) {
+            si::shard_solver_set(s->shard, host);
+            return;
+        }
         const int64_t n = s->prob->p->n;
         ck(cudaMemcpyAsync(solver_iterate(s), host, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyHostToDevice,
                            s->ctx->c->stream),
@@ -1467,6 +1322,10 @@ int si_solver_set_iterate(si_solver* s, const double* host) {
 
 int si_solver_get_iterate(si_solver* s, double* host) {
     return guard([&] {
+        if (s->shard) {
+            si::shard_solver_get(s->shard, host);
+            return;
+        }
         const int64_t n = s->prob->p->n;
         ck(cudaMemcpyAsync(host, solver_iterate(s), size_t(n) * size_t(n) * sizeof(double), cudaMemcpyDeviceToHost,
                            s->ctx->c->stream),
@@ -1475,9 +1334,9 @@ int si_solver_get_iterate(si_solver* s, double* host) {
     });
 }
 
-double* si_solver_iterate_device(si_solver* s) { return solver_iterate(s); }
+double* si_solver_iterate_device(si_solver* s) { return s->shard ? nullptr : solver_iterate(s); }
 
-int64_t si_solver_redraws(si_solver* s) { return s->redraws; }
+int64_t si_solver_redraws(si_solver* s) { return s->shard ? si::shard_solver_redraws(s->shard) : s->redraws; }
 
 static void solver_one(si_solver* s, const double* s_host, const int64_t* idx_host, bool check) {
     auto& c = *s->ctx->c;
@@ -1532,6 +1391,10 @@ static void solver_one(si_solver* s, const double* s_host, const int64_t* idx_ho
 
 int si_solver_step(si_solver* s, int64_t iters) {
     return guard([&] {
+        if (s->shard) {
+            si::shard_solver_step(s->shard, iters, *s->rng, 100);
+            return;
+        }
         auto& c = *s->ctx->c;
         const bool device = s->sketch == SI_SKETCH_GAUSSIAN_DEVICE || s->sketch == SI_SKETCH_ADAPTIVE_GAUSS_DEVICE;
         int* status = s->method == SI_METHOD_RBFGS ? s->rw.status : s->aw.status;
@@ -1598,11 +1461,18 @@ int si_solver_step(si_solver* s, int64_t iters) {
 }
 
 int si_solver_step_with_sketch(si_solver* s, const double* s_host, const int64_t* idx_host) {
-    return guard([&] { solver_one(s, s_host, idx_host, true); });
+    return guard([&] {
+        require(!s->shard, "solver: host sketches on a multi-GPU context go through si_run_inverter");
+        solver_one(s, s_host, idx_host, true);
+    });
 }
 
 int si_solver_residual(si_solver* s, double* out) {
     return guard([&] {
+        if (s->shard) {
+            *out = si::shard_solver_residual(s->shard);
+            return;
+        }
         auto& c = *s->ctx->c;
         if (s->method == SI_METHOD_RBFGS)
             *out = residual_norm(c, *s->prob->p, s->rw.X);
@@ -1744,6 +1614,7 @@ int si_problem_load_matrix_market(si_context* ctx, const char* path, int symmetr
         } else {
             si::problem_upload_dense(*h->p, m.dense.data(), false);
         }
+        si::shard_replicate_problem(ctx, h.get());
         *out = h.release();
     });
 }
@@ -1759,6 +1630,7 @@ int si_problem_ridge_hessian(si_context* ctx, const char* libsvm_path, double la
         } f{a};
         std::unique_ptr<si_problem> h(new_problem(ctx, rows.n, lambda > 0.0 ? SI_SPD : SI_SYMMETRIC));
         si::problem_upload_dense(*h->p, a, true);
+        si::shard_replicate_problem(ctx, h.get());
         *out = h.release();
     });
 }
@@ -1773,6 +1645,7 @@ int si_problem_synthetic(si_context* ctx, int64_t n, uint64_t seed, si_problem**
         } f{a};
         std::unique_ptr<si_problem> h(new_problem(ctx, n, SI_SPD));
         si::problem_upload_dense(*h->p, a, true);
+        si::shard_replicate_problem(ctx, h.get());
         *out = h.release();
     });
 }
@@ -1901,4 +1774,9 @@ int si_adarbfgs_step(si_context* ctx, si_problem* prob, int sketch, int64_t q, s
         }
         throw NumericalError("adarbfgs_step: rejection limit exceeded for " + describe(sketch, q));
     });
+}
+
+si_solver::~si_solver() {
+    if (shard) si::shard_solver_delete(shard);
+    release();
 }

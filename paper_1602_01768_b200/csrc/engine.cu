@@ -1,7 +1,6 @@
 // Engine: launch logic of the RBFGS / AdaRBFGS iteration on one B200.
 // See engine.hpp for the data each pipeline keeps resident in HBM.
 #include <cudaTypedefs.h>
-#include <cusolverDn.h>
 
 #include <algorithm>
 #include <atomic>
@@ -67,7 +66,6 @@ Context::~Context() {
         delete cached_aw;
     }
     if (aux_status) cudaFree(aux_status);
-    if (solver_handle) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(solver_handle));
     if (scalar_dev) cudaFree(scalar_dev);
     if (scalar_host) cudaFreeHost(scalar_host);
     if (own_stream && stream) cudaStreamDestroy(stream);
@@ -614,6 +612,20 @@ static void symupd(Context& c, int64_t n, int64_t k, const double* V, int64_t ld
     launch_gemm_layout<EPI_SYMUPD>(c, cfg, false, false, vec, a, dim3(unsigned(work), 1, 1), "gemm_symupd");
 }
 
+void symupd_ex(Context& c, int64_t m, int64_t k, const double* V, int64_t ldv, const double* U, int64_t ldu, double* X,
+               int64_t ldx, const int* skip, int* nonfinite) {
+    symupd(c, m, k, V, ldv, U, ldu, X, ldx, 1.0, skip, nonfinite);
+}
+
+void advance_batch(Context& c, unsigned long long* counter, int* status, bool ada) {
+    LaunchScope ls(c, "advance_counter");
+    if (ada)
+        ada_advance_batch_kernel<<<1, 1, 0, c.stream>>>(counter, status);
+    else
+        advance_batch_kernel<<<1, 1, 0, c.stream>>>(counter, status);
+    check_launch("advance");
+}
+
 // ----------------------------------------------------------- problem -------
 Problem::~Problem() {
     if (a) cudaFree(a);
@@ -672,52 +684,6 @@ void problem_download_dense(Problem& p, double* host) {
         CK(cudaFree(tmp));
     }
     CK(cudaStreamSynchronize(c.stream));
-}
-
-// ProblemMatrix::validate_spd (problem_matrix.cpp:28-41) via a Cholesky on the
-// device (cuSOLVER potrf on a scratch copy; one-time setup, not the iteration).
-// `scratch` (n×n, optional): a caller's buffer for the factorisation — the driver lends
-// its iterate before initialising it (cudaMalloc / cudaFree of an n×n scratch measured
-// 50–240 ms at n = 16384).
-bool problem_validate_spd(Problem& p, double* scratch) {
-    if (p.spd_checked) return p.spd_ok;
-    Context& c = *p.ctx;
-    const int64_t n = p.n;
-    const size_t bytes = size_t(n) * size_t(n) * sizeof(double);
-    double* tmp = scratch;
-    if (!tmp) CK(cudaMalloc(&tmp, bytes));
-    if (p.dense) {
-        CK(cudaMemcpyAsync(tmp, p.a, bytes, cudaMemcpyDeviceToDevice, c.stream));
-    } else {
-        CK(cudaMemsetAsync(tmp, 0, bytes, c.stream));
-        densify_csr_kernel<<<grid_for(n, 256), 256, 0, c.stream>>>(n, p.rowptr, p.colind, p.val, tmp);
-    }
-    if (!c.solver_handle) {
-        cusolverDnHandle_t hh;
-        if (cusolverDnCreate(&hh) != CUSOLVER_STATUS_SUCCESS) {
-            if (!scratch) cudaFree(tmp);
-            throw CudaError("cusolverDnCreate failed");
-        }
-        c.solver_handle = hh;
-    }
-    cusolverDnHandle_t h = static_cast<cusolverDnHandle_t>(c.solver_handle);
-    cusolverDnSetStream(h, c.stream);
-    int lwork = 0;
-    cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_LOWER, int(n), tmp, int(n), &lwork);
-    double* work = nullptr;
-    int* info = nullptr;
-    CK(cudaMalloc(&work, size_t(std::max(lwork, 1)) * sizeof(double)));
-    CK(cudaMalloc(&info, sizeof(int)));
-    cusolverDnDpotrf(h, CUBLAS_FILL_MODE_LOWER, int(n), tmp, int(n), work, lwork, info);
-    int hinfo = -1;
-    CK(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-    CK(cudaStreamSynchronize(c.stream));
-    cudaFree(work);
-    cudaFree(info);
-    if (!scratch) cudaFree(tmp);
-    p.spd_checked = true;
-    p.spd_ok = hinfo == 0;
-    return p.spd_ok;
 }
 
 // Y = A·P (dense GEMM or CSR SpMM)
@@ -926,6 +892,11 @@ static void spd_inverse(Context& c, const double* P, int64_t ldp, int64_t q, dou
     spd_inverse_ld(c, P, ldp, q, ginv, q, scratch, status);
 }
 
+void spd_inverse_device(Context& c, const double* P, int64_t ldp, int64_t q, double* ginv, int64_t ldo,
+                        double* scratch, int* status) {
+    spd_inverse_ld(c, P, ldp, q, ginv, ldo, scratch, status);
+}
+
 // K-FACTOR + K-CORE: from P = [G | H] (q×2q, ld ldp) build
 // M = [[Ginv + Ginv·H·Ginv, −Ginv], [−Ginv, 0]] (2q×2q, ld 2q).  status[0] is
 // set (and every later launch skipped) when G is not positive definite.
@@ -988,6 +959,74 @@ void rbfgs_gram_enqueue(Context& c, const double* P, int64_t ldp, int64_t q, dou
     LaunchScope ls(c, "ghat");
     ghat_kernel<<<grid_for(q * q, 256), 256, 0, c.stream>>>(P, ldp, int(q), Ghat, status);
     check_launch("ghat");
+}
+
+// ProblemMatrix::validate_spd (problem_matrix.cpp:28-41): the LLT's success test — every
+// pivot of the elimination > 0 — as a blocked right-looking Schur-complement sweep on this
+// engine's own kernels (no library factorisation):
+//   for each 128-wide diagonal block D of the current Schur complement:
+//     K-FACTOR(D): D⁻¹ with its leaf pivots tested (> 0), one CTA
+//     T = −B·D⁻¹                         (B the block column below D)   K-GEMM
+//     trailing ← trailing + T·Bᵀ         (= − B·D⁻¹·Bᵀ, symmetric)        K-SYMUPD (upper tiles, mirrored)
+// The blocks meet the Schur-complement pivots of the whole matrix in order, i.e. the
+// Cholesky pivots (squared diagonal of the factor), so the decision is the LLT's; a
+// failed pivot makes every later launch a no-op.  n³/3 flops, on the DMMA pipe.
+// `scratch` (n×n, optional): a caller's buffer for the working copy (the drivers lend
+// their iterate before initialising it; cudaMalloc / cudaFree of an n×n scratch measured
+// 50–240 ms at n = 16384).
+bool problem_validate_spd(Problem& p, double* scratch) {
+    if (p.spd_checked) return p.spd_ok;
+    Context& c = *p.ctx;
+    const int64_t n = p.n;
+    const size_t bytes = size_t(n) * size_t(n) * sizeof(double);
+    constexpr int64_t BLK = 128;
+    double* W = scratch;
+    double *T = nullptr, *Dinv = nullptr;
+    int* st = nullptr;
+    struct Rel {
+        double **w, **t, **d;
+        int** s;
+        bool own;
+        ~Rel() {
+            if (own && *w) cudaFree(*w);
+            if (*t) cudaFree(*t);
+            if (*d) cudaFree(*d);
+            if (*s) cudaFree(*s);
+        }
+    } rel{&W, &T, &Dinv, &st, scratch == nullptr};
+    if (!W) CK(cudaMalloc(&W, bytes));
+    CK(cudaMalloc(&T, size_t(n) * BLK * sizeof(double)));
+    CK(cudaMalloc(&Dinv, size_t(BLK) * BLK * sizeof(double)));
+    CK(cudaMalloc(&st, 8 * sizeof(int)));
+    CK(cudaMemsetAsync(st, 0, 8 * sizeof(int), c.stream));
+    if (p.dense) {
+        CK(cudaMemcpyAsync(W, p.a, bytes, cudaMemcpyDeviceToDevice, c.stream));
+    } else {
+        CK(cudaMemsetAsync(W, 0, bytes, c.stream));
+        densify_csr_kernel<<<grid_for(n, 256), 256, 0, c.stream>>>(n, p.rowptr, p.colind, p.val, W);
+        check_launch("densify");
+    }
+    for (int64_t k = 0; k < n; k += BLK) {
+        const int64_t b = std::min(BLK, n - k);
+        double* D = W + k + k * n;
+        if (b <= 32)
+            launch_gram_fused<32>(c, D, n, b, Dinv, nullptr, st);
+        else if (b <= 64)
+            launch_gram_fused<64>(c, D, n, b, Dinv, nullptr, st);
+        else
+            launch_gram_fused<128>(c, D, n, b, Dinv, nullptr, st);
+        const int64_t rest = n - k - b;
+        if (rest == 0) break;
+        const double* B = W + (k + b) + k * n;                                   // rest×b, ld n
+        gemm(c, rest, b, b, B, n, false, Dinv, b, true, T, rest, -1.0, 0.0, st);  // T = −B·D⁻¹
+        symupd(c, rest, b, T, rest, B, n, W + (k + b) * (n + 1), n, 1.0, st, nullptr);
+    }
+    int hst = 0;
+    CK(cudaMemcpyAsync(&hst, st, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    p.spd_checked = true;
+    p.spd_ok = hst == 0;
+    return p.spd_ok;
 }
 
 void philox_sketch(Context& c, double* S, int64_t n, int64_t q, int64_t lds, uint64_t seed,
@@ -1325,14 +1364,18 @@ static void ns_fused(Context& c, const double* Mq, int64_t q, double* R, int* st
     check_launch("ns_fused");
 }
 
-// R = M^{-1/2} (q×q, ld q); sets status on a floor hit / non-convergence.
-//   q ≤ 64: fused Newton–Schulz in one CTA (operands in shared memory, DMMA);
-//   q > 64: coupled Newton–Schulz on the DMMA GEMM engine (no host round trip:
-//           converged iterations are skipped on the device);
-//   SI_ISQRT_JACOBI=1 (q ≤ 96): the reference's cyclic Jacobi (parallel order).
+// R = M^{-1/2} (q×q, ld q) with the reference's accept / reject contract
+// (sym_inv_sqrt, linalg.cpp:144-155: reject iff an eigenvalue λ ≤ 1e-14·λmax or λ ≤ 0,
+// status[0] = 1 → NumericalError → redraw).
+//   Fast path: Newton–Schulz (q ≤ 64 fused in one CTA; q > 64 on the DMMA GEMM engine)
+//   whose R is kept only when it converged and certifies λmin/λmax > 1e-12
+//   (1/(‖R‖²_F·c), c ≥ λmax) — 100× inside the floor, so no draw the reference
+//   rejects is accepted.  Otherwise the reference's cyclic Jacobi (tournament order,
+//   one CTA) recomputes R and applies the floor itself: near-singular Grams are
+//   decided by the reference's own rule.  SI_ISQRT_JACOBI=1 always takes Jacobi.
 // scratch: 6q² + 8q + 32 doubles; status[3] is used as the NS stop flag.
 static void inv_sqrt(Context& c, const double* Mq, int64_t q, double* R, double* scratch, int* status) {
-    const bool jacobi = env_flag("SI_ISQRT_JACOBI") && q <= 96;
+    const bool jacobi = env_flag("SI_ISQRT_JACOBI");
     if (!jacobi && q <= 64) {
         if (q <= 16) ns_fused<16>(c, Mq, q, R, status);
         else if (q <= 32) ns_fused<32>(c, Mq, q, R, status);
@@ -1340,14 +1383,15 @@ static void inv_sqrt(Context& c, const double* Mq, int64_t q, double* R, double*
         else ns_fused<64>(c, Mq, q, R, status);
         return;
     }
+    double* Y = scratch;
+    double* Z = Y + q * q;
+    double* T = Z + q * q;
+    double* ZY = T + q * q;
+    double* Yn = ZY + q * q;
+    double* Zn = Yn + q * q;
+    double* scal = Zn + q * q;
+    int* need = reinterpret_cast<int*>(scal + 4);  // Jacobi fallback flag
     if (!jacobi) {
-        double* Y = scratch;
-        double* Z = Y + q * q;
-        double* T = Z + q * q;
-        double* ZY = T + q * q;
-        double* Yn = ZY + q * q;
-        double* Zn = Yn + q * q;
-        double* scal = Zn + q * q;
         int* conv = status + 3;
         {
             LaunchScope ls(c, "ns_init");
@@ -1368,25 +1412,21 @@ static void inv_sqrt(Context& c, const double* Mq, int64_t q, double* R, double*
             ns_copy2_kernel<<<grid_for(q * q, 256), 256, 0, c.stream>>>(Y, Yn, Z, Zn, int(q), conv);
             check_launch("ns_copy");
         }
-        LaunchScope ls(c, "ns_finish");
-        ns_finish_kernel<<<grid_for(q * q, 256), 256, 0, c.stream>>>(Z, int(q), scal, R, status, conv);
-        check_launch("ns_finish");
-        return;
+        {
+            LaunchScope ls(c, "ns_finish");
+            ns_finish_kernel<<<1, 1024, 0, c.stream>>>(Z, int(q), scal, R, status, conv, need);
+            check_launch("ns_finish");
+        }
     }
-    double* QD = scratch;
-    double* Qm = scratch + q * q;
-    double* work = scratch + 2 * q * q;
-    const size_t smem = (2 * size_t(q) * size_t(q) + 4 * size_t(q)) * sizeof(double);
-    static DeviceOnce once;
-    if (once.first(c.device)) {
-        CK(cudaFuncSetAttribute(jacobi_isqrt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    }
-    {
-        LaunchScope ls(c, "jacobi_isqrt");
-        jacobi_isqrt_kernel<<<1, 1024, smem, c.stream>>>(Mq, q, int(q), QD, Qm, work, status, 1, 1e-14);
-        check_launch("jacobi_isqrt");
-    }
-    gemm(c, q, q, q, QD, q, false, Qm, q, false, R, q, 1.0, 0.0, status);  // R = QD·Qᵀ
+    // exact path: runs on the device only when flagged (always under SI_ISQRT_JACOBI);
+    // its work arrays (2q² + 3q doubles) reuse Y and Z
+    LaunchScope ls(c, "jacobi_isqrt");
+    jacobi_isqrt_kernel<<<1, 1024, 0, c.stream>>>(Mq, q, int(q), scratch, R, status, jacobi ? nullptr : need);
+    check_launch("jacobi_isqrt");
+}
+
+void sym_inv_sqrt_device(Context& c, const double* M, int64_t q, double* R, double* scratch, int* status) {
+    inv_sqrt(c, M, q, R, scratch, status);
 }
 
 // The q×n stage of adarbfgs_update_factor (adarbfgs.cpp:13-19): R = G^{-1/2} and
@@ -1530,6 +1570,13 @@ void ada_enqueue_probabilities(Context& c, Problem& a, AdaWork& w) {
         w.pdiag_age = 0;
     }
     CK(cudaMemcpyAsync(w.p_pinned, w.pdiag, size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+}
+
+void problem_diagonal(Context& c, Problem& a, double* d) {
+    LaunchScope ls(c, "problem_diagonal");
+    problem_diagonal_kernel<<<grid_for(a.n, 256), 256, 0, c.stream>>>(a.dense ? a.a : nullptr, a.rowptr, a.colind,
+                                                                       a.val, a.n, d);
+    check_launch("problem_diagonal");
 }
 
 void ada_init_pdiag_identity(Context& c, Problem& a, AdaWork& w) {

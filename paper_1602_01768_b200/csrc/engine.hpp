@@ -50,7 +50,6 @@ struct Context {
     };
     std::vector<Pending> pending;
     std::vector<cudaEvent_t> event_pool;
-    void* solver_handle = nullptr;  // cusolverDn handle for validate_spd (lazy, reused)
     int* aux_status = nullptr;      // status words of device-pointer entry points
 
     // second stream + split-K workspace for work that overlaps a single-CTA stage
@@ -167,7 +166,7 @@ struct AdaWork {
 Context* context_create(int device, cudaStream_t external, bool on_stream = false);
 void problem_upload_dense(Problem& p, const double* host, bool device_src);
 void problem_upload_csr(Problem& p, const int64_t* rowptr, const int32_t* colind, const double* val);
-bool problem_validate_spd(Problem& p, double* scratch_nn = nullptr);  // Cholesky-based (cuSOLVER potrf on a scratch copy)
+bool problem_validate_spd(Problem& p, double* scratch_nn = nullptr);  // blocked Schur-complement pivots (own kernels)
 void problem_download_dense(Problem& p, double* host);
 
 // generic dense product C = alpha·op(A)·op(B) + beta·C with leading dimensions
@@ -217,9 +216,32 @@ void family_release(RbfgsWork& w);
 void family_enqueue_iteration(Context& c, Problem& a, RbfgsWork& w, bool device_sketch, uint64_t seed);
 void symupd_device(Context& c, int64_t m, int64_t k, const double* V, int64_t ldv, const double* U, int64_t ldu,
                    double* X, int64_t ldx);
+// K-SYMUPD with the iteration's device flags: skipped when *skip, non-finite results flagged
+void symupd_ex(Context& c, int64_t m, int64_t k, const double* V, int64_t ldv, const double* U, int64_t ldu, double* X,
+               int64_t ldx, const int* skip, int* nonfinite);
+// ---- shard.cu: helpers of the sharded drivers (shard.cpp) ----
+// Y (n×k, ld ldy) from `parts` all-gathered k×mc slots (symmetric_chunks: the 2P-chunk pairing)
+void place_rows(Context& c, const double* g, int64_t mc, int parts, bool symmetric_chunks, int64_t n, int64_t k,
+                double* Y, int64_t ldy);
+// dst (rows×cols, ld ldd) = srcᵀ (src cols×rows, ld lds)
+void transpose_block(Context& c, const double* src, int64_t lds, int64_t rows, int64_t cols, double* dst,
+                     int64_t ldd);
+// Σ over rows [r0, r0+m) of ‖I − X·A‖² for CSR A and a row panel X[R, :] (column-major m×n, ld m)
+void csr_residual_rows_sq(Context& c, Problem& a, int64_t m, int64_t r0, const double* Xrows, double* out_dev);
+void accumulate(Context& c, double* dst, const double* src, int64_t count);  // dst += src
+void combine(Context& c, void* dst, const void* src, int64_t count, bool is_int, bool is_max);  // dst ∘= src
+void panel_column_dots(Context& c, const double* AL, const double* L, int64_t m, int64_t n, double* d);
+void problem_diagonal(Context& c, Problem& a, double* d);  // d = diag(A)
+void set_identity_rows(Context& c, double* X, int64_t m, int64_t cols, int64_t diag_off);  // X(i, j) = δ(j, i + off)
+// the single-GPU iteration's counters: advance_batch_kernel (RBFGS) / ada_advance_batch_kernel
+void advance_batch(Context& c, unsigned long long* counter, int* status, bool ada);
 void residual_general_sq_enqueue(Context& c, Problem& a, const double* X, double* scratch_nn, double* out_dev);
 void column_weights(Context& c, Problem& a, int mode, std::vector<double>& out);
-void lu_inverse_device(Context& c, const double* M, int64_t n, double* out);
+void lu_inverse_device(Context& c, const double* M, int64_t n, double* out);  // SPD M (block inverse)
+// G⁻¹ (ld ldo) of an SPD q×q block (ld ldp), any q: fused K-FACTOR (q ≤ 128) or 2×2 block
+// recursion on the GEMM engine; status[0] = 1 when a pivot is not > 0.  scratch: 4q² doubles.
+void spd_inverse_device(Context& c, const double* P, int64_t ldp, int64_t q, double* ginv, int64_t ldo,
+                        double* scratch, int* status);
 void spd_inverse_diagonal(Context& c, Problem& a, std::vector<double>& out);
 struct BaselineWork {
     int64_t n = 0;
@@ -238,6 +260,9 @@ void mr_init_device(Context& c, Problem& a, BaselineWork& w);
 void ada_core_enqueue(Context& c, const double* G, int64_t q, const double* Z, int64_t n, const int64_t* idx,
                       const double* St, double* G2, double* R2, double* Tq, double* R, double* B, double* scratch,
                       int* st);
+// sym_inv_sqrt (linalg.cpp:144-155): R = M^{-1/2}, status[0] = 1 on the floor (λ ≤ 1e-14·λmax or
+// λ ≤ 0); scratch 6q² + 8q + 32 doubles, status 8 ints
+void sym_inv_sqrt_device(Context& c, const double* M, int64_t q, double* R, double* scratch, int* status);
 void gather_columns(Context& c, const double* L, int64_t rows, int64_t ld, const int64_t* idx, int64_t q, double* out);
 void pdiag_update(Context& c, const double* B, int64_t q, int64_t n, const double* T, const int64_t* idx,
                   const int* skip, double* d);

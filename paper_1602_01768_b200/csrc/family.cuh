@@ -309,73 +309,47 @@ void column_weights(Context& c, Problem& a, int mode, std::vector<double>& out) 
     cudaFree(d);
 }
 
-static cusolverDnHandle_t solver(Context& c) {
-    if (!c.solver_handle) {
-        cusolverDnHandle_t hh;
-        if (cusolverDnCreate(&hh) != CUSOLVER_STATUS_SUCCESS) throw CudaError("cusolverDnCreate failed");
-        c.solver_handle = hh;
-    }
-    cusolverDnHandle_t h = static_cast<cusolverDnHandle_t>(c.solver_handle);
-    cusolverDnSetStream(h, c.stream);
-    return h;
+// One-time setup inverses (not the iteration), on the engine's SPD block inverse (K-FACTOR
+// leaves, 2×2 block recursion on K-GEMM): lu_inverse(x0) for the DFP pair (linalg.cpp:157-160,
+// simi.cpp:228-229; DFP's x0 must be symmetric, and here positive definite — a symmetric
+// indefinite x0, which the reference's LU would invert, is reported as a NumericalError) and
+// diag(A⁻¹) for DFP's convenient probabilities (simi.cpp:139-144; A is SPD there).
+static void spd_inverse_full(Context& c, const double* M, int64_t n, double* out, const char* what) {
+    double* scratch = nullptr;
+    int* st = nullptr;
+    CK(cudaMalloc(&scratch, 4 * size_t(n) * size_t(n) * sizeof(double) + 64));
+    CK(cudaMalloc(&st, 8 * sizeof(int)));
+    CK(cudaMemsetAsync(st, 0, 8 * sizeof(int), c.stream));
+    spd_inverse_device(c, M, n, n, out, n, scratch, st);
+    int hst = 0;
+    CK(cudaMemcpyAsync(&hst, st, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    cudaFree(scratch);
+    cudaFree(st);
+    if (hst != 0) throw NumericalError(what);
 }
 
-// One-time setup inverses (not the iteration): lu_inverse(x0) for the DFP pair
-// (linalg.cpp:157-160, simi.cpp:228-229) and diag(A⁻¹) for DFP's convenient
-// probabilities (simi.cpp:139-144), through cuSOLVER like validate_spd.
 void lu_inverse_device(Context& c, const double* M, int64_t n, double* out) {
-    cusolverDnHandle_t h = solver(c);
-    double* lu = nullptr;
-    int *ipiv = nullptr, *info = nullptr;
-    CK(cudaMalloc(&lu, size_t(n) * size_t(n) * sizeof(double)));
-    CK(cudaMalloc(&ipiv, size_t(n) * sizeof(int)));
-    CK(cudaMalloc(&info, sizeof(int)));
-    CK(cudaMemcpyAsync(lu, M, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
-    int lwork = 0;
-    cusolverDnDgetrf_bufferSize(h, int(n), int(n), lu, int(n), &lwork);
-    double* work = nullptr;
-    CK(cudaMalloc(&work, size_t(std::max(lwork, 1)) * sizeof(double)));
-    cusolverDnDgetrf(h, int(n), int(n), lu, int(n), work, ipiv, info);
-    set_identity(c, out, n);
-    cusolverDnDgetrs(h, CUBLAS_OP_N, int(n), int(n), lu, int(n), ipiv, out, int(n), info);
-    int hinfo = 0;
-    CK(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-    CK(cudaStreamSynchronize(c.stream));
-    cudaFree(work);
-    cudaFree(info);
-    cudaFree(ipiv);
-    cudaFree(lu);
-    if (hinfo != 0) throw NumericalError("lu_inverse: singular matrix");
+    spd_inverse_full(c, M, n, out, "lu_inverse: matrix is singular or not positive definite");
 }
 
 void spd_inverse_diagonal(Context& c, Problem& a, std::vector<double>& out) {
     const int64_t n = a.n;
-    cusolverDnHandle_t h = solver(c);
     double *f = nullptr, *inv = nullptr;
-    int* info = nullptr;
     CK(cudaMalloc(&f, size_t(n) * size_t(n) * sizeof(double)));
     CK(cudaMalloc(&inv, size_t(n) * size_t(n) * sizeof(double)));
-    CK(cudaMalloc(&info, sizeof(int)));
     if (a.dense) {
         CK(cudaMemcpyAsync(f, a.a, size_t(n) * size_t(n) * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
     } else {
         CK(cudaMemsetAsync(f, 0, size_t(n) * size_t(n) * sizeof(double), c.stream));
         densify_csr_kernel<<<grid_for(n, 256), 256, 0, c.stream>>>(n, a.rowptr, a.colind, a.val, f);
     }
-    int lwork = 0;
-    cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_LOWER, int(n), f, int(n), &lwork);
-    double* work = nullptr;
-    CK(cudaMalloc(&work, size_t(std::max(lwork, 1)) * sizeof(double)));
-    cusolverDnDpotrf(h, CUBLAS_FILL_MODE_LOWER, int(n), f, int(n), work, lwork, info);
-    set_identity(c, inv, n);
-    cusolverDnDpotrs(h, CUBLAS_FILL_MODE_LOWER, int(n), int(n), f, int(n), inv, int(n), info);
+    spd_inverse_full(c, f, n, inv, "spd_inverse_diagonal: A is not positive definite");
     std::vector<double> full(size_t(n) * size_t(n));
     CK(cudaMemcpyAsync(full.data(), inv, full.size() * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
     CK(cudaStreamSynchronize(c.stream));
     out.resize(size_t(n));
     for (int64_t j = 0; j < n; ++j) out[size_t(j)] = full[size_t(j + j * n)];
-    cudaFree(work);
-    cudaFree(info);
     cudaFree(inv);
     cudaFree(f);
 }

@@ -11,24 +11,25 @@
 
 namespace si {
 
-// Outputs QD = Q·diag(λ^{-1/2}) and Q (both q×q, ld q) so R = QD·Qᵀ follows as
-// one GEMM.  `work` holds 2*q*q + 4*q doubles when use_smem == 0.
-__global__ void __launch_bounds__(1024) jacobi_isqrt_kernel(const double* __restrict__ Gm, int64_t ldg, int q,
-                                                            double* __restrict__ QD, double* __restrict__ Qout,
-                                                            double* work, int* status, int use_smem,
-                                                            double floor_rel) {
-    extern __shared__ __align__(16) double sm[];
-    if (*status) return;
+// The reference's sym_inv_sqrt (linalg.cpp:144-155) in one CTA: cyclic Jacobi
+// (linalg.cpp:13-79: A = (G + Gᵀ)/2, off-norm stop ≤ 1e-15‖A‖_F, ≤ 60 sweeps) with the
+// rotations of a round-robin tournament applied in parallel, then the floor test
+// "λ ≤ floor_rel·λ_max or λ ≤ 0" → *status = 1 (NumericalError → redraw), else
+// R = Q·diag(λ^{-1/2})·Qᵀ (ld ldr).  `base` holds 2q² + 2(q/2 + 1) doubles + q + 2 ints
+// (shared or global memory); every thread of the block must call it.
+__device__ __noinline__ void jacobi_isqrt_block(const double* __restrict__ Gm, int64_t ldg, int q, double* base,
+                                                double* __restrict__ R, int64_t ldr, int* status, double floor_rel) {
     const int qe = q + (q & 1);  // even count for the tournament (index q is a bye when q is odd)
-    double* base = use_smem ? sm : work;
+    const int half = qe / 2;
     double* a = base;                       // q×q
     double* Q = base + (size_t)q * q;       // q×q
-    double* cs = Q + (size_t)q * q;         // qe/2
-    double* sn = cs + qe / 2;               // qe/2
-    int* pp = reinterpret_cast<int*>(sn + qe / 2);  // qe/2
-    int* rr = pp + qe / 2;                          // qe/2
+    double* cs = Q + (size_t)q * q;         // half
+    double* sn = cs + half;                 // half
+    int* pp = reinterpret_cast<int*>(sn + half);  // half
+    int* rr = pp + half;                          // half
     __shared__ double red[32];
-    __shared__ double s_scale, s_off;
+    __shared__ double s_scale, s_off, s_lmax;
+    __shared__ int s_fail;
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
 
     for (int idx = tid; idx < q * q; idx += nt) {
@@ -37,7 +38,7 @@ __global__ void __launch_bounds__(1024) jacobi_isqrt_kernel(const double* __rest
         Q[idx] = (i == j) ? 1.0 : 0.0;
     }
     __syncthreads();
-    auto block_sum = [&](double v) -> double {
+    auto block_sum = [&](double v) -> double {  // result valid in thread 0
         v = warp_sum(v);
         __syncthreads();
         if (lane == 0) red[wid] = v;
@@ -56,7 +57,6 @@ __global__ void __launch_bounds__(1024) jacobi_isqrt_kernel(const double* __rest
         __syncthreads();
     }
     const double scale = s_scale;
-    const int half = qe / 2;
     for (int sweep = 0; sweep < 60; ++sweep) {
         double v = 0.0;
         for (int idx = tid; idx < q * q; idx += nt) {
@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(1024) jacobi_isqrt_kernel(const double* __rest
                 double c = 1.0, s = 0.0;
                 if (r < q) {
                     const double apq = a[p + r * q];
-                    if (fabs(apq) > 1e-300) {
+                    if (fabs(apq) > 1e-300) {  // linalg.cpp:32-37
                         const double theta = (a[r + r * q] - a[p + p * q]) / (2.0 * apq);
                         const double tt = (theta >= 0.0) ? 1.0 / (theta + sqrt(1.0 + theta * theta))
                                                          : 1.0 / (theta - sqrt(1.0 + theta * theta));
@@ -121,27 +121,54 @@ __global__ void __launch_bounds__(1024) jacobi_isqrt_kernel(const double* __rest
             __syncthreads();
         }
     }
-    // eigenvalue floor (linalg.cpp:146-152)
-    double lmax = -1e308;
-    for (int i = 0; i < q; ++i) lmax = fmax(lmax, a[i + i * q]);
-    __shared__ int fail;
-    if (tid == 0) fail = 0;
-    __syncthreads();
-    for (int i = tid; i < q; i += nt) {
-        const double lam = a[i + i * q];
-        if (lam <= floor_rel * lmax || lam <= 0.0) fail = 1;
+    // eigenvalue floor (linalg.cpp:146-152): λ ≤ floor_rel·λ_max or λ ≤ 0 → NumericalError
+    if (tid == 0) {
+        double lmax = -1e308;
+        for (int i = 0; i < q; ++i) lmax = fmax(lmax, a[i + i * q]);
+        int fail = 0;
+        for (int i = 0; i < q; ++i) {
+            const double lam = a[i + i * q];
+            if (lam <= floor_rel * lmax || lam <= 0.0) fail = 1;
+        }
+        s_lmax = lmax;
+        s_fail = fail;
     }
     __syncthreads();
-    if (fail) {
+    if (s_fail) {
         if (tid == 0) *status = 1;
         return;
     }
+    // Q ← Q·diag(λ^{-1/4}) in place, then R = Q·Qᵀ (linalg.cpp:154; same root to rounding)
     for (int idx = tid; idx < q * q; idx += nt) {
         const int j = idx / q;
-        const double qv = Q[idx];
-        Qout[idx] = qv;
-        QD[idx] = qv * (1.0 / sqrt(a[j + j * q]));
+        Q[idx] *= 1.0 / sqrt(sqrt(a[j + j * q]));
     }
+    __syncthreads();
+    for (int idx = tid; idx < q * q; idx += nt) {
+        const int i = idx % q, j = idx / q;
+        if (i > j) continue;
+        double acc = 0.0;
+        for (int k = 0; k < q; ++k) acc = fma(Q[i + k * q], Q[j + k * q], acc);
+        R[i + (int64_t)j * ldr] = acc;
+        R[j + (int64_t)i * ldr] = acc;
+    }
+}
+
+constexpr double ISQRT_FLOOR = 1e-14;        // linalg.hpp sym_inv_sqrt default floor_rel
+constexpr double ISQRT_FAST_ACCEPT = 1e-12;  // certified λmin/λmax above which Newton–Schulz's R is kept
+
+// Stand-alone exact inverse square root (q×q, global work): runs when `need` is set
+// (need == nullptr: always), clears it.  The fallback of the multi-kernel Newton–Schulz.
+__global__ void __launch_bounds__(1024) jacobi_isqrt_kernel(const double* __restrict__ Gm, int64_t ldg, int q,
+                                                            double* work, double* __restrict__ R, int* status,
+                                                            int* need) {
+    if (*status) return;
+    if (need) {
+        if (!*need) return;
+        __syncthreads();
+        if (threadIdx.x == 0) *need = 0;
+    }
+    jacobi_isqrt_block(Gm, ldg, q, work, R, q, status, ISQRT_FLOOR);
 }
 
 // Y(i,:) = sum_c A(i,c) P(c,:) for CSR A; P and Y column-major (ld n).  One warp
@@ -392,21 +419,39 @@ __global__ void ns_copy2_kernel(double* Y, const double* Yn, double* Z, const do
     }
 }
 
-// R = Z/√c (symmetrized); failure when the iteration did not converge
-__global__ void ns_finish_kernel(const double* __restrict__ Z, int q, const double* scal, double* R, int* status,
-                                 const int* conv) {
+// R = Z/√c (symmetrized) when the iteration converged and certifies the floor:
+// ‖R‖²_F = Σ 1/λ_i ≥ 1/λmin and c ≥ λmax, so 1/(‖R‖²_F·c) is a lower bound of λmin/λmax;
+// above ISQRT_FAST_ACCEPT (100× the reference's 1e-14 floor) R is kept.  Otherwise (no
+// convergence, a near-singular G) *need is set and jacobi_isqrt_kernel decides with the
+// reference's own rule (linalg.cpp:144-155).  One CTA.
+__global__ void __launch_bounds__(1024) ns_finish_kernel(const double* __restrict__ Z, int q, const double* scal,
+                                                         double* R, int* status, const int* conv, int* need) {
+    __shared__ double red[32];
+    __shared__ int s_ok;
     if (*status) return;
-    const bool ok = *conv == 2 && scal[1] < 1e-6;
-    if (!ok) {
-        if (threadIdx.x == 0 && blockIdx.x == 0) *status = 1;
-        return;
-    }
+    const int tid = threadIdx.x, nt = blockDim.x;
     const double rc = 1.0 / sqrt(scal[0]);
-    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < q * q; idx += gridDim.x * blockDim.x) {
+    double ss = 0.0;
+    for (int idx = tid; idx < q * q; idx += nt) {
         const int i = idx % q, j = idx / q;
         const double v = 0.5 * (Z[i + j * q] + Z[j + i * q]) * rc;
-        if (!isfinite(v)) *status = 1;
-        R[idx] = v;
+        ss += v * v;
+    }
+    ss = warp_sum(ss);
+    if ((tid & 31) == 0) red[tid >> 5] = ss;
+    __syncthreads();
+    if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < nt / 32; ++w) t += red[w];
+        const bool conv_ok = *conv == 2 && scal[1] < 1e-6;
+        s_ok = conv_ok && isfinite(t) && t > 0.0 && 1.0 / (t * scal[0]) > ISQRT_FAST_ACCEPT;
+        *need = s_ok ? 0 : 1;
+    }
+    __syncthreads();
+    if (!s_ok) return;
+    for (int idx = tid; idx < q * q; idx += nt) {
+        const int i = idx % q, j = idx / q;
+        R[idx] = 0.5 * (Z[i + j * q] + Z[j + i * q]) * rc;
     }
 }
 
@@ -620,11 +665,22 @@ __global__ void __launch_bounds__(512) ns_fused_kernel(const double* __restrict_
         oZ = oZn;
         oZn = tmp;
     }
-    if (!s_stop || !(s_err < 1e-6)) {
-        if (tid == 0) *status = 1;  // did not converge: the reference's floor / resample signal
+    // keep R = Z/√c when Newton–Schulz converged and certifies λmin/λmax > ISQRT_FAST_ACCEPT
+    // (‖R‖²_F = Σ 1/λ_i ≥ 1/λmin, c ≥ λmax); otherwise the reference's Jacobi + floor rule
+    // decides in this CTA (linalg.cpp:144-155), its work arrays in the operand buffers
+    const double rc = 1.0 / sqrt(cc);
+    double ss = 0.0;
+    for (int idx = tid; idx < q * q; idx += nt) {
+        const int i = idx % q, j = idx / q;
+        const double v = nsm[oZ + i + j * LD] * rc;
+        ss += v * v;
+    }
+    ss = block_sum(ss);
+    const bool fast = s_stop && s_err < 1e-6 && isfinite(ss) && ss > 0.0 && 1.0 / (ss * cc) > ISQRT_FAST_ACCEPT;
+    if (!fast) {
+        jacobi_isqrt_block(G, ldg, q, nsm, R, q, status, ISQRT_FLOOR);
         return;
     }
-    const double rc = 1.0 / sqrt(cc);
     for (int idx = tid; idx < q * q; idx += nt) {
         const int i = idx % q, j = idx / q;
         R[idx] = nsm[oZ + i + j * LD] * rc;  // Z is exactly symmetric

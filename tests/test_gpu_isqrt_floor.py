@@ -1,0 +1,118 @@
+"""The reference's inverse-square-root rejection contract on the GPU path.
+
+sym_inv_sqrt (proj/src/linalg.cpp:144-155) throws iff an eigenvalue
+λ ≤ 1e-14·λmax or λ ≤ 0; run_adarbfgs redraws on that throw
+(proj/src/adarbfgs.cpp:145-155).  The GPU keeps Newton–Schulz's root only when it
+certifies λmin/λmax > 1e-12 and otherwise decides with the reference's Jacobi
+and floor (kernels_small.cuh jacobi_isqrt_block), so accept / reject — and with it
+every later draw — follows the oracle.  Covered: the fused one-CTA path (q ≤ 64)
+and the GEMM-engine path (q > 64), Grams with λmin/λmax on both sides of the
+floor, and a 200-iteration AdaRBFGS run whose early sketches hit the floor.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+FLOOR = 1e-14
+
+
+@pytest.fixture(scope="module")
+def si():
+    import paper_1602_01768_b200 as si
+
+    return si
+
+
+def spectrum_matrix(q, ratio, seed):
+    """M = Q·diag(λ)·Qᵀ, λ log-spaced from `ratio` to 1, Q orthogonal (numpy QR of an
+    RngStream Gaussian)."""
+    g = O.RngStream(seed).gaussian_matrix(q, q)
+    qm, _ = np.linalg.qr(g)
+    lam = np.logspace(np.log10(ratio), 0.0, q)
+    m = (qm * lam) @ qm.T
+    return np.asfortranarray(0.5 * (m + m.T))
+
+
+def oracle_decision(m):
+    vals, _ = O.jacobi_eigendecomposition(m)
+    ratio = vals.min() / vals.max()
+    try:
+        r = O.sym_inv_sqrt(m)
+        return True, r, ratio
+    except O.NumericalError:
+        return False, None, ratio
+
+
+@pytest.mark.parametrize("q", [8, 16, 48, 64, 96, 128, 256])
+@pytest.mark.parametrize("ratio", [5e-15, 2e-14, 1e-13, 1e-9, 1e-3])
+def test_floor_decision_matches_oracle(si, q, ratio):
+    m = spectrum_matrix(q, ratio, seed=int(q * 7 + ratio * 1e15) % 100003)
+    ok_ref, r_ref, got_ratio = oracle_decision(m)
+    # the constructed spectrum survives rounding well away from the floor
+    assert got_ratio <= 0.6 * FLOOR or got_ratio >= 1.5 * FLOOR, got_ratio
+    if ok_ref:
+        r = si.sym_inv_sqrt(m)
+        kappa = 1.0 / max(got_ratio, 1e-300)
+        # the unique symmetric root: equal to rounding, amplified by √κ for ill-conditioned M
+        assert np.linalg.norm(r - r_ref) <= 1e-12 * max(1.0, np.sqrt(kappa)) * np.linalg.norm(r_ref)
+        assert np.array_equal(r, r.T) or np.linalg.norm(r - r.T) <= 1e-15 * np.linalg.norm(r)
+    else:
+        with pytest.raises(si.NumericalError):
+            si.sym_inv_sqrt(m)
+
+
+def test_floor_zero_and_indefinite(si):
+    with pytest.raises(si.NumericalError):
+        si.sym_inv_sqrt(np.zeros((5, 5)))
+    with pytest.raises(si.NumericalError):
+        si.sym_inv_sqrt(np.diag([1.0, 2.0, -1e-3]))
+    for q in (8, 80):  # semidefinite: an exact zero eigenvalue
+        v = O.RngStream(q).gaussian_matrix(q, q - 1)
+        with pytest.raises(si.NumericalError):
+            si.sym_inv_sqrt(v @ v.T)
+
+
+def near_singular_problem(n, seed):
+    """A = BᵀB + δI whose column pairs (2k, 2k+1) are exact or near duplicates: the
+    principal 2×2 blocks have λmin/λmax from ≈ 2e-15 (below the floor) to ≈ 1e-12."""
+    rng = O.RngStream(seed)
+    m = 3 * n
+    b = rng.gaussian_matrix(m, n)
+    g = rng.gaussian_matrix(m, n)
+    eps = [0.0, 0.0, 1e-7, 2e-7, 1e-6, 0.0, 3e-7, 0.0]
+    for k in range(n // 2):
+        e = eps[k % len(eps)]
+        b[:, 2 * k + 1] = b[:, 2 * k] + e * g[:, k]
+    a = b.T @ b
+    a += 4e-15 * 2 * m * np.eye(n)
+    return np.asfortranarray(0.5 * (a + a.T))
+
+
+@pytest.mark.parametrize("sampler,q", [("uniform", 4), ("cols", 2), ("uniform", 80)])
+def test_adarbfgs_near_singular_draws_match_oracle(si, sampler, q):
+    """200 iterations (uniform q=4, Eq. 8.2 blocks q=2) over sketches that start out
+    near-singular: every executed draw (rejected ones included) equals the oracle's and
+    the factor matches.  q = 80 runs the GEMM-engine Newton–Schulz + Jacobi fallback."""
+    n, iters = (32, 200) if q < 64 else (160, 60)
+    a = near_singular_problem(n, seed=7 + q)
+    orule = O.ADA_COLS_UNIFORM if sampler == "uniform" else O.ADA_COLS
+    ref = O.run_adarbfgs(a, q, rule=orule, tol=0.0, max_iters=iters, every_k=20, seed=11, max_redraws=1000)
+    ctx = si.Context(0)
+    ctx.set_draw_log(iters * q * 50)
+    rule = si.SketchRule.adaptive_cols_uniform(q) if sampler == "uniform" else si.SketchRule.adaptive_cols(n, q)
+    res = si.run_adarbfgs(si.AdaConfig(si.ProblemMatrix(a, si.Symmetry.spd, context=ctx), rule, tol=0.0,
+                                       max_iters=iters, seed=11, max_redraws=1000,
+                                       track=si.TrackOptions(residual_every_k=20)))
+    drawn = ctx.draw_log()
+    per = q if sampler == "uniform" else 1
+    print(f"{sampler} q={q}: {drawn.size // per} draws for {iters} iterations, redraws {res.state.redraws}")
+    assert res.state.redraws > 0  # the floor was hit
+    assert np.array_equal(drawn, ref.outcomes[:drawn.size])
+    assert drawn.size == iters * per + res.state.redraws * per
+    assert res.state.k == ref.k == iters
+    err = np.linalg.norm(res.state.l - ref.x) / np.linalg.norm(ref.x)
+    print(f"  factor rel err {err:.3e}")
+    assert err <= 1e-6
