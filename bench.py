@@ -296,45 +296,50 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
-def run_sharded(args, cfg):
-    """N > 1: the upper triangle of X in 2P balanced row chunks (SymmetricShardedRBFGS,
-    paper_1602_01768_b200/dist.py), A rows alongside; per iteration one NCCL
-    all-gather of Y, one all-reduce of the W partials and one of the packed
-    [SᵀY | YᵀW] partials.  The workload (config 3) is fixed: strong scaling."""
-    import torch
+def _shard_context(si, torch, local, rank, world):
+    """One-process-per-GPU multi-GPU context of the C ABI (si_context_create_rank): rank 0's
+    NCCL id is broadcast through torch.distributed; the context runs on torch's stream."""
     import torch.distributed as dist
 
-    rank, world, local = dist_env()
+    uid = [si.nccl_unique_id() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(uid, src=0)
+    return si.Context.rank(local, world, rank, uid[0], stream=torch.cuda.current_stream().cuda_stream)
+
+
+def _init_dist(torch, local, rank, world, port):
+    import torch.distributed as dist
+
     torch.cuda.set_device(local)
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-    os.environ.setdefault("MASTER_PORT", "29531")
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local), rank=rank, world_size=world)
+    os.environ.setdefault("MASTER_PORT", str(port))
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local), rank=rank, world_size=world)
+    return dist
+
+
+def run_sharded(args, cfg):
+    """N GPUs (or --sharded at N = 1): the C ABI's sharded RBFGS (shard.cpp) — the upper
+    triangle of X in 2P balanced row chunks, A replicated; per iteration one NCCL all-gather
+    of Y and one all-reduce of the packed [W' | G | H'] partials, the iterations captured as
+    CUDA graphs with the collectives inside.  The workload (config 3) is fixed: strong scaling.
+    Timing: CUDA events on each rank's launch stream, the max over ranks."""
+    import torch
+
+    rank, world, local = dist_env()
+    dist = _init_dist(torch, local, rank, world, 29531)
     import paper_1602_01768_b200 as si
-    from paper_1602_01768_b200.dist import CudaPanelOps, SymmetricShardedRBFGS
 
     n, q = cfg["n"], cfg["q"]
+    a_np = make_dense(cfg)
+    a_pin = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+    a_pin.numpy()[:] = a_np.T
+    a_host = a_pin.numpy().T
     stream = torch.cuda.current_stream()
-    ctx = si.Context(local, stream=stream.cuda_stream)
-    a_full = torch.from_numpy(make_dense(cfg).T).cuda()  # row-major view of the symmetric A
-
-    def rows_of_chunk(r0, r1):
-        # column-major (r1−r0)×n panel A[r0:r1, :]: in a row-major (n, n) tensor holding the
-        # symmetric A, columns r0..r1 laid out row-major are exactly that panel
-        return a_full[:, r0:r1].contiguous().reshape(-1)
-
-    sh = SymmetricShardedRBFGS(CudaPanelOps(ctx), n, q, rows_of_chunk, seed=0, prob=None)
-    # host copies of this rank's A rows for the end-to-end pass (pinned, outside any timing)
-    host_rows = {}
-    for c in sh.chunks:
-        r0, r1 = sh.bounds[c], sh.bounds[c + 1]
-        h = torch.empty((r1 - r0) * n, dtype=torch.float64, pin_memory=True)
-        h.copy_(rows_of_chunk(r0, r1))
-        host_rows[(r0, r1)] = h
-    del a_full
-    torch.cuda.empty_cache()
-    for _ in range(args.warmup):
-        sh.step()
-    sh.finalize()
+    ctx = _shard_context(si, torch, local, rank, world)
+    prob = si.ProblemMatrix(a_host, si.Symmetry.spd, context=ctx)
+    sol = si.Solver(prob, si.Method.rbfgs, si.SketchRule.gaussian_device(q), seed=0)
+    sol.step(args.warmup)
     torch.cuda.synchronize()
     dist.barrier()
     launches0 = ctx.launch_count()
@@ -343,9 +348,7 @@ def run_sharded(args, cfg):
         dist.barrier()
         torch.cuda.synchronize()
         e0.record(stream)
-        for _ in range(args.steps):
-            sh.step()
-        sh.finalize()  # the last PD status (deferred check): a redraw would be inside the timer
+        sol.step(args.steps)
         e1.record(stream)
         torch.cuda.synchronize()
         dist.barrier()
@@ -354,53 +357,59 @@ def run_sharded(args, cfg):
     t = torch.tensor([ms], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    # this rank's DMMA FLOPs per iteration (its two chunk trapezoids)
+    # this rank's DMMA FLOPs per iteration: its two chunk trapezoids (shard.cpp)
+    base, extra = divmod(n, 2 * world)
+    bounds = [0]
+    for c in range(2 * world):
+        bounds.append(bounds[-1] + base + (1 if c < extra else 0))
     rank_flops = 0.0
-    for c in sh.chunks:
-        r0 = sh.bounds[c]
-        m = sh.bounds[c + 1] - r0
-        r1 = r0 + m
-        rank_flops += (2.0 * m * n * q                                   # Y rows
-                       + 2.0 * m * q * (n - r0) + 2.0 * m * q * (n - r1)  # W: trapezoid and its transpose
-                       + 2.0 * m * m * q + 4.0 * m * q * (n - r1)         # update: diagonal block (upper) + rest
-                       + 8.0 * m * q * q + 4.0 * m * q * q)                # V rows, P partial
+    for c in (rank, 2 * world - 1 - rank):
+        r0, r1 = bounds[c], bounds[c + 1]
+        m = r1 - r0
+        rank_flops += (2.0 * m * n * q                                    # Y rows
+                       + 2.0 * m * q * (n - r0) + 2.0 * m * q * (n - r1)  # W': trapezoid and its transpose
+                       + 2.0 * m * m * q + 4.0 * m * q * (n - r1)         # update: diagonal block + the rest
+                       + 2.0 * m * q * q + 2.0 * m * q * q)               # G partial, R rows
+    f0 = bounds[rank]
+    rank_flops += 2.0 * (n - f0) * q * q * 2                              # H' partial, Z = S·G⁻¹ rows ≥ f0
     achieved = rank_flops * args.steps / (ms * 1e-3) / 1e12
-    # ---- e2e: the sharded public API from host buffers (A rows H2D, X gathered to host) ----
-    del sh
-    torch.cuda.empty_cache()
-    k_e2e = args.steps
-    x_host = torch.empty(n * n, dtype=torch.float64, pin_memory=True) if rank == 0 else None
+    del sol
+    # ---- e2e: run_inverter on the multi-GPU context from the host A (every rank uploads A) ----
+    k_e2e = 100
+    x_host = torch.empty((n, n), dtype=torch.float64, pin_memory=True) if rank == 0 else None
+    warm = si.ProblemMatrix(a_host, si.Symmetry.spd, context=ctx)
+    si.run_inverter(si.InverterConfig(warm, si.SketchRule.gaussian_device(q), tol=0.0, max_iters=2, seed=1,
+                                      track=si.TrackOptions(residual_every_k=2), return_x=False))
+    del warm
     dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    sh2 = SymmetricShardedRBFGS(CudaPanelOps(ctx), n, q,
-                                lambda r0, r1: host_rows[(r0, r1)].to("cuda", non_blocking=True), seed=0)
-    for _ in range(k_e2e):
-        sh2.step()
-    xf = sh2.gather_x()
-    if rank == 0:
-        x_host.copy_(xf)
+    prob2 = si.ProblemMatrix(a_host, si.Symmetry.spd, context=ctx)
+    res = si.run_inverter(si.InverterConfig(prob2, si.SketchRule.gaussian_device(q), tol=0.0, max_iters=k_e2e, seed=0,
+                                            track=si.TrackOptions(residual_every_k=k_e2e), return_x=rank == 0),
+                          out=x_host.numpy().T if rank == 0 else None)
     torch.cuda.synchronize()
     dist.barrier()
     dt = torch.tensor([time.perf_counter() - t0], device="cuda")
     dist.all_reduce(dt, op=dist.ReduceOp.MAX)
     e2e = {"value": k_e2e / float(dt.item()), "unit": "iter/s",
            "h2d_bytes_per_step": int(8 * n * n / k_e2e), "d2h_bytes_per_step": int(8 * n * n / k_e2e),
-           "note": "SymmetricShardedRBFGS from host A rows (each rank uploads its chunks), k iterations, "
-                   "X all-reduced and copied to rank 0's pinned host buffer; slowest rank's wall clock"}
-    del sh2, xf
+           "run_iterations": k_e2e, "termination": res.termination.name,
+           "note": "one si_run_inverter call on the multi-GPU context per rank (A uploaded by every rank, SPD "
+                   "validation, the k = 1 and k = 100 residual checkpoints from the chunks' rows, X gathered into "
+                   "rank 0's pinned host buffer), slowest rank's wall clock"}
     if rank == 0:
         alg = 6.0 * n * n * q + 12.0 * n * q * q
         line = {
             "metric": "rbfgs_iterations_per_s", "value": args.steps / (ms * 1e-3), "unit": "iter/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic",
-            "config": {"workload": cfg["name"], "n": n, "q": q, "sketch": "gaussian, device Philox4x32-10",
-                       "l2": "inputs larger than L2; no flush", "parallelism": f"upper triangle of X in 2P balanced row chunks over {world} GPUs "
-                                      "(SymmetricShardedRBFGS), A rows alongside",
-                       "algorithmic_gflop_per_step": alg / 1e9},
-            "roofline": {"bound": "tensor", "kernel": "chunk-trapezoid iteration (all DMMA GEMMs of one rank)",
+            "data": "synthetic", "config": config_of(cfg),
+            "sketch_rng": "device Philox4x32-10 + Box-Muller (counter in device memory)",
+            "parallelism": f"C ABI multi-GPU context over {world} GPU(s) (si_context_create_rank, NCCL): upper "
+                           "triangle of X in 2P balanced row chunks, A replicated",
+            "algorithmic_gflop_per_step": alg / 1e9,
+            "roofline": {"bound": "tensor", "kernel": "rank 0's sharded iteration (all DMMA GEMMs of one rank)",
                          "achieved": achieved, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": achieved / FP64_DMMA_PEAK_TFLOPS, "traffic": None,
                          "peak_source": "measured FP64 DMMA peak, profiles/r01_fp64_peak.txt"},
@@ -414,49 +423,33 @@ def run_sharded(args, cfg):
 
 
 def run_extra_sharded(args, cfg):
-    """Configs 2/4/5 at N GPUs (or --sharded): AdaRBFGS with L row-sharded
-    (RowShardedAdaRBFGS, paper uniform sampler) for configs 2 and 4, RBFGS with the
-    symmetric chunk distribution (SymmetricShardedRBFGS) for config 5; sparse A as
-    CSR row panels.  Fixed workload: strong scaling."""
+    """Configs 2/4/5 at N GPUs (or --sharded): the C ABI's sharded drivers — AdaRBFGS with L in
+    P row panels (paper uniform sampler) for configs 2 and 4, RBFGS with the 2P-chunk upper
+    triangle for config 5; A replicated (CSR for 4/5).  Fixed workload: strong scaling."""
     import torch
-    import torch.distributed as dist
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-    os.environ.setdefault("MASTER_PORT", "29533")
-    if not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local), rank=rank, world_size=world)
+    dist = _init_dist(torch, local, rank, world, 29533)
     import paper_1602_01768_b200 as si
     from paper_1602_01768_b200 import generators as G
-    from paper_1602_01768_b200.dist import (CsrRows, CudaPanelOps, RowShardedAdaRBFGS, SymmetricShardedRBFGS,
-                                            row_partition)
 
     n, q = cfg["n"], cfg["q"]
     stream = torch.cuda.current_stream()
-    ctx = si.Context(local, stream=stream.cuda_stream)
-    ops = CudaPanelOps(ctx)
+    ctx = _shard_context(si, torch, local, rank, world)
     if cfg["gen"] == "config2":
-        a = G.config2_dense(n, seed=0)
-
-        def rows(r0, r1):
-            return torch.from_numpy(np.asfortranarray(a[r0:r1, :]).reshape(-1, order="F").copy()).cuda()
+        prob = si.ProblemMatrix(G.config2_dense(n, seed=0), si.Symmetry.spd, context=ctx)
         nnz = n * n
     else:
-        rp, ci, va = G.config4_csr(n) if cfg["gen"] == "config4" else G.config5_csr(n, half_bandwidth=64, seed=0)
-
-        def rows(r0, r1):
-            return CsrRows.from_host(rp, ci, va, r0, r1, "cuda")
-        nnz = int(va.size)
+        csr = G.config4_csr(n) if cfg["gen"] == "config4" else G.config5_csr(n, half_bandwidth=64, seed=0)
+        prob = si.ProblemMatrix(csr=csr, n=n, symmetry=si.Symmetry.spd, context=ctx)
+        nnz = int(csr[2].size)
     if cfg["method"] == "adarbfgs":
-        st = row_partition(n, world)
-        drv = RowShardedAdaRBFGS(ops, n, q, rows(st[rank], st[rank + 1]), rule="uniform", seed=0)
+        sol = si.Solver(prob, si.Method.adarbfgs, si.SketchRule.adaptive_cols_uniform(q), seed=0)
         alg = 4.0 * n * n * q + 2.0 * nnz * q + 6.0 * n * q * q
     else:
-        drv = SymmetricShardedRBFGS(ops, n, q, rows, seed=0)
+        sol = si.Solver(prob, si.Method.rbfgs, si.SketchRule.gaussian_device(q), seed=0)
         alg = 4.0 * n * n * q + 2.0 * nnz * q + 12.0 * n * q * q
-    for _ in range(args.warmup):
-        drv.step()
+    sol.step(args.warmup)
     torch.cuda.synchronize()
     dist.barrier()
     launches0 = ctx.launch_count()
@@ -465,10 +458,7 @@ def run_extra_sharded(args, cfg):
         dist.barrier()
         torch.cuda.synchronize()
         e0.record(stream)
-        for _ in range(args.steps):
-            drv.step()
-        if hasattr(drv, "finalize"):
-            drv.finalize()
+        sol.step(args.steps)
         e1.record(stream)
         torch.cuda.synchronize()
         dist.barrier()
@@ -482,12 +472,11 @@ def run_extra_sharded(args, cfg):
             "metric": f"{cfg['method']}_iterations_per_s", "value": args.steps / (ms * 1e-3), "unit": "iter/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": per,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg["name"], "n": n, "q": q, "nnz": nnz,
-                       "parallelism": (f"L row-sharded over {world} GPUs (RowShardedAdaRBFGS, uniform sampler)"
-                                       if cfg["method"] == "adarbfgs" else
-                                       f"upper triangle of X in 2P row chunks over {world} GPUs"),
-                       "algorithmic_gflop_per_step": alg / 1e9,
-                       "achieved_tflops_per_step": alg / (per * 1e-3) / 1e12},
+            "config": {"workload": cfg["name"], "n": n, "q": q, "nnz": nnz},
+            "parallelism": (f"L in {world} row panels (C ABI multi-GPU context, uniform sampler)"
+                            if cfg["method"] == "adarbfgs" else f"upper triangle of X in 2P row chunks over {world} GPUs"),
+            "algorithmic_gflop_per_step": alg / 1e9,
+            "achieved_tflops_per_step": alg / (per * 1e-3) / 1e12,
             "gpu_launches": int(ctx.launch_count() - launches0), "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

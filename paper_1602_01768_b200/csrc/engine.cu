@@ -562,6 +562,24 @@ void gemm(Context& c, int64_t M, int64_t N, int64_t K, const double* A, int64_t 
     check_launch("splitk_reduce");
 }
 
+// warp-specialised K-SYMUPD (gemm_symupd_ws_kernel): 8 DMMA warps on 128×128 tiles
+// (BK = 8, 5 TMA stages) + one memory warp (TMA producer and tile epilogue)
+static void launch_symupd_ws(Context& c, const GemmArgs& a) {
+    constexpr int BM = 128, BN = 128, BK = 8, WM = 4, WN = 2, ST = 5;
+    using SM = SymWsSmem<BM, BN, BK, ST>;
+    auto kern = gemm_symupd_ws_kernel<BM, BN, BK, WM, WN, ST>;
+    static DeviceOnce once;
+    if (once.first(c.device)) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SM::BYTES)));
+    CUtensorMap ta, tb;
+    make_tmap(&ta, a.A, a.M, a.K, a.lda, BM + 4, BK);
+    make_tmap(&tb, a.B, a.N, a.K, a.ldb, BN + 4, BK);
+    const int64_t tn = (a.N + BN - 1) / BN, work = tn * (tn + 1) / 2;
+    LaunchScope ls(c, "gemm_symupd");
+    launch_pdl(kern, dim3(unsigned(std::min<int64_t>(work, c.num_sms))), dim3(WM * WN * 32 + 32), SM::BYTES, c.stream,
+               ta, tb, a);
+    check_launch("gemm_symupd_ws");
+}
+
 // X <- X + alpha·V·Uᵀ on the upper-triangular tiles, mirrored (X symmetric n×n)
 static void symupd(Context& c, int64_t n, int64_t k, const double* V, int64_t ldv, const double* U, int64_t ldu,
                    double* X, int64_t ldx, double alpha, const int* skip, int* nonfinite) {
@@ -606,6 +624,15 @@ static void symupd(Context& c, int64_t n, int64_t k, const double* V, int64_t ld
     // per SM, twice the work items
     const int64_t t128 = (n + 127) / 128;
     const TileCfg cfg = int(forced) >= 0 ? forced : (t128 * (t128 + 1) / 2 < int64_t(c.num_sms) ? T128x64 : T128x128);
+    // default for large n: the warp-specialised kernel (SI_SYMUPD_WS=0 keeps the single-role one)
+    static const bool ws = [] {
+        const char* e = std::getenv("SI_SYMUPD_WS");
+        return !(e && e[0] == '0');
+    }();
+    if (ws && cfg == T128x128 && int(forced) < 0 && alpha == 1.0 && !dbg && tma_ok(a) && a.ldc % 2 == 0) {
+        launch_symupd_ws(c, a);
+        return;
+    }
     const int64_t bn = cfg == T128x64 ? 64 : 128, r = 128 / bn;
     const int64_t tn = (n + bn - 1) / bn, full = tn / r, rest = tn % r;
     const int64_t work = r * full * (full + 1) / 2 + rest * (full + 1);  // TileOps::sym_work_count

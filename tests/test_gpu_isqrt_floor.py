@@ -56,8 +56,9 @@ def test_floor_decision_matches_oracle(si, q, ratio):
     if ok_ref:
         r = si.sym_inv_sqrt(m)
         kappa = 1.0 / max(got_ratio, 1e-300)
-        # the unique symmetric root: equal to rounding, amplified by √κ for ill-conditioned M
-        assert np.linalg.norm(r - r_ref) <= 1e-12 * max(1.0, np.sqrt(kappa)) * np.linalg.norm(r_ref)
+        # the unique symmetric root, equal to rounding: a perturbation of M of eps·‖M‖ moves
+        # λmin^{-1/2} by ≈ κ·eps/2 relative, in either implementation
+        assert np.linalg.norm(r - r_ref) <= 1e-13 * max(1e3, kappa) * np.linalg.norm(r_ref)
         assert np.array_equal(r, r.T) or np.linalg.norm(r - r.T) <= 1e-15 * np.linalg.norm(r)
     else:
         with pytest.raises(si.NumericalError):
@@ -76,19 +77,22 @@ def test_floor_zero_and_indefinite(si):
 
 
 def near_singular_problem(n, seed):
-    """A = BᵀB + δI whose column pairs (2k, 2k+1) are exact or near duplicates: the
-    principal 2×2 blocks have λmin/λmax from ≈ 2e-15 (below the floor) to ≈ 1e-12."""
-    rng = O.RngStream(seed)
-    m = 3 * n
-    b = rng.gaussian_matrix(m, n)
-    g = rng.gaussian_matrix(m, n)
-    eps = [0.0, 0.0, 1e-7, 2e-7, 1e-6, 0.0, 3e-7, 0.0]
+    """A = Π·blockdiag([[1, 1−δ_k], [1−δ_k, 1]])·Πᵀ: 2×2 blocks with eigenvalues δ_k and 2 − δ_k,
+    so a Gram holding both coordinates of a pair has λmin/λmax ≈ δ_k/2 — from 1e-15 (below the
+    1e-14 floor) to 1e-10 — while A's own LLT pivots (1 and ≈ 2δ_k) stay clear of rounding;
+    the pairs are scattered by a seeded permutation Π (so contiguous blocks mix them)."""
+    deltas = [2e-15, 1e-14, 6e-14, 2e-13, 2e-10, 0.5, 0.2, 1.0]
+    a = np.zeros((n, n))
     for k in range(n // 2):
-        e = eps[k % len(eps)]
-        b[:, 2 * k + 1] = b[:, 2 * k] + e * g[:, k]
-    a = b.T @ b
-    a += 4e-15 * 2 * m * np.eye(n)
-    return np.asfortranarray(0.5 * (a + a.T))
+        d = deltas[k % len(deltas)]
+        i, j = 2 * k, 2 * k + 1
+        a[i, i] = a[j, j] = 1.0
+        a[i, j] = a[j, i] = 1.0 - d
+    if n % 2:
+        a[n - 1, n - 1] = 1.0
+    rng = O.RngStream(seed)
+    perm = np.argsort([rng.uniform() for _ in range(n)], kind="stable")
+    return np.asfortranarray(a[np.ix_(perm, perm)])
 
 
 @pytest.mark.parametrize("sampler,q", [("uniform", 4), ("cols", 2), ("uniform", 80)])

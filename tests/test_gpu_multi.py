@@ -42,6 +42,15 @@ def traces(res):
     return [h.k for h in res.state.history], np.array([h.residual for h in res.state.history])
 
 
+def trace_gap(got, ref, floor=1e-10):
+    """Max relative gap over the points above the rounding floor (below it — finite
+    termination at machine precision — both must be tiny)."""
+    got, ref = np.asarray(got), np.asarray(ref)
+    live = ref > floor
+    assert np.all(got[~live] <= 1e3 * floor)
+    return float(np.max(np.abs(got[live] - ref[live]) / ref[live])) if live.any() else 0.0
+
+
 def contexts(si, kind, P):
     if kind == "loopback":
         return si.Context.loopback(0, P)
@@ -73,7 +82,7 @@ def test_rbfgs_sharded_device_sketch_matches_single(si, kind, P):
     kg, tg = traces(got)
     kr, tr = traces(ref)
     assert kg == kr
-    assert np.max(np.abs(tg - tr) / tr) <= TRACE_TOL
+    assert trace_gap(tg, tr) <= TRACE_TOL
     assert got.state.flops == pytest.approx(ref.state.flops)
 
 
@@ -86,7 +95,7 @@ def test_rbfgs_sharded_host_sketch_matches_oracle(si, P):
     assert rel(got.state.x, ref.x) <= ITER_TOL
     kg, tg = traces(got)
     assert kg == [h[0] for h in ref.history]
-    assert np.max(np.abs(tg - np.array([h[1] for h in ref.history])) / np.array([h[1] for h in ref.history])) <= TRACE_TOL
+    assert trace_gap(tg, [h[1] for h in ref.history]) <= TRACE_TOL
 
 
 def test_rbfgs_sharded_coordinate_block_draws(si):
@@ -114,7 +123,7 @@ def test_rbfgs_sharded_csr(si, P):
     got = run_rbfgs(si, si.Context.loopback(0, P), dense, q, si.SketchRule.gaussian_device(q), iters, 10, seed,
                     csr=(rp, ci, va))
     assert rel(got.state.x, ref.state.x) <= ITER_TOL
-    assert np.max(np.abs(traces(got)[1] - traces(ref)[1]) / traces(ref)[1]) <= TRACE_TOL
+    assert trace_gap(traces(got)[1], traces(ref)[1]) <= TRACE_TOL
 
 
 def test_rbfgs_sharded_x0_and_errors(si):
@@ -131,7 +140,9 @@ def test_rbfgs_sharded_x0_and_errors(si):
     assert abs(got.state.history[-1].residual - ref.history[-1][1]) <= 1e-2 * ref.history[-1][1]
     bad = a.copy()
     bad[0, 0] = -1.0
-    with pytest.raises(si.NumericalError):  # validate_spd: Cholesky fails
+    # validate_spd: "spd flag set but Cholesky failed" is a plain std::runtime_error in the reference
+    # (problem_matrix.cpp:36-40), which the C ABI maps like the CLI does (exit 2: ConfigError)
+    with pytest.raises((si.ConfigError, si.NumericalError)):
         si.run_inverter(si.InverterConfig(si.ProblemMatrix(bad, si.Symmetry.spd, context=ctx),
                                           si.SketchRule.gaussian(q), max_iters=2))
     with pytest.raises(si.ConfigError):
@@ -157,7 +168,7 @@ def test_adarbfgs_sharded_matches_oracle(si, kind, P, rule):
     kg, tg = traces(got)
     rt = np.array([h[1] for h in ref.history])
     assert kg == [h[0] for h in ref.history]
-    assert np.max(np.abs(tg - rt) / rt) <= TRACE_TOL
+    assert trace_gap(tg, rt) <= TRACE_TOL
     if rule != "gauss":
         drawn = ctx.draw_log()
         assert drawn.size > 0 and np.array_equal(drawn, ref.outcomes[:drawn.size])
@@ -176,7 +187,7 @@ def test_adarbfgs_sharded_device_gauss_and_csr(si):
             runs.append(si.run_adarbfgs(si.AdaConfig(prob, rule, tol=0.0, max_iters=iters, seed=seed,
                                                      track=si.TrackOptions(residual_every_k=10))))
         assert rel(runs[1].state.l, runs[0].state.l) <= ITER_TOL
-        assert np.max(np.abs(traces(runs[1])[1] - traces(runs[0])[1]) / traces(runs[0])[1]) <= TRACE_TOL
+        assert trace_gap(traces(runs[1])[1], traces(runs[0])[1]) <= TRACE_TOL
     assert np.isfinite(dense).all()
 
 
