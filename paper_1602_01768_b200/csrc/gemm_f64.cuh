@@ -464,10 +464,10 @@ struct SymWsSmem {
     static constexpr size_t BYTES = BAR_OFFSET + (2 * STAGES + 2) * sizeof(uint64_t);
 };
 
-// 9 warps at up to 224 registers (64 512 ≤ 65 536): __maxnreg__ instead of launch bounds,
-// which would budget registers for 12 warps (168 each) and spill the accumulators
+// 9 warps: the register file is granted in 4-warp units (12 warps × 168 ≤ 65 536), so the
+// kernel is capped at 168 registers (__maxnreg__; the compute warps need ≈ 170 without the epilogue)
 template <int BM, int BN, int BK, int WM, int WN, int STAGES>
-__global__ void __maxnreg__(224)
+__global__ void __maxnreg__(168)
     gemm_symupd_ws_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs p) {
     using SM = SymWsSmem<BM, BN, BK, STAGES>;
     using T = TileOps<BM, BN, BK, WM, WN, false, false, EPI_SYMUPD>;
