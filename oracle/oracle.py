@@ -294,7 +294,7 @@ def run_inverter_bfgs(a, q, *, rule=RULE_GAUSSIAN, tol=1e-2, max_iters=1000, eve
 
 
 def run_adarbfgs(a, q, *, rule=ADA_COLS, tol=1e-2, max_iters=1000, every_k=10, seed=0, max_redraws=100,
-                 l0=None) -> RunResult:
+                 l0=None, max_outcomes=None) -> RunResult:
     """run_adarbfgs (adarbfgs.cpp:91-200); rule ADA_COLS_UNIFORM is the paper sampler."""
     a = _f(a)
     n = a.shape[0]
@@ -306,7 +306,7 @@ def run_adarbfgs(a, q, *, rule=ADA_COLS, tol=1e-2, max_iters=1000, every_k=10, s
     cap = max_iters + 2
     hk = np.zeros(cap, dtype=np.int64)
     hr, hf, hs = np.zeros(cap), np.zeros(cap), np.zeros(cap)
-    ocap = max_iters * (q if rule == ADA_COLS_UNIFORM else 1) * 2 + 16
+    ocap = max_outcomes or max_iters * (q if rule == ADA_COLS_UNIFORM else 1) * 2 + 16
     outc = np.zeros(ocap, dtype=np.int64)
     term, k, hc = C.c_int(), C.c_int64(), C.c_int64()
     _check(lib().or_run_adarbfgs(n, _p(a), rule, q, tol, max_iters, every_k, seed, max_redraws, l0p, _p(lo),

@@ -699,7 +699,12 @@ int si_run_inverter(si_context* ctx, si_problem* prob, const si_inverter_config*
 
 int si_run_inverter_pair(si_context* ctx, si_problem* prob, const si_inverter_config* cfg, double* x_out,
                          double* x_inv_out, si_history_point* history, int64_t history_cap, si_run_result* result) {
-    return guard([&] { run_inverter_impl(ctx, prob, cfg, x_out, x_inv_out, history, history_cap, result); });
+    return guard([&] {
+        if (ctx->group)  // multi-GPU context: the sharded driver (bfgs; other updates are rejected there)
+            si::shard_run_inverter(ctx, prob, cfg, x_out, history, history_cap, result);
+        else
+            run_inverter_impl(ctx, prob, cfg, x_out, x_inv_out, history, history_cap, result);
+    });
 }
 
 // ---------------------------------------------------------- run_baseline ---

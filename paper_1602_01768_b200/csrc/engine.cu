@@ -563,7 +563,7 @@ void gemm(Context& c, int64_t M, int64_t N, int64_t K, const double* A, int64_t 
 }
 
 // warp-specialised K-SYMUPD (gemm_symupd_ws_kernel): 8 DMMA warps on 128×128 tiles
-// (BK = 8, 5 TMA stages) + one memory warp (TMA producer and tile epilogue)
+// (BK = 8, 5 TMA stages) + 4 memory warps (TMA producer and tile epilogue)
 static void launch_symupd_ws(Context& c, const GemmArgs& a) {
     constexpr int BM = 128, BN = 128, BK = 8, WM = 4, WN = 2, ST = 5;
     using SM = SymWsSmem<BM, BN, BK, ST>;
@@ -575,7 +575,8 @@ static void launch_symupd_ws(Context& c, const GemmArgs& a) {
     make_tmap(&tb, a.B, a.N, a.K, a.ldb, BN + 4, BK);
     const int64_t tn = (a.N + BN - 1) / BN, work = tn * (tn + 1) / 2;
     LaunchScope ls(c, "gemm_symupd");
-    launch_pdl(kern, dim3(unsigned(std::min<int64_t>(work, c.num_sms))), dim3(WM * WN * 32 + 32), SM::BYTES, c.stream,
+    launch_pdl(kern, dim3(unsigned(std::min<int64_t>(work, c.num_sms))), dim3(WM * WN * 32 + 32 * SM::MEM_WARPS),
+               SM::BYTES, c.stream,
                ta, tb, a);
     check_launch("gemm_symupd_ws");
 }

@@ -446,13 +446,14 @@ __global__ void __launch_bounds__(WM* WN * 32, ((EPI == EPI_SYMUPD || EPI == EPI
 // tile epilogue taken off the DMMA warps.  Warps 0..7 only compute: they run the TMA-fed
 // mainloop from zero accumulators, drop the accumulators into a shared-memory hand-off
 // buffer (interleaved by thread: conflict-free on both sides) and go straight on to their
-// next tile.  Warp 8 is the memory warp: lane 0 issues the TMA operand stages (running
-// ahead across tiles, polling between epilogue rounds), and the whole warp retires the
-// previous tile — it prefetches the tile's X block to L2 while the tile is computed, then
-// for each of the 256 compute threads' fragments adds X and writes the tile and its mirror
-// (8-byte stores down a column, 16-byte stores along the mirror row: full sectors), so the
-// X read and the 2·BM·BN·8-byte write of a tile overlap the next tile's DMMA work instead
-// of stalling it (the measured ≈ 2.9 µs per tile of the single-role kernel).
+// next tile.  Warps 8..11 are memory warps: lane 0 of warp 8 issues the TMA operand stages
+// (running ahead across tiles, polled between epilogue chunks), and the four warps retire
+// the previous tile — its X block is prefetched to L2 while the tile is computed, then each
+// memory warp adds X to two compute warps' fragments and writes them and their mirror (8-byte
+// stores down a column, 16-byte stores along the mirror row: full sectors) — so the X read
+// and the 2·BM·BN·8-byte write of a tile overlap the next tile's DMMA work instead of
+// stalling it (the ≈ 2.9 µs per tile of the single-role kernel).  Registers are granted in
+// 4-warp units, so the 4 memory warps cost no more than 1 (12 warps × 168 ≤ 65 536).
 template <int BM, int BN, int BK, int STAGES>
 struct SymWsSmem {
     static constexpr int A_ELEMS = BK * (BM + 4);
@@ -462,10 +463,10 @@ struct SymWsSmem {
     static constexpr size_t HAND_OFFSET = size_t(STAGES) * STAGE_ELEMS * sizeof(double);
     static constexpr size_t BAR_OFFSET = (HAND_OFFSET + size_t(HAND_ELEMS) * sizeof(double) + 127) / 128 * 128;
     static constexpr size_t BYTES = BAR_OFFSET + (2 * STAGES + 2) * sizeof(uint64_t);
+    static constexpr int MEM_WARPS = 4;
 };
 
-// 9 warps: the register file is granted in 4-warp units (12 warps × 168 ≤ 65 536), so the
-// kernel is capped at 168 registers (__maxnreg__; the compute warps need ≈ 170 without the epilogue)
+// 12 warps at ≤ 168 registers (__maxnreg__; the compute warps need ≈ 166 without the epilogue)
 template <int BM, int BN, int BK, int WM, int WN, int STAGES>
 __global__ void __maxnreg__(168)
     gemm_symupd_ws_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs p) {
@@ -473,15 +474,15 @@ __global__ void __maxnreg__(168)
     using T = TileOps<BM, BN, BK, WM, WN, false, false, EPI_SYMUPD>;
     constexpr int NW = WM * WN;            // compute warps
     constexpr int NC = NW * 32;            // compute threads
-    constexpr int FR = T::MI * T::NI * 4;  // accumulators per compute thread
+    constexpr int NMEM = SM::MEM_WARPS;    // memory warps
     constexpr uint32_t STAGE_BYTES = SM::STAGE_ELEMS * sizeof(double);
 
     extern __shared__ __align__(128) double smem[];
     double* hand = smem + size_t(STAGES) * SM::STAGE_ELEMS;
     uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(smem) + SM::BAR_OFFSET);
     uint64_t* empty = full + STAGES;
-    uint64_t* hfull = empty + STAGES;  // compute warps → memory warp (count NW)
-    uint64_t* hfree = hfull + 1;       // memory warp → compute warps (count 1)
+    uint64_t* hfull = empty + STAGES;  // compute warps → memory warps (count NW)
+    uint64_t* hfree = hfull + 1;       // memory warps → compute warps (count NMEM)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == NC) {
@@ -490,7 +491,7 @@ __global__ void __maxnreg__(168)
             mbar_init(&empty[s], NW);
         }
         mbar_init(hfull, NW);
-        mbar_init(hfree, 1);
+        mbar_init(hfree, NMEM);
         mbar_fence_init();
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
@@ -541,8 +542,9 @@ __global__ void __maxnreg__(168)
         return;
     }
 
-    // ------------------------------------------------------------- memory warp
-    const bool producer = lane == 0;
+    // ------------------------------------------------------------ memory warps
+    const int mw = warp - NW;
+    const bool producer = mw == 0 && lane == 0;
     int64_t pw = blockIdx.x;
     int pk = 0, ps = 0, pround = 0;
     int64_t ptm = 0, ptn = 0;
@@ -584,7 +586,7 @@ __global__ void __maxnreg__(168)
         const int64_t m0 = tm * BM, n0 = tn * BN;
         {  // the tile's X block to L2 while it is computed: one prefetch per 128-byte line
             constexpr int LINES = BN * (BM / 16);  // 16 doubles per line
-            for (int l = lane; l < LINES; l += 32) {
+            for (int l = mw * 32 + lane; l < LINES; l += NMEM * 32) {
                 const int64_t c = n0 + l / (BM / 16), r = m0 + (l % (BM / 16)) * 16;
                 if (r < p.M && c < p.N) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p.C + r + c * p.ldc));
             }
@@ -598,7 +600,7 @@ __global__ void __maxnreg__(168)
         const bool fast = m0 + BM <= n0 && m0 + BM <= p.M && n0 + BN <= p.N && (p.ldc & 1) == 0 &&
                           (reinterpret_cast<uintptr_t>(p.C) & 15) == 0;
         bool bad = false;
-        for (int cw = 0; cw < NW; ++cw) {  // retire compute warp cw's fragments as its lane `lane` would
+        for (int cw = mw; cw < NW; cw += NMEM) {  // retire compute warp cw's fragments as its lane would
             const int ct = cw * 32 + lane;
             const int g = lane >> 2, t4 = lane & 3;
             const int64_t wm0 = (cw / WN) * (BM / WM), wn0 = (cw % WN) * (BN / WN);
@@ -648,7 +650,7 @@ __global__ void __maxnreg__(168)
         }
         if (bad && p.nonfinite) atomicOr(p.nonfinite, 1);
         __syncwarp();
-        if (producer) mbar_arrive(hfree);
+        if (lane == 0) mbar_arrive(hfree);
     }
 }
 

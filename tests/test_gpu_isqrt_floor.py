@@ -103,7 +103,8 @@ def test_adarbfgs_near_singular_draws_match_oracle(si, sampler, q):
     n, iters = (32, 200) if q < 64 else (160, 60)
     a = near_singular_problem(n, seed=7 + q, bad_every=1 if q < 64 else 20)
     orule = O.ADA_COLS_UNIFORM if sampler == "uniform" else O.ADA_COLS
-    ref = O.run_adarbfgs(a, q, rule=orule, tol=0.0, max_iters=iters, every_k=20, seed=11, max_redraws=1000)
+    ref = O.run_adarbfgs(a, q, rule=orule, tol=0.0, max_iters=iters, every_k=20, seed=11, max_redraws=1000,
+                         max_outcomes=iters * q * 50)
     ctx = si.Context(0)
     ctx.set_draw_log(iters * q * 50)
     rule = si.SketchRule.adaptive_cols_uniform(q) if sampler == "uniform" else si.SketchRule.adaptive_cols(n, q)
