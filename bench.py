@@ -883,13 +883,18 @@ def main():
     p.add_argument("--no-tte", action="store_true", help="skip the time_to_eps block")
     p.add_argument("--tte-cap", type=int, default=1000, help="iteration cap of the config-3 time-to-eps run")
     p.add_argument("--sharded", action="store_true", help="use the row-sharded driver even at N=1")
+    p.add_argument("--n", type=int, default=0, help="override n of the workload (diagnostic lines, e.g. the sharded "
+                                                   "driver's fixed cost at small n)")
     p.add_argument("--sampler", default="uniform", choices=["uniform", "eq82"],
                    help="AdaRBFGS configs 2/4: paper uniform sampler or the reference's Eq. 8.2 blocks")
     args = p.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(self_launch(args.gpus))
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.n:
+        cfg["n"] = args.n
+        cfg["name"] = cfg["name"].replace(f"n{CONFIGS[args.config]['n']}", f"n{args.n}")
     if args.impl == "reference":
         run_reference(args, cfg)
     else:
