@@ -562,6 +562,38 @@ void gemm(Context& c, int64_t M, int64_t N, int64_t K, const double* A, int64_t 
     check_launch("splitk_reduce");
 }
 
+// C += A·B for a short-K update of a large block (the sharded driver's off-diagonal trapezoid
+// part, X[R_c, r1:] += V·Uᵀ): the K-SYMUPD tiling (128×128, 8 warps, accumulators seeded from
+// the C tile, persistent) without the mirror — the default short-K choice (128×64 C-panel
+// tiles) suits K ≤ q updates with a narrower output
+void gemm_update(Context& c, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
+                 int64_t ldb, double* C, int64_t ldc, const int* skip, int* nonfinite) {
+    if (M <= 0 || N <= 0) return;
+    GemmArgs a{};
+    a.M = M;
+    a.N = N;
+    a.K = K;
+    a.A = A;
+    a.lda = lda;
+    a.B = B;
+    a.ldb = ldb;
+    a.C = C;
+    a.ldc = ldc;
+    a.alpha = 1.0;
+    a.beta = 1.0;
+    a.c_in_acc = 1;
+    a.k_chunk = std::max<int64_t>(K, 1);
+    a.skip = skip;
+    a.nonfinite = nonfinite;
+    const bool big = ((M + 127) / 128) * ((N + 127) / 128) >= int64_t(c.num_sms);
+    if (!big || !tma_ok(a)) {
+        gemm(c, M, N, K, A, lda, false, B, ldb, false, C, ldc, 1.0, 1.0, skip, nonfinite);
+        return;
+    }
+    launch_gemm_layout<EPI_STORE>(c, T128x128, false, false, pick_vec(a), a,
+                                  dim3(unsigned((M + 127) / 128), unsigned((N + 127) / 128), 1), "gemm_update");
+}
+
 // warp-specialised K-SYMUPD (gemm_symupd_ws_kernel): 8 DMMA warps on 128×128 tiles
 // (BK = 8, 5 TMA stages) + 4 memory warps (TMA producer and tile epilogue)
 static void launch_symupd_ws(Context& c, const GemmArgs& a) {

@@ -216,6 +216,10 @@ void family_release(RbfgsWork& w);
 void family_enqueue_iteration(Context& c, Problem& a, RbfgsWork& w, bool device_sketch, uint64_t seed);
 void symupd_device(Context& c, int64_t m, int64_t k, const double* V, int64_t ldv, const double* U, int64_t ldu,
                    double* X, int64_t ldx);
+// C += A·B (A M×K, B(k, j) = B[j + k·ldb]) on 128×128 persistent tiles seeded from C: the
+// sharded driver's off-diagonal update block
+void gemm_update(Context& c, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
+                 int64_t ldb, double* C, int64_t ldc, const int* skip, int* nonfinite);
 // K-SYMUPD with the iteration's device flags: skipped when *skip, non-finite results flagged
 void symupd_ex(Context& c, int64_t m, int64_t k, const double* V, int64_t ldv, const double* U, int64_t ldu, double* X,
                int64_t ldx, const int* skip, int* nonfinite);
