@@ -109,6 +109,19 @@ struct SideScope {
     }
 };
 
+SideHi::SideHi(Context& ctx) : c(ctx), s0(ctx.stream), w0(ctx.ws), n0(ctx.ws_doubles) {
+    c.stream = c.side_hi;
+    c.ws = c.ws_side;
+    c.ws_doubles = c.ws_side_doubles;
+}
+SideHi::~SideHi() {
+    c.ws_side = c.ws;
+    c.ws_side_doubles = c.ws_doubles;
+    c.stream = s0;
+    c.ws = w0;
+    c.ws_doubles = n0;
+}
+
 RbfgsWork* Context::take_rbfgs(int64_t n, int64_t q) {
     if (!cached_rw || cached_rw->n != n || cached_rw->q != q) return nullptr;
     RbfgsWork* w = cached_rw;

@@ -236,6 +236,16 @@ void accumulate(Context& c, double* dst, const double* src, int64_t count);  // 
 void combine(Context& c, void* dst, const void* src, int64_t count, bool is_int, bool is_max);  // dst ∘= src
 void panel_column_dots(Context& c, const double* AL, const double* L, int64_t m, int64_t n, double* d);
 void problem_diagonal(Context& c, Problem& a, double* d);  // d = diag(A)
+void ghat_split(Context& c, const double* G, const double* H, int64_t q, double* Ghat, const int* skip);  // Ĝ = G − H'
+// enqueue on the context's highest-priority side stream (fork() / join(true) around it)
+struct SideHi {
+    Context& c;
+    cudaStream_t s0;
+    double* w0;
+    size_t n0;
+    explicit SideHi(Context& ctx);
+    ~SideHi();
+};
 void set_identity_rows(Context& c, double* X, int64_t m, int64_t cols, int64_t diag_off);  // X(i, j) = δ(j, i + off)
 // the single-GPU iteration's counters: advance_batch_kernel (RBFGS) / ada_advance_batch_kernel
 void advance_batch(Context& c, unsigned long long* counter, int* status, bool ada);

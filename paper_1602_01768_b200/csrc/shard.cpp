@@ -353,7 +353,7 @@ struct ShardSolver {
                 r.chunk[1] = 2 * P - 1 - r.g;
                 for (int j = 0; j < 2; ++j)
                     r.X[j] = dalloc<double>(r, size_t(rows(r.chunk[j])) * size_t(n - r0(r.chunk[j])));
-                r.U = dalloc<double>(r, 4 * nq + 2 * qq);  // [S | R | Z | W' | G H']
+                r.U = dalloc<double>(r, 4 * nq + 2 * qq);  // [S | R | Z | W' | H' | G]
                 r.Y = dalloc<double>(r, nq);
                 r.send = dalloc<double>(r, 2 * size_t(mc) * size_t(q));
                 r.gath = P > 1 ? dalloc<double>(r, 2 * size_t(P) * size_t(mc) * size_t(q)) : r.send;
@@ -385,7 +385,7 @@ struct ShardSolver {
         cuda_check(cudaMallocHost(&st_host, 8 * sizeof(int)), "pinned");
         cuda_check(cudaMallocHost(&scal_host, 8 * sizeof(double)), "pinned");
         if (method == SI_METHOD_RBFGS)
-            G.comm->reserve((nq + 2 * qq) * sizeof(double));
+            G.comm->reserve((nq + 2 * qq) * sizeof(double));  // [W' | H'] is the largest reduction
         else
             G.comm->reserve((nq + qq) * sizeof(double));
         sync();
@@ -462,6 +462,16 @@ struct ShardSolver {
                 else
                     spmm_csr_rows(c, m, n, r.a->rowptr + a0, r.a->colind, r.a->val, S, n, qq, dst, mc);
             }
+            // G = Σ_c Y[R_c]ᵀ·S[R_c] from the local rows (before the gather), all-reduced in the
+            // same NCCL group as the Y all-gather, so its one-CTA K-FACTOR can run on the
+            // high-priority side stream under the W' products (the single-GPU arrangement); W' and
+            // H' share the second all-reduce.  Buffer tail after W': [H' | G] (q×q each).
+            double* Gq = r.U + 4 * nq + size_t(qq) * size_t(qq);
+            for (int j = 0; j < 2; ++j) {
+                const int ch = r.chunk[j];
+                gemm(c, qq, qq, rows(ch), r.send + size_t(j) * size_t(mc) * size_t(qq), mc, true, S + r0(ch), n, true,
+                     Gq, qq, 1.0, j ? 1.0 : 0.0, skip);
+            }
         }
         if (P > 1) {
             G.comm->group_start();
@@ -469,6 +479,8 @@ struct ShardSolver {
                 auto& r = R[size_t(l)];
                 dev(r.c);
                 G.comm->all_gather(l, r.send, r.gath, 2 * size_t(mc) * size_t(qq), r.c->stream);
+                G.comm->all_reduce(l, r.U + 4 * nq + size_t(qq) * size_t(qq), size_t(qq) * size_t(qq), false,
+                                   RedOp::sum, r.c->stream);
             }
             G.comm->group_end();
         }
@@ -476,10 +488,15 @@ struct ShardSolver {
             dev(r.c);
             Context& c = *r.c;
             const int* skip = r.status;
-            double* S = r.U;
             double* Wn = r.U + 3 * nq;
-            double* Pq = Wn + nq;  // [G | H'] (q×2q, ld qq)
+            double* Hq = Wn + nq;
+            double* Gq = Hq + qq * qq;
             place_rows(c, r.gath, mc, 2 * P, true, n, qq, r.Y, n);
+            c.fork(true);
+            {
+                SideHi side(c);
+                rbfgs_gram_enqueue(c, Gq, qq, qq, r.Ginv, nullptr, r.fscr, r.status);  // G⁻¹ + PD test
+            }
             cuda_check(cudaMemsetAsync(Wn, 0, nq * sizeof(double), c.stream), "memset W");
             for (int j = 0; j < 2; ++j) {
                 const int ch = r.chunk[j];
@@ -488,20 +505,15 @@ struct ShardSolver {
                 if (a1 < n)
                     gemm(c, n - a1, qq, m, r.X[j] + m * m, m, true, r.Y + a0, n, true, Wn + a1, n, -1.0, 1.0, skip);
             }
-            for (int j = 0; j < 2; ++j) {  // G = Σ_c Y[R_c]ᵀ·S[R_c]
-                const int ch = r.chunk[j];
-                const int64_t a0 = r0(ch), m = rows(ch);
-                gemm(c, qq, qq, m, r.Y + a0, n, true, S + a0, n, true, Pq, qq, 1.0, j ? 1.0 : 0.0, skip);
-            }
             const int64_t f0 = r0(r.chunk[0]);  // H' = Y[f0:]ᵀ·W'loc[f0:] (W'loc is zero above f0)
-            gemm(c, qq, qq, n - f0, r.Y + f0, n, true, Wn + f0, n, true, Pq + qq * qq, qq, 1.0, 0.0, skip);
+            gemm(c, qq, qq, n - f0, r.Y + f0, n, true, Wn + f0, n, true, Hq, qq, 1.0, 0.0, skip);
         }
         if (P > 1) {
             G.comm->group_start();
             for (int l = 0; l < NL; ++l) {
                 auto& r = R[size_t(l)];
                 dev(r.c);
-                G.comm->all_reduce(l, r.U + 3 * nq, nq + 2 * size_t(qq) * size_t(qq), false, RedOp::sum, r.c->stream);
+                G.comm->all_reduce(l, r.U + 3 * nq, nq + size_t(qq) * size_t(qq), false, RedOp::sum, r.c->stream);
             }
             G.comm->group_end();
         }
@@ -513,8 +525,10 @@ struct ShardSolver {
             double* Rm = r.U + nq;
             double* Z = r.U + 2 * nq;
             double* Wn = r.U + 3 * nq;
-            double* Pq = Wn + nq;
-            rbfgs_gram_enqueue(c, Pq, qq, qq, r.Ginv, r.Ghat, r.fscr, r.status);  // G⁻¹ (PD test), Ĝ = G − H'
+            double* Hq = Wn + nq;
+            double* Gq = Hq + qq * qq;
+            c.join(true);
+            ghat_split(c, Gq, Hq, qq, r.Ghat, r.status);  // Ĝ = G − H'
             const int64_t f0 = r0(r.chunk[0]);
             gemm(c, n - f0, qq, qq, S + f0, n, false, r.Ginv, qq, true, Z + f0, n, 1.0, 0.0, skip);  // Z = S·G⁻¹
             for (int j = 0; j < 2; ++j) {

@@ -143,6 +143,19 @@ __global__ void panel_column_dots_kernel(const double* __restrict__ AL, const do
     }
 }
 
+// Ĝ = G − H' with G read from its upper triangle and H' symmetrised (ghat_kernel's formula,
+// kernels_aux.cuh) when G and H' sit in separate buffers (ld q)
+__global__ void ghat_split_kernel(const double* __restrict__ G, const double* __restrict__ H, int q,
+                                  double* __restrict__ gh, const int* skip) {
+    if (skip && *skip) return;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < q * q; idx += gridDim.x * blockDim.x) {
+        const int i = idx % q, j = idx / q;
+        const double g = i <= j ? G[i + (int64_t)j * q] : G[j + (int64_t)i * q];
+        const double h = 0.5 * (H[i + (int64_t)j * q] + H[j + (int64_t)i * q]);
+        gh[idx] = g - h;
+    }
+}
+
 int blocks_for(int64_t work) { return int(std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, 148 * 8))); }
 
 }  // namespace
@@ -197,6 +210,12 @@ void panel_column_dots(Context& c, const double* AL, const double* L, int64_t m,
     LaunchScope ls(c, "column_dots");
     panel_column_dots_kernel<<<blocks_for(n * 32), 256, 0, c.stream>>>(AL, L, m, n, d);
     cuda_check(cudaGetLastError(), "panel_column_dots");
+}
+
+void ghat_split(Context& c, const double* G, const double* H, int64_t q, double* Ghat, const int* skip) {
+    LaunchScope ls(c, "ghat");
+    ghat_split_kernel<<<blocks_for(q * q), 256, 0, c.stream>>>(G, H, int(q), Ghat, skip);
+    cuda_check(cudaGetLastError(), "ghat_split");
 }
 
 void set_identity_rows(Context& c, double* X, int64_t m, int64_t cols, int64_t diag_off) {
