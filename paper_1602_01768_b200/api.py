@@ -85,6 +85,9 @@ class Context:
                 _check(lib.si_context_create_on_stream(device, C.c_void_p(stream), C.byref(h)))
         self._h = h
         self.device = device
+        # the CUDA stream the context launches on when the caller chose it (None: the
+        # context's private stream); dist.CudaPanelOps requires torch's current stream here
+        self.stream = stream
 
     @classmethod
     def multi(cls, devices: Sequence[int]) -> "Context":
@@ -99,7 +102,9 @@ class Context:
         buf = C.create_string_buffer(bytes(nccl_id), NCCL_ID_BYTES)
         _check(L.load().si_context_create_rank(device, C.c_void_p(stream) if stream else None, nranks, rank, buf,
                                                C.byref(h)))
-        return cls(device, _handle=h)
+        ctx = cls(device, _handle=h)
+        ctx.stream = stream
+        return ctx
 
     @classmethod
     def loopback(cls, device: int, nranks: int) -> "Context":

@@ -688,6 +688,40 @@ void symupd_ex(Context& c, int64_t m, int64_t k, const double* V, int64_t ldv, c
     symupd(c, m, k, V, ldv, U, ldu, X, ldx, 1.0, skip, nonfinite);
 }
 
+// X (m×ncols, ld ldx: rows [0, m) of a symmetric block, columns from the block's first row
+// on) += V·Uᵀ with V m×k, U ncols×k: the leading m×m block by upper tiles mirrored inside it,
+// the columns right of it as plain tiles — one persistent K-SYMUPD launch over the trapezoid
+void symupd_trapezoid(Context& c, int64_t m, int64_t ncols, int64_t k, const double* V, int64_t ldv, const double* U,
+                      int64_t ldu, double* X, int64_t ldx, const int* skip, int* nonfinite) {
+    if (ncols <= m) {
+        symupd(c, m, k, V, ldv, U, ldu, X, ldx, 1.0, skip, nonfinite);
+        return;
+    }
+    GemmArgs a{};
+    a.M = m;
+    a.N = ncols;
+    a.K = k;
+    a.A = V;
+    a.lda = ldv;
+    a.B = U;
+    a.ldb = ldu;
+    a.C = X;
+    a.ldc = ldx;
+    a.alpha = 1.0;
+    a.beta = 1.0;
+    a.k_chunk = k;
+    a.skip = skip;
+    a.nonfinite = nonfinite;
+    const int64_t t128 = (m + 127) / 128, tn128 = (ncols + 127) / 128;
+    const int64_t tiles128 = t128 * (t128 + 1) / 2 + (tn128 - t128) * t128;
+    const TileCfg cfg = tiles128 < int64_t(c.num_sms) ? T128x64 : T128x128;
+    const int64_t bn = cfg == T128x64 ? 64 : 128, r = 128 / bn;
+    const int64_t tn = (m + bn - 1) / bn, full = tn / r, rest = tn % r;
+    const int64_t sq = r * full * (full + 1) / 2 + rest * (full + 1);
+    const int64_t work = sq + ((ncols + bn - 1) / bn - tn) * ((m + 127) / 128);
+    launch_gemm_layout<EPI_SYMUPD>(c, cfg, false, false, pick_vec(a), a, dim3(unsigned(work), 1, 1), "gemm_symupd");
+}
+
 void advance_batch(Context& c, unsigned long long* counter, int* status, bool ada) {
     LaunchScope ls(c, "advance_counter");
     if (ada)

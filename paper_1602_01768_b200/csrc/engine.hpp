@@ -223,6 +223,9 @@ void gemm_update(Context& c, int64_t M, int64_t N, int64_t K, const double* A, i
 // K-SYMUPD with the iteration's device flags: skipped when *skip, non-finite results flagged
 void symupd_ex(Context& c, int64_t m, int64_t k, const double* V, int64_t ldv, const double* U, int64_t ldu, double* X,
                int64_t ldx, const int* skip, int* nonfinite);
+// the same on a trapezoid X (m×ncols, ld ldx): leading m×m block mirrored, the rest plain
+void symupd_trapezoid(Context& c, int64_t m, int64_t ncols, int64_t k, const double* V, int64_t ldv, const double* U,
+                      int64_t ldu, double* X, int64_t ldx, const int* skip, int* nonfinite);
 // ---- shard.cu: helpers of the sharded drivers (shard.cpp) ----
 // Y (n×k, ld ldy) from `parts` all-gathered k×mc slots (symmetric_chunks: the 2P-chunk pairing)
 void place_rows(Context& c, const double* g, int64_t mc, int parts, bool symmetric_chunks, int64_t n, int64_t k,

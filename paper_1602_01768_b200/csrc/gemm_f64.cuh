@@ -98,10 +98,24 @@ struct TileOps {
         tile_n = (int64_t)(c * R_SYM + rem / (c + 1));
         tile_m = (int64_t)(rem % (c + 1));
     }
+    // Trapezoid SYMUPD (M < N: the rows [0, M) of a symmetric block's row panel, X[R, r0:],
+    // the sharded driver's chunk): the upper tiles of the leading M×M block (mirrored inside
+    // it), then every tile of the columns right of it (no mirror)
+    __host__ __device__ __forceinline__ static int64_t sym_trap_count(int64_t M, int64_t N) {
+        const int64_t tmM = (M + BM - 1) / BM, tnM = (M + BN - 1) / BN, tn = (N + BN - 1) / BN;
+        return sym_work_count(M) + (tn - tnM) * tmM;
+    }
     __device__ __forceinline__ static Work decode(int64_t w, const GemmArgs& p) {
         Work r;
         if constexpr (EPI == EPI_SYMUPD) {
-            sym_tile(w, r.tile_m, r.tile_n);
+            const int64_t wsq = p.M < p.N ? sym_work_count(p.M) : INT64_MAX;
+            if (w < wsq) {
+                sym_tile(w, r.tile_m, r.tile_n);
+            } else {
+                const int64_t tmM = (p.M + BM - 1) / BM, tnM = (p.M + BN - 1) / BN, v = w - wsq;
+                r.tile_m = v % tmM;
+                r.tile_n = tnM + v / tmM;
+            }
             r.split = 0;
         } else {
             const uint32_t tm = (uint32_t)((p.M + BM - 1) / BM), tn = (uint32_t)((p.N + BN - 1) / BN);
@@ -114,7 +128,7 @@ struct TileOps {
     }
     __device__ __forceinline__ static int64_t work_count(const GemmArgs& p) {
         const int64_t tm = (p.M + BM - 1) / BM, tn = (p.N + BN - 1) / BN;
-        if constexpr (EPI == EPI_SYMUPD) return sym_work_count(p.N);
+        if constexpr (EPI == EPI_SYMUPD) return p.M < p.N ? sym_trap_count(p.M, p.N) : sym_work_count(p.N);
         return tm * tn * ((p.K + p.k_chunk - 1) / p.k_chunk > 0 ? (p.K + p.k_chunk - 1) / p.k_chunk : 1);
     }
     __device__ __forceinline__ void setup_work(int64_t w, const GemmArgs& p, int warp, int lane) {
@@ -130,9 +144,11 @@ struct TileOps {
         wn0 = (warp % WN) * (BN / WN);
     }
 
-    __device__ __forceinline__ void setup(int warp, int lane) {
+    __device__ __forceinline__ void setup(int warp, int lane, const GemmArgs& p) {
         if constexpr (EPI == EPI_SYMUPD) {
-            sym_tile(blockIdx.x, tile_m, tile_n);
+            const Work r = decode(blockIdx.x, p);
+            tile_m = r.tile_m;
+            tile_n = r.tile_n;
         } else {
             tile_m = blockIdx.x;
             tile_n = blockIdx.y;
@@ -254,8 +270,23 @@ struct TileOps {
             if constexpr (EPI == EPI_SYMUPD) {
                 // off-diagonal full tiles: the mirror X(c, r), X(c+1, r) of the fragment
                 // pair (r, c), (r, c+1) is one aligned 16-byte store
-                const bool fast = m0 + BM <= n0 && m0 + BM <= p.M && n0 + BN <= p.N && (p.ldc & 1) == 0 &&
+                const bool fast = m0 + BM <= n0 && m0 + BM <= p.M && n0 + BN <= p.M && (p.ldc & 1) == 0 &&
                                   (reinterpret_cast<uintptr_t>(p.C) & 15) == 0;
+                if (n0 >= p.M && m0 + BM <= p.M && n0 + BN <= p.N) {  // trapezoid columns right of the block
+                    bool bad = false;
+#pragma unroll
+                    for (int i = 0; i < MI; ++i)
+#pragma unroll
+                        for (int j = 0; j < NI; ++j)
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const int64_t r = row(i, e), c = col(j, e);
+                                p.C[r + c * p.ldc] = acc[i][j][e];
+                                bad |= !isfinite(acc[i][j][e]);
+                            }
+                    if (bad && p.nonfinite) atomicOr(p.nonfinite, 1);
+                    return;
+                }
                 if (fast && (p.dbg & 1)) {  // experiment: keep the accumulators live, store nothing
                     double t = 0.0;
 #pragma unroll
@@ -306,7 +337,7 @@ struct TileOps {
                         } else {  // EPI_SYMUPD: X(r,c) = acc (= X + V·Uᵀ) on the upper triangle, mirrored
                             if (r <= c) {
                                 p.C[r + c * p.ldc] = v;
-                                if (r != c) p.C[c + r * p.ldc] = v;
+                                if (r != c && c < p.M) p.C[c + r * p.ldc] = v;
                                 if (!isfinite(v) && p.nonfinite) atomicOr(p.nonfinite, 1);
                             }
                         }
@@ -835,7 +866,7 @@ __global__ void __launch_bounds__(WM* WN * 32, 1)
     griddep_launch();
     if (p.skip && *p.skip) return;
     T t;
-    t.setup(warp, lane);
+    t.setup(warp, lane, p);
     const int64_t k_begin = (int64_t)blockIdx.z * p.k_chunk;
     const int64_t k_end = min(p.K, k_begin + p.k_chunk);
     const int num_kt = (int)((k_end - k_begin + BK - 1) / BK);
@@ -891,7 +922,7 @@ __global__ void __launch_bounds__(WM* WN * 32) gemm_f64_kernel(GemmArgs p) {
     extern __shared__ __align__(128) double smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     T t;
-    t.setup(warp, lane);
+    t.setup(warp, lane, p);
     const int64_t m0 = t.m0, n0 = t.n0;
     const int64_t k_begin = (int64_t)blockIdx.z * p.k_chunk;
     const int64_t k_end = min(p.K, k_begin + p.k_chunk);

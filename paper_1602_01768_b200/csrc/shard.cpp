@@ -536,11 +536,10 @@ struct ShardSolver {
                 const int64_t a0 = r0(ch), m = rows(ch), a1 = a0 + m;
                 gemm(c, m, qq, qq, Z + a0, n, false, r.Ghat, qq, true, Rm + a0, n, 1.0, 1.0, skip, nullptr,
                      Wn + a0);  // R = Z·Ĝ + W'
-                symupd_ex(c, m, 2 * qq, Rm + a0, n, Z + a0, n, r.X[j], m, skip, r.status + 1);  // diagonal block
-                if (a1 < n)  // X[R_c, r1:] += [R Z][R_c]·[Z W'][r1:]ᵀ (short-K C-panel tiles: 6.61 ms/iteration
-                             // at config 3, P = 1, against 7.04 ms on 128×128 seeded tiles, gemm_update)
-                    gemm(c, m, n - a1, 2 * qq, Rm + a0, n, false, Z + a1, n, false, r.X[j] + m * m, m, 1.0, 1.0, skip,
-                         r.status + 1);
+                // X_c += [R Z][R_c]·[Z W'][r0:]ᵀ: the whole trapezoid in one K-SYMUPD launch (the
+                // diagonal block by upper tiles mirrored, the rest plain)
+                symupd_trapezoid(c, m, n - a0, 2 * qq, Rm + a0, n, Z + a0, n, r.X[j], m, skip, r.status + 1);
+                (void)a1;
             }
             if (batch) advance_batch(c, r.counter, r.status, false);
         }

@@ -49,9 +49,21 @@ def row_partition(n: int, world: int):
 
 
 class CudaPanelOps:
-    """Panel operations on CUDA tensors through libstochinv_b200 (no fallback)."""
+    """Panel operations on CUDA tensors through libstochinv_b200 (no fallback).
+
+    The drivers below interleave these launches with torch ops (copies, fills, NCCL
+    collectives, event records) and rely on stream order between the two, so the context
+    must launch on torch's current stream — create it as
+    ``Context(device, stream=torch.cuda.current_stream().cuda_stream)`` — and the current
+    torch stream must not change while a driver is in use.  A context on any other stream
+    (e.g. ``Context(device)``'s private non-blocking stream) would race the torch ops, and
+    is rejected here."""
 
     def __init__(self, ctx):
+        cur = torch.cuda.current_stream().cuda_stream if torch.cuda.is_available() else None
+        if cur is not None and getattr(ctx, "stream", None) != cur:
+            raise ValueError("CudaPanelOps: the context must launch on torch's current stream "
+                             "(Context(device, stream=torch.cuda.current_stream().cuda_stream))")
         self.ctx = ctx
         self.lib = L.load()
 
@@ -505,6 +517,7 @@ class SymmetricShardedRBFGS:
         self._pending = []        # (slot, event) of attempts whose PD status is not read yet
         self._consecutive = 0     # rejections since the last accepted attempt
         self._attempts = 0
+        self._steps_done = 0      # step() calls returned
         self.world = dist.get_world_size() if dist.is_initialized() else 1
         self.rank = dist.get_rank() if dist.is_initialized() else 0
         self.bounds = chunk_bounds(n, self.world)
@@ -577,15 +590,22 @@ class SymmetricShardedRBFGS:
         self.Y.view(q, n).index_copy_(1, self._y_dst, cols.index_select(1, self._y_src))
 
     def step(self):
+        """One accepted iteration (redraws included).  In the deferred mode the Gram status of
+        this step's attempt is read during a later call, so a rejection-limit failure of step k
+        raises GramRankDeficientError from step k+1 or from finalize() / gather_x() / residual()
+        (the exception's `failed_step` attribute names k); the synchronous mode
+        (SI_SHARD_SYNC_PD=1) raises from step k itself."""
         if not self.deferred:
             return self._step_sync()
         if self._consecutive:  # inside a rejection run: no speculation past the redraw limit
             self._settle(keep=0)
         self._attempt()
         self._settle(keep=1)
+        self._steps_done += 1
 
     def finalize(self):
-        """Read every outstanding PD status (redrawing for the rejected ones)."""
+        """Read every outstanding PD status (redrawing for the rejected ones); may raise the
+        rejection-limit error of an earlier step (see step())."""
         if self.deferred:
             self._settle(keep=0)
 
@@ -617,7 +637,9 @@ class SymmetricShardedRBFGS:
                 self._consecutive += 1
                 if self._consecutive > self.max_redraws:
                     self._consecutive = 0
-                    raise GramRankDeficientError("sketch rejection limit exceeded")
+                    err = GramRankDeficientError("sketch rejection limit exceeded")
+                    err.failed_step = self._steps_done  # 1-based: the step whose draws ran out
+                    raise err
                 owed += 1
             if not self._pending and owed:
                 owed -= 1
