@@ -252,13 +252,20 @@ def _reference_iteration(O, rng, x, a, n, q):
 
 
 def run_reference(args, cfg):
-    """The reference's CPU RBFGS (the oracle port of simi.cpp:287-357 with OpenBLAS on
-    all host threads) on the same config: rank 0 only, no GPU, no import of this
-    package or torch; A from generators.py over the oracle's RngStream."""
+    """The reference's CPU RBFGS on the same config, rank 0 only, no GPU, no import of this
+    package or torch; A from generators.py over the oracle's RngStream.
+
+    With oracle/_ref built (the reference's own sources, unmodified, compiled against the
+    oracle/ref_shim Eigen-API subset over multi-threaded OpenBLAS): its run_inverter for
+    MethodSpec::named_method(bfgs) with SketchRule::gaussian(q), one warm-up call of W
+    iterations and one timed call of K; the rate is K ÷ the reference's own step timer
+    (HistoryPoint.seconds: bfgs_step + symmetrize, the draw and the residual checkpoints
+    excluded, simi.cpp:298-357).  Without it, the oracle port of the same loop."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     from oracle import oracle as O
+    from oracle import ref as R
 
     cores = os.cpu_count()
     n, q = cfg["n"], cfg["q"]
@@ -266,17 +273,32 @@ def run_reference(args, cfg):
     a = make_dense(cfg, O.RngStream)
     t_gen = time.perf_counter() - t_gen
     O.set_threads(0)  # OpenBLAS and the elementwise passes on every host thread
-    rng = O.RngStream(0)
-    x = np.asfortranarray(np.eye(n))
-    for _ in range(args.warmup):
-        x = _reference_iteration(O, rng, x, a, n, q)
-    t0 = time.perf_counter()
-    marks = [t0]
-    for _ in range(args.steps):
-        x = _reference_iteration(O, rng, x, a, n, q)
-        marks.append(time.perf_counter())
-    dt = marks[-1] - t0
-    per = np.diff(marks)
+    if R.available():
+        R.run_inverter_bfgs(a, q, tol=0.0, max_iters=args.warmup, every_k=args.warmup, seed=1, want_x=False)
+        t0 = time.perf_counter()
+        r = R.run_inverter_bfgs(a, q, tol=0.0, max_iters=args.steps, every_k=args.steps, seed=0, want_x=False)
+        wall = time.perf_counter() - t0
+        assert r.k == args.steps
+        dt = r.history[-1][3]
+        kind = "reference"
+        sample = (f"the reference's run_inverter (bfgs, gaussian(q={q}), seed 0, {args.steps} iterations after a "
+                  f"{args.warmup}-iteration warm-up call): its own sources compiled unmodified into oracle/_ref "
+                  "against oracle/ref_shim (Eigen-API subset, products on multi-threaded OpenBLAS); rate = "
+                  "iterations / the reference's step timer (HistoryPoint.seconds, simi.cpp:298-357)")
+        extra = {"wall_s_including_validation_and_checkpoints": wall}
+    else:
+        rng = O.RngStream(0)
+        x = np.asfortranarray(np.eye(n))
+        for _ in range(args.warmup):
+            x = _reference_iteration(O, rng, x, a, n, q)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            x = _reference_iteration(O, rng, x, a, n, q)
+        dt = time.perf_counter() - t0
+        kind = "port"
+        sample = (f"{args.steps} run_inverter iterations after {args.warmup} warm-up ones (draw S, bfgs_step, "
+                  f"symmetrize; simi.cpp:287-357) at n={n}, q={q}: the oracle restatement (oracle/_ref not built)")
+        extra = {}
     v = args.steps / dt
     line = {
         "impl": "reference", "metric": "rbfgs_iterations_per_s", "value": v, "unit": "iter/s",
@@ -284,15 +306,12 @@ def run_reference(args, cfg):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_of(cfg),
         "sketch_rng": "host RngStream (mt19937_64 + std::normal_distribution, rng.hpp:42-49)",
-        "cpu_baseline": {"value": v, "unit": "iter/s", "cores": cores, "kind": "port", "cpu_model": cpu_model(),
-                         "sample": f"{args.steps} run_inverter iterations after {args.warmup} warm-up ones (draw S, "
-                                   f"bfgs_step, symmetrize; simi.cpp:287-357) at n={n}, q={q}: oracle restatement "
-                                   "with OpenBLAS dgemm and the elementwise passes on all host threads; the reference "
-                                   "itself (Eigen) cannot be built in this image"},
+        "cpu_baseline": {"value": v, "unit": "iter/s", "cores": cores, "kind": kind, "cpu_model": cpu_model(),
+                         "sample": sample},
         "e2e": {"value": v, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "input_generation_s": t_gen,
-        "step_seconds": {"min": float(per.min()), "median": float(np.median(per)), "max": float(per.max())},
     }
+    line.update(extra)
     print(json.dumps(line), flush=True)
 
 
