@@ -274,17 +274,22 @@ def run_reference(args, cfg):
     t_gen = time.perf_counter() - t_gen
     O.set_threads(0)  # OpenBLAS and the elementwise passes on every host thread
     if R.available():
-        R.run_inverter_bfgs(a, q, tol=0.0, max_iters=args.warmup, every_k=args.warmup, seed=1, want_x=False)
+        wrng = O.RngStream(1)  # warm-up: W of the reference's own bfgs_step (spins up the BLAS threads)
+        xw = np.asfortranarray(np.eye(n))
+        for _ in range(args.warmup):
+            xw = R.bfgs_step(xw, a, wrng.gaussian_matrix(n, q))
+        del xw
         t0 = time.perf_counter()
         r = R.run_inverter_bfgs(a, q, tol=0.0, max_iters=args.steps, every_k=args.steps, seed=0, want_x=False)
         wall = time.perf_counter() - t0
         assert r.k == args.steps
         dt = r.history[-1][3]
         kind = "reference"
-        sample = (f"the reference's run_inverter (bfgs, gaussian(q={q}), seed 0, {args.steps} iterations after a "
-                  f"{args.warmup}-iteration warm-up call): its own sources compiled unmodified into oracle/_ref "
+        sample = (f"the reference's run_inverter (bfgs, gaussian(q={q}), seed 0, {args.steps} iterations, after "
+                  f"{args.warmup} warm-up bfgs_step calls): its own sources compiled unmodified into oracle/_ref "
                   "against oracle/ref_shim (Eigen-API subset, products on multi-threaded OpenBLAS); rate = "
-                  "iterations / the reference's step timer (HistoryPoint.seconds, simi.cpp:298-357)")
+                  "iterations / the reference's step timer (HistoryPoint.seconds, simi.cpp:298-357); element-wise passes "
+                  "on all host threads (OpenMP)")
         extra = {"wall_s_including_validation_and_checkpoints": wall}
     else:
         rng = O.RngStream(0)

@@ -9,8 +9,9 @@
 //   bundled library), asDiagonal, diagonal, norms, reductions, cwise ops, LLT (LAPACKE
 //   dpotrf / dpotrs), PartialPivLU (dgetrf / dgetri), FullPivLU (complete pivoting, here).
 // Expression templates are not reproduced: every operation evaluates eagerly.  Products
-// go through multi-threaded dgemm (the reference's Eigen is single-threaded), so timings
-// taken with this shim favour the reference.
+// go through multi-threaded dgemm and the element-wise passes and reductions run on all
+// host threads (OpenMP) â€” the reference's Eigen is single-threaded â€” so timings taken with
+// this shim favour the reference.
 #pragma once
 #include <dlfcn.h>
 #include <glob.h>
@@ -74,6 +75,14 @@ struct Blas {
     }
 };
 }  // namespace shim
+
+#if defined(_OPENMP)
+#define SI_SHIM_PAR _Pragma("omp parallel for schedule(static) if (count > 65536)")
+#define SI_SHIM_PAR_SUM _Pragma("omp parallel for schedule(static) reduction(+ : s) if (count > 65536)")
+#else
+#define SI_SHIM_PAR
+#define SI_SHIM_PAR_SUM
+#endif
 
 class MatrixXd;
 class VectorXd;
@@ -184,13 +193,19 @@ public:
 
     double squaredNorm() const {
         double s = 0.0;
-        for (double v : d_) s += v * v;
+        const int64_t count = int64_t(d_.size());
+        const double* d = d_.data();
+        SI_SHIM_PAR_SUM
+        for (int64_t i = 0; i < count; ++i) s += d[i] * d[i];
         return s;
     }
     double norm() const { return std::sqrt(squaredNorm()); }
     double sum() const {
         double s = 0.0;
-        for (double v : d_) s += v;
+        const int64_t count = int64_t(d_.size());
+        const double* d = d_.data();
+        SI_SHIM_PAR_SUM
+        for (int64_t i = 0; i < count; ++i) s += d[i];
         return s;
     }
     double trace() const {
@@ -237,17 +252,23 @@ public:
     template <class F>
     MatrixXd map(F f) const {
         MatrixXd m(r_, c_);
-        for (size_t i = 0; i < d_.size(); ++i) m.d_[i] = f(d_[i]);
+        const int64_t count = int64_t(d_.size());
+        SI_SHIM_PAR
+        for (int64_t i = 0; i < count; ++i) m.d_[size_t(i)] = f(d_[size_t(i)]);
         return m;
     }
     MatrixXd& operator+=(const MatrixXd& o) {
         check_same(o);
-        for (size_t i = 0; i < d_.size(); ++i) d_[i] += o.d_[i];
+        const int64_t count = int64_t(d_.size());
+        SI_SHIM_PAR
+        for (int64_t i = 0; i < count; ++i) d_[size_t(i)] += o.d_[size_t(i)];
         return *this;
     }
     MatrixXd& operator-=(const MatrixXd& o) {
         check_same(o);
-        for (size_t i = 0; i < d_.size(); ++i) d_[i] -= o.d_[i];
+        const int64_t count = int64_t(d_.size());
+        SI_SHIM_PAR
+        for (int64_t i = 0; i < count; ++i) d_[size_t(i)] -= o.d_[size_t(i)];
         return *this;
     }
     MatrixXd& operator*=(double s) {
@@ -438,8 +459,12 @@ inline Transpose MatrixXd::transpose() && { return Transpose(std::move(*this)); 
 inline Transpose ConstBlock::transpose() const { return Transpose(MatrixXd(*this)); }
 inline MatrixXd::MatrixXd(const Transpose& t) : MatrixXd(t.rows(), t.cols()) {
     const MatrixXd& b = t.base();
-    for (Index j = 0; j < c_; ++j)
-        for (Index i = 0; i < r_; ++i) (*this)(i, j) = b(j, i);
+    const int64_t count = int64_t(c_) * int64_t(r_);
+    const Index cols = c_, rows = r_;
+    SI_SHIM_PAR
+    for (Index j = 0; j < cols; ++j)
+        for (Index i = 0; i < rows; ++i) (*this)(i, j) = b(j, i);
+    (void)count;
 }
 inline MatrixXd& MatrixXd::operator=(const Transpose& t) { return *this = MatrixXd(t); }
 
@@ -477,7 +502,9 @@ template <class F>
 inline MatrixXd zip(const MatrixXd& a, const MatrixXd& b, F f) {
     a.check_same(b);
     MatrixXd m(a.rows(), a.cols());
-    for (Index i = 0; i < a.size(); ++i) m(i) = f(a(i), b(i));
+    const int64_t count = int64_t(a.size());
+    SI_SHIM_PAR
+    for (Index i = 0; i < count; ++i) m(i) = f(a(i), b(i));
     return m;
 }
 template <class F>
@@ -485,8 +512,12 @@ inline MatrixXd zip_t(const MatrixXd& a, const Transpose& b, F f) {  // a âˆ˜ bá
     if (a.rows() != b.rows() || a.cols() != b.cols()) throw std::invalid_argument("eigen shim: dimension mismatch");
     MatrixXd m(a.rows(), a.cols());
     const MatrixXd& bb = b.base();
-    for (Index j = 0; j < a.cols(); ++j)
-        for (Index i = 0; i < a.rows(); ++i) m(i, j) = f(a(i, j), bb(j, i));
+    const int64_t count = int64_t(a.size());
+    const Index cols = a.cols(), rows = a.rows();
+    SI_SHIM_PAR
+    for (Index j = 0; j < cols; ++j)
+        for (Index i = 0; i < rows; ++i) m(i, j) = f(a(i, j), bb(j, i));
+    (void)count;
     return m;
 }
 }  // namespace shim

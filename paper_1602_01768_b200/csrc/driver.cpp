@@ -1157,10 +1157,14 @@ int si_run_adarbfgs(si_context* ctx, si_problem* prob, const si_inverter_config*
                 }
                 ck(cudaMemsetAsync(w.status, 0, 8 * sizeof(int), c.stream), "reset");
                 for (int64_t b = 0; b < nb; ++b) {
-                    if (mode == 0) w.idx_dev = w.idx_ring + b * q;
+                    if (mode == 0) {
+                        w.idx_dev = w.idx_ring + b * q;
+                        w.idx_next = b + 1 < nb ? w.idx_ring + (b + 1) * q : nullptr;  // S pipelined ahead
+                    }
                     si::ada_enqueue_update(c, a, w, mode, cfg->seed);
                 }
                 w.idx_dev = idx0;
+                w.idx_next = nullptr;
                 ck(cudaMemcpyAsync(st, w.status, 8 * sizeof(int), cudaMemcpyDeviceToHost, c.stream), "status d2h");
                 ck(cudaStreamSynchronize(c.stream), "sync");
                 const auto t1 = std::chrono::steady_clock::now();
@@ -1403,6 +1407,58 @@ int si_solver_step(si_solver* s, int64_t iters) {
         auto& c = *s->ctx->c;
         const bool device = s->sketch == SI_SKETCH_GAUSSIAN_DEVICE || s->sketch == SI_SKETCH_ADAPTIVE_GAUSS_DEVICE;
         int* status = s->method == SI_METHOD_RBFGS ? s->rw.status : s->aw.status;
+        if (!device && s->method == SI_METHOD_ADARBFGS && s->sketch == SI_SKETCH_ADAPTIVE_COLS_UNIFORM &&
+            std::getenv("SI_RUN_EAGER") == nullptr) {
+            // the paper sampler's draws do not depend on the iterate: up to 64 index sets are
+            // drawn ahead, uploaded once and enqueued back to back (run_adarbfgs's batched loop;
+            // a rejected attempt stops the batch on the device and the stream is rewound to it)
+            si::AdaWork& w = s->aw;
+            const int64_t n = s->prob->p->n, q = s->q;
+            constexpr int64_t CAP = 64;
+            w.ensure_ring(int(CAP));
+            int64_t* const idx0 = w.idx_dev;
+            std::vector<si::RngStream> snaps;
+            int st[8];
+            int consecutive = 0;
+            for (int64_t done = 0; done < iters;) {
+                const int64_t nb = std::min(iters - done, CAP);
+                snaps.clear();
+                for (int64_t b = 0; b < nb; ++b) {
+                    snaps.push_back(*s->rng);
+                    const auto idx = si::uniform_subset(*s->rng, n, q);
+                    for (int64_t j = 0; j < q; ++j) w.idx_ring_pinned[b * q + j] = idx[size_t(j)];
+                }
+                snaps.push_back(*s->rng);
+                ck(cudaMemcpyAsync(w.idx_ring, w.idx_ring_pinned, size_t(nb) * size_t(q) * sizeof(int64_t),
+                                   cudaMemcpyHostToDevice, c.stream),
+                   "h2d idx");
+                ck(cudaMemsetAsync(w.status, 0, 8 * sizeof(int), c.stream), "reset");
+                w.batch = true;
+                for (int64_t b = 0; b < nb; ++b) {
+                    w.idx_dev = w.idx_ring + b * q;
+                    w.idx_next = b + 1 < nb ? w.idx_ring + (b + 1) * q : nullptr;
+                    si::ada_enqueue_update(c, *s->prob->p, w, 0, s->seed);
+                }
+                w.batch = false;
+                w.idx_dev = idx0;
+                w.idx_next = nullptr;
+                ck(cudaMemcpyAsync(st, w.status, 8 * sizeof(int), cudaMemcpyDeviceToHost, c.stream), "status d2h");
+                ck(cudaStreamSynchronize(c.stream), "sync");
+                const int64_t accepted = st[5];
+                done += accepted;
+                s->redraws += st[2];
+                if (st[1]) throw NumericalError("diverged: non-finite iterate");
+                if (st[4]) {
+                    *s->rng = snaps[size_t(accepted) + 1];
+                    consecutive = (accepted > 0 ? 0 : consecutive) + 1;
+                    if (consecutive > 100) throw NumericalError("solver: rejection limit exceeded");
+                } else {
+                    consecutive = 0;
+                }
+            }
+            ck(cudaMemsetAsync(w.status, 0, 8 * sizeof(int), c.stream), "reset");
+            return;
+        }
         if (!device) {
             // host-drawn sketches share one pinned staging buffer: one iteration at a time
             for (int64_t i = 0; i < iters;) {

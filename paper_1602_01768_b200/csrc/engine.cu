@@ -1433,6 +1433,11 @@ void AdaWork::alloc(int64_t n_, int64_t q_, bool gaussian) {
 }
 
 void AdaWork::release() {
+    for (double* p : {S_next, AS_next, G_next, Bsel})
+        if (p) cudaFree(p);
+    S_next = AS_next = G_next = Bsel = nullptr;
+    have_next = false;
+    idx_next = nullptr;
     if (idx_ring) cudaFree(idx_ring);
     if (idx_ring_pinned) cudaFreeHost(idx_ring_pinned);
     idx_ring = nullptr;
@@ -1600,7 +1605,18 @@ void pdiag_update(Context& c, const double* B, int64_t q, int64_t n, const doubl
 void ada_enqueue_update(Context& c, Problem& a, AdaWork& w, int mode, uint64_t seed) {
     const int64_t n = w.n, q = w.q;
     int* st = w.status;
-    if (mode == 0) {
+    static const bool pipeline = [] {  // SI_ADA_PIPELINE=0: no sketch pipelining
+        const char* e = std::getenv("SI_ADA_PIPELINE");
+        return !(e && e[0] == '0');
+    }();
+    const bool precomputed = mode == 0 && w.have_next;
+    if (precomputed) {  // S, A·S and G of this attempt were computed under the previous L update
+        std::swap(w.S, w.S_next);
+        std::swap(w.AS, w.AS_next);
+        std::swap(w.G, w.G_next);
+        w.have_next = false;
+        c.join();
+    } else if (mode == 0) {
         gather_columns(c, w.L, n, n, w.idx_dev, q, w.S);
     } else {
         if (mode == 1) {
@@ -1614,8 +1630,10 @@ void ada_enqueue_update(Context& c, Problem& a, AdaWork& w, int mode, uint64_t s
         }
         gemm(c, n, q, n, w.L, n, false, w.St, n, true, w.S, n, 1.0, 0.0, st);  // S = L·S̃
     }
-    apply_a(c, a, w.S, n, q, w.AS, n, st);                                 // AS = A·S
-    gemm(c, q, q, n, w.S, n, true, w.AS, n, true, w.G, q, 1.0, 0.0, st);   // G = Sᵀ·AS
+    if (!precomputed) {
+        apply_a(c, a, w.S, n, q, w.AS, n, st);                                 // AS = A·S
+        gemm(c, q, q, n, w.S, n, true, w.AS, n, true, w.G, q, 1.0, 0.0, st);   // G = Sᵀ·AS
+    }
     // Z = (AS)ᵀ·L does not depend on R: it runs on the side stream (every SM but the
     // one holding the inverse square root) while the q×q stage and SR = S·R run here
     static const bool overlap = std::getenv("SI_ADA_SERIAL") == nullptr;
@@ -1634,6 +1652,27 @@ void ada_enqueue_update(Context& c, Problem& a, AdaWork& w, int mode, uint64_t s
         ada_core_enqueue(c, w.G, q, w.Z, n, w.idx_dev, mode == 0 ? nullptr : w.St, w.G2, w.R2, w.Tm, w.R, w.B,
                          w.eig_scratch, st);
         gemm(c, n, q, q, w.S, n, false, w.R, q, true, w.SR, n, 1.0, 0.0, st);  // SR = S·R
+    }
+    if (pipeline && mode == 0 && w.batch && w.idx_next) {
+        // the next attempt's S' = L⁺[:, idx'] = L[:, idx'] + SR·B[:, idx'] (n×q×q), then A·S' and
+        // G' = S'ᵀ·A·S' on the side stream, overlapping the L update below (config 2: the L update
+        // runs memory-bound at ≈ 55% of the DMMA rate, A·S' fills the gap)
+        if (!w.S_next) {
+            dmalloc(&w.S_next, size_t(n) * size_t(q));
+            dmalloc(&w.AS_next, size_t(n) * size_t(q));
+            dmalloc(&w.G_next, size_t(q) * size_t(q));
+            dmalloc(&w.Bsel, size_t(q) * size_t(q));
+        }
+        gather_columns(c, w.L, n, n, w.idx_next, q, w.S_next);
+        gather_columns(c, w.B, q, q, w.idx_next, q, w.Bsel);                          // B[:, idx'] (q×q)
+        gemm(c, n, q, q, w.SR, n, false, w.Bsel, q, true, w.S_next, n, 1.0, 1.0, st);  // S' += SR·B[:, idx']
+        c.fork();
+        {
+            SideScope side(c);
+            apply_a(c, a, w.S_next, n, q, w.AS_next, n, st);                                   // A·S'
+            gemm(c, q, q, n, w.S_next, n, true, w.AS_next, n, true, w.G_next, q, 1.0, 0.0, st);  // S'ᵀ·A·S'
+        }
+        w.have_next = true;
     }
     gemm(c, n, n, q, w.SR, n, false, w.B, q, true, w.L, n, 1.0, 1.0, st, st + 1);  // L += SR·B (+ finite check)
     if (w.pdiag_valid) {  // carry diag(LᵀAL) across the accepted update (App. C3)

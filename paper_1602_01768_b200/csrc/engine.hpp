@@ -149,6 +149,12 @@ struct AdaWork {
     int64_t* idx_ring_pinned = nullptr;
     int ring_cap = 0;
     void ensure_ring(int cap);
+    // the next attempt's sketch pipelined ahead (coordinate sampler, batched loops):
+    // S' = L[:, idx'] + SR·B[:, idx'] (= the next L's columns) and A·S', S'ᵀ·A·S' computed on the
+    // side stream while the main stream runs this attempt's L update
+    const int64_t* idx_next = nullptr;  // device, q entries; null: no next attempt in this batch
+    bool have_next = false;
+    double *S_next = nullptr, *AS_next = nullptr, *G_next = nullptr, *Bsel = nullptr;
     bool pdiag_valid = false;
     int pdiag_age = 0;       // incremental updates since the last exact refresh
     int pdiag_refresh = 64;  // exact A·L refresh period (SI_PDIAG_REFRESH; 1 = every iteration)
