@@ -29,8 +29,9 @@ time_to_eps: config 1 (n = 1024, q = 32) to ‖I−AX‖_F/√n ≤ 1e-2 and to 
          iteration cap (labelled, with the residual reached).
 cpu_baseline: the oracle (C++ restatement of the reference, OpenBLAS) running
          run_inverter iterations on the host cores, a bounded sample of steps.
---impl reference: the reference algorithm on all host cores (the oracle port —
-         the reference itself needs Eigen, absent here), same config,
+--impl reference: the reference's own run_inverter on the host cores — its
+         sources compiled unmodified into oracle/_ref against the Eigen-API shim
+         (the oracle port when oracle/_ref is absent) — same config,
          metric and steps; it imports neither this package nor torch.
 --gpus N without WORLD_SIZE in the environment relaunches itself under
 torch.distributed.run with N ranks (127.0.0.1) and rank 0 prints the line.

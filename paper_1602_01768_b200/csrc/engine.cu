@@ -378,6 +378,31 @@ static void launch_cpanel_cfg(Context& c, const GemmArgs& a, int64_t work) {
                ta, tb, tc, a);
 }
 
+// C-panel launch with the bulk-copy epilogue (gemm_tma_cbulk_kernel): C = beta·Csrc + A·B, 128×64
+// tiles, 8 warps, 3 stages, one C-in and one C-out tile in shared memory, one CTA per SM
+template <bool AK, bool BKM>
+static void launch_cbulk_cfg(Context& c, const GemmArgs& a, int64_t work) {
+    constexpr int BM = 128, BN = 64, BK = 16, WM = 4, WN = 2, ST = 3;
+    using CB = CBulkSmem<BM, BN, BK, WM, WN, ST, AK, BKM>;
+    static_assert(CB::BYTES <= 232448, "shared memory per CTA");
+    auto kern = gemm_tma_cbulk_kernel<BM, BN, BK, WM, WN, ST, AK, BKM>;
+    static DeviceOnce once;
+    if (once.first(c.device)) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(CB::BYTES)));
+    CUtensorMap ta, tb, tc;
+    if (AK)
+        make_tmap(&ta, a.A, a.K, a.M, a.lda, BK + 4, BM);
+    else
+        make_tmap(&ta, a.A, a.M, a.K, a.lda, BM + 4, BK);
+    if (BKM)
+        make_tmap(&tb, a.B, a.K, a.N, a.ldb, BK + 4, BN);
+    else
+        make_tmap(&tb, a.B, a.N, a.K, a.ldb, BN + 4, BK);
+    make_tmap(&tc, a.Csrc ? a.Csrc : a.C, a.M, a.N, a.ldc, BM + 4, BN);  // the seed (beta·Csrc or beta·C)
+    LaunchScope ls(c, "gemm_cpanel");
+    launch_pdl(kern, dim3(unsigned(std::min<int64_t>(work, int64_t(c.num_sms)))), dim3(WM * WN * 32), CB::BYTES, c.stream,
+               ta, tb, tc, a);
+}
+
 template <bool AK, bool BKM, int VEC, int EPI>
 static void launch_gemm_tile(Context& c, TileCfg t, const GemmArgs& a, dim3 grid, const char* name, bool tma) {
     if (EPI == EPI_SYMUPD && t == T64x128) throw std::logic_error("gemm_symupd: tile height must be a multiple of its width");
@@ -551,6 +576,21 @@ void gemm(Context& c, int64_t M, int64_t N, int64_t K, const double* A, int64_t 
         }();
         if (cpanel && t == T128x64 && a.c_in_acc && K <= cpanel_kmax && tma_ok(a) && a.ldc % 2 == 0 &&
             aligned_ptr(C, 16) && aligned_ptr(Csrc ? Csrc : C, 16)) {
+            // the finished tiles leave by bulk copies from shared memory (SI_CPANEL_BULK=0: stores from
+            // registers); an even M keeps every column segment a multiple of 16 bytes
+            static const bool cbulk = [] {
+                const char* e = std::getenv("SI_CPANEL_BULK");
+                return !(e && e[0] == '0');
+            }();
+            if (cbulk && M % 2 == 0) {
+                if (!a_kmajor && b_kmajor)
+                    launch_cbulk_cfg<false, true>(c, a, tm * tn);
+                else if (!a_kmajor && !b_kmajor)
+                    launch_cbulk_cfg<false, false>(c, a, tm * tn);
+                else
+                    launch_cbulk_cfg<true, true>(c, a, tm * tn);
+                return;
+            }
             if (!a_kmajor && b_kmajor)
                 launch_cpanel_cfg<false, true>(c, a, tm * tn);
             else if (!a_kmajor && !b_kmajor)
@@ -626,6 +666,51 @@ static void launch_symupd_ws(Context& c, const GemmArgs& a) {
     check_launch("gemm_symupd_ws");
 }
 
+// deferred-epilogue K-SYMUPD (gemm_symupd_deferred_kernel): 8 DMMA warps on 128×128 tiles, the
+// previous tile retired by L2 reductions under the mainloop; square and trapezoid launches.
+// Opt-in (SI_SYMUPD_DEFER; default 0 = the single-role kernel): measured 2.16–2.18 ms against 2.22 ms
+// at config 3 (B), but the reductions fetch the mirror tiles too (+1 GB of DRAM reads per launch),
+// DESIGN.md §9.  B = BK 16 × 3 stages + 15-block hand-off, A / D = BK 16 × 5 / 6 stages with the
+// reductions straight from registers, C = BK 8 × 5 stages + 16-block hand-off, E / F = 4 stages +
+// 11 / 8 blocks.
+static int symupd_defer_mode() {
+    static const int mode = [] {
+        const char* e = std::getenv("SI_SYMUPD_DEFER");
+        if (!e || !e[0]) return 0;
+        return e[0] == '0' ? 0 : int(e[0]);
+    }();
+    return mode;
+}
+static bool symupd_defer_ok(const GemmArgs& a) {
+    return symupd_defer_mode() != 0 && a.alpha == 1.0 && !(a.dbg & 1023) && tma_ok(a) && a.ldc % 2 == 0 && aligned16(a.C);
+}
+template <int BK, int ST, int HB>
+static void launch_symupd_deferred_cfg(Context& c, const GemmArgs& a, int64_t work) {
+    constexpr int BM = 128, BN = 128, WM = 4, WN = 2;
+    using SM = SymDefSmem<BM, BN, BK, WM, WN, ST, HB>;
+    static_assert(SM::BYTES <= 232448, "shared memory per CTA");
+    auto kern = gemm_symupd_deferred_kernel<BM, BN, BK, WM, WN, ST, HB>;
+    static DeviceOnce once;
+    if (once.first(c.device)) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SM::BYTES)));
+    CUtensorMap ta, tb;
+    make_tmap(&ta, a.A, a.M, a.K, a.lda, BM + 4, BK);
+    make_tmap(&tb, a.B, a.N, a.K, a.ldb, BN + 4, BK);
+    LaunchScope ls(c, "gemm_symupd");
+    launch_pdl(kern, dim3(unsigned(std::min<int64_t>(work, c.num_sms))), dim3(WM * WN * 32), SM::BYTES, c.stream, ta, tb,
+               a);
+    check_launch("gemm_symupd_deferred");
+}
+static void launch_symupd_deferred(Context& c, const GemmArgs& a, int64_t work) {
+    switch (symupd_defer_mode()) {
+        case 'A': launch_symupd_deferred_cfg<16, 5, 0>(c, a, work); break;
+        case 'D': launch_symupd_deferred_cfg<16, 6, 0>(c, a, work); break;
+        case 'E': launch_symupd_deferred_cfg<16, 4, 11>(c, a, work); break;
+        case 'F': launch_symupd_deferred_cfg<16, 4, 8>(c, a, work); break;
+        case 'C': launch_symupd_deferred_cfg<8, 5, 16>(c, a, work); break;
+        default: launch_symupd_deferred_cfg<16, 3, 15>(c, a, work); break;
+    }
+}
+
 // X <- X + alpha·V·Uᵀ on the upper-triangular tiles, mirrored (X symmetric n×n)
 static void symupd(Context& c, int64_t n, int64_t k, const double* V, int64_t ldv, const double* U, int64_t ldu,
                    double* X, int64_t ldx, double alpha, const int* skip, int* nonfinite) {
@@ -680,6 +765,10 @@ static void symupd(Context& c, int64_t n, int64_t k, const double* V, int64_t ld
     const int64_t bn = cfg == T128x64 ? 64 : 128, r = 128 / bn;
     const int64_t tn = (n + bn - 1) / bn, full = tn / r, rest = tn % r;
     const int64_t work = r * full * (full + 1) / 2 + rest * (full + 1);  // TileOps::sym_work_count
+    if (cfg == T128x128 && int(forced) < 0 && symupd_defer_ok(a)) {
+        launch_symupd_deferred(c, a, work);
+        return;
+    }
     launch_gemm_layout<EPI_SYMUPD>(c, cfg, false, false, vec, a, dim3(unsigned(work), 1, 1), "gemm_symupd");
 }
 
@@ -719,6 +808,10 @@ void symupd_trapezoid(Context& c, int64_t m, int64_t ncols, int64_t k, const dou
     const int64_t tn = (m + bn - 1) / bn, full = tn / r, rest = tn % r;
     const int64_t sq = r * full * (full + 1) / 2 + rest * (full + 1);
     const int64_t work = sq + ((ncols + bn - 1) / bn - tn) * ((m + 127) / 128);
+    if (cfg == T128x128 && symupd_defer_ok(a)) {
+        launch_symupd_deferred(c, a, work);
+        return;
+    }
     launch_gemm_layout<EPI_SYMUPD>(c, cfg, false, false, pick_vec(a), a, dim3(unsigned(work), 1, 1), "gemm_symupd");
 }
 
@@ -791,6 +884,31 @@ void problem_download_dense(Problem& p, double* host) {
     CK(cudaStreamSynchronize(c.stream));
 }
 
+// row-major SpMM launch: the row-blocked kernel when k is a multiple of 64 (SI_SPMM_ROWBLOCK=0:
+// the warp-per-row kernel), 4 rows × 64·NS columns per warp
+static void launch_spmm_rowmajor(Context& c, int64_t m, const int64_t* rowptr, const int32_t* colind, const double* val,
+                                 const double* Pr, int64_t k, double* Y, int64_t ldy, const int* skip) {
+    static const bool rowblock = [] {
+        const char* e = std::getenv("SI_SPMM_ROWBLOCK");
+        return !(e && e[0] == '0');
+    }();
+    if (rowblock && k >= 64 && k % 64 == 0) {
+        constexpr int R = 4;
+        const int ns = k % 256 == 0 ? 4 : (k % 128 == 0 ? 2 : 1);
+        const int64_t units = ((m + R - 1) / R) * (k / (64 * ns));
+        const dim3 grid(grid_for(units * 32, 256, c.num_sms * 32));
+        if (ns == 4)
+            spmm_csr_rowblock_kernel<R, 4><<<grid, 256, 0, c.stream>>>(m, rowptr, colind, val, Pr, k, Y, ldy, skip);
+        else if (ns == 2)
+            spmm_csr_rowblock_kernel<R, 2><<<grid, 256, 0, c.stream>>>(m, rowptr, colind, val, Pr, k, Y, ldy, skip);
+        else
+            spmm_csr_rowblock_kernel<R, 1><<<grid, 256, 0, c.stream>>>(m, rowptr, colind, val, Pr, k, Y, ldy, skip);
+        return;
+    }
+    spmm_csr_rowmajor_kernel<<<grid_for(m * 32, 256, c.num_sms * 32), 256, 0, c.stream>>>(m, rowptr, colind, val, Pr, k, Y,
+                                                                                         ldy, skip);
+}
+
 // Y = A·P (dense GEMM or CSR SpMM)
 void apply_a(Context& c, Problem& a, const double* P, int64_t ldp, int64_t k, double* Y, int64_t ldy, const int* skip) {
     const int64_t n = a.n;
@@ -814,8 +932,7 @@ void apply_a(Context& c, Problem& a, const double* P, int64_t ldp, int64_t k, do
         check_launch("transpose");
     }
     LaunchScope ls(c, "spmm_csr");
-    spmm_csr_rowmajor_kernel<<<grid_for(n * 32, 256, c.num_sms * 32), 256, 0, c.stream>>>(n, a.rowptr, a.colind, a.val,
-                                                                                         Pr, k, Y, ldy, skip);
+    launch_spmm_rowmajor(c, n, a.rowptr, a.colind, a.val, Pr, k, Y, ldy, skip);
     check_launch("spmm_csr");
 }
 
@@ -831,8 +948,7 @@ void spmm_csr_rows(Context& c, int64_t m, int64_t n, const int64_t* rowptr, cons
         check_launch("transpose");
     }
     LaunchScope ls(c, "spmm_csr");
-    spmm_csr_rowmajor_kernel<<<grid_for(m * 32, 256, c.num_sms * 32), 256, 0, c.stream>>>(m, rowptr, colind, val, Pr,
-                                                                                         k, Y, ldy, nullptr);
+    launch_spmm_rowmajor(c, m, rowptr, colind, val, Pr, k, Y, ldy, nullptr);
     check_launch("spmm_csr");
 }
 
@@ -1605,9 +1721,9 @@ void pdiag_update(Context& c, const double* B, int64_t q, int64_t n, const doubl
 void ada_enqueue_update(Context& c, Problem& a, AdaWork& w, int mode, uint64_t seed) {
     const int64_t n = w.n, q = w.q;
     int* st = w.status;
-    static const bool pipeline = [] {  // SI_ADA_PIPELINE=0: no sketch pipelining
+    static const bool pipeline = [] {  // SI_ADA_PIPELINE=1: sketch pipelining (measured 0.327 vs 0.315 ms at config 2: off)
         const char* e = std::getenv("SI_ADA_PIPELINE");
-        return !(e && e[0] == '0');
+        return e && e[0] == '1';
     }();
     const bool precomputed = mode == 0 && w.have_next;
     if (precomputed) {  // S, A·S and G of this attempt were computed under the previous L update

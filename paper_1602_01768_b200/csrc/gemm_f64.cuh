@@ -213,8 +213,13 @@ struct TileOps {
     }
 
     __device__ __forceinline__ void compute_stage(double (&acc)[MI][NI][4], const double* As, const double* Bs) const {
+        compute_part<0, BK>(acc, As, Bs);
+    }
+    // the k8 steps [K0, K1) of a stage
+    template <int K0, int K1>
+    __device__ __forceinline__ void compute_part(double (&acc)[MI][NI][4], const double* As, const double* Bs) const {
 #pragma unroll
-        for (int kk = 0; kk < BK; kk += 8) {
+        for (int kk = K0; kk < K1; kk += 8) {
             double a[MI][4], b[NI][2];
 #pragma unroll
             for (int i = 0; i < MI; ++i)
@@ -685,6 +690,219 @@ __global__ void __maxnreg__(168)
     }
 }
 
+// ------------------------------------------- deferred-epilogue K-SYMUPD --
+// X ← X + V·Uᵀ on the upper BM×BN tiles, mirrored, with the tile epilogue folded into the
+// NEXT tile's mainloop and the X read-modify-write done by the L2 (red.global.add.f64).
+// In the single-role kernel all 8 warps reach the epilogue together: 64 X loads and 96 stores
+// per thread go through the LSU while the DMMA pipe idles (≈ 2–3 µs of a 36 µs tile).  Here
+// the accumulators start from zero; a finished tile's fragment blocks are dropped into a
+// shared-memory hand-off area — thread-interleaved, so every thread only ever reads back its
+// own slots: no barrier, no bank conflict — and the warps start the next tile at once.  After
+// each k8 step of that tile a thread retires one 16×8 fragment block of the previous one:
+// eight fire-and-forget reductions, X(r, c) += v on the tile and X(c, r) += v on its mirror.
+// Both halves start bitwise equal and receive the same addend, so X stays exactly symmetric;
+// every element receives exactly one addend per launch, so the result is deterministic and
+// rounded once (X + Σ instead of a running sum seeded with X).  No X value ever enters a
+// register: register loads of X measured +0.6 ms per launch at config 3 (their scoreboard
+// is shared with the fragment loads, so every DMMA waited on L2), cp.async staging +0.19 ms,
+// the reductions +0.06 ms.  HB = fragment blocks handed off per thread (of MI·NI); the
+// remaining blocks are retired from registers at the hand-off.  HB = 15 of 16 leaves room
+// for three BK = 16 stages beside the 120 KB hand-off area (BK = 8 × 5 stages with all 16
+// blocks measured 15% slower in the mainloop).  Diagonal and ragged tiles take a guarded
+// load-add-store epilogue.
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int HB>
+struct SymDefSmem {
+    static constexpr int A_ELEMS = BK * (BM + 4);
+    static constexpr int B_ELEMS = BK * (BN + 4);
+    static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
+    static constexpr size_t HAND_OFFSET = size_t(STAGES) * STAGE_ELEMS * sizeof(double);
+    static constexpr size_t HAND_BYTES = size_t(HB) * 4 * WM * WN * 32 * sizeof(double);
+    static constexpr size_t BAR_OFFSET = (HAND_OFFSET + HAND_BYTES + 127) / 128 * 128;
+    static constexpr size_t BYTES = BAR_OFFSET + 2 * STAGES * sizeof(uint64_t);
+};
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int HB>
+__global__ void __launch_bounds__(WM* WN * 32, 1)
+    gemm_symupd_deferred_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                                GemmArgs p) {
+    using SM = SymDefSmem<BM, BN, BK, WM, WN, STAGES, HB>;
+    using T = TileOps<BM, BN, BK, WM, WN, false, false, EPI_SYMUPD>;
+    constexpr int NW = WM * WN, NC = NW * 32;
+    constexpr int MI = T::MI, NI = T::NI, NBLK = MI * NI;
+    constexpr uint32_t STAGE_BYTES = SM::STAGE_ELEMS * sizeof(double);
+    static_assert(BM == BN, "mirror classification assumes square tiles");
+    static_assert(HB >= 0 && HB <= NBLK, "hand-off blocks");
+
+    extern __shared__ __align__(128) double smem[];
+    double2* hand = reinterpret_cast<double2*>(reinterpret_cast<char*>(smem) + SM::HAND_OFFSET);
+    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(smem) + SM::BAR_OFFSET);
+    uint64_t* empty = full + STAGES;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool producer = tid == 0;
+    if (producer) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NW);
+        }
+        mbar_fence_init();
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+    }
+    griddep_wait();
+    griddep_launch();
+    if (p.skip && *p.skip) return;
+    const int64_t W = T::work_count(p);
+    const int nk = (int)((p.K + BK - 1) / BK);
+    const int64_t ldc = p.ldc;
+
+    // TMA producer cursor (thread 0), STAGES−1 stages ahead across work items
+    int64_t pw = blockIdx.x;
+    int pk = 0, ps = 0, pround = 0, pissued = 0;
+    typename T::Work pwork{};
+    if (producer && pw < W) pwork = T::decode(pw, p);
+    auto issue_next = [&]() {
+        const int s = ps;
+        if (pround > 0) mbar_wait(&empty[s], (uint32_t)((pround - 1) & 1));
+        double* As = smem + s * SM::STAGE_ELEMS;
+        double* Bs = As + SM::A_ELEMS;
+        const int32_t kc = (int32_t)(pk * BK);
+        mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+        tma_load_2d(As, &tmA, (int32_t)(pwork.tile_m * BM), kc, &full[s]);
+        tma_load_2d(Bs, &tmB, (int32_t)(pwork.tile_n * BN), kc, &full[s]);
+        ++pissued;
+        if (++ps == STAGES) {
+            ps = 0;
+            ++pround;
+        }
+        if (++pk == nk) {
+            pk = 0;
+            pw += gridDim.x;
+            if (pw < W) pwork = T::decode(pw, p);
+        }
+    };
+    auto pump = [&](int cg) {
+        while (pw < W && pissued < cg + STAGES - 1) issue_next();
+    };
+    __syncthreads();
+    if (producer) pump(0);
+
+    // deferred tile (control flow below is CTA-uniform)
+    bool d_mirror = false, bad = false;
+    int d_blk = HB;             // next handed-off block to retire (HB: none pending)
+    double* d_base = nullptr;   // &X(m0 + wm0 + g, n0 + wn0 + 2·t4) of the deferred tile
+    double* d_mbase = nullptr;  // &X(n0 + wn0 + 2·t4, m0 + wm0 + g): its mirror
+    const double2* myhand = hand + tid;
+    // X += v on one fragment block (16×8: rows g, g+8; columns 2·t4, 2·t4+1) and on its mirror
+    auto red_block = [&](double* base, double* mbase, bool mirror, int i, int j, double v0, double v1, double v2,
+                         double v3) {
+        double* x = base + i * 16 + (int64_t)(j * 8) * ldc;
+        atomicAdd(x, v0);
+        atomicAdd(x + ldc, v1);
+        atomicAdd(x + 8, v2);
+        atomicAdd(x + 8 + ldc, v3);
+        if (mirror) {
+            double* m = mbase + (int64_t)(i * 16) * ldc + j * 8;
+            atomicAdd(m, v0);
+            atomicAdd(m + 1, v1);
+            atomicAdd(m + 8 * ldc, v2);
+            atomicAdd(m + 8 * ldc + 1, v3);
+        }
+        bad |= !isfinite(v0) || !isfinite(v1) || !isfinite(v2) || !isfinite(v3);
+    };
+    auto hook = [&]() {  // one handed-off block of the deferred tile per call
+        if (d_blk >= HB) return;
+        const double2 h0 = myhand[(d_blk * 2 + 0) * NC], h1 = myhand[(d_blk * 2 + 1) * NC];
+        red_block(d_base, d_mbase, d_mirror, d_blk / NI, d_blk % NI, h0.x, h0.y, h1.x, h1.y);
+        ++d_blk;
+    };
+
+    T t;
+    int cg = 0, cs = 0;
+    uint32_t cphase = 0;
+    for (int64_t w = blockIdx.x; w < W; w += gridDim.x) {
+        t.setup_work(w, p, warp, lane);
+        const int64_t m0 = t.m0, n0 = t.n0;
+        // full off-diagonal tile of the symmetric block (mirrored) / full tile right of it (plain)
+        const bool t_mirror = m0 + BM <= n0 && n0 + BN <= p.M;
+        const bool t_plain = n0 >= p.M && m0 + BM <= p.M && n0 + BN <= p.N;
+        {  // this tile's X block (and its mirror) to L2 while it is computed: one prefetch per line
+            constexpr int LINES = BN * (BM / 16);
+            for (int l = tid; l < LINES; l += NC) {
+                const int64_t c = n0 + l / (BM / 16), r = m0 + (l % (BM / 16)) * 16;
+                if (r < p.M && c < p.N) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p.C + r + c * ldc));
+                if (t_mirror) {
+                    const int64_t mc = m0 + l / (BN / 16), mr = n0 + (l % (BN / 16)) * 16;
+                    asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p.C + mr + mc * ldc));
+                }
+            }
+        }
+        double acc[MI][NI][4];
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+            for (int j = 0; j < NI; ++j)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
+        for (int kt = 0; kt < nk; ++kt, ++cg) {
+            if (warp == 0) {
+                if (producer) pump(cg);
+                __syncwarp();
+            }
+            const int s = cs;
+            mbar_wait(&full[s], cphase);
+            if (++cs == STAGES) {
+                cs = 0;
+                cphase ^= 1u;
+            }
+            const double* As = smem + s * SM::STAGE_ELEMS;
+            t.compute_stage(acc, As, As + SM::A_ELEMS);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+#pragma unroll
+            for (int h = 0; h < BK / 8; ++h) hook();
+        }
+        while (d_blk < HB) hook();  // short K: the rest of the previous tile
+        if (t_mirror || t_plain) {
+            const int64_t r = t.row(0, 0), c = t.col(0, 0);
+            double* base = p.C + r + c * ldc;
+            double* mbase = p.C + c + r * ldc;
+#pragma unroll
+            for (int i = 0; i < MI; ++i)
+#pragma unroll
+                for (int j = 0; j < NI; ++j) {
+                    if (i * NI + j < HB) {
+                        hand[((i * NI + j) * 2 + 0) * NC + tid] = make_double2(acc[i][j][0], acc[i][j][1]);
+                        hand[((i * NI + j) * 2 + 1) * NC + tid] = make_double2(acc[i][j][2], acc[i][j][3]);
+                    } else {
+                        red_block(base, mbase, t_mirror, i, j, acc[i][j][0], acc[i][j][1], acc[i][j][2], acc[i][j][3]);
+                    }
+                }
+            d_base = base;
+            d_mbase = mbase;
+            d_mirror = t_mirror;
+            d_blk = 0;
+        } else {  // diagonal / ragged tiles: immediate guarded epilogue
+#pragma unroll
+            for (int i = 0; i < MI; ++i)
+#pragma unroll
+                for (int j = 0; j < NI; ++j)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int64_t r = t.row(i, e), c = t.col(j, e);
+                        if (r < p.M && c < p.N && r <= c) {
+                            const double v = p.C[r + c * ldc] + acc[i][j][e];
+                            p.C[r + c * ldc] = v;
+                            if (r != c && c < p.M) p.C[c + r * ldc] = v;
+                            bad |= !isfinite(v);
+                        }
+                    }
+        }
+    }
+    while (d_blk < HB) hook();
+    if (bad && p.nonfinite) atomicOr(p.nonfinite, 1);
+}
+
 // ------------------------------------------------------ C-panel TMA path --
 // Short-K panel updates C ← beta·C + A·B (the AdaRBFGS factor update L += SR·B, K = q):
 // with only a few k-stages per tile the C-tile loads dominate (ncu: long-scoreboard
@@ -836,6 +1054,189 @@ __global__ void __launch_bounds__(WM* WN * 32, 1)
         }
         t.epilogue(acc, p, tid, NW * 32, [] {});  // c_in_acc: store-only
     }
+}
+
+// ------------------------------------------- C-panel, bulk-store epilogue --
+// C ← beta·C + A·B for a short-K panel update (the AdaRBFGS factor update L += SR·B, K = q)
+// with both directions of the C traffic on the bulk-copy engine.  The C-panel kernel above still
+// pays, per 128×64 tile of only K/16 stages, a 64 KB store burst from registers (SM → L2 at
+// ≈ 64 B/clk: every warp stalled in its stores while the DMMA pipe idles).  Here a tile's C
+// block arrives by TMA into `cin` during the previous tile's mainloop (issued as soon as every
+// warp has seeded its accumulators from the previous block), and the finished tile is written
+// to a second shared-memory tile `cout` (column pitch BM + 4: the conflict-free fragment
+// layout) and leaves as BN bulk copies of one 1 KB column each (cp.async.bulk shared → global,
+// SASS UBLKCP, one per thread of warps 0–1) that drain while the warps are already in the
+// next tile's mainloop.  `cout` is rewritten only after its issuing threads saw their copies'
+// reads complete (mbarrier ofree), a whole mainloop later.  (Letting the L2 do the
+// read-modify-write — cp.reduce.async.bulk .add.f64 from a zero-seeded tile, no C load at all —
+// measured 94 µs against 105 µs at config 2 but is capped by the L2's FP64 atomic rate,
+// ≈ 190 G elements/s: 88 µs for n² = 16.8 M elements.)
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool A_KMAJOR, bool B_KMAJOR>
+struct CBulkSmem {
+    using SM = GemmSmem<BM, BN, BK, WM, WN, STAGES, A_KMAJOR, B_KMAJOR>;
+    static constexpr int LDC = BM + 4;  // pitch of both C tiles (column-major)
+    static constexpr size_t RING = size_t(STAGES) * SM::STAGE_ELEMS * sizeof(double);
+    static constexpr size_t CBUF = size_t(BN) * LDC * sizeof(double);
+    static constexpr size_t BAR_OFFSET = (RING + 2 * CBUF + 127) / 128 * 128;
+    static constexpr size_t BYTES = BAR_OFFSET + (2 * STAGES + 3) * sizeof(uint64_t);
+};
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool A_KMAJOR, bool B_KMAJOR>
+__global__ void __launch_bounds__(WM* WN * 32, 1)
+    gemm_tma_cbulk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                          const __grid_constant__ CUtensorMap tmC, GemmArgs p) {
+    using SM = GemmSmem<BM, BN, BK, WM, WN, STAGES, A_KMAJOR, B_KMAJOR>;
+    using CB = CBulkSmem<BM, BN, BK, WM, WN, STAGES, A_KMAJOR, B_KMAJOR>;
+    using T = TileOps<BM, BN, BK, WM, WN, A_KMAJOR, B_KMAJOR, EPI_STORE>;
+    constexpr int NW = WM * WN, NC = NW * 32;
+    constexpr uint32_t STAGE_BYTES = SM::STAGE_ELEMS * sizeof(double);
+    constexpr uint32_t C_BYTES = uint32_t(BN) * CB::LDC * sizeof(double);
+    static_assert(BN <= NC, "one bulk copy per thread");
+
+    extern __shared__ __align__(128) double smem[];
+    double* cin = reinterpret_cast<double*>(reinterpret_cast<char*>(smem) + CB::RING);
+    double* cout = cin + size_t(BN) * CB::LDC;
+    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(smem) + CB::BAR_OFFSET);
+    uint64_t* empty = full + STAGES;
+    uint64_t* cfull = empty + STAGES;  // the item's C block has landed in cin
+    uint64_t* cseeded = cfull + 1;     // every warp has read cin (count NW)
+    uint64_t* ofree = cseeded + 1;     // the previous item's bulk copies have left cout (count BN)
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool producer = tid == 0;
+    if (producer) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NW);
+        }
+        mbar_init(cfull, 1);
+        mbar_init(cseeded, NW);
+        mbar_init(ofree, BN);
+        mbar_fence_init();
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+        tma_prefetch_desc(&tmC);
+    }
+    griddep_wait();
+    griddep_launch();
+    if (p.skip && *p.skip) return;
+    const int64_t W = T::work_count(p);
+    const int nk = (int)((p.K + BK - 1) / BK);  // unsplit
+
+    auto issue_c = [&](int64_t w) {  // C block of work item w into cin
+        const typename T::Work wk = T::decode(w, p);
+        mbar_arrive_expect_tx(cfull, C_BYTES);
+        tma_load_2d(cin, &tmC, (int32_t)(wk.tile_m * BM), (int32_t)(wk.tile_n * BN), cfull);
+    };
+    int64_t pw = blockIdx.x;
+    int pk = 0, ps = 0, pround = 0, pissued = 0;
+    typename T::Work pwork{};
+    if (producer && pw < W) pwork = T::decode(pw, p);
+    auto issue_next = [&]() {
+        const int s = ps;
+        if (pround > 0) mbar_wait(&empty[s], (uint32_t)((pround - 1) & 1));
+        double* As = smem + s * SM::STAGE_ELEMS;
+        double* Bs = As + SM::A_ELEMS;
+        const int32_t kc = (int32_t)((int64_t)pk * BK);
+        const int32_t mc = (int32_t)(pwork.tile_m * BM), nc = (int32_t)(pwork.tile_n * BN);
+        mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+        if constexpr (A_KMAJOR)
+            tma_load_2d(As, &tmA, kc, mc, &full[s]);
+        else
+            tma_load_2d(As, &tmA, mc, kc, &full[s]);
+        if constexpr (B_KMAJOR)
+            tma_load_2d(Bs, &tmB, kc, nc, &full[s]);
+        else
+            tma_load_2d(Bs, &tmB, nc, kc, &full[s]);
+        ++pissued;
+        if (++ps == STAGES) {
+            ps = 0;
+            ++pround;
+        }
+        if (++pk == nk) {
+            pk = 0;
+            pw += gridDim.x;
+            if (pw < W) pwork = T::decode(pw, p);
+        }
+    };
+    auto pump = [&](int cg) {
+        while (pw < W && pissued < cg + STAGES - 1) issue_next();
+    };
+    __syncthreads();
+    if (producer) {
+        if (blockIdx.x < W) issue_c(blockIdx.x);
+        pump(0);
+    }
+
+    T t;
+    int cg = 0, cs = 0, item = 0;
+    uint32_t cphase = 0;
+    bool bad = false;
+    for (int64_t w = blockIdx.x; w < W; w += gridDim.x, ++item) {
+        t.setup_work(w, p, warp, lane);
+        double acc[T::MI][T::NI][4];
+        {  // seed from the C block in shared memory (beta·C)
+            mbar_wait(cfull, (uint32_t)(item & 1));
+#pragma unroll
+            for (int i = 0; i < T::MI; ++i)
+#pragma unroll
+                for (int j = 0; j < T::NI; ++j)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int lr = t.wm0 + i * 16 + t.g + ((e >> 1) << 3), lc = t.wn0 + j * 8 + 2 * t.t4 + (e & 1);
+                        acc[i][j][e] = p.beta * cin[lc * CB::LDC + lr];
+                    }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(cseeded);
+            if (producer && w + gridDim.x < W) {  // cin is free once every warp has seeded: fetch the next block
+                mbar_wait(cseeded, (uint32_t)(item & 1));
+                issue_c(w + gridDim.x);
+            }
+        }
+        for (int kt = 0; kt < nk; ++kt, ++cg) {
+            if (warp == 0) {
+                if (producer) pump(cg);
+                __syncwarp();
+            }
+            const int s = cs;
+            mbar_wait(&full[s], cphase);
+            if (++cs == STAGES) {
+                cs = 0;
+                cphase ^= 1u;
+            }
+            const double* As = smem + s * SM::STAGE_ELEMS;
+            t.compute_stage(acc, As, As + SM::A_ELEMS);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+        // the finished tile leaves through cout; the previous item's copies were issued a mainloop ago
+        if (item >= 1) {
+            if (tid < BN) {
+                bulk_wait_read<0>();
+                mbar_arrive(ofree);
+            }
+            mbar_wait(ofree, (uint32_t)((item - 1) & 1));
+        }
+#pragma unroll
+        for (int i = 0; i < T::MI; ++i)
+#pragma unroll
+            for (int j = 0; j < T::NI; ++j)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int lr = t.wm0 + i * 16 + t.g + ((e >> 1) << 3), lc = t.wn0 + j * 8 + 2 * t.t4 + (e & 1);
+                    cout[lc * CB::LDC + lr] = acc[i][j][e];
+                    bad |= !isfinite(acc[i][j][e]);
+                }
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (tid < BN) {
+            const int64_t col = t.n0 + tid;
+            const int64_t rows = min((int64_t)BM, p.M - t.m0);
+            if (col < p.N && rows > 0) bulk_store(p.C + t.m0 + col * p.ldc, cout + tid * CB::LDC, (uint32_t)(rows * sizeof(double)));
+            bulk_commit();
+        }
+    }
+    if (tid < BN) bulk_wait<0>();
+    if (bad && p.nonfinite) atomicOr(p.nonfinite, 1);
 }
 
 // One CTA per work item (grid = tiles × splits): the long-K products (Y = A·S,

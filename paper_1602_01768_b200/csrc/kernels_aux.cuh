@@ -411,6 +411,7 @@ __global__ void philox_gaussian_kernel(double* __restrict__ S, int64_t n, int64_
     const uint64_t draw = draw_counter ? *draw_counter : draw_value;
     const int64_t total = n * q;
     const int64_t pairs = (total + 1) / 2;
+    const bool pair16 = (n & 1) == 0 && (lds & 1) == 0 && (reinterpret_cast<uintptr_t>(S) & 15) == 0;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < pairs; e += (int64_t)gridDim.x * blockDim.x) {
         uint32_t c[4] = {(uint32_t)e, (uint32_t)(e >> 32), (uint32_t)draw, (uint32_t)(draw >> 32)};
         Philox::gen(c, (uint32_t)seed, (uint32_t)(seed >> 32));
@@ -435,8 +436,12 @@ __global__ void philox_gaussian_kernel(double* __restrict__ S, int64_t n, int64_
             j1 = l1 / n;
             i1 = l1 - j1 * n;
         }
-        S[i0 + j0 * lds] = r * cs;
-        if (l1 < total) S[i1 + j1 * lds] = r * sn;
+        if (pair16) {  // n even: the pair shares a column and is 16-byte aligned — one full-width store
+            *reinterpret_cast<double2*>(S + i0 + j0 * lds) = make_double2(r * cs, r * sn);
+        } else {
+            S[i0 + j0 * lds] = r * cs;
+            if (l1 < total) S[i1 + j1 * lds] = r * sn;
+        }
     }
 }
 

@@ -224,6 +224,87 @@ __global__ void spmm_csr_rowmajor_kernel(int64_t n, const int64_t* __restrict__ 
     }
 }
 
+// Row-blocked row-major SpMM: one warp computes R consecutive rows of Y for 64·NS columns.
+// The warp-per-row kernel above reads one k-row of Pr per nonzero (config 5: 129 nonzeros per
+// row, q = 512: 52 GB of L2 → SM traffic per product, 54× the algorithmic bytes) although
+// neighbouring rows of a banded or stencil matrix touch nearly the same columns.  Here the R
+// rows' column lists are walked together, smallest pending column first: its Pr row is
+// loaded once (NS 16-byte loads per lane) and used by every row of the block that holds that
+// column, and each (colind, val) load is amortised over 64·NS columns.  Every row still
+// accumulates its nonzeros in storage order, so the result is bitwise that of the per-row
+// kernel; unsorted or duplicate column indices only cost sharing, not correctness.
+template <int R, int NS>
+__global__ void __launch_bounds__(256)
+    spmm_csr_rowblock_kernel(int64_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
+                             const double* __restrict__ val, const double* __restrict__ Pr, int64_t k,
+                             double* __restrict__ Y, int64_t ldy, const int* skip) {
+    if (skip && *skip) return;
+    static_assert(R % 2 == 0, "row pairs are stored together");
+    constexpr int32_t NONE = 0x7fffffff;
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t passes = k / (64 * NS), blocks = (n + R - 1) / R;
+    const bool pair16 = (ldy & 1) == 0 && (reinterpret_cast<uintptr_t>(Y) & 15) == 0;
+    for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < blocks * passes; u += warps) {
+        const int64_t rb = u / passes, pass = u - rb * passes;
+        const int64_t row0 = rb * R, c0 = pass * (64 * NS) + 2 * lane;
+        int64_t ptr[R], end[R];
+        int32_t cur[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const bool ok = row0 + r < n;
+            ptr[r] = ok ? rowptr[row0 + r] : 0;
+            end[r] = ok ? rowptr[row0 + r + 1] : 0;
+            cur[r] = ptr[r] < end[r] ? __ldg(colind + ptr[r]) : NONE;
+        }
+        double2 acc[R][NS];
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int s = 0; s < NS; ++s) acc[r][s] = make_double2(0.0, 0.0);
+        for (;;) {
+            int32_t cmin = cur[0];
+#pragma unroll
+            for (int r = 1; r < R; ++r) cmin = min(cmin, cur[r]);
+            if (cmin == NONE) break;
+            const double2* prow = reinterpret_cast<const double2*>(Pr + (int64_t)cmin * k + c0);
+            double2 x[NS];
+#pragma unroll
+            for (int s = 0; s < NS; ++s) x[s] = __ldg(prow + s * 32);
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                if (cur[r] == cmin) {
+                    const double v = __ldg(val + ptr[r]);
+#pragma unroll
+                    for (int s = 0; s < NS; ++s) {
+                        acc[r][s].x += v * x[s].x;
+                        acc[r][s].y += v * x[s].y;
+                    }
+                    ++ptr[r];
+                    cur[r] = ptr[r] < end[r] ? __ldg(colind + ptr[r]) : NONE;
+                }
+        }
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            double* y0 = Y + row0 + (c0 + s * 64) * ldy;  // column c, rows row0..; column c + 1 at y0 + ldy
+#pragma unroll
+            for (int r = 0; r < R; r += 2) {
+                if (pair16 && row0 + r + 1 < n) {
+                    *reinterpret_cast<double2*>(y0 + r) = make_double2(acc[r][s].x, acc[r + 1][s].x);
+                    *reinterpret_cast<double2*>(y0 + ldy + r) = make_double2(acc[r][s].y, acc[r + 1][s].y);
+                } else {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+                        if (row0 + r + h < n) {
+                            y0[r + h] = acc[r + h][s].x;
+                            y0[ldy + r + h] = acc[r + h][s].y;
+                        }
+                }
+            }
+        }
+    }
+}
+
 // Column-major SpMM for very wide dense operands (k ≫ 1, e.g. A·L with k = n):
 // thread per (row i, column j); consecutive rows of a banded / stencil A touch
 // consecutive rows of P, so the P loads of a warp coalesce.

@@ -1,7 +1,9 @@
 """AdaRBFGS iterations of config 2's shape (paper uniform sampler) for launch-list
 profiling: `ncu --metrics gpu__time_duration.sum ... python tools/prof_ada.py` (development tool)."""
+import os
 import sys
 
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1602_01768_b200 as si
 from paper_1602_01768_b200 import generators as G
 
