@@ -22,7 +22,7 @@ e2e    : the same metric through the public driver si_run_inverter (the call a
          timer.
 roofline: the dominant kernel class (split-K long-K GEMMs Y = A·S and
          W' = −X·Y): algorithmic FLOPs per launch (2n²q) ÷ its CUDA-event time,
-         against the measured FP64 DMMA peak (profiles/r01_fp64_peak.txt);
+         against the measured FP64 DMMA peak (profiles/r02_fp64_peak.txt);
          roofline_secondary is K-SYMUPD (2n²q on the upper tiles).
 time_to_eps: config 1 (n = 1024, q = 32) to ‖I−AX‖_F/√n ≤ 1e-2 and to the
          reference normalisation ‖I−AX_k‖_F/‖I−AX_0‖_F ≤ 1e-2; config 3 with an
@@ -52,13 +52,14 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-FP64_DMMA_PEAK_TFLOPS = 36.94  # profiles/r01_fp64_peak.txt (mma.sync m16n8k8 .f64, 148 SMs)
+FP64_DMMA_PEAK_TFLOPS = 37.14  # profiles/r02_fp64_peak.txt (mma.sync m16n8k8 .f64, 148 SMs at 1965 MHz, clocks recorded;
+                               # 148 x 64 FMA/clk x 2 x 1.965 GHz = 37.2)
 HBM_PEAK_GBS = None
 
 
 def load_traffic():
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as f:
             return json.load(f)
     except Exception:
         return {}
@@ -437,7 +438,7 @@ def run_sharded(args, cfg):
             "roofline": {"bound": "tensor", "kernel": "rank 0's sharded iteration (all DMMA GEMMs of one rank)",
                          "achieved": achieved, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": achieved / FP64_DMMA_PEAK_TFLOPS, "traffic": None,
-                         "peak_source": "measured FP64 DMMA peak, profiles/r01_fp64_peak.txt"},
+                         "peak_source": "measured FP64 DMMA peak, profiles/r02_fp64_peak.txt"},
             "cpu_baseline": None,
             "e2e": e2e,
             "gpu_launches": int(launches),
@@ -828,9 +829,9 @@ def run_ours(args, cfg):
 
     dom_name = max((k for k in prof if k in class_flops), key=lambda k: prof[k][1])
     roofline = roof(dom_name)
-    roofline.update({"peak_source": "measured FP64 DMMA peak, profiles/r01_fp64_peak.txt (MEASURED_PEAKS.json has "
+    roofline.update({"peak_source": "measured FP64 DMMA peak, profiles/r02_fp64_peak.txt (MEASURED_PEAKS.json has "
                                     "no FP64 entry; tcgen05 has no f64 kind)",
-                     "traffic_source": "profiles/r01_traffic.json (ncu --set full, bytes per launch)",
+                     "traffic_source": "profiles/r02_traffic.json (ncu --set full, bytes per launch)",
                      "kernel_share_of_step": shares,
                      "kernel_share_note": "per-launch CUDA events in an eager profiling pass (shares of the summed kernel times); K-FACTOR (gram_inverse) runs on a second stream under W' = -X·Y, so its time overlaps gemm_splitk"})
     secondary = roof("gemm_symupd") if "gemm_symupd" in prof and dom_name != "gemm_symupd" else None

@@ -894,7 +894,12 @@ static void launch_spmm_rowmajor(Context& c, int64_t m, const int64_t* rowptr, c
     }();
     if (rowblock && k >= 64 && k % 64 == 0) {
         constexpr int R = 4;
-        const int ns = k % 256 == 0 ? 4 : (k % 128 == 0 ? 2 : 1);
+        static const int ns_cap = [] {  // SI_SPMM_NS: the most 64-column slabs per warp pass (1, 2, 4)
+            const char* e = std::getenv("SI_SPMM_NS");
+            return e ? std::atoi(e) : 4;
+        }();
+        int ns = k % 256 == 0 ? 4 : (k % 128 == 0 ? 2 : 1);
+        while (ns > ns_cap && ns > 1) ns /= 2;
         const int64_t units = ((m + R - 1) / R) * (k / (64 * ns));
         const dim3 grid(grid_for(units * 32, 256, c.num_sms * 32));
         if (ns == 4)
