@@ -340,6 +340,24 @@ __global__ void transpose_kernel(const double* __restrict__ P, int64_t n, int64_
     }
 }
 
+// out(j, i) = P(i, j) for an n×k block P (ld ldp) into a k×n block (ld ldo): the block row of a
+// symmetric working matrix refreshed from its block column (validate_spd's left-looking sweep)
+__global__ void transpose_ld_kernel(const double* __restrict__ P, int64_t n, int64_t k, int64_t ldp,
+                                    double* __restrict__ out, int64_t ldo, const int* skip) {
+    if (skip && *skip) return;
+    __shared__ double tile[32][33];
+    const int64_t i0 = (int64_t)blockIdx.x * 32, j0 = (int64_t)blockIdx.y * 32;
+    for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+        const int64_t i = i0 + threadIdx.x, j = j0 + dy;
+        if (i < n && j < k) tile[dy][threadIdx.x] = P[i + j * ldp];
+    }
+    __syncthreads();
+    for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+        const int64_t i = i0 + dy, j = j0 + threadIdx.x;
+        if (i < n && j < k) out[j + i * ldo] = tile[threadIdx.x][dy];
+    }
+}
+
 // d_j = sum_i AL(i,j) * L(i,j)  (diag(Lᵀ A L)); one warp per column.
 __global__ void column_dots_kernel(const double* __restrict__ AL, const double* __restrict__ L, int64_t n,
                                    double* __restrict__ d) {
