@@ -1240,27 +1240,54 @@ bool problem_validate_spd(Problem& p, double* scratch) {
     //     S_k = A[k:, k:k+b] + W[k:, 0:k] · W[0:k, k:k+b]      (T, M-major) · (Bᵀ, K-major),
     // its leading b×b block goes through K-FACTOR (pivots tested), its remainder B_k is mirrored
     // into the block row and T_k = −B_k·D_k⁻¹ is computed from that mirror into the block column.
+    // Look-ahead: K-FACTOR(D_k) → B_kᵀ → T_k is a chain of small launches (≈ 0.1 ms per panel, 128
+    // panels); it runs on the high-priority side stream while the main stream already forms the
+    // part of S_{k+1} that does not depend on panel k (the product over panels < k); panel k's own
+    // rank-b term is added after the join.  SI_VALIDATE_SERIAL=1 keeps everything on one stream.
     static const bool right_looking = std::getenv("SI_VALIDATE_RIGHT") != nullptr;
+    static const bool lookahead = std::getenv("SI_VALIDATE_SERIAL") == nullptr;
     for (int64_t k = 0; !right_looking && k < n; k += BLK) {
         const int64_t b = std::min(BLK, n - k), rest = n - k - b;
         double* D = W + k + k * n;
-        if (k > 0) gemm(c, n - k, b, k, W + k, n, false, W + k * n, n, true, D, n, 1.0, 1.0, st);  // S_k
-        if (b <= 32)
-            launch_gram_fused<32>(c, D, n, b, Dinv, nullptr, st);
-        else if (b <= 64)
-            launch_gram_fused<64>(c, D, n, b, Dinv, nullptr, st);
-        else
-            launch_gram_fused<128>(c, D, n, b, Dinv, nullptr, st);
-        if (rest == 0) break;
-        double* Bcol = W + (k + b) + k * n;   // B_k: rest×b, ld n
-        double* Brow = W + k + (k + b) * n;   // B_kᵀ: b×rest, ld n
-        {
-            LaunchScope ls(c, "transpose");
-            dim3 grid(unsigned((rest + 31) / 32), unsigned((b + 31) / 32));
-            transpose_ld_kernel<<<grid, dim3(32, 8), 0, c.stream>>>(Bcol, rest, b, n, Brow, n, st);
-            check_launch("transpose_ld");
+        // S_k is complete here (k = 0: A itself)
+        auto chain = [&]() {
+            if (b <= 32)
+                launch_gram_fused<32>(c, D, n, b, Dinv, nullptr, st);
+            else if (b <= 64)
+                launch_gram_fused<64>(c, D, n, b, Dinv, nullptr, st);
+            else
+                launch_gram_fused<128>(c, D, n, b, Dinv, nullptr, st);
+            if (rest == 0) return;
+            double* Bcol = W + (k + b) + k * n;   // B_k: rest×b, ld n
+            double* Brow = W + k + (k + b) * n;   // B_kᵀ: b×rest, ld n
+            {
+                LaunchScope ls(c, "transpose");
+                dim3 grid(unsigned((rest + 31) / 32), unsigned((b + 31) / 32));
+                transpose_ld_kernel<<<grid, dim3(32, 8), 0, c.stream>>>(Bcol, rest, b, n, Brow, n, st);
+                check_launch("transpose_ld");
+            }
+            gemm(c, rest, b, b, Brow, n, true, Dinv, b, true, Bcol, n, -1.0, 0.0, st);  // T_k = −B_k·D_k⁻¹
+        };
+        if (rest == 0) {
+            chain();
+            break;
         }
-        gemm(c, rest, b, b, Brow, n, true, Dinv, b, true, Bcol, n, -1.0, 0.0, st);  // T_k = −B_k·D_k⁻¹
+        const int64_t k1 = k + b, b1 = std::min(BLK, n - k1);
+        double* S1 = W + k1 + k1 * n;  // S_{k+1}: (n − k1)×b1, ld n
+        if (lookahead && k > 0) {
+            c.fork(true);
+            {
+                SideScope side(c, true);
+                chain();
+            }
+            gemm(c, n - k1, b1, k, W + k1, n, false, W + k1 * n, n, true, S1, n, 1.0, 1.0, st);  // panels < k
+            c.join(true);
+        } else {
+            chain();
+            if (k > 0) gemm(c, n - k1, b1, k, W + k1, n, false, W + k1 * n, n, true, S1, n, 1.0, 1.0, st);
+        }
+        // panel k's own term: S_{k+1} += T_k[b:, :]·B_k[0:b1, :]ᵀ
+        gemm(c, n - k1, b1, b, W + k1 + k * n, n, false, W + k + k1 * n, n, true, S1, n, 1.0, 1.0, st);
     }
     for (int64_t k = 0; right_looking && k < n; k += BLK) {
         const int64_t b = std::min(BLK, n - k);
