@@ -41,6 +41,31 @@ def test_cpanel_update_shapes(env, ak, bk, M, N, K):
         assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max() * K
 
 
+@pytest.mark.parametrize("M,N,K,pad", [(300, 130, 64, 6), (512, 192, 128, 2), (258, 66, 32, 10)])
+def test_cpanel_update_guard_bands(env, M, N, K, pad):
+    # C with a leading dimension larger than M inside a sentinel-filled buffer: the bulk copies
+    # must write exactly the M rows of each column — not the padding rows, nothing before or after
+    si, torch, ctx, ops = env
+    rng = np.random.default_rng(M + N + K + pad)
+    a = rng.standard_normal((M, K))
+    b = rng.standard_normal((K, N))
+    c0 = rng.standard_normal((M, N))
+    ldc, guard, sentinel = M + pad, 4096, -7.25
+    A = torch.from_numpy(a.T.copy().reshape(-1)).cuda()
+    B = torch.from_numpy(b.T.copy().reshape(-1)).cuda()
+    buf = torch.full((guard + ldc * N + guard,), sentinel, dtype=torch.float64, device="cuda")
+    view = buf[guard:guard + ldc * N].view(N, ldc)
+    view[:, :M] = torch.from_numpy(c0.T.copy()).cuda()
+    ops.gemm(M, N, K, A, M, False, B, K, True, buf[guard:], ldc, 1.0, 1.0)
+    torch.cuda.synchronize()
+    out = buf.cpu().numpy()
+    assert (out[:guard] == sentinel).all() and (out[guard + ldc * N:] == sentinel).all()
+    body = out[guard:guard + ldc * N].reshape((N, ldc))
+    assert (body[:, M:] == sentinel).all()
+    ref = a @ b + c0
+    assert np.abs(body[:, :M].T - ref).max() <= 1e-13 * np.abs(ref).max() * K
+
+
 def test_cpanel_update_many_tiles_per_cta(env):
     # more work items than SMs: every CTA walks several tiles (C-in / C-out buffer reuse)
     si, torch, ctx, ops = env
@@ -89,9 +114,14 @@ def test_spmm_rowblock(env, n, k, kind):
     P = rng.standard_normal((n, k))
     rp, ci, va = (torch.from_numpy(x).cuda() for x in (rowptr, colind, val))
     Pd = torch.from_numpy(P.T.copy().reshape(-1)).cuda()  # column-major n×k
-    Y = torch.full((k * n,), np.nan, dtype=torch.float64, device="cuda")
+    guard = 1024
+    buf = torch.full((guard + k * n + guard,), np.nan, dtype=torch.float64, device="cuda")
+    buf[:guard] = -7.25
+    buf[guard + k * n:] = -7.25
+    Y = buf[guard:guard + k * n]
     ops.spmm(n, n, rp, ci, va, Pd, n, k, Y, n)
     torch.cuda.synchronize()
+    assert (buf[:guard] == -7.25).all().item() and (buf[guard + k * n:] == -7.25).all().item()
     got = Y.cpu().numpy().reshape((k, n)).T
     ref = _csr_reference(rowptr, colind, val, P)
     assert np.isfinite(got).all()
