@@ -403,6 +403,25 @@ static void launch_cbulk_cfg(Context& c, const GemmArgs& a, int64_t work) {
                ta, tb, tc, a);
 }
 
+// A-stationary C-panel launch (gemm_tma_cstat_kernel): C = beta·Csrc + A·B for K ≤ 64, A M-major,
+// B K-major; 128×64 tiles in row-strip order, 8 warps, one CTA per SM
+static void launch_cstat(Context& c, const GemmArgs& a) {
+    constexpr int BM = 128, BN = 64, KMAX = 64, WM = 4, WN = 2;
+    using SM = CStatSmem<BM, BN, KMAX>;
+    static_assert(SM::BYTES <= 232448, "shared memory per CTA");
+    auto kern = gemm_tma_cstat_kernel<BM, BN, KMAX, WM, WN>;
+    static DeviceOnce once;
+    if (once.first(c.device)) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SM::BYTES)));
+    CUtensorMap ta, tb, tc;
+    make_tmap(&ta, a.A, a.M, a.K, a.lda, BM + 4, KMAX);
+    make_tmap(&tb, a.B, a.K, a.N, a.ldb, KMAX + 4, BN);
+    make_tmap(&tc, a.Csrc ? a.Csrc : a.C, a.M, a.N, a.ldc, BM + 4, BN);
+    const int64_t work = ((a.M + BM - 1) / BM) * ((a.N + BN - 1) / BN);
+    LaunchScope ls(c, "gemm_cpanel");
+    launch_pdl(kern, dim3(unsigned(std::min<int64_t>(work, int64_t(c.num_sms)))), dim3(WM * WN * 32), SM::BYTES, c.stream,
+               ta, tb, tc, a);
+}
+
 template <bool AK, bool BKM, int VEC, int EPI>
 static void launch_gemm_tile(Context& c, TileCfg t, const GemmArgs& a, dim3 grid, const char* name, bool tma) {
     if (EPI == EPI_SYMUPD && t == T64x128) throw std::logic_error("gemm_symupd: tile height must be a multiple of its width");
@@ -557,6 +576,11 @@ void gemm(Context& c, int64_t M, int64_t N, int64_t K, const double* A, int64_t 
         }
     }
     const int vec = pick_vec(a);
+    static const int force_split = [] {  // SI_SPLITK_FORCE (experiments): the split of every split-K product
+        const char* e = std::getenv("SI_SPLITK_FORCE");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (force_split > 0 && splits > 1) splits = force_split;
     if (K == 0) {
         splits = 1;
     }
@@ -578,6 +602,16 @@ void gemm(Context& c, int64_t M, int64_t N, int64_t K, const double* A, int64_t 
             aligned_ptr(C, 16) && aligned_ptr(Csrc ? Csrc : C, 16)) {
             // the finished tiles leave by bulk copies from shared memory (SI_CPANEL_BULK=0: stores from
             // registers); an even M keeps every column segment a multiple of 16 bytes
+            // K ≤ 64 (AdaRBFGS at q ≤ 64): the whole A slice of a row strip stays in shared memory
+            // (SI_CPANEL_STAT=0: the ring kernels below)
+            static const bool cstat = [] {
+                const char* e = std::getenv("SI_CPANEL_STAT");
+                return !(e && e[0] == '0');
+            }();
+            if (cstat && K <= 64 && !a_kmajor && b_kmajor) {
+                launch_cstat(c, a);
+                return;
+            }
             static const bool cbulk = [] {
                 const char* e = std::getenv("SI_CPANEL_BULK");
                 return !(e && e[0] == '0');

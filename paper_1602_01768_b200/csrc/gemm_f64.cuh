@@ -1239,6 +1239,165 @@ __global__ void __launch_bounds__(WM* WN * 32, 1)
     if (bad && p.nonfinite) atomicOr(p.nonfinite, 1);
 }
 
+// ------------------------------------------- C-panel, A-stationary (K ≤ 64) --
+// C ← beta·C + A·B for a panel update whose whole K fits one shared-memory operand (the
+// AdaRBFGS factor update L += SR·B at q ≤ 64).  With K = 64 a 128×64 tile is only four BK = 16
+// stages: the ring kernels above spend as long waiting on operand stages and tile changes as
+// on DMMA (ncu: the warps sit on full[]; 100 µs for 58 µs of DMMA work at config 2).  Here
+// each CTA owns a contiguous run of tiles in row-strip order, so the 128×K slice of A stays
+// in shared memory for the whole strip (reloaded at most once per CTA), the K×64 slice of B
+// arrives as ONE TMA box per tile (double-buffered, a whole tile ahead) and the C tile by TMA
+// into a third buffer, one tile ahead: two barrier waits per tile instead of five, and
+// 100 KB instead of 170 KB fetched per tile.  A not K-major, B K-major (the L-update layout).
+template <int BM, int BN, int KMAX>
+struct CStatSmem {
+    static constexpr int LDA = BM + 4, LDB = KMAX + 4, LDC = BM + 4;
+    static constexpr size_t A_BYTES = size_t(KMAX) * LDA * sizeof(double);
+    static constexpr size_t B_BYTES = size_t(BN) * LDB * sizeof(double);
+    static constexpr size_t C_BYTES = size_t(BN) * LDC * sizeof(double);
+    static constexpr size_t B_OFFSET = A_BYTES, C_OFFSET = A_BYTES + 2 * B_BYTES;
+    static constexpr size_t BAR_OFFSET = (C_OFFSET + C_BYTES + 127) / 128 * 128;
+    static constexpr size_t BYTES = BAR_OFFSET + 8 * sizeof(uint64_t);
+};
+
+template <int BM, int BN, int KMAX, int WM, int WN>
+__global__ void __launch_bounds__(WM* WN * 32, 1)
+    gemm_tma_cstat_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                          const __grid_constant__ CUtensorMap tmC, GemmArgs p) {
+    using SM = CStatSmem<BM, BN, KMAX>;
+    using T = TileOps<BM, BN, KMAX, WM, WN, false, true, EPI_STORE>;
+    constexpr int NW = WM * WN;
+    static_assert(SM::A_BYTES % 128 == 0 && SM::B_BYTES % 128 == 0 && SM::C_BYTES % 128 == 0, "TMA destinations");
+
+    extern __shared__ __align__(128) double smem[];
+    double* As = smem;
+    double* Bs = reinterpret_cast<double*>(reinterpret_cast<char*>(smem) + SM::B_OFFSET);
+    double* Cs = reinterpret_cast<double*>(reinterpret_cast<char*>(smem) + SM::C_OFFSET);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(smem) + SM::BAR_OFFSET);
+    uint64_t* afull = bars;        // the strip's A slice has landed
+    uint64_t* adone = bars + 1;    // every warp has finished the strip (count NW)
+    uint64_t* bfull = bars + 2;    // [2] B slice of item i in buffer i & 1
+    uint64_t* bdone = bars + 4;    // [2] every warp has finished with that buffer (count NW)
+    uint64_t* cfull = bars + 6;    // the item's C block has landed
+    uint64_t* cseeded = bars + 7;  // every warp has read it (count NW)
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool producer = tid == 0;
+    if (producer) {
+        mbar_init(afull, 1);
+        mbar_init(adone, NW);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&bfull[b], 1);
+            mbar_init(&bdone[b], NW);
+        }
+        mbar_init(cfull, 1);
+        mbar_init(cseeded, NW);
+        mbar_fence_init();
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+        tma_prefetch_desc(&tmC);
+    }
+    griddep_wait();
+    griddep_launch();
+    if (p.skip && *p.skip) return;
+    // this CTA's run of tiles, row strips outermost: item t = strip · tn + column tile
+    const int64_t tm = (p.M + BM - 1) / BM, tn = (p.N + BN - 1) / BN, W = tm * tn;
+    const int64_t w0 = W * blockIdx.x / gridDim.x, w1 = W * (blockIdx.x + 1) / gridDim.x;
+    auto issue_a = [&](int64_t strip) {
+        mbar_arrive_expect_tx(afull, (uint32_t)SM::A_BYTES);
+        tma_load_2d(As, &tmA, (int32_t)(strip * BM), 0, afull);
+    };
+    auto issue_b = [&](int64_t w, int item) {
+        const int b = item & 1;
+        if (item >= 2) mbar_wait(&bdone[b], (uint32_t)(((item >> 1) - 1) & 1));
+        mbar_arrive_expect_tx(&bfull[b], (uint32_t)SM::B_BYTES);
+        tma_load_2d(Bs + size_t(b) * BN * SM::LDB, &tmB, 0, (int32_t)((w % tn) * BN), &bfull[b]);
+    };
+    auto issue_c = [&](int64_t w) {
+        mbar_arrive_expect_tx(cfull, (uint32_t)SM::C_BYTES);
+        tma_load_2d(Cs, &tmC, (int32_t)((w / tn) * BM), (int32_t)((w % tn) * BN), cfull);
+    };
+    __syncthreads();
+    if (producer && w0 < w1) {
+        issue_a(w0 / tn);
+        issue_c(w0);
+        issue_b(w0, 0);
+        if (w0 + 1 < w1) issue_b(w0 + 1, 1);
+    }
+
+    T t;
+    int strips = 0;  // A slices consumed so far
+    int64_t cur_strip = -1;
+    bool bad = false;
+    for (int64_t w = w0; w < w1; ++w) {
+        const int item = (int)(w - w0);
+        // TileOps::setup_work decodes column-major tile order; this kernel walks strips, so set the tile here
+        t.tile_m = w / tn;
+        t.tile_n = w % tn;
+        t.split = 0;
+        t.m0 = t.tile_m * BM;
+        t.n0 = t.tile_n * BN;
+        t.g = lane >> 2;
+        t.t4 = lane & 3;
+        t.wm0 = (warp / WN) * (BM / WM);
+        t.wn0 = (warp % WN) * (BN / WN);
+        if (t.tile_m != cur_strip) {
+            if (cur_strip >= 0) {  // the previous strip is finished: its A slice may be replaced
+                __syncwarp();
+                if (lane == 0) mbar_arrive(adone);
+                if (producer) {
+                    mbar_wait(adone, (uint32_t)((strips - 1) & 1));
+                    issue_a(t.tile_m);
+                }
+            }
+            cur_strip = t.tile_m;
+            mbar_wait(afull, (uint32_t)(strips & 1));
+            ++strips;
+        }
+        double acc[T::MI][T::NI][4];
+        mbar_wait(cfull, (uint32_t)(item & 1));
+#pragma unroll
+        for (int i = 0; i < T::MI; ++i)
+#pragma unroll
+            for (int j = 0; j < T::NI; ++j)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int lr = t.wm0 + i * 16 + t.g + ((e >> 1) << 3), lc = t.wn0 + j * 8 + 2 * t.t4 + (e & 1);
+                    acc[i][j][e] = p.beta * Cs[lc * SM::LDC + lr];
+                }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(cseeded);
+        if (producer && w + 1 < w1) {  // the C buffer is free once every warp has seeded
+            mbar_wait(cseeded, (uint32_t)(item & 1));
+            issue_c(w + 1);
+        }
+        const int b = item & 1;
+        mbar_wait(&bfull[b], (uint32_t)((item >> 1) & 1));
+        {
+            const double* Bb = Bs + size_t(b) * BN * SM::LDB;
+#pragma unroll 1
+            for (int kk = 0; kk < KMAX; kk += 16)  // rolled: a full unroll keeps every fragment of the slice live
+                t.template compute_part<0, 16>(acc, As + kk * SM::LDA, Bb + kk);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bdone[b]);
+        // store-only epilogue (the accumulators hold beta·C + A·B)
+#pragma unroll
+        for (int i = 0; i < T::MI; ++i)
+#pragma unroll
+            for (int j = 0; j < T::NI; ++j)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int64_t r = t.row(i, e), c = t.col(j, e);
+                    if (r < p.M && c < p.N) {
+                        p.C[r + c * p.ldc] = acc[i][j][e];
+                        bad |= !isfinite(acc[i][j][e]);
+                    }
+                }
+        if (producer && w + 2 < w1) issue_b(w + 2, item + 2);  // buffer b again, once every warp has left it
+    }
+    if (bad && p.nonfinite) atomicOr(p.nonfinite, 1);
+}
+
 // One CTA per work item (grid = tiles × splits): the long-K products (Y = A·S,
 // W = X·Y), whose pipeline fill is amortised over ≥ 100 k-stages.
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool A_KMAJOR, bool B_KMAJOR, int EPI>
