@@ -856,27 +856,35 @@ def run_ours(args, cfg):
         si.run_inverter(si.InverterConfig(warm, si.SketchRule.gaussian_device(q), tol=0.0, max_iters=2, seed=1,
                                           track=si.TrackOptions(residual_every_k=2)), out=x_out)
         del warm
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        prob2 = si.ProblemMatrix(a_np, si.Symmetry.spd, context=ctx)  # H2D of A
-        t_prob = time.perf_counter()
-        res = si.run_inverter(si.InverterConfig(prob2, si.SketchRule.gaussian_device(q), tol=0.0, max_iters=k_e2e,
-                                                seed=0, track=si.TrackOptions(residual_every_k=k_e2e)),
-                              out=x_out)
-        t1 = time.perf_counter()
-        assert res.state.k == k_e2e
-        e2e_v = k_e2e / (t1 - t0)
+        # the whole run is timed by the host wall clock (allocator calls, pinned copies): three complete
+        # runs, each a fresh ProblemMatrix from the host A, and the median is reported (all three listed)
+        runs = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            prob2 = si.ProblemMatrix(a_np, si.Symmetry.spd, context=ctx)  # H2D of A
+            t_prob = time.perf_counter()
+            res = si.run_inverter(si.InverterConfig(prob2, si.SketchRule.gaussian_device(q), tol=0.0, max_iters=k_e2e,
+                                                    seed=0, track=si.TrackOptions(residual_every_k=k_e2e)),
+                                  out=x_out)
+            t1 = time.perf_counter()
+            assert res.state.k == k_e2e
+            runs.append((t1 - t0, t_prob - t0, t1 - t_prob))
+            del prob2
+        runs.sort()
+        dt, dt_prob, dt_run = runs[1]
+        e2e_v = k_e2e / dt
         e2e = {"value": e2e_v, "unit": "iter/s", "h2d_bytes_per_step": int(8 * n * n / k_e2e),
                "d2h_bytes_per_step": int(16 + 8 * n * n / k_e2e + 8 * 2 / k_e2e),
                "run_iterations": k_e2e,
-               "phases_ms": {"problem_upload_validate": 1e3 * (t_prob - t0), "run_inverter": 1e3 * (t1 - t_prob)},
+               "phases_ms": {"problem_upload_validate": 1e3 * dt_prob, "run_inverter": 1e3 * dt_run},
+               "runs_iter_per_s": [k_e2e / r[0] for r in runs], "statistic": "median of 3 complete runs",
                "note": "one run_inverter call (si_run_inverter) of the BASELINE run length from a host A, after one "
                        "untimed 2-iteration warm-up call of the same shapes: H2D of A, SPD validation, device "
                        "sketches with the iterations between checkpoints enqueued back to back, the reference's "
                        "forced residual checkpoints at k=1 (X1 = I + [Z R]·[W' Z]ᵀ: 4n²·2q from the rank-2q form) "
                        "and k=max (2n^3), X returned to host, all inside the timer; byte counts per step with the "
                        "A/X transfers amortised over the run"}
-        del prob2
 
     # ---- time to ε: config 1 (both normalisations) + config 3 (capped) ----
     tte = None

@@ -200,7 +200,10 @@ struct TileOps {
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const int64_t r = row(i, e), c = col(j, e);
-                        acc[i][j][e] = (r < p.M && c < p.N) ? b * src[r + c * p.ldc] : 0.0;
+                        if constexpr (EPI == EPI_SYMUPD)  // SI_SYMUPD_DBG & 64: streaming (evict-first) X loads and stores
+                            acc[i][j][e] = (r < p.M && c < p.N) ? ((p.dbg & 64) ? __ldcs(src + r + c * p.ldc) : src[r + c * p.ldc]) : 0.0;
+                        else
+                            acc[i][j][e] = (r < p.M && c < p.N) ? b * src[r + c * p.ldc] : 0.0;
                     }
         } else {
 #pragma unroll
@@ -313,9 +316,15 @@ struct TileOps {
                             for (int h = 0; h < 2; ++h) {
                                 const int64_t r = row(i, 2 * h), c = col(j, 2 * h);
                                 const double v0 = acc[i][j][2 * h], v1 = acc[i][j][2 * h + 1];
-                                p.C[r + c * p.ldc] = v0;
-                                p.C[r + (c + 1) * p.ldc] = v1;
-                                *reinterpret_cast<double2*>(p.C + c + r * p.ldc) = make_double2(v0, v1);
+                                if (!(p.dbg & 64)) {
+                                    p.C[r + c * p.ldc] = v0;
+                                    p.C[r + (c + 1) * p.ldc] = v1;
+                                    *reinterpret_cast<double2*>(p.C + c + r * p.ldc) = make_double2(v0, v1);
+                                } else {  // experiment: DRAM reads 1.42 -> 1.26 GB per launch at config 3, 0.5% slower
+                                    __stcs(p.C + r + c * p.ldc, v0);
+                                    __stcs(p.C + r + (c + 1) * p.ldc, v1);
+                                    __stcs(reinterpret_cast<double2*>(p.C + c + r * p.ldc), make_double2(v0, v1));
+                                }
                                 bad |= !isfinite(v0) || !isfinite(v1);
                             }
                     if (bad && p.nonfinite) atomicOr(p.nonfinite, 1);
@@ -402,6 +411,7 @@ __global__ void __launch_bounds__(WM* WN * 32, ((EPI == EPI_SYMUPD || EPI == EPI
     int pk = 0, ps = 0, pround = 0, pissued = 0;
     typename T::Work pwork{};
     int pnk = 0;
+    const uint64_t keep = EPI == EPI_SYMUPD ? l2_policy_evict_last() : 0;
     if (producer && pw < W) {
         pwork = T::decode(pw, p);
         pnk = chunk_kt(pwork.split);
@@ -414,14 +424,22 @@ __global__ void __launch_bounds__(WM* WN * 32, ((EPI == EPI_SYMUPD || EPI == EPI
         const int32_t kc = (int32_t)(pwork.split * p.k_chunk + (int64_t)pk * BK);
         const int32_t mc = (int32_t)(pwork.tile_m * BM), nc = (int32_t)(pwork.tile_n * BN);
         mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
-        if constexpr (A_KMAJOR)
-            tma_load_2d(As, &tmA, kc, mc, &full[s]);
-        else
-            tma_load_2d(As, &tmA, mc, kc, &full[s]);
-        if constexpr (B_KMAJOR)
-            tma_load_2d(Bs, &tmB, kc, nc, &full[s]);
-        else
-            tma_load_2d(Bs, &tmB, nc, kc, &full[s]);
+        if (EPI == EPI_SYMUPD && !A_KMAJOR && !B_KMAJOR && !(p.dbg & 32)) {
+            // the rank-2q panels are re-read by every tile of their block row / column while 4 GB of
+            // X stream through the L2: keep them (evict-last; DRAM reads 1.63 -> 1.42 GB per launch at
+            // config 3, time unchanged; SI_SYMUPD_DBG & 32 turns the hint off)
+            tma_load_2d_hint(As, &tmA, mc, kc, &full[s], keep);
+            tma_load_2d_hint(Bs, &tmB, nc, kc, &full[s], keep);
+        } else {
+            if constexpr (A_KMAJOR)
+                tma_load_2d(As, &tmA, kc, mc, &full[s]);
+            else
+                tma_load_2d(As, &tmA, mc, kc, &full[s]);
+            if constexpr (B_KMAJOR)
+                tma_load_2d(Bs, &tmB, kc, nc, &full[s]);
+            else
+                tma_load_2d(Bs, &tmB, nc, kc, &full[s]);
+        }
         ++pissued;
         if (++ps == STAGES) {
             ps = 0;
