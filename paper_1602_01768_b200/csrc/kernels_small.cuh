@@ -28,7 +28,7 @@ __device__ __noinline__ void jacobi_isqrt_block(const double* __restrict__ Gm, i
     int* pp = reinterpret_cast<int*>(sn + half);  // half
     int* rr = pp + half;                          // half
     __shared__ double red[32];
-    __shared__ double s_scale, s_off, s_lmax;
+    __shared__ double s_scale, s_off;
     __shared__ int s_fail;
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
 
@@ -130,7 +130,6 @@ __device__ __noinline__ void jacobi_isqrt_block(const double* __restrict__ Gm, i
             const double lam = a[i + i * q];
             if (lam <= floor_rel * lmax || lam <= 0.0) fail = 1;
         }
-        s_lmax = lmax;
         s_fail = fail;
     }
     __syncthreads();
