@@ -23,7 +23,7 @@ def env():
 # K <= 256, M, N > 64, alpha = 1, beta != 0: the C-panel kernels (gemm_tma_cbulk_kernel for even M)
 @pytest.mark.parametrize("ak,bk", [(False, True), (False, False), (True, True)])
 @pytest.mark.parametrize("M,N,K", [(512, 256, 64), (300, 130, 64), (1026, 190, 32), (640, 448, 256), (258, 66, 16),
-                                   (301, 130, 64)])
+                                   (301, 130, 64), (770, 322, 40), (4100, 260, 8), (20000, 70, 64), (140, 9000, 48)])
 def test_cpanel_update_shapes(env, ak, bk, M, N, K):
     si, torch, ctx, ops = env
     rng = np.random.default_rng(7 * M + N + K)
